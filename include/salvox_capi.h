@@ -1,0 +1,235 @@
+/* salvox_capi.h -- the C-ABI boundary of the B200 salient-region hot path.
+ *
+ * This is the thin layer the reference's C++ API (and any FFI: ctypes, cgo,
+ * JNI) binds to. Plain pointers and sizes only; no C++/torch types. Every entry
+ * point names the reference interface it replaces (paths relative to
+ * /root/reference/proj). See INTEGRATION.md for the bindings.
+ *
+ * Conventions
+ *  - Volumes are float32, x fastest: index = x + nx*(y + ny*z)
+ *    (include/salvox/volume.hpp:43-46). A 2D image has nz == 1.
+ *  - Every function returns a status: SALVOX_OK, or an error whose message is
+ *    available from salvox_last_error() (thread-local). The status classes
+ *    mirror the reference's exception types: SALVOX_EINVAL <-> std::invalid_argument
+ *    (same message text), SALVOX_ERUNTIME <-> std::runtime_error.
+ *  - There is no CPU fallback: without a usable CUDA device every compute
+ *    entry point fails with SALVOX_ECUDA.
+ *  - A context owns one device's streams and buffers; use one context per
+ *    host thread at a time (calls on one context are serialized internally).
+ */
+#ifndef SALVOX_CAPI_H
+#define SALVOX_CAPI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define SALVOX_API __attribute__((visibility("default")))
+#else
+#define SALVOX_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SALVOX_OK 0
+#define SALVOX_EINVAL 1      /* std::invalid_argument */
+#define SALVOX_ECUDA 2       /* CUDA / device failure */
+#define SALVOX_EUNSUPPORTED 3 /* valid for the reference, not implemented on device */
+#define SALVOX_ERUNTIME 4    /* std::runtime_error (phantom spec, IO) */
+
+#define SALVOX_KERNEL_IDENTITY 0     /* kernel.hpp:11-15 */
+#define SALVOX_KERNEL_EPANECHNIKOV 1
+#define SALVOX_KERNEL_GAUSSIAN 2
+
+#define SALVOX_METHOD_QUADRANT 0 /* pipeline.hpp:19 Method */
+#define SALVOX_METHOD_SHIFT 1
+#define SALVOX_METHOD_ABMSOD 2 /* out of scope: SALVOX_EUNSUPPORTED */
+#define SALVOX_METHOD_OCTANT 3 /* NEW: 3D generalisation of quadrant.cpp */
+
+#define SALVOX_FLAG_CONVERGED 1u /* detection.hpp:11-15 */
+#define SALVOX_FLAG_DEGENERATE 2u
+#define SALVOX_FLAG_BOUNDARY_CLAMPED 4u
+
+typedef struct salvox_ctx salvox_ctx;
+
+/* IntensityWindow (volume.hpp:91-113). full_range != 0 replaces low/high by the
+ * observed range, computed on the device (IntensityWindow::full_range). */
+typedef struct {
+  double low;
+  double high;
+  int32_t bins;
+  int32_t full_range;
+} salvox_window;
+
+/* SaliencyMaximum (pipeline.hpp:32-36) + its linear voxel index. */
+typedef struct {
+  double position[3];
+  double score;
+  double scale;
+  int64_t linear_index;
+} salvox_maximum;
+
+/* Detection (detection.hpp:18-37); H row-major. 136 bytes. */
+typedef struct {
+  double center[3];
+  double H[9];
+  double entropy_bits;
+  double pdf_diff;
+  double bhattacharyya;
+  int32_t iterations;
+  uint32_t flags;
+  int32_t seed_index;
+  int32_t reserved;
+} salvox_detection;
+
+/* DetectParams (pipeline.hpp:88-99) + SeedPlan (seeds.hpp:16-32) + the method
+ * parameter blocks (quadrant.hpp:14-28, shift.hpp:18-34). workers is accepted
+ * and ignored (the device replaces parallel_for). */
+typedef struct {
+  int32_t method;
+  int32_t seed_mode; /* 0 lattice, 1 random */
+  double seed_spacing;
+  int32_t seed_count;
+  int32_t top_k;
+  uint64_t rng_seed;
+  const double* scales;
+  int32_t n_scales;
+  int32_t workers;
+  double dedupe_radius;
+  double entropy_quantile;
+  double pdf_quantile;
+  double quadrant_eta;
+  int32_t quadrant_max_iters;
+  int32_t n_quadrant_scales; /* 0 -> lround(scales) (pipeline.cpp:323-324) */
+  const int32_t* quadrant_scales;
+  double shift_min_step;
+  int32_t shift_max_iters;
+  int32_t shift_step_kernel;
+  int32_t shift_hist_kernel;
+  int32_t reserved;
+  double shift_min_inbounds_fraction;
+  const double* shift_target; /* NULL -> uniform over bins */
+} salvox_detect_params;
+
+/* ------------------------------------------------------------------ context */
+SALVOX_API const char* salvox_last_error(void);
+SALVOX_API int salvox_version(void);
+/* Creates a context on CUDA device `device`. */
+SALVOX_API int salvox_ctx_create(int device, salvox_ctx** out);
+SALVOX_API int salvox_ctx_destroy(salvox_ctx* ctx);
+/* Binds the context to an external CUDA stream (cudaStream_t as void*); NULL
+ * restores the context's own stream. Device-pointer entry points run on it. */
+SALVOX_API int salvox_ctx_set_stream(salvox_ctx* ctx, void* stream);
+/* Number of this library's kernel launches issued through ctx so far. */
+SALVOX_API int salvox_ctx_launch_count(salvox_ctx* ctx, uint64_t* out);
+
+/* ------------------------------------------------------- exhaustive pass (E1)
+ * Replaces kadir_brady_exhaustive (include/salvox/pipeline.hpp:49-53,
+ * src/pipeline.cpp:63-166). Same validation and messages (scales >= 2,
+ * budget). kernel: identity only on device (others -> SALVOX_EUNSUPPORTED).
+ * score_out / best_scale_out (nx*ny*nz floats, nullable) receive the dense map;
+ * up to `cap` maxima (score-descending, ties by linear index -- the
+ * reference's stable_sort order) go to `maxima`; *n_maxima is the full count
+ * (fetch all with salvox_last_maxima when it exceeds cap). *visits gets the
+ * reference's EvalCounter increment (nullable). */
+SALVOX_API int salvox_exhaustive(salvox_ctx* ctx, const float* volume, int32_t nx, int32_t ny, int32_t nz,
+                      const salvox_window* iw, const double* scales, int32_t n_scales,
+                      int32_t kernel, uint64_t budget, float* score_out, float* best_scale_out,
+                      salvox_maximum* maxima, int64_t cap, int64_t* n_maxima, uint64_t* visits);
+
+/* z-slab form for multi-GPU sharding: `slab` holds planes [zs0, zs1) of a
+ * volume nx*ny*nz (host pointer); the call scores and selects maxima for the
+ * owned planes [z0, z1) (it needs zs0 <= max(0, z0-R-1), zs1 >= min(nz, z1+R+1),
+ * R = max scale + 1). Maps cover the owned planes only; maxima positions and
+ * linear indices are global. budget applies to the whole volume. */
+SALVOX_API int salvox_exhaustive_slab(salvox_ctx* ctx, const float* slab, int32_t nx, int32_t ny,
+                           int32_t nz, int32_t zs0, int32_t zs1, int32_t z0, int32_t z1,
+                           const salvox_window* iw, const double* scales, int32_t n_scales,
+                           int32_t kernel, uint64_t budget, float* score_out,
+                           float* best_scale_out, salvox_maximum* maxima, int64_t cap,
+                           int64_t* n_maxima, uint64_t* visits);
+
+/* Device-resident form (inputs already in HBM; used for the kernel-only
+ * timing): d_volume, d_score, d_best_scale are device pointers (d_score and
+ * d_best_scale nullable). Runs on the context stream; *n_maxima is written
+ * after the stream synchronises. */
+SALVOX_API int salvox_exhaustive_device(salvox_ctx* ctx, const float* d_volume, int32_t nx, int32_t ny,
+                             int32_t nz, const salvox_window* iw, const double* scales,
+                             int32_t n_scales, int32_t kernel, uint64_t budget, float* d_score,
+                             float* d_best_scale, int64_t* n_maxima);
+
+/* Copies the maxima of the last exhaustive call on ctx. */
+SALVOX_API int salvox_last_maxima(salvox_ctx* ctx, salvox_maximum* out, int64_t cap, int64_t* n_out);
+
+/* Exact integer identity-kernel histograms of the last exhaustive call, for
+ * `n` voxels (global linear indices in the owned planes) at every needed
+ * radius r (ascending, written to radii_out): out[v][r][0..bins-1] = S_b(r) and
+ * out[v][r][bins] = T(r) = sum_b S_b(r) (uint32; out holds n*n_radii*(bins+1)).
+ * Debug / parity entry point: recomputes those voxels with the same kernel
+ * body (one CTA per voxel). radii_out must hold 3*n_scales doubles. */
+SALVOX_API int salvox_exhaustive_debug_hist(salvox_ctx* ctx, const int64_t* voxels, int32_t n,
+                                 uint32_t* out, double* radii_out, int32_t* n_radii);
+
+/* ---------------------------------------------------- seed-grid detector (E2/E3)
+ * Replaces detect (include/salvox/pipeline.hpp:103-104, src/pipeline.cpp:311-402):
+ * seed planning, per-seed seek (shift / quadrant / octant) on the device, then
+ * thresholds + dedupe on the device. out receives up to cap detections;
+ * *n_out the count. per_seed (nullable, cap_seed) receives every trajectory's
+ * pre-selection detection in seed order; *n_seed its count. */
+SALVOX_API int salvox_detect(salvox_ctx* ctx, const float* volume, int32_t nx, int32_t ny, int32_t nz,
+                  const salvox_window* iw, const salvox_detect_params* params,
+                  salvox_detection* out, int64_t cap, int64_t* n_out,
+                  salvox_detection* per_seed, int64_t cap_seed, int64_t* n_seed,
+                  uint64_t* visits);
+
+/* Device-resident form of detect over a batch of `batch` volumes stored back
+ * to back at d_volumes (device pointer). For each volume the selected
+ * detections go to out[v*cap ...] and the count to n_out[v] (host arrays). */
+SALVOX_API int salvox_detect_batch_device(salvox_ctx* ctx, const float* d_volumes, int32_t batch,
+                               int32_t nx, int32_t ny, int32_t nz, const salvox_window* iw,
+                               const salvox_detect_params* params, salvox_detection* out,
+                               int64_t cap, int64_t* n_out, uint64_t* visits);
+
+/* Per-seed seek only (saliency_shift shift.hpp:57-59 / quadrant_seek
+ * quadrant.hpp:73-76 / octant), seeds given explicitly: positions (3 per seed),
+ * seed_scales (shift: isotropic half extent s, window (s,s,s) or (s,s,1) in 2D;
+ * ignored for quadrant/octant), seed_half_extents (nullable, 3 per seed:
+ * ShiftParams::half_extents, overrides seed_scales; z is pinned to 1 in 2D as
+ * shift.cpp:9 does), seed indices (nullable -> 0..n-1). Writes one detection
+ * per seed in seed order. */
+SALVOX_API int salvox_seek(salvox_ctx* ctx, const float* volume, int32_t nx, int32_t ny, int32_t nz,
+                const salvox_window* iw, const salvox_detect_params* params,
+                const double* seed_positions, const double* seed_scales,
+                const double* seed_half_extents, const int32_t* seed_index, int64_t n,
+                salvox_detection* out, uint64_t* visits);
+
+/* Thresholds + dedupe (pipeline.cpp:383-401, :54-59, :168-183) on the device. */
+SALVOX_API int salvox_select(salvox_ctx* ctx, const salvox_detection* dets, int64_t n, double q_entropy,
+                  double q_pdf, int32_t k, double radius, salvox_detection* out,
+                  int64_t* n_out);
+/* dedupe_top_k alone (pipeline.hpp:57). */
+SALVOX_API int salvox_dedupe_top_k(salvox_ctx* ctx, const salvox_detection* dets, int64_t n, int32_t k,
+                        double radius, salvox_detection* out, int64_t* n_out);
+
+/* ------------------------------------------------------- host-side data formats */
+/* plan_seeds (seeds.hpp:43): pass cap = 0 to query the count. */
+SALVOX_API int salvox_plan_seeds(int32_t nx, int32_t ny, int32_t nz, int32_t mode, double spacing,
+                      int32_t count, const double* scales, int32_t n_scales, uint64_t rng_seed,
+                      double* positions, double* seed_scales, int64_t cap, int64_t* n_out);
+
+/* make_phantom (phantom.hpp:125, src/phantom.cpp:364-421). shape 0 box, 1 ball,
+ * 2 ellipsoid; fill_type 0 uniform(levels), 1 constant(value); bg_type 0
+ * constant, 1 gaussian. Writes the volume and 3 centroid doubles per region. */
+SALVOX_API int salvox_make_phantom(int32_t nx, int32_t ny, int32_t nz, int32_t bg_type, double bg_value,
+                        double bg_mean, double bg_sigma, int32_t n_regions,
+                        const int32_t* shape, const double* center, const double* half_extents,
+                        const double* radius, const double* axes, const int32_t* fill_type,
+                        const int32_t* fill_levels, const double* fill_value, uint64_t rng_seed,
+                        float* out_volume, double* out_centroids);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,196 @@
+/* salvox_oracle.h -- TEST INFRASTRUCTURE ONLY.
+ *
+ * Plain-C restatement of the reference (salvox, /root/reference/proj) hot path,
+ * used as the CHECKER by tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline leg. Nothing in the product (paper_1310_6736_b200/) links,
+ * imports or calls this code.
+ *
+ * Parity status: the reference cannot be compiled here (Eigen3 and vendor/
+ * headers are absent), so this restatement is pinned against the reference's
+ * own known-answer tests and fixtures (tests/test_oracle_*.py port them), not
+ * against reference binaries. Eigen 3x3 inverse/determinant rounding is
+ * restated from Eigen 3.3/3.4 InverseImpl.h / Determinant.h (not verifiable
+ * offline) -- see DESIGN.md "Parity".
+ *
+ * Arithmetic convention: compiled with -ffp-contract=off so every fp64
+ * expression rounds exactly as the reference's (x86-64, no -march => no FMA).
+ */
+#ifndef SALVOX_ORACLE_H
+#define SALVOX_ORACLE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- rng.hpp:11-51 ---- */
+typedef struct {
+  uint64_t state;
+  int have_spare;
+  double spare;
+} sxo_rng;
+
+void sxo_rng_init(sxo_rng* r, uint64_t seed);
+uint64_t sxo_rng_next_u64(sxo_rng* r);
+double sxo_rng_next_double(sxo_rng* r);
+uint64_t sxo_rng_next_below(sxo_rng* r, uint64_t n);
+double sxo_rng_next_range(sxo_rng* r, double lo, double hi);
+double sxo_rng_next_gaussian(sxo_rng* r);
+
+/* ---- phantom.cpp:364-421 (make_phantom). shape: 0 box, 1 ball, 2 ellipsoid.
+ * fill_type: 0 uniform(levels), 1 constant(value). bg_type: 0 constant, 1 gaussian.
+ * Writes nx*ny*nz floats and 3 centroid doubles per region. Returns 0 or -1 (err). */
+int sxo_make_phantom(int nx, int ny, int nz, int bg_type, double bg_value, double bg_mean,
+                     double bg_sigma, int n_regions, const int* shape, const double* center,
+                     const double* half_extents, const double* radius, const double* axes,
+                     const int* fill_type, const int* fill_levels, const double* fill_value,
+                     uint64_t rng_seed, float* out_volume, double* out_centroids, char* err,
+                     int err_len);
+
+/* ---- volume.hpp:102-105 ---- */
+int sxo_bin_of(double low, double high, int bins, double intensity);
+
+/* ---- pipeline.cpp:63-166 kadir_brady_exhaustive ----
+ * mode 0 = literal (reference loop order, fp64 fl(n/r^2) sums);
+ * mode 1 = exact (integer shell sums S_b(r), p_b = S_b/T in fp64).
+ * kernel: 0 identity, 1 epanechnikov, 2 gaussian (literal mode only for 2).
+ * z_begin/z_end restrict the scored planes (bounded CPU-baseline samples);
+ * pass 0, nz for the whole volume. threads >= 1 splits z planes over pthreads.
+ * Returns 0, or -1 with err (invalid_argument semantics). */
+int sxo_exhaustive(const float* vol, int nx, int ny, int nz, double low, double high, int bins,
+                   const double* scales, int n_scales, int kernel, uint64_t budget, int mode,
+                   int threads, int z_begin, int z_end, float* score, float* best_scale,
+                   uint64_t* visits, char* err, int err_len);
+
+/* Exact integer histograms S_b(r) (b = 0..bins-1) and T(r) around one voxel
+ * for the identity kernel: S_b(r) = sum over in-bounds offsets o with
+ * make_sphere_offsets membership of |o|^2 for voxels in bin b. */
+int sxo_voxel_shell_hist(const float* vol, int nx, int ny, int nz, double low, double high,
+                         int bins, int x, int y, int z, double radius, uint64_t* S);
+
+/* pipeline.cpp:143-165 strict 26-neighbour maxima, stable-sorted by score desc.
+ * Writes up to cap records; returns the total count found. */
+int64_t sxo_local_maxima(const float* score, const float* best_scale, int nx, int ny, int nz,
+                         double* pos, double* sc, double* scale, int64_t* lin, int64_t cap);
+
+/* ---- detection.hpp:18-37 ---- */
+typedef struct {
+  double center[3];
+  double H[9]; /* row-major */
+  double entropy_bits;
+  double pdf_diff;
+  double bhattacharyya;
+  int32_t iterations;
+  uint32_t flags;
+  int32_t seed_index;
+  int32_t pad_;
+} sxo_detection;
+
+/* ---- seeds.cpp:7-45 ---- mode 0 lattice, 1 random. Writes positions (3 per
+ * seed) and scales, index = order. Returns seed count (or -1 on invalid plan);
+ * pass cap=0 to query. */
+int64_t sxo_plan_seeds(int nx, int ny, int nz, int mode, double spacing, int count,
+                       const double* scales, int n_scales, uint64_t rng_seed, double* pos,
+                       double* seed_scale, int64_t cap);
+
+/* entropy variant for quadrant/octant box entropies and final scores:
+ * 0 = glibc log (reference), 1 = the shared portable log (sx_log). */
+void sxo_set_log_mode(int mode);
+
+/* ---- shift.cpp:15-34 shift_step. kernels: 0 id, 1 epan, 2 gauss.
+ * target may be NULL (uniform). Returns 1 and writes out[3], or 0 (nullopt). */
+int sxo_shift_step(const float* vol, int nx, int ny, int nz, double low, double high, int bins,
+                   const double x[3], const double half[3], int step_kernel, int hist_kernel,
+                   const double* target, double out[3], uint64_t* visits);
+
+/* ---- shift.cpp:36-107 saliency_shift ---- */
+int sxo_saliency_shift(const float* vol, int nx, int ny, int nz, double low, double high, int bins,
+                       const double seed[3], const double half[3], int step_kernel,
+                       int hist_kernel, int max_iters, double min_step, const double* target,
+                       double min_inbounds_fraction, sxo_detection* out, uint64_t* visits);
+
+/* ---- window.cpp:5-19 / :30-46 / :54-60 (isotropic or diagonal windows) ---- */
+int sxo_candidate_histogram(const float* vol, int nx, int ny, int nz, double low, double high,
+                            int bins, const double center[3], const double H[9], int kernel,
+                            double* p_out, uint64_t* visits);
+int sxo_pdf_difference(const float* vol, int nx, int ny, int nz, double low, double high, int bins,
+                       const double center[3], const double H[9], int kernel, double* out,
+                       uint64_t* visits);
+double sxo_entropy_bits(const double* p, int bins);
+
+/* ---- quadrant.cpp:18-81 ---- */
+double sxo_box_entropy_bits(const float* vol, int nx, int ny, int nz, double low, double high,
+                            int bins, double x0, double x1, double y0, double y1, double z0,
+                            double z1, int min_voxels, uint64_t* visits);
+typedef struct {
+  double entropy[8];
+  int32_t best_scale[8];
+  double norm_entropy[8];
+  double displacement[3];
+  int32_t degenerate;
+  int32_t pad_;
+} sxo_ascent_state;
+/* dims = 2 (quadrant, nz must be 1) or 3 (octant, NEW -- generalises quadrant). */
+int sxo_ascent_step(const float* vol, int nx, int ny, int nz, double low, double high, int bins,
+                    int dims, const double p[3], const int* scales, int n_scales,
+                    double moved[3], sxo_ascent_state* st, uint64_t* visits);
+typedef struct {
+  double position[3];
+  int32_t best_scale;
+  int32_t iterations;
+  double entropy_bits;
+  int32_t converged;
+  int32_t degenerate;
+} sxo_ascent_result;
+int sxo_ascent_seek_one(const float* vol, int nx, int ny, int nz, double low, double high,
+                        int bins, int dims, const double seed[3], const int* scales, int n_scales,
+                        double eta, int max_iters, sxo_ascent_result* out, uint64_t* visits);
+
+/* ---- pipeline.cpp:311-402 detect ----
+ * method: 0 quadrant, 1 shift, 3 octant (2 = abmsod is out of scope -> -1).
+ * per_seed (optional, cap_seed) receives the pre-selection detections in seed
+ * order; out receives the selected detections. Returns the number selected or -1. */
+typedef struct {
+  int method;
+  int seed_mode;
+  double seed_spacing;
+  int seed_count;
+  uint64_t rng_seed;
+  const double* scales;
+  int n_scales;
+  int top_k;
+  double dedupe_radius;
+  double entropy_quantile;
+  double pdf_quantile;
+  int workers;
+  double quadrant_eta;
+  int quadrant_max_iters;
+  const int* quadrant_scales; /* NULL -> lround(scales) */
+  int n_quadrant_scales;
+  double shift_min_step;
+  int shift_max_iters;
+  int shift_step_kernel;
+  int shift_hist_kernel;
+  double shift_min_inbounds_fraction;
+} sxo_detect_params;
+int64_t sxo_detect(const float* vol, int nx, int ny, int nz, double low, double high, int bins,
+                   const sxo_detect_params* params, sxo_detection* per_seed, int64_t cap_seed,
+                   int64_t* n_seed_out, sxo_detection* out, int64_t cap, uint64_t* visits,
+                   char* err, int err_len);
+
+/* pipeline.cpp:54-59 / :383-401 / :168-183 */
+int64_t sxo_select(const sxo_detection* dets, int64_t n, double q_entropy, double q_pdf, int k,
+                   double radius, sxo_detection* out);
+int64_t sxo_dedupe_top_k(const sxo_detection* dets, int64_t n, int k, double radius,
+                         sxo_detection* out);
+
+/* Eigen 3x3 inverse / determinant restatement (exported for tests). */
+void sxo_eigen_inverse3(const double m[9], double out[9]);
+double sxo_eigen_det3(const double m[9]);
+double sxo_log_portable(double x);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,14 @@
+"""paper_1310_6736_b200 -- B200-native hot path of the salvox 3D salient-region detector.
+
+Drop-in for the reference's exhaustive Kadir-Brady pass, seed-grid detector
+(shift / quadrant / octant ascent) and detection selection, computed by
+hand-written sm_100a kernels behind the C-ABI in include/salvox_capi.h.
+"""
+from ._lib import (DET_DTYPE, MAX_DTYPE, Context, SalvoxCudaError, SalvoxError,
+                   default_context)
+from .api import (DEFAULT_BUDGET, dedupe_top_k, detect, detect_records, detection_to_dict,
+                  exhaustive_debug_hist, kadir_brady_exhaustive, kadir_brady_exhaustive_records,
+                  kadir_brady_exhaustive_slab, make_phantom, plan_seeds, quadrant_seek,
+                  saliency_shift, seek_records, select)
+
+__version__ = "0.1.0"

@@ -1,0 +1,362 @@
+"""The reference's public API for the hot path, backed by the B200 C-ABI.
+
+Mirrors the Python binding of the reference (/root/reference/proj/bindings/
+py_module.cpp) -- same function names, argument names, defaults, return shapes
+and exception types -- for the functions on the accelerated path:
+
+  kadir_brady_exhaustive   py_module.cpp:186-204  (pipeline.cpp:63-166)
+  detect                   py_module.cpp:206-230  (pipeline.cpp:311-402)
+  saliency_shift           py_module.cpp:159-170  (shift.cpp:36-107)
+  make_phantom             py_module.cpp:96-112   (phantom.cpp:364-421)
+
+plus the C++-level entry points the binding does not expose (plan_seeds,
+quadrant_seek / octant_seek, dedupe_top_k, select, the z-slab exhaustive).
+
+Volumes are numpy arrays indexed [z, y, x] (2D arrays are [y, x], nz = 1).
+Everything computes on the GPU; there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+
+import numpy as np
+
+from . import _lib
+from ._lib import DET_DTYPE, MAX_DTYPE, KERNELS, METHODS, check, default_context, ptr
+
+DEFAULT_BUDGET = 2_000_000  # include/salvox/pipeline.hpp:53
+
+
+def _volume(arr):
+    a = np.ascontiguousarray(arr, dtype=np.float32)
+    if a.ndim == 2:
+        a = a[None]
+    if a.ndim != 3:
+        raise ValueError("expected a 2D or 3D array")
+    nz, ny, nx = a.shape
+    return a, nx, ny, nz
+
+
+def _window(low, high, bins):
+    """window_or_full (py_module.cpp:73-77): explicit window, else observed range on device."""
+    if low is not None and high is not None:
+        if not (low < high):
+            raise ValueError("IntensityWindow: low must be < high")
+        return _lib.Window(float(low), float(high), int(bins), 0)
+    return _lib.Window(0.0, 1.0, int(bins), 1)
+
+
+def _ctx(ctx):
+    return ctx if ctx is not None else default_context()
+
+
+_FLAG_NAMES = [(1, "converged"), (2, "degenerate"), (4, "boundary-clamped")]
+
+
+def detection_to_dict(d) -> dict:
+    """detection_to_dict (py_module.cpp:58-70)."""
+    flags = int(d["flags"])
+    return {
+        "center": tuple(float(v) for v in d["center"]),
+        "H": np.array(d["H"], dtype=np.float64).reshape(3, 3),
+        "entropy_bits": float(d["entropy_bits"]),
+        "pdf_diff": float(d["pdf_diff"]),
+        "bhattacharyya": float(d["bhattacharyya"]),
+        "iterations": int(d["iterations"]),
+        "flags": [n for f, n in _FLAG_NAMES if flags & f],
+        "seed_index": int(d["seed_index"]),
+    }
+
+
+# ------------------------------------------------------------------ exhaustive (E1)
+def kadir_brady_exhaustive_records(volume, scales, window_low=None, window_high=None, bins=64,
+                                   kernel="identity", budget=DEFAULT_BUDGET, ctx=None,
+                                   want_maps=True):
+    """Structured form: (score[z,y,x] f32, best_scale[z,y,x] f32, maxima MAX_DTYPE, visits)."""
+    v, nx, ny, nz = _volume(volume)
+    sc = np.ascontiguousarray(scales, dtype=np.float64)
+    iw = _window(window_low, window_high, bins)
+    c = _ctx(ctx)
+    score = np.empty(v.shape, np.float32) if want_maps else None
+    best = np.empty(v.shape, np.float32) if want_maps else None
+    cap = 4096
+    maxima = np.empty(cap, MAX_DTYPE)
+    n = C.c_int64(0)
+    visits = C.c_uint64(0)
+    check(_lib.load().salvox_exhaustive(
+        c.handle, ptr(v), nx, ny, nz, C.byref(iw), ptr(sc), len(sc), KERNELS[kernel], int(budget),
+        ptr(score), ptr(best), ptr(maxima), cap, C.byref(n), C.byref(visits)))
+    if n.value > cap:
+        maxima = np.empty(n.value, MAX_DTYPE)
+        check(_lib.load().salvox_last_maxima(c.handle, ptr(maxima), n.value, C.byref(n)))
+    return score, best, maxima[: n.value], int(visits.value)
+
+
+def kadir_brady_exhaustive(volume, scales, window_low=None, window_high=None, bins=64,
+                           kernel="identity", budget=DEFAULT_BUDGET, ctx=None):
+    """Dense scan; returns (score map [z,y,x], ranked local maxima) like py_module.cpp:186-204.
+
+    The reference binding always uses the default budget (2e6 voxel-scale
+    evaluations) and raises ValueError above it; pass ``budget`` to lift it.
+    """
+    score, _, maxima, _ = kadir_brady_exhaustive_records(volume, scales, window_low, window_high,
+                                                         bins, kernel, budget, ctx)
+    out = [{"position": tuple(float(p) for p in m["position"]), "score": float(m["score"]),
+            "scale": float(m["scale"])} for m in maxima]
+    return score, out
+
+
+def kadir_brady_exhaustive_slab(slab, nz_total, zs0, z0, z1, scales, window_low, window_high,
+                                bins=64, kernel="identity", budget=DEFAULT_BUDGET, ctx=None):
+    """z-slab form (salvox_exhaustive_slab): `slab` holds planes [zs0, zs0+len) of a volume
+    with nz_total planes; returns owned-plane maps [z0, z1) and global maxima."""
+    s = np.ascontiguousarray(slab, dtype=np.float32)
+    nzs, ny, nx = s.shape
+    sc = np.ascontiguousarray(scales, dtype=np.float64)
+    iw = _window(window_low, window_high, bins)
+    if iw.full_range:
+        raise ValueError("exhaustive slab: pass an explicit (global) intensity window")
+    c = _ctx(ctx)
+    score = np.empty((z1 - z0, ny, nx), np.float32)
+    best = np.empty((z1 - z0, ny, nx), np.float32)
+    cap = 4096
+    maxima = np.empty(cap, MAX_DTYPE)
+    n = C.c_int64(0)
+    visits = C.c_uint64(0)
+    check(_lib.load().salvox_exhaustive_slab(
+        c.handle, ptr(s), nx, ny, int(nz_total), int(zs0), int(zs0 + nzs), int(z0), int(z1),
+        C.byref(iw), ptr(sc), len(sc), KERNELS[kernel], int(budget), ptr(score), ptr(best),
+        ptr(maxima), cap, C.byref(n), C.byref(visits)))
+    if n.value > cap:
+        maxima = np.empty(n.value, MAX_DTYPE)
+        check(_lib.load().salvox_last_maxima(c.handle, ptr(maxima), n.value, C.byref(n)))
+    return score, best, maxima[: n.value], int(visits.value)
+
+
+def exhaustive_debug_hist(voxels, bins, n_scales, ctx=None):
+    """Exact S_b(r) / T(r) of the last exhaustive call for the given linear voxel indices.
+    Returns (radii, hist[n, n_radii, bins+1] uint32; column `bins` holds T(r))."""
+    c = _ctx(ctx)
+    vox = np.ascontiguousarray(voxels, dtype=np.int64)
+    radii = np.zeros(3 * n_scales + 1)
+    nr = C.c_int32(0)
+    tmp = np.zeros(max(len(vox), 1) * 3 * n_scales * (bins + 1), np.uint32)
+    check(_lib.load().salvox_exhaustive_debug_hist(c.handle, ptr(vox), len(vox), ptr(tmp),
+                                                   ptr(radii), C.byref(nr)))
+    R = nr.value
+    return radii[:R], tmp[: len(vox) * R * (bins + 1)].reshape(len(vox), R, bins + 1)
+
+
+# --------------------------------------------------------------------- detect (E2/E3)
+def _detect_params(method="shift", seed_spacing=16.0, scales=(8.0,), k=20, dedupe_radius=5.0,
+                   entropy_quantile=0.9, pdf_quantile=0.0, workers=1, seed_mode="lattice",
+                   seed_count=400, rng_seed=0, quadrant_eta=0.5, quadrant_max_iters=50,
+                   quadrant_scales=None, shift_min_step=0.1, shift_max_iters=50,
+                   shift_step_kernel="identity", shift_hist_kernel="identity",
+                   min_inbounds_fraction=0.1, target=None):
+    keep = []
+    P = _lib.DetectParams()
+    P.method = METHODS[method]
+    P.seed_mode = 0 if seed_mode == "lattice" else 1
+    P.seed_spacing = float(seed_spacing)
+    P.seed_count = int(seed_count)
+    P.top_k = int(k)
+    P.rng_seed = int(rng_seed)
+    sc = (C.c_double * len(scales))(*[float(s) for s in scales])
+    keep.append(sc)
+    P.scales = sc
+    P.n_scales = len(scales)
+    P.workers = int(workers)
+    P.dedupe_radius = float(dedupe_radius)
+    P.entropy_quantile = float(entropy_quantile)
+    P.pdf_quantile = float(pdf_quantile)
+    P.quadrant_eta = float(quadrant_eta)
+    P.quadrant_max_iters = int(quadrant_max_iters)
+    if quadrant_scales is not None:
+        qs = (C.c_int32 * len(quadrant_scales))(*[int(q) for q in quadrant_scales])
+        keep.append(qs)
+        P.quadrant_scales = qs
+        P.n_quadrant_scales = len(quadrant_scales)
+    P.shift_min_step = float(shift_min_step)
+    P.shift_max_iters = int(shift_max_iters)
+    P.shift_step_kernel = KERNELS[shift_step_kernel]
+    P.shift_hist_kernel = KERNELS[shift_hist_kernel]
+    P.shift_min_inbounds_fraction = float(min_inbounds_fraction)
+    if target is not None:
+        t = np.ascontiguousarray(target, np.float64)
+        keep.append(t)
+        P.shift_target = t.ctypes.data_as(C.POINTER(C.c_double))
+    return P, keep
+
+
+def detect_records(volume, method="shift", seed_spacing=16.0, scales=(8.0,), k=20,
+                   dedupe_radius=5.0, window_low=None, window_high=None, bins=64,
+                   entropy_quantile=0.9, pdf_quantile=0.0, workers=1, ctx=None, per_seed=False,
+                   **extra):
+    """Structured form of detect: (selected DET_DTYPE, per-seed DET_DTYPE or None, visits)."""
+    v, nx, ny, nz = _volume(volume)
+    iw = _window(window_low, window_high, bins)
+    P, keep = _detect_params(method, seed_spacing, scales, k, dedupe_radius, entropy_quantile,
+                             pdf_quantile, workers, **extra)
+    c = _ctx(ctx)
+    ns = C.c_int64(0)
+    check(_lib.load().salvox_plan_seeds(nx, ny, nz, P.seed_mode, P.seed_spacing, P.seed_count,
+                                        C.cast(P.scales, C.c_void_p), P.n_scales, P.rng_seed,
+                                        None, None, 0, C.byref(ns)))
+    out = np.empty(max(int(k), 1), DET_DTYPE)
+    n_out = C.c_int64(0)
+    seeds = np.empty(max(ns.value, 1), DET_DTYPE) if per_seed else None
+    n_seed = C.c_int64(0)
+    visits = C.c_uint64(0)
+    check(_lib.load().salvox_detect(
+        c.handle, ptr(v), nx, ny, nz, C.byref(iw), C.byref(P), ptr(out), len(out),
+        C.byref(n_out), ptr(seeds), len(seeds) if per_seed else 0, C.byref(n_seed),
+        C.byref(visits)))
+    del keep
+    return (out[: n_out.value].copy(), seeds[: n_seed.value].copy() if per_seed else None,
+            int(visits.value))
+
+
+def detect(volume, method="shift", seed_spacing=16.0, scales=(8.0,), k=20, dedupe_radius=5.0,
+           window_low=None, window_high=None, bins=64, entropy_quantile=0.9, pdf_quantile=0.0,
+           workers=1, ctx=None, **extra):
+    """Seed, seek, threshold and dedupe in one call; returns detection dicts
+    (py_module.cpp:206-230). method: "shift", "quadrant" (2D) or "octant" (3D, new)."""
+    sel, _, _ = detect_records(volume, method, seed_spacing, scales, k, dedupe_radius, window_low,
+                               window_high, bins, entropy_quantile, pdf_quantile, workers, ctx,
+                               **extra)
+    return [detection_to_dict(d) for d in sel]
+
+
+def seek_records(volume, positions, scales=None, half_extents=None, method="shift",
+                 window_low=None, window_high=None, bins=64, seed_index=None, ctx=None, **extra):
+    """Per-seed trajectories (salvox_seek) in seed order -> (DET_DTYPE[n], visits)."""
+    v, nx, ny, nz = _volume(volume)
+    pos = np.ascontiguousarray(np.asarray(positions, np.float64).reshape(-1, 3))
+    n = len(pos)
+    sc = None if scales is None else np.ascontiguousarray(np.broadcast_to(
+        np.asarray(scales, np.float64), (n,)))
+    he = None if half_extents is None else np.ascontiguousarray(np.broadcast_to(
+        np.asarray(half_extents, np.float64), (n, 3)))
+    si = None if seed_index is None else np.ascontiguousarray(seed_index, np.int32)
+    iw = _window(window_low, window_high, bins)
+    P, keep = _detect_params(method, **extra)
+    c = _ctx(ctx)
+    out = np.empty(max(n, 1), DET_DTYPE)
+    visits = C.c_uint64(0)
+    check(_lib.load().salvox_seek(c.handle, ptr(v), nx, ny, nz, C.byref(iw), C.byref(P), ptr(pos),
+                                  ptr(sc), ptr(he), ptr(si), n, ptr(out), C.byref(visits)))
+    del keep
+    return out[:n].copy(), int(visits.value)
+
+
+def saliency_shift(volume, seed, half_extents, window_low=None, window_high=None, bins=64,
+                   max_iters=50, min_step=0.1, ctx=None, **extra):
+    """Fixed-bandwidth mean shift toward the uniform pmf (py_module.cpp:159-170)."""
+    d, _ = seek_records(volume, [seed], half_extents=[half_extents], method="shift",
+                        window_low=window_low, window_high=window_high, bins=bins, ctx=ctx,
+                        shift_max_iters=max_iters, shift_min_step=min_step, **extra)
+    return detection_to_dict(d[0])
+
+
+def quadrant_seek(volume, seeds, scale_range, window_low=None, window_high=None, bins=64, eta=0.5,
+                  max_iters=50, ctx=None, octant=False):
+    """quadrant_seek (quadrant.hpp:73-76); octant=True runs the 3D octant ascent.
+    Returns DET_DTYPE records: center, iterations, converged/degenerate flags,
+    post-scored entropy / Bhattacharyya / pdf_diff as detect() fills them."""
+    s = np.asarray(seeds, np.float64)
+    if s.shape[-1] == 2:
+        s = np.concatenate([s, np.zeros(s.shape[:-1] + (1,))], axis=-1)
+    d, visits = seek_records(volume, s, method="octant" if octant else "quadrant",
+                             window_low=window_low, window_high=window_high, bins=bins, ctx=ctx,
+                             quadrant_scales=list(scale_range), quadrant_eta=eta,
+                             quadrant_max_iters=max_iters)
+    return d
+
+
+def select(dets, entropy_quantile=0.9, pdf_quantile=0.0, k=20, dedupe_radius=5.0, ctx=None):
+    """Alive filter + population-quantile thresholds + dedupe (pipeline.cpp:383-401)."""
+    d = np.ascontiguousarray(dets, DET_DTYPE)
+    out = np.empty(max(len(d), 1), DET_DTYPE)
+    n = C.c_int64(0)
+    check(_lib.load().salvox_select(_ctx(ctx).handle, ptr(d), len(d), entropy_quantile,
+                                    pdf_quantile, int(k), dedupe_radius, ptr(out), C.byref(n)))
+    return out[: n.value].copy()
+
+
+def dedupe_top_k(dets, k, radius, ctx=None):
+    """dedupe_top_k (pipeline.hpp:57)."""
+    d = np.ascontiguousarray(dets, DET_DTYPE)
+    out = np.empty(max(len(d), 1), DET_DTYPE)
+    n = C.c_int64(0)
+    check(_lib.load().salvox_dedupe_top_k(_ctx(ctx).handle, ptr(d), len(d), int(k), radius,
+                                          ptr(out), C.byref(n)))
+    return out[: n.value].copy()
+
+
+# ----------------------------------------------------------------- data formats
+def plan_seeds(shape_zyx, mode="lattice", spacing=16.0, count=0, scales=(8.0,), rng_seed=0):
+    """plan_seeds (seeds.hpp:43) -> (positions (n,3), scales (n,))."""
+    nz, ny, nx = shape_zyx if len(shape_zyx) == 3 else (1,) + tuple(shape_zyx)
+    sc = np.ascontiguousarray(scales, np.float64)
+    m = 0 if mode == "lattice" else 1
+    n = C.c_int64(0)
+    check(_lib.load().salvox_plan_seeds(nx, ny, nz, m, float(spacing), int(count), ptr(sc),
+                                        len(sc), int(rng_seed), None, None, 0, C.byref(n)))
+    pos = np.empty((n.value, 3))
+    ss = np.empty(n.value)
+    check(_lib.load().salvox_plan_seeds(nx, ny, nz, m, float(spacing), int(count), ptr(sc),
+                                        len(sc), int(rng_seed), ptr(pos), ptr(ss), n.value,
+                                        C.byref(n)))
+    return pos, ss
+
+
+_SHAPES = {"box": 0, "ball": 1, "ellipsoid": 2}
+
+
+def make_phantom(spec):
+    """make_phantom (py_module.cpp:96-112): spec is PhantomSpec JSON text or a dict
+    (phantom.cpp:226-277). Returns (array[z,y,x], regions[{center, H}])."""
+    if isinstance(spec, str):
+        spec = json.loads(spec)
+    nx, ny, nz = (int(d) for d in spec["dims"])
+    bg = spec.get("background", {"type": "constant", "value": 0.0})
+    regions = spec.get("regions", [])
+    n = max(len(regions), 1)
+    shape = np.zeros(n, np.int32)
+    center = np.zeros(3 * n)
+    half = np.zeros(3 * n)
+    radius = np.zeros(n)
+    axes = np.tile(np.eye(3).ravel(), n).astype(np.float64)
+    ftype = np.zeros(n, np.int32)
+    flev = np.full(n, 64, np.int32)
+    fval = np.zeros(n)
+    Hs = []
+    for i, r in enumerate(regions):
+        shape[i] = _SHAPES[r["shape"]]
+        center[3 * i:3 * i + 3] = r["center"]
+        if r["shape"] == "box":
+            half[3 * i:3 * i + 3] = r["half_extents"]
+            H = np.diag(np.square(np.asarray(r["half_extents"], float)))
+        elif r["shape"] == "ball":
+            radius[i] = r["radius"]
+            H = np.eye(3) * r["radius"] * r["radius"]
+        else:
+            ax = np.asarray(r["axes"], np.float64)
+            axes[9 * i:9 * i + 9] = ax.ravel()
+            H = ax @ ax.T
+        Hs.append(H)
+        f = r.get("fill", {"type": "uniform", "levels": 64})
+        ftype[i] = 0 if f["type"] == "uniform" else 1
+        flev[i] = int(f.get("levels", 64))
+        fval[i] = float(f.get("value", 0.0))
+    out = np.empty((nz, ny, nx), np.float32)
+    cent = np.zeros(3 * n)
+    check(_lib.load().salvox_make_phantom(
+        nx, ny, nz, 0 if bg["type"] == "constant" else 1, float(bg.get("value", 0.0)),
+        float(bg.get("mean", 0.0)), float(bg.get("sigma", 1.0)), len(regions), ptr(shape),
+        ptr(center), ptr(half), ptr(radius), ptr(axes), ptr(ftype), ptr(flev), ptr(fval),
+        int(spec.get("rng_seed", 0)), ptr(out), ptr(cent)))
+    gt = [{"center": tuple(cent[3 * i:3 * i + 3]), "H": Hs[i]} for i in range(len(regions))]
+    return out, gt

@@ -1,0 +1,155 @@
+// common.cuh -- shared internals of libsalvox_b200 (C-ABI implementation).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/salvox_capi.h"
+
+namespace sx {
+
+struct Error : std::exception {
+  int code;
+  std::string msg;
+  Error(int c, std::string m) : code(c), msg(std::move(m)) {}
+  const char* what() const noexcept override { return msg.c_str(); }
+};
+
+[[noreturn]] inline void fail(int code, const std::string& msg) { throw Error(code, msg); }
+
+#define SX_CUDA(call)                                                                    \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      ::sx::fail(SALVOX_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));      \
+  } while (0)
+
+// After every launch: surface launch errors; with SALVOX_DEBUG_SYNC=1 also
+// synchronise and name the kernel that faulted.
+bool debug_sync_enabled();
+#define SX_LAUNCH_CHECK(ctx)                                                               \
+  do {                                                                                     \
+    cudaError_t e_ = cudaGetLastError();                                                   \
+    if (e_ != cudaSuccess)                                                                 \
+      ::sx::fail(SALVOX_ECUDA, std::string("kernel launch (") + __FILE__ + ":" +           \
+                                   std::to_string(__LINE__) + "): " + cudaGetErrorString(e_)); \
+    if (::sx::debug_sync_enabled()) {                                                      \
+      e_ = cudaStreamSynchronize((ctx)->stream);                                           \
+      if (e_ != cudaSuccess)                                                               \
+        ::sx::fail(SALVOX_ECUDA, std::string("kernel at ") + __FILE__ + ":" +              \
+                                     std::to_string(__LINE__) + ": " + cudaGetErrorString(e_)); \
+    }                                                                                      \
+    (ctx)->launches++;                                                                     \
+  } while (0)
+
+// Growable device buffer (never shrinks; freed with the context).
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  void* ensure(size_t n) {
+    if (n > bytes) {
+      if (p) cudaFree(p);
+      p = nullptr;
+      bytes = 0;
+      SX_CUDA(cudaMalloc(&p, n < 256 ? 256 : n));
+      bytes = n < 256 ? 256 : n;
+    }
+    return p;
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+};
+
+// Pinned host staging buffer.
+struct HostBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  void* ensure(size_t n) {
+    if (n > bytes) {
+      if (p) cudaFreeHost(p);
+      p = nullptr;
+      bytes = 0;
+      SX_CUDA(cudaMallocHost(&p, n));
+      bytes = n;
+    }
+    return p;
+  }
+  void release() {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    bytes = 0;
+  }
+};
+
+// Geometry of the last exhaustive call kept for salvox_exhaustive_debug_hist.
+struct ExhState {
+  bool valid = false;
+  int nx = 0, ny = 0, nz = 0, zs0 = 0, zs1 = 0, z0 = 0, z1 = 0;
+  int bins = 0;
+  std::vector<double> radii;
+  std::vector<double> scales;
+};
+
+}  // namespace sx
+
+struct salvox_ctx {
+  int device = 0;
+  int sm_count = 0;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  std::mutex mu;
+  uint64_t launches = 0;
+  // exhaustive path
+  sx::DevBuf d_vol, d_bins, d_score, d_best, d_keys, d_keys_alt, d_cub, d_counter, d_maxima,
+      d_minmax, d_dbg;
+  sx::HostBuf h_stage;
+  std::vector<salvox_maximum> last_maxima;
+  sx::ExhState exh;
+  // seek path
+  sx::DevBuf d_seeds, d_dets, d_geom, d_sel_a, d_sel_b, d_sel_c, d_sel_d, d_visits, d_target,
+      d_seek_vol, d_seek_bins;
+  ~salvox_ctx();
+};
+
+namespace sx {
+
+void set_last_error(const std::string& msg);
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return SALVOX_OK;
+  } catch (const Error& e) {
+    set_last_error(e.msg);
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    set_last_error("out of host memory");
+    return SALVOX_ERUNTIME;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return SALVOX_ERUNTIME;
+  }
+}
+
+// Bin volume pre-pass (volume.hpp:102-105): u8 (bin + 1), 0 = outside.
+void launch_bin_volume(salvox_ctx* ctx, const float* d_vol, uint8_t* d_bins, int nx, int ny,
+                       int nzs, int pitch, double low, double high, int bins);
+// Observed intensity range (IntensityWindow::full_range, volume.hpp:108-112).
+void device_full_range(salvox_ctx* ctx, const float* d_vol, size_t n, double* low, double* high);
+
+}  // namespace sx

@@ -1,0 +1,870 @@
+// exhaustive.cu -- the exhaustive Kadir-Brady pass on sm_100a.
+//
+// Replaces kadir_brady_exhaustive (/root/reference/proj/src/pipeline.cpp:63-166).
+//
+// Kernels
+//  K1 bin_volume_kernel   f32 -> u8 (bin_of + 1, 0 = outside), HBM-bound pre-pass
+//                         (volume.hpp:102-105, same fp64 op order).
+//  K2 kb_kernel           one CTA per output tile; the tile's u8 bins plus an
+//                         R-voxel halo arrive in shared memory by ONE TMA 3D
+//                         tensor copy (out-of-volume voxels are zero-filled by
+//                         TMA, i.e. land in the "outside" bin 0). Each thread owns
+//                         one voxel and a lane-private histogram column
+//                         hist[bin][thread] (bank = thread, conflict-free). It
+//                         walks the ball offsets sorted by |o|^2 (constant-memory
+//                         table of +-o pairs) adding the integer identity-kernel
+//                         weight n = |o|^2 with shared-memory atomics
+//                         (ATOMS.ADD, no return). At every needed radius the
+//                         column holds S_b(r) exactly (pipeline.cpp:110-117
+//                         with the 1/r^2 factor cancelled by normalisation).
+//                         Two register snapshots (a ring of 3 radii) give the
+//                         inter-scale L1 exactly in integers; entropy in fp32.
+//  K3 maxima_kernel       strict 26-neighbour maxima (pipeline.cpp:143-161) ->
+//                         u64 keys (score desc, linear index asc), then a cub
+//                         radix sort reproduces the stable_sort order (:163-164).
+#include <cub/cub.cuh>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <array>
+#include <climits>
+#include <cmath>
+
+#include "common.cuh"
+
+namespace sx {
+
+// ----------------------------------------------------------------------------- K1
+__global__ void bin_volume_kernel(const float* __restrict__ vol, uint8_t* __restrict__ bins,
+                                  int nx, long long rows, int pitch, double low, double range,
+                                  double m, int M) {
+  for (long long row = blockIdx.x; row < rows; row += gridDim.x) {
+    const float* src = vol + row * nx;
+    uint8_t* dst = bins + row * pitch;
+    for (int x = threadIdx.x; x < nx; x += blockDim.x) {
+      // floor((I - low) / (high - low) * bins), IEEE ops in the reference order
+      const double t = __dmul_rn(__ddiv_rn(__dsub_rn((double)src[x], low), range), m);
+      int b = (int)floor(t);
+      b = b < 0 ? 0 : (b > M - 1 ? M - 1 : b);
+      dst[x] = (uint8_t)(b + 1);
+    }
+  }
+}
+
+void launch_bin_volume(salvox_ctx* ctx, const float* d_vol, uint8_t* d_bins, int nx, int ny,
+                       int nzs, int pitch, double low, double high, int bins) {
+  const long long rows = (long long)ny * nzs;
+  const int grid = (int)std::min<long long>(rows, (long long)ctx->sm_count * 32);
+  const int block = nx >= 256 ? 256 : ((nx + 31) / 32) * 32;
+  bin_volume_kernel<<<grid, block, 0, ctx->stream>>>(d_vol, d_bins, nx, rows, pitch, low,
+                                                      high - low, (double)bins, bins);
+  SX_LAUNCH_CHECK(ctx);
+}
+
+__device__ __forceinline__ uint32_t ordered_key(float f) {
+  const uint32_t u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__host__ __device__ inline float key_to_float(uint32_t k) {
+  const uint32_t u = (k & 0x80000000u) ? (k & 0x7fffffffu) : ~k;
+  float f;
+  memcpy(&f, &u, 4);
+  return f;
+}
+
+__global__ void minmax_kernel(const float* __restrict__ v, size_t n, uint32_t* out) {
+  uint32_t lo = 0xffffffffu, hi = 0u;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const uint32_t k = ordered_key(v[i]);
+    lo = min(lo, k);
+    hi = max(hi, k);
+  }
+  for (int o = 16; o; o >>= 1) {
+    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(out, lo);
+    atomicMax(out + 1, hi);
+  }
+}
+
+void device_full_range(salvox_ctx* ctx, const float* d_vol, size_t n, double* low, double* high) {
+  uint32_t* d = ctx->d_minmax.as<uint32_t>();
+  if (!d) d = static_cast<uint32_t*>(ctx->d_minmax.ensure(64));
+  SX_CUDA(cudaMemsetAsync(d, 0xff, 4, ctx->stream));
+  SX_CUDA(cudaMemsetAsync(d + 1, 0x00, 4, ctx->stream));
+  minmax_kernel<<<ctx->sm_count * 4, 256, 0, ctx->stream>>>(d_vol, n, d);
+  SX_LAUNCH_CHECK(ctx);
+  uint32_t h[2];
+  SX_CUDA(cudaMemcpyAsync(h, d, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  SX_CUDA(cudaStreamSynchronize(ctx->stream));
+  const float lo = key_to_float(h[0]);
+  float hi = key_to_float(h[1]);
+  if (!(lo < hi)) hi = lo + 1.0f;  // volume.hpp:110
+  *low = lo;
+  *high = hi;
+}
+
+// ----------------------------------------------------------------------------- K2
+struct KbBound {
+  int32_t end;    // end of this radius' segment in the pair table (multiple of 4)
+  int32_t flags;  // bit0: r_i is a scale (entropy); bit1: evaluate scale r_{i-1}
+  int32_t rank;   // first position of scale r_{i-1} in the caller's list
+  float scale;    // (float) r_{i-1}
+  double fac;     // s * s / 2.0 (pipeline.cpp:131)
+};
+
+constexpr int kMaxPairs = 12288;  // 48 KB of constant memory
+constexpr int kMaxRadii = 192;
+__constant__ int4 c_pairs[kMaxPairs / 4];
+__constant__ KbBound c_bounds[kMaxRadii];
+
+struct KbParams {
+  int nx, ny, nz;   // global dims
+  int zs0;          // global z of slab plane 0
+  int zc0, zc1;     // computed (scored) global planes
+  int R, Rz, SY, SZ;  // halo (Rz = 0 for 2D) and shared-memory strides
+  int n_radii;
+  int bins;
+  uint32_t tile_bytes;
+  float* score;     // planes [zc0, zc1)
+  float* best;
+  const long long* dbg_vox;  // debug launch: one block per voxel
+  uint32_t* dbg_out;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+template <int NB, int TX, int TY, int TZ, bool DBG>
+__global__ void __launch_bounds__(TX* TY* TZ, 1)
+    kb_kernel(const __grid_constant__ CUtensorMap tmap, const KbParams p) {
+  constexpr int NT = TX * TY * TZ;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint32_t* hist = reinterpret_cast<uint32_t*>(smem);
+  uint8_t* tile = smem + NB * NT * 4;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(tile + ((p.tile_bytes + 15u) & ~15u));
+  const int tid = threadIdx.x;
+
+  int tx0, ty0, tz0;
+  long long dbg_lin = -1;
+  if (DBG) {
+    dbg_lin = p.dbg_vox[blockIdx.x];
+    const int vx = (int)(dbg_lin % p.nx);
+    const int vy = (int)((dbg_lin / p.nx) % p.ny);
+    const int vz = (int)(dbg_lin / ((long long)p.nx * p.ny));
+    tx0 = vx / TX * TX;
+    ty0 = vy / TY * TY;
+    tz0 = p.zc0 + (vz - p.zc0) / TZ * TZ;
+  } else {
+    tx0 = blockIdx.x * TX;
+    ty0 = blockIdx.y * TY;
+    tz0 = p.zc0 + blockIdx.z * TZ;
+  }
+
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  // TMA needs the innermost box coordinate 16-byte aligned: start the box at
+  // floor16(tx0 - R) and shift this block's voxels right by delta.
+  const int xs = tx0 - p.R;
+  const int xa = xs - (((xs % 16) + 16) % 16);
+  const int delta = xs - xa;
+  if (tid == 0) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(p.tile_bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(tile)),
+        "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(xa), "r"(ty0 - p.R),
+        "r"(tz0 - p.Rz - p.zs0), "r"(smem_u32(bar))
+        : "memory");
+  }
+  {
+    uint4* h4 = reinterpret_cast<uint4*>(hist);
+    for (int i = tid; i < NB * NT / 4; i += NT) h4[i] = make_uint4(0u, 0u, 0u, 0u);
+  }
+  const int lx = tid % TX, ly = (tid / TX) % TY, lz = tid / (TX * TY);
+  const int gx = tx0 + lx, gy = ty0 + ly, gz = tz0 + lz;
+  const uint8_t* tb = tile + (lz + p.Rz) * p.SZ + (ly + p.R) * p.SY + (lx + p.R + delta);
+  uint32_t* hc = hist + tid;
+  {
+    uint32_t done = 0;
+    while (!done) {
+      asm volatile(
+          "{ .reg .pred q; mbarrier.try_wait.parity.shared::cta.b64 q, [%1], 0; selp.u32 %0, 1, 0, q; }"
+          : "=r"(done)
+          : "r"(smem_u32(bar))
+          : "memory");
+    }
+  }
+  __syncthreads();
+  const bool valid = gx < p.nx && gy < p.ny && gz < p.zc1;
+  if (!valid) return;
+  const bool dbg_me =
+      DBG && ((long long)gx + (long long)p.nx * ((long long)gy + (long long)p.ny * gz)) == dbg_lin;
+  if (DBG && !dbg_me) return;
+
+  uint32_t A[NB], B[NB];
+#pragma unroll
+  for (int b = 0; b < NB; ++b) A[b] = B[b] = 0u;
+  uint32_t TA = 0u, TB = 0u;
+  float Hb = 0.f;
+  double best = 0.0;
+  float best_s = 0.f;
+  int best_rank = INT_MAX;
+
+  int e4 = 0;  // index into c_pairs (int4 units)
+  for (int i = 0; i < p.n_radii; ++i) {
+    const KbBound bd = c_bounds[i];
+    const int end4 = bd.end >> 2;
+#pragma unroll 2
+    for (; e4 < end4; ++e4) {
+      const int4 w = c_pairs[e4];
+      const int o0 = w.x >> 9, o1 = w.y >> 9, o2 = w.z >> 9, o3 = w.w >> 9;
+      const uint32_t b0 = tb[o0], b1 = tb[-o0], b2 = tb[o1], b3 = tb[-o1];
+      const uint32_t b4 = tb[o2], b5 = tb[-o2], b6 = tb[o3], b7 = tb[-o3];
+      const uint32_t n0 = (uint32_t)w.x & 511u, n1 = (uint32_t)w.y & 511u;
+      const uint32_t n2 = (uint32_t)w.z & 511u, n3 = (uint32_t)w.w & 511u;
+      atomicAdd(hc + b0 * NT, n0);
+      atomicAdd(hc + b1 * NT, n0);
+      atomicAdd(hc + b2 * NT, n1);
+      atomicAdd(hc + b3 * NT, n1);
+      atomicAdd(hc + b4 * NT, n2);
+      atomicAdd(hc + b5 * NT, n2);
+      atomicAdd(hc + b6 * NT, n3);
+      atomicAdd(hc + b7 * NT, n3);
+    }
+    // ---- boundary: the column now holds S_b(r_i) for b = 1..NB-1 (0 = outside)
+    uint32_t T = 0u;
+#pragma unroll
+    for (int b = 1; b < NB; ++b) T += hc[b * NT];
+    const bool doH = (bd.flags & 1) && T > 0u;
+    const bool doE = (bd.flags & 2) && T > 0u && TA > 0u && TB > 0u;
+    const float invT = doH ? 1.0f / (float)T : 0.f;
+    float hacc = 0.f;
+    unsigned long long num = 0ull;
+#pragma unroll
+    for (int b = 1; b < NB; ++b) {
+      const uint32_t c = hc[b * NT];
+      if (doH && c) {
+        const float pb = (float)c * invT;
+        float lg;
+        if (2u * c > T) {  // the one dominant bin: log(1 - q) with q exact-ish
+          lg = log1pf(-(float)(T - c) * invT) * 1.4426950408889634f;
+        } else {
+          lg = __log2f(pb);
+        }
+        hacc -= pb * lg;
+      }
+      if (doE) {
+        const unsigned long long x = (unsigned long long)c * TA;
+        const unsigned long long y = (unsigned long long)A[b] * T;
+        num += x > y ? x - y : y - x;
+      }
+      if (DBG && b - 1 < p.bins) p.dbg_out[(size_t)i * (p.bins + 1) + (b - 1)] = c;
+      A[b] = B[b];
+      B[b] = c;
+    }
+    if (DBG) p.dbg_out[(size_t)i * (p.bins + 1) + p.bins] = T;
+    if (doE) {
+      const double l1 = (double)num / ((double)T * (double)TA);
+      const double y = ((double)Hb * bd.fac) * l1;
+      if (y > best || (y == best && y > 0.0 && bd.rank < best_rank)) {
+        best = y;
+        best_s = bd.scale;
+        best_rank = bd.rank;
+      }
+    }
+    TA = TB;
+    TB = T;
+    Hb = doH ? fmaxf(hacc, 0.f) : 0.f;
+  }
+  if (!DBG) {
+    const size_t o = ((size_t)(gz - p.zc0) * p.ny + gy) * p.nx + gx;
+    p.score[o] = (float)best;
+    p.best[o] = best_s;
+  }
+}
+
+// ----------------------------------------------------------------------------- K3
+__global__ void maxima_kernel(const float* __restrict__ score, int nx, int ny, int nz, int zc0,
+                              int z0, int z1, unsigned long long* keys, unsigned int* counter) {
+  const long long rows = (long long)ny * (z1 - z0);
+  for (long long row = blockIdx.x; row < rows; row += gridDim.x) {
+    const int y = (int)(row % ny);
+    const int z = z0 + (int)(row / ny);
+    for (int x = threadIdx.x; x < nx; x += blockDim.x) {
+      const float s0 = score[((size_t)(z - zc0) * ny + y) * nx + x];
+      if (!(s0 > 0.0f)) continue;
+      bool is_max = true;
+      for (int dz = -1; dz <= 1 && is_max; ++dz) {
+        const int sz = z + dz;
+        if (sz < 0 || sz >= nz) continue;
+        for (int dy = -1; dy <= 1 && is_max; ++dy) {
+          const int sy = y + dy;
+          if (sy < 0 || sy >= ny) continue;
+          const float* r = score + ((size_t)(sz - zc0) * ny + sy) * nx;
+          for (int dx = -1; dx <= 1; ++dx) {
+            const int sx = x + dx;
+            if ((dx | dy | dz) == 0 || sx < 0 || sx >= nx) continue;
+            if (r[sx] >= s0) {
+              is_max = false;
+              break;
+            }
+          }
+        }
+      }
+      if (is_max) {
+        const unsigned long long lin =
+            (unsigned long long)x + (unsigned long long)nx * ((unsigned long long)y + (unsigned long long)ny * z);
+        const unsigned int slot = atomicAdd(counter, 1u);
+        keys[slot] = ((unsigned long long)(~__float_as_uint(s0)) << 32) | (lin & 0xffffffffull);
+      }
+    }
+  }
+}
+
+__global__ void decode_maxima_kernel(const unsigned long long* __restrict__ keys, long long n,
+                                     const float* __restrict__ best, int nx, int ny, int zc0,
+                                     salvox_maximum* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const unsigned long long k = keys[i];
+    const unsigned long long lin = k & 0xffffffffull;
+    const float s = __uint_as_float(~(uint32_t)(k >> 32));
+    const int x = (int)(lin % nx);
+    const int y = (int)((lin / nx) % ny);
+    const int z = (int)(lin / ((unsigned long long)nx * ny));
+    salvox_maximum m;
+    m.position[0] = x;
+    m.position[1] = y;
+    m.position[2] = z;
+    m.score = (double)s;
+    m.scale = (double)best[((size_t)(z - zc0) * ny + y) * nx + x];
+    m.linear_index = (long long)lin;
+    out[i] = m;
+  }
+}
+
+// ------------------------------------------------------------------------ host plan
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  });
+  if (!fn) fail(SALVOX_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  return fn;
+}
+
+struct TileCfg {
+  int nb, tx, ty, tz;
+};
+
+TileCfg pick_tile(int bins, bool two_d) {
+  const int nb = bins <= 16 ? 17 : (bins <= 32 ? 33 : 65);
+  if (two_d) return nb == 65 ? TileCfg{65, 32, 8, 1} : TileCfg{nb, 32, 16, 1};
+  return nb == 65 ? TileCfg{65, 8, 8, 4} : TileCfg{nb, 8, 8, 8};
+}
+
+// Offsets of make_sphere_offsets (pipeline.cpp:37-52) for every needed radius,
+// as one |o|^2-sorted table of +-o representatives with per-radius prefix ends.
+struct Plan {
+  std::vector<double> radii;
+  std::vector<KbBound> bounds;
+  std::vector<int32_t> pairs;  // packed (tile offset << 9) | n, padded per radius to 4
+  std::vector<uint64_t> ball_size;  // |B(r_i)| incl. centre (EvalCounter, :118)
+  int R = 0;
+};
+
+bool member(int x, int y, int z, double r) {  // pipeline.cpp:39-46
+  const int ri = (int)std::floor(r);
+  if (std::abs(x) > ri || std::abs(y) > ri || std::abs(z) > ri) return false;
+  const double d = ((double)x * x + (double)y * y + (double)z * z) / (r * r);
+  return d <= 1.0;
+}
+
+Plan make_plan(const double* scales, int n_scales, bool two_d, const TileCfg& tc, int* SYo,
+               int* SZo) {
+  Plan pl;
+  for (int i = 0; i < n_scales; ++i) {
+    pl.radii.push_back(scales[i] - 1.0);
+    pl.radii.push_back(scales[i]);
+    pl.radii.push_back(scales[i] + 1.0);
+  }
+  std::sort(pl.radii.begin(), pl.radii.end());
+  pl.radii.erase(std::unique(pl.radii.begin(), pl.radii.end()), pl.radii.end());
+  const int NR = (int)pl.radii.size();
+  if (NR > kMaxRadii) fail(SALVOX_EUNSUPPORTED, "exhaustive (device): too many radii");
+  const double rmax = pl.radii.back();
+  pl.R = (int)std::floor(rmax);
+  if (pl.R > 16)
+    fail(SALVOX_EUNSUPPORTED,
+         "exhaustive (device): max scale + 1 must be <= 16 voxels (shared-memory halo)");
+  const int R = pl.R;
+  int dmax = 0;  // worst shift of the 16-byte-aligned box start (see kb_kernel)
+  for (int k = 0; k < 16; ++k) dmax = std::max(dmax, (((tc.tx * k - R) % 16) + 16) % 16);
+  const int BX = ((tc.tx + 2 * R + dmax) + 15) / 16 * 16;
+  const int BY = tc.ty + 2 * R;
+  const int SY = BX, SZ = BX * BY;
+  *SYo = SY;
+  *SZo = SZ;
+  const int zr = two_d ? 0 : R;
+  struct Off {
+    int x, y, z, n;
+  };
+  std::vector<Off> cand;
+  for (int z = -zr; z <= zr; ++z)
+    for (int y = -R; y <= R; ++y)
+      for (int x = -R; x <= R; ++x)
+        if ((x | y | z) != 0 && member(x, y, z, rmax)) cand.push_back({x, y, z, x * x + y * y + z * z});
+  std::stable_sort(cand.begin(), cand.end(), [](const Off& a, const Off& b) { return a.n < b.n; });
+  // per radius: membership must be the |o|^2-prefix {n <= N_i}
+  std::vector<int> Nmax(NR, 0);
+  pl.ball_size.assign(NR, 1);
+  for (int i = 0; i < NR; ++i) {
+    int nm = 0;
+    for (const Off& o : cand)
+      if (member(o.x, o.y, o.z, pl.radii[i])) {
+        nm = std::max(nm, o.n);
+        pl.ball_size[i]++;
+      }
+    for (const Off& o : cand) {
+      const bool m = member(o.x, o.y, o.z, pl.radii[i]);
+      if (m != (o.n <= nm))
+        fail(SALVOX_EUNSUPPORTED, "exhaustive (device): radius set is not |o|^2-nested");
+    }
+    Nmax[i] = nm;
+  }
+  // ring of 3: every scale's s-1, s, s+1 must be adjacent radii
+  auto idx = [&](double r) {
+    return (int)(std::lower_bound(pl.radii.begin(), pl.radii.end(), r) - pl.radii.begin());
+  };
+  std::vector<int> eval_rank(NR, INT_MAX);
+  std::vector<bool> is_scale(NR, false);
+  for (int k = 0; k < n_scales; ++k) {
+    const double s = scales[k];
+    const int il = idx(s - 1.0), ic = idx(s), ih = idx(s + 1.0);
+    if (ic != il + 1 || ih != ic + 1)
+      fail(SALVOX_EUNSUPPORTED,
+           "exhaustive (device): scales need adjacent s-1, s, s+1 radii (integer scales)");
+    is_scale[ic] = true;
+    eval_rank[ih] = std::min(eval_rank[ih], k);
+  }
+  int p_at = 0;
+  size_t c = 0;
+  for (int i = 0; i < NR; ++i) {
+    for (; c < cand.size() && cand[c].n <= Nmax[i]; ++c) {
+      const Off& o = cand[c];
+      const bool rep = o.z > 0 || (o.z == 0 && (o.y > 0 || (o.y == 0 && o.x > 0)));
+      if (!rep) continue;
+      const int off = o.z * SZ + o.y * SY + o.x;
+      pl.pairs.push_back((int32_t)((uint32_t)off << 9 | (uint32_t)o.n));
+      ++p_at;
+    }
+    while (p_at % 4) {  // pad with zero-weight entries (harmless adds of 0)
+      pl.pairs.push_back(0);
+      ++p_at;
+    }
+    KbBound b{};
+    b.end = p_at;
+    b.flags = (is_scale[i] ? 1 : 0) | (eval_rank[i] != INT_MAX ? 2 : 0);
+    if (eval_rank[i] != INT_MAX) {
+      const double s = pl.radii[i - 1];
+      b.rank = eval_rank[i];
+      b.scale = (float)s;
+      b.fac = s * s / 2.0;
+    }
+    pl.bounds.push_back(b);
+  }
+  if ((int)pl.pairs.size() > kMaxPairs) fail(SALVOX_EUNSUPPORTED, "exhaustive (device): table too large");
+  return pl;
+}
+
+// The constant-memory tables are module-global: serialise their reuse across
+// streams with an event recorded after each consuming launch.
+std::mutex g_const_mu;
+cudaEvent_t g_const_done = nullptr;
+
+template <int NB, int TX, int TY, int TZ, bool DBG>
+void launch_kb(salvox_ctx* ctx, const CUtensorMap& map, const KbParams& kp, dim3 grid,
+               size_t smem) {
+  auto k = kb_kernel<NB, TX, TY, TZ, DBG>;
+  SX_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k<<<grid, TX * TY * TZ, smem, ctx->stream>>>(map, kp);
+  SX_LAUNCH_CHECK(ctx);
+}
+
+template <bool DBG>
+void dispatch_kb(salvox_ctx* ctx, const TileCfg& tc, const CUtensorMap& map, const KbParams& kp,
+                 dim3 grid, size_t smem) {
+#define SX_KB(NB, TX, TY, TZ)                                             \
+  if (tc.nb == NB && tc.tx == TX && tc.ty == TY && tc.tz == TZ) {         \
+    launch_kb<NB, TX, TY, TZ, DBG>(ctx, map, kp, grid, smem);             \
+    return;                                                               \
+  }
+  SX_KB(17, 8, 8, 8)
+  SX_KB(33, 8, 8, 8)
+  SX_KB(65, 8, 8, 4)
+  SX_KB(17, 32, 16, 1)
+  SX_KB(33, 32, 16, 1)
+  SX_KB(65, 32, 8, 1)
+#undef SX_KB
+  fail(SALVOX_EUNSUPPORTED, "exhaustive (device): no kernel for this tile configuration");
+}
+
+struct ExhRun {
+  TileCfg tc;
+  Plan pl;
+  CUtensorMap map;
+  KbParams kp;
+  dim3 grid;
+  size_t smem;
+};
+
+void upload_tables(salvox_ctx* ctx, const Plan& pl) {
+  if (!g_const_done) SX_CUDA(cudaEventCreateWithFlags(&g_const_done, cudaEventDisableTiming));
+  SX_CUDA(cudaStreamWaitEvent(ctx->stream, g_const_done, 0));
+  SX_CUDA(cudaMemcpyToSymbolAsync(c_pairs, pl.pairs.data(), pl.pairs.size() * 4, 0,
+                                  cudaMemcpyHostToDevice, ctx->stream));
+  SX_CUDA(cudaMemcpyToSymbolAsync(c_bounds, pl.bounds.data(), pl.bounds.size() * sizeof(KbBound),
+                                  0, cudaMemcpyHostToDevice, ctx->stream));
+}
+
+void validate_exhaustive(int nx, int ny, int nz, const salvox_window* iw, const double* scales,
+                         int n_scales, int kernel, uint64_t budget) {
+  if (nx < 1 || ny < 1 || nz < 1) fail(SALVOX_EINVAL, "Volume: dims must be >= 1");
+  if (!iw) fail(SALVOX_EINVAL, "IntensityWindow: missing");
+  if (!iw->full_range && !(iw->low < iw->high))
+    fail(SALVOX_EINVAL, "IntensityWindow: low must be < high");
+  if (iw->bins < 2) fail(SALVOX_EINVAL, "IntensityWindow: bins must be >= 2");
+  // pipeline.cpp:66-72
+  if (n_scales < 1 || !scales) fail(SALVOX_EINVAL, "exhaustive scan: no scales");
+  for (int i = 0; i < n_scales; ++i)
+    if (scales[i] < 2.0) fail(SALVOX_EINVAL, "exhaustive scan: scales must be >= 2 voxels");
+  const uint64_t evals = (uint64_t)nx * ny * nz * (uint64_t)n_scales;
+  if (evals > budget)
+    fail(SALVOX_EINVAL, "exhaustive scan: budget exceeded (" + std::to_string(evals) +
+                            " voxel-scale evaluations)");
+  if (kernel != SALVOX_KERNEL_IDENTITY)
+    fail(SALVOX_EUNSUPPORTED, "exhaustive (device): only the identity kernel is implemented");
+  if (iw->bins > 64) fail(SALVOX_EUNSUPPORTED, "exhaustive (device): bins must be <= 64");
+  if ((uint64_t)nx * ny * nz > 0xffffffffull)
+    fail(SALVOX_EUNSUPPORTED, "exhaustive (device): volume exceeds 2^32 voxels");
+}
+
+// Core: d_slab holds planes [zs0, zs1) of the volume (device, f32). Scores planes
+// [zc0, zc1) = [z0-1, z1+1) clipped, finds maxima of [z0, z1), sorts them.
+// Leaves: ctx->d_score/d_best (planes zc0..zc1), sorted keys, count.
+long long run_exhaustive(salvox_ctx* ctx, const float* d_slab, int nx, int ny, int nz, int zs0,
+                         int zs1, int z0, int z1, double low, double high, int bins,
+                         const double* scales, int n_scales, ExhRun* run_out) {
+  const bool two_d = nz == 1;
+  ExhRun run;
+  run.tc = pick_tile(bins, two_d);
+  int SY = 0, SZ = 0;
+  run.pl = make_plan(scales, n_scales, two_d, run.tc, &SY, &SZ);
+  const int R = run.pl.R;
+  if (zs0 > std::max(0, z0 - R - 1) || zs1 < std::min(nz, z1 + R + 1))
+    fail(SALVOX_EINVAL, "exhaustive slab: the slab must cover the owned planes plus the halo");
+  const int nzs = zs1 - zs0;
+  const int pitch = (nx + 15) / 16 * 16;
+  uint8_t* d_bins = static_cast<uint8_t*>(ctx->d_bins.ensure((size_t)pitch * ny * nzs));
+  launch_bin_volume(ctx, d_slab, d_bins, nx, ny, nzs, pitch, low, high, bins);
+
+  const int zc0 = std::max(0, z0 - 1), zc1 = std::min(nz, z1 + 1);
+  const size_t nscore = (size_t)nx * ny * (zc1 - zc0);
+  float* d_score = static_cast<float*>(ctx->d_score.ensure(nscore * 4));
+  float* d_best = static_cast<float*>(ctx->d_best.ensure(nscore * 4));
+
+  const int BX = SY, BY = SZ / SY, BZ = run.tc.tz + 2 * R;
+  cuuint64_t gdim[3] = {(cuuint64_t)nx, (cuuint64_t)ny, (cuuint64_t)nzs};
+  cuuint64_t gstride[2] = {(cuuint64_t)pitch, (cuuint64_t)pitch * ny};
+  cuuint32_t box[3] = {(cuuint32_t)BX, (cuuint32_t)BY, (cuuint32_t)(two_d ? 1 : BZ)};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult cr = encode_fn()(&run.map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, d_bins, gdim, gstride, box,
+                            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS) fail(SALVOX_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)cr));
+
+  KbParams& kp = run.kp;
+  kp.nx = nx;
+  kp.ny = ny;
+  kp.nz = nz;
+  kp.zs0 = zs0;
+  kp.zc0 = zc0;
+  kp.zc1 = zc1;
+  kp.R = R;
+  kp.Rz = two_d ? 0 : R;
+  kp.SY = SY;
+  kp.SZ = SZ;
+  kp.n_radii = (int)run.pl.radii.size();
+  kp.bins = bins;
+  kp.tile_bytes = (uint32_t)(BX * BY * (two_d ? 1 : BZ));
+  kp.score = d_score;
+  kp.best = d_best;
+  kp.dbg_vox = nullptr;
+  kp.dbg_out = nullptr;
+  const int NT = run.tc.tx * run.tc.ty * run.tc.tz;
+  run.smem = (size_t)run.tc.nb * NT * 4 + ((kp.tile_bytes + 15u) & ~15u) + 16;
+  run.grid = dim3((nx + run.tc.tx - 1) / run.tc.tx, (ny + run.tc.ty - 1) / run.tc.ty,
+                  (zc1 - zc0 + run.tc.tz - 1) / run.tc.tz);
+  {
+    std::lock_guard<std::mutex> lk(g_const_mu);
+    upload_tables(ctx, run.pl);
+    dispatch_kb<false>(ctx, run.tc, run.map, kp, run.grid, run.smem);
+    SX_CUDA(cudaEventRecord(g_const_done, ctx->stream));
+  }
+
+  // K3: maxima of the owned planes + sort
+  const size_t nown = (size_t)nx * ny * (z1 - z0);
+  const size_t kcap = nown / 2 + 1;
+  unsigned long long* d_keys = static_cast<unsigned long long*>(ctx->d_keys.ensure(kcap * 8));
+  unsigned long long* d_keys2 = static_cast<unsigned long long*>(ctx->d_keys_alt.ensure(kcap * 8));
+  unsigned int* d_cnt = static_cast<unsigned int*>(ctx->d_counter.ensure(64));
+  SX_CUDA(cudaMemsetAsync(d_cnt, 0, 4, ctx->stream));
+  const long long rows = (long long)ny * (z1 - z0);
+  maxima_kernel<<<(int)std::min<long long>(std::max<long long>(rows, 1), ctx->sm_count * 32),
+                  nx >= 128 ? 128 : 32, 0, ctx->stream>>>(d_score, nx, ny, nz, zc0, z0, z1, d_keys,
+                                                         d_cnt);
+  SX_LAUNCH_CHECK(ctx);
+  unsigned int cnt = 0;
+  SX_CUDA(cudaMemcpyAsync(&cnt, d_cnt, 4, cudaMemcpyDeviceToHost, ctx->stream));
+  SX_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (cnt > 1) {
+    size_t tmp = 0;
+    SX_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, d_keys, d_keys2, (int)cnt, 0, 64,
+                                           ctx->stream));
+    void* d_tmp = ctx->d_cub.ensure(tmp);
+    SX_CUDA(cub::DeviceRadixSort::SortKeys(d_tmp, tmp, d_keys, d_keys2, (int)cnt, 0, 64,
+                                           ctx->stream));
+    ctx->launches += 4;  // cub onesweep: histogram + exclusive-sum + passes (approx.)
+  } else if (cnt == 1) {
+    SX_CUDA(cudaMemcpyAsync(d_keys2, d_keys, 8, cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  salvox_maximum* d_max =
+      static_cast<salvox_maximum*>(ctx->d_maxima.ensure(std::max<size_t>(cnt, 1) * sizeof(salvox_maximum)));
+  if (cnt > 0) {
+    decode_maxima_kernel<<<(int)std::min<long long>((cnt + 255) / 256, ctx->sm_count * 8), 256, 0,
+                           ctx->stream>>>(d_keys2, cnt, d_best, nx, ny, zc0, d_max);
+    SX_LAUNCH_CHECK(ctx);
+  }
+  if (run_out) *run_out = run;
+  // remember for the debug entry point
+  ctx->exh.valid = true;
+  ctx->exh.nx = nx;
+  ctx->exh.ny = ny;
+  ctx->exh.nz = nz;
+  ctx->exh.zs0 = zs0;
+  ctx->exh.zs1 = zs1;
+  ctx->exh.z0 = z0;
+  ctx->exh.z1 = z1;
+  ctx->exh.bins = bins;
+  ctx->exh.radii = run.pl.radii;
+  ctx->exh.scales.assign(scales, scales + n_scales);
+  return cnt;
+}
+
+uint64_t closed_form_visits(const Plan& pl, uint64_t voxels) {
+  uint64_t per = 0;
+  for (uint64_t b : pl.ball_size) per += b;
+  return per * voxels;
+}
+
+void fetch_maxima(salvox_ctx* ctx, long long cnt, salvox_maximum* out, int64_t cap) {
+  ctx->last_maxima.resize((size_t)cnt);
+  if (cnt > 0)
+    SX_CUDA(cudaMemcpyAsync(ctx->last_maxima.data(), ctx->d_maxima.p, cnt * sizeof(salvox_maximum),
+                            cudaMemcpyDeviceToHost, ctx->stream));
+  SX_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (out && cap > 0)
+    std::memcpy(out, ctx->last_maxima.data(),
+                (size_t)std::min<long long>(cnt, cap) * sizeof(salvox_maximum));
+}
+
+int exhaustive_host(salvox_ctx* ctx, const float* slab, int32_t nx, int32_t ny, int32_t nz,
+                    int32_t zs0, int32_t zs1, int32_t z0, int32_t z1, const salvox_window* iw,
+                    const double* scales, int32_t n_scales, int32_t kernel, uint64_t budget,
+                    float* score_out, float* best_scale_out, salvox_maximum* maxima, int64_t cap,
+                    int64_t* n_maxima, uint64_t* visits, bool slab_form) {
+  return guarded([&] {
+    if (!ctx) fail(SALVOX_EINVAL, "null context");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    validate_exhaustive(nx, ny, nz, iw, scales, n_scales, kernel, budget);
+    if (!slab) fail(SALVOX_EINVAL, "null volume");
+    if (!(0 <= zs0 && zs0 <= z0 && z0 < z1 && z1 <= zs1 && zs1 <= nz))
+      fail(SALVOX_EINVAL, "exhaustive slab: need 0 <= zs0 <= z0 < z1 <= zs1 <= nz");
+    if (slab_form && iw->full_range)
+      fail(SALVOX_EINVAL, "exhaustive slab: pass an explicit (global) intensity window");
+    SX_CUDA(cudaSetDevice(ctx->device));
+    const size_t nslab = (size_t)nx * ny * (zs1 - zs0);
+    float* d_vol = static_cast<float*>(ctx->d_vol.ensure(nslab * 4));
+    SX_CUDA(cudaMemcpyAsync(d_vol, slab, nslab * 4, cudaMemcpyHostToDevice, ctx->stream));
+    double low = iw->low, high = iw->high;
+    if (iw->full_range) device_full_range(ctx, d_vol, nslab, &low, &high);
+    ExhRun run;
+    const long long cnt = run_exhaustive(ctx, d_vol, nx, ny, nz, zs0, zs1, z0, z1, low, high,
+                                         iw->bins, scales, n_scales, &run);
+    const size_t nown = (size_t)nx * ny * (z1 - z0);
+    const size_t off = (size_t)nx * ny * (z0 - run.kp.zc0);
+    if (score_out)
+      SX_CUDA(cudaMemcpyAsync(score_out, ctx->d_score.as<float>() + off, nown * 4,
+                              cudaMemcpyDeviceToHost, ctx->stream));
+    if (best_scale_out)
+      SX_CUDA(cudaMemcpyAsync(best_scale_out, ctx->d_best.as<float>() + off, nown * 4,
+                              cudaMemcpyDeviceToHost, ctx->stream));
+    fetch_maxima(ctx, cnt, maxima, cap);
+    if (n_maxima) *n_maxima = cnt;
+    if (visits) *visits += closed_form_visits(run.pl, nown);
+  });
+}
+
+}  // namespace
+}  // namespace sx
+
+using namespace sx;
+
+extern "C" int salvox_exhaustive(salvox_ctx* ctx, const float* volume, int32_t nx, int32_t ny,
+                                 int32_t nz, const salvox_window* iw, const double* scales,
+                                 int32_t n_scales, int32_t kernel, uint64_t budget,
+                                 float* score_out, float* best_scale_out, salvox_maximum* maxima,
+                                 int64_t cap, int64_t* n_maxima, uint64_t* visits) {
+  return exhaustive_host(ctx, volume, nx, ny, nz, 0, nz, 0, nz, iw, scales, n_scales, kernel,
+                         budget, score_out, best_scale_out, maxima, cap, n_maxima, visits, false);
+}
+
+extern "C" int salvox_exhaustive_slab(salvox_ctx* ctx, const float* slab, int32_t nx, int32_t ny,
+                                      int32_t nz, int32_t zs0, int32_t zs1, int32_t z0,
+                                      int32_t z1, const salvox_window* iw, const double* scales,
+                                      int32_t n_scales, int32_t kernel, uint64_t budget,
+                                      float* score_out, float* best_scale_out,
+                                      salvox_maximum* maxima, int64_t cap, int64_t* n_maxima,
+                                      uint64_t* visits) {
+  return exhaustive_host(ctx, slab, nx, ny, nz, zs0, zs1, z0, z1, iw, scales, n_scales, kernel,
+                         budget, score_out, best_scale_out, maxima, cap, n_maxima, visits, true);
+}
+
+extern "C" int salvox_exhaustive_device(salvox_ctx* ctx, const float* d_volume, int32_t nx,
+                                        int32_t ny, int32_t nz, const salvox_window* iw,
+                                        const double* scales, int32_t n_scales, int32_t kernel,
+                                        uint64_t budget, float* d_score, float* d_best_scale,
+                                        int64_t* n_maxima) {
+  return guarded([&] {
+    if (!ctx) fail(SALVOX_EINVAL, "null context");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    validate_exhaustive(nx, ny, nz, iw, scales, n_scales, kernel, budget);
+    SX_CUDA(cudaSetDevice(ctx->device));
+    double low = iw->low, high = iw->high;
+    const size_t n = (size_t)nx * ny * nz;
+    if (iw->full_range) device_full_range(ctx, d_volume, n, &low, &high);
+    ExhRun run;
+    const long long cnt = run_exhaustive(ctx, d_volume, nx, ny, nz, 0, nz, 0, nz, low, high,
+                                         iw->bins, scales, n_scales, &run);
+    if (d_score)
+      SX_CUDA(cudaMemcpyAsync(d_score, ctx->d_score.p, n * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+    if (d_best_scale)
+      SX_CUDA(cudaMemcpyAsync(d_best_scale, ctx->d_best.p, n * 4, cudaMemcpyDeviceToDevice,
+                              ctx->stream));
+    SX_CUDA(cudaStreamSynchronize(ctx->stream));
+    ctx->last_maxima.clear();
+    ctx->last_maxima.resize((size_t)cnt);
+    if (cnt > 0)
+      SX_CUDA(cudaMemcpy(ctx->last_maxima.data(), ctx->d_maxima.p, cnt * sizeof(salvox_maximum),
+                         cudaMemcpyDeviceToHost));
+    if (n_maxima) *n_maxima = cnt;
+  });
+}
+
+extern "C" int salvox_last_maxima(salvox_ctx* ctx, salvox_maximum* out, int64_t cap,
+                                  int64_t* n_out) {
+  return guarded([&] {
+    if (!ctx) fail(SALVOX_EINVAL, "null context");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    const int64_t n = (int64_t)ctx->last_maxima.size();
+    if (out && cap > 0)
+      std::memcpy(out, ctx->last_maxima.data(), (size_t)std::min(n, cap) * sizeof(salvox_maximum));
+    if (n_out) *n_out = n;
+  });
+}
+
+extern "C" int salvox_exhaustive_debug_hist(salvox_ctx* ctx, const int64_t* voxels, int32_t n,
+                                            uint32_t* out, double* radii_out, int32_t* n_radii) {
+  return guarded([&] {
+    if (!ctx) fail(SALVOX_EINVAL, "null context");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (!ctx->exh.valid) fail(SALVOX_EINVAL, "no exhaustive call on this context yet");
+    const ExhState& st = ctx->exh;
+    SX_CUDA(cudaSetDevice(ctx->device));
+    const bool two_d = st.nz == 1;
+    ExhRun run;
+    run.tc = pick_tile(st.bins, two_d);
+    int SY = 0, SZ = 0;
+    run.pl = make_plan(st.scales.data(), (int)st.scales.size(), two_d, run.tc, &SY, &SZ);
+    const int R = run.pl.R;
+    const int NR = (int)run.pl.radii.size();
+    const int nzs = st.zs1 - st.zs0;
+    const int pitch = (st.nx + 15) / 16 * 16;
+    const int BX = SY, BY = SZ / SY, BZ = run.tc.tz + 2 * R;
+    cuuint64_t gdim[3] = {(cuuint64_t)st.nx, (cuuint64_t)st.ny, (cuuint64_t)nzs};
+    cuuint64_t gstride[2] = {(cuuint64_t)pitch, (cuuint64_t)pitch * st.ny};
+    cuuint32_t box[3] = {(cuuint32_t)BX, (cuuint32_t)BY, (cuuint32_t)(two_d ? 1 : BZ)};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult cr = encode_fn()(&run.map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, ctx->d_bins.p, gdim,
+                              gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                              CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS) fail(SALVOX_ECUDA, "cuTensorMapEncodeTiled failed");
+    const long long plane = (long long)st.nx * st.ny;
+    for (int i = 0; i < n; ++i)
+      if (voxels[i] < plane * st.z0 || voxels[i] >= plane * st.z1)
+        fail(SALVOX_EINVAL, "debug voxel outside the owned planes");
+    KbParams kp{};
+    kp.nx = st.nx;
+    kp.ny = st.ny;
+    kp.nz = st.nz;
+    kp.zs0 = st.zs0;
+    kp.zc0 = std::max(0, st.z0 - 1);
+    kp.zc1 = std::min(st.nz, st.z1 + 1);
+    kp.R = R;
+    kp.Rz = two_d ? 0 : R;
+    kp.SY = SY;
+    kp.SZ = SZ;
+    kp.n_radii = NR;
+    kp.bins = st.bins;
+    kp.tile_bytes = (uint32_t)(BX * BY * (two_d ? 1 : BZ));
+    long long* d_vox = static_cast<long long*>(ctx->d_dbg.ensure(
+        (size_t)n * 8 + (size_t)n * NR * (st.bins + 1) * 4 + 256));
+    uint32_t* d_out = reinterpret_cast<uint32_t*>(d_vox + n);
+    SX_CUDA(cudaMemcpyAsync(d_vox, voxels, (size_t)n * 8, cudaMemcpyHostToDevice, ctx->stream));
+    SX_CUDA(cudaMemsetAsync(d_out, 0, (size_t)n * NR * (st.bins + 1) * 4, ctx->stream));
+    const int NT = run.tc.tx * run.tc.ty * run.tc.tz;
+    const size_t smem = (size_t)run.tc.nb * NT * 4 + ((kp.tile_bytes + 15u) & ~15u) + 16;
+    std::lock_guard<std::mutex> lk2(g_const_mu);
+    upload_tables(ctx, run.pl);
+    for (int i = 0; i < n; ++i) {  // one block per voxel, each writes its own slice
+      kp.dbg_vox = d_vox + i;
+      kp.dbg_out = d_out + (size_t)i * NR * (st.bins + 1);
+      dispatch_kb<true>(ctx, run.tc, run.map, kp, dim3(1), smem);
+    }
+    SX_CUDA(cudaEventRecord(g_const_done, ctx->stream));
+    SX_CUDA(cudaMemcpyAsync(out, d_out, (size_t)n * NR * (st.bins + 1) * 4, cudaMemcpyDeviceToHost,
+                            ctx->stream));
+    SX_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (radii_out) std::memcpy(radii_out, run.pl.radii.data(), NR * sizeof(double));
+    if (n_radii) *n_radii = NR;
+  });
+}

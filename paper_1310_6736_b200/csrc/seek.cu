@@ -1,0 +1,1072 @@
+// seek.cu -- the seed-grid detector on sm_100a: one warp per seed.
+//
+// Replaces the per-seed work of detect (/root/reference/proj/src/pipeline.cpp:311-381):
+//  * saliency_shift (src/shift.cpp:36-107) with shift_step (:15-34),
+//    try_candidate_histogram (src/window.cpp:5-19), pdf_difference (:30-46),
+//    inbounds_support_fraction (:54-60), for_each_support_voxel (window.hpp:81-110);
+//  * quadrant_seek_one / quadrant_step / box_entropy_bits (src/quadrant.cpp:18-114);
+//  * NEW octant ascent: the same algorithm with 8 corner-anchored cubes.
+//
+// Bit-exactness: every fp64 expression that feeds a trajectory is evaluated with
+// the _rn intrinsics in the reference's operation order (no FMA contraction);
+// sums that the reference accumulates sequentially (per-bin histogram masses,
+// the centroid num/den) are accumulated in the reference's z->y->x order: lanes
+// evaluate 32 consecutive bounding-box voxels, then __match_any_sync groups the
+// lanes by bin and each group's leader adds its members in lane order; four lanes
+// run the num.x/num.y/num.z/den chains over the ballot of support voxels.
+// Order-free integer work (support counts, box counts) uses ballots/atomics.
+// Logs go through sx_log (include/salvox/sx_log.h), shared with the host oracle.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <map>
+
+#include "../../include/salvox/sx_log.h"
+#include "common.cuh"
+#include "host_math.h"
+
+namespace sx {
+
+constexpr int kMaxBins = 64;
+constexpr unsigned kFull = 0xffffffffu;
+constexpr double kLn2 = 0.693147180559945309417232121458176568;  // std::numbers::ln2
+
+struct WinGeom {
+  double Hinv[9];
+  double ext[3];
+  double det_fac;         // 1 / sqrt(max(det H, 1e-300))   (window.cpp:9)
+  double support_volume;  // window.hpp:69-75
+};
+
+struct ScaleGeom {
+  WinGeom main, lo, hi;   // window, scaled_to(s-1), scaled_to(s+1)
+  double H[9];
+  double pdf_fac;         // s * s / (2.0 * ds)               (window.cpp:45)
+  int pdf_ok;             // s - ds >= 1                      (window.cpp:33-34)
+  int pad_;
+};
+
+struct SeedIn {
+  double pos[3];
+  int geom;        // shift: ScaleGeom index of the seed's scale
+  int seed_index;
+};
+
+struct SeekParams {
+  int nx, ny, nz, bins, method, two_d;
+  int max_iters;
+  int step_kernel, hist_kernel;
+  double min_step, min_frac, eta;
+  int n_ascent;
+  int ascent_scales[64];
+  int geom_of_k[129];   // ascent post-scoring: ScaleGeom index for window half-size k
+  const uint8_t* binvol;  // bin + 1, x fastest, pitch nx
+  const double* q;        // target pmf (bins)
+  const ScaleGeom* geoms;
+  const SeedIn* seeds;
+  int n_seeds;
+  salvox_detection* out;
+  unsigned long long* visits;
+};
+
+struct WarpScratch {
+  double h[kMaxBins];
+  double p[kMaxBins];     // last normalized candidate histogram
+  double w[kMaxBins];     // mean-shift weights / scratch pmf
+  double v[32];
+  int xyz[3][32];
+  unsigned cnt[1][kMaxBins];  // ascent box counts (one octant at a time)
+};
+
+struct Box {
+  int x0, x1, y0, y1, z0, z1;
+};
+
+__device__ __forceinline__ long long box_size(const Box& b) {
+  if (b.x0 > b.x1 || b.y0 > b.y1 || b.z0 > b.z1) return 0;
+  return (long long)(b.x1 - b.x0 + 1) * (b.y1 - b.y0 + 1) * (b.z1 - b.z0 + 1);
+}
+
+// Visits a box in z->y->x order, 32 voxels per step (uniform control flow).
+template <class F>
+__device__ __forceinline__ void warp_box_iter(const Box& b, int lane, F&& f) {
+  const int Lx = b.x1 - b.x0 + 1, Ly = b.y1 - b.y0 + 1, Lz = b.z1 - b.z0 + 1;
+  if (Lx <= 0 || Ly <= 0 || Lz <= 0) return;
+  const int total = Lx * Ly * Lz;
+  for (int base = 0; base < total; base += 32) {
+    const int L = base + lane;
+    const bool act = L < total;
+    int x = 0, y = 0, z = 0;
+    if (act) {
+      const int t = L / Lx;
+      x = b.x0 + (L - t * Lx);
+      const int zz = t / Ly;
+      y = b.y0 + (t - zz * Ly);
+      z = b.z0 + zz;
+    }
+    f(act, x, y, z);
+  }
+}
+
+__device__ __forceinline__ Box window_box(const double c[3], const WinGeom& g, int nx, int ny,
+                                          int nz) {  // window.hpp:84-89
+  Box b;
+  b.x0 = max(0, (int)ceil(__dsub_rn(c[0], g.ext[0])));
+  b.x1 = min(nx - 1, (int)floor(__dadd_rn(c[0], g.ext[0])));
+  b.y0 = max(0, (int)ceil(__dsub_rn(c[1], g.ext[1])));
+  b.y1 = min(ny - 1, (int)floor(__dadd_rn(c[1], g.ext[1])));
+  b.z0 = max(0, (int)ceil(__dsub_rn(c[2], g.ext[2])));
+  b.z1 = min(nz - 1, (int)floor(__dadd_rn(c[2], g.ext[2])));
+  return b;
+}
+
+// Squared Mahalanobis distance, window.hpp:95-103 operation order.
+__device__ __forceinline__ double maha(const WinGeom& g, const double c[3], int x, int y, int z) {
+  const double dz = __dsub_rn((double)z, c[2]);
+  const double dy = __dsub_rn((double)y, c[1]);
+  const double c0 = __dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(g.Hinv[4], dy), dy),
+                                        __dmul_rn(__dmul_rn(__dmul_rn(2.0, g.Hinv[5]), dy), dz)),
+                              __dmul_rn(__dmul_rn(g.Hinv[8], dz), dz));
+  const double c1 = __dmul_rn(2.0, __dadd_rn(__dmul_rn(g.Hinv[1], dy), __dmul_rn(g.Hinv[2], dz)));
+  const double dx = __dsub_rn((double)x, c[0]);
+  return __dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(g.Hinv[0], dx), dx), __dmul_rn(c1, dx)), c0);
+}
+
+__device__ __forceinline__ double kernel_value(int k, double d) {  // kernel.hpp:17-24
+  if (k == 0) return d;
+  if (k == 1) return __dsub_rn(1.0, d);
+  return exp(__dmul_rn(-0.5, d));
+}
+__device__ __forceinline__ double kernel_step_weight(int k, double d) {  // kernel.hpp:29-36
+  if (k == 2) return __dmul_rn(0.5, exp(__dmul_rn(-0.5, d)));
+  return 1.0;
+}
+
+__device__ __forceinline__ int bin_at(const SeekParams& P, int x, int y, int z) {
+  return (int)__ldg(P.binvol + ((size_t)z * P.ny + y) * P.nx + x) - 1;
+}
+
+// try_candidate_histogram (window.cpp:5-19): sequential per-bin fp64 masses in
+// support order, normalized into s.p. Returns ok; *support, *visited.
+__device__ bool warp_candidate_hist(const SeekParams& P, WarpScratch& s, const double c[3],
+                                    const WinGeom& g, int kernel, int lane, unsigned* support_out,
+                                    long long* visited) {
+  const int M = P.bins;
+  for (int b = lane; b < M; b += 32) s.h[b] = 0.0;
+  __syncwarp();
+  const Box bb = window_box(c, g, P.nx, P.ny, P.nz);
+  *visited = box_size(bb);
+  unsigned support = 0;
+  warp_box_iter(bb, lane, [&](bool act, int x, int y, int z) {
+    bool in = false;
+    int bin = 0;
+    double val = 0.0;
+    if (act) {
+      const double d = maha(g, c, x, y, z);
+      in = d <= 1.0;
+      if (in) {
+        bin = bin_at(P, x, y, z);
+        val = __dmul_rn(g.det_fac, kernel_value(kernel, d));
+      }
+    }
+    support += __popc(__ballot_sync(kFull, in));
+    const unsigned grp = __match_any_sync(kFull, in ? bin : -1 - lane);
+    s.v[lane] = val;
+    __syncwarp();
+    if (in && (grp & ((1u << lane) - 1u)) == 0u) {  // group leader: members in lane order
+      double acc = s.h[bin];
+      unsigned m = grp;
+      while (m) {
+        const int j = __ffs(m) - 1;
+        acc = __dadd_rn(acc, s.v[j]);
+        m &= m - 1u;
+      }
+      s.h[bin] = acc;
+    }
+    __syncwarp();
+  });
+  double mass = 0.0;
+  if (lane == 0)
+    for (int b = 0; b < M; ++b) mass = __dadd_rn(mass, s.h[b]);  // Histogram::mass
+  mass = __shfl_sync(kFull, mass, 0);
+  *support_out = support;
+  if (support == 0 || mass <= 0.0) return false;
+  for (int b = lane; b < M; b += 32) s.p[b] = __ddiv_rn(s.h[b], mass);
+  __syncwarp();
+  return true;
+}
+
+// entropy_bits (histogram.hpp:56-67) of pmf p, sequential in bin order.
+__device__ double warp_entropy_bits(const double* p, int M, int lane, double* tmp) {
+  for (int b = lane; b < M; b += 32) tmp[b] = p[b] > 0.0 ? __dmul_rn(p[b], sx_log(p[b])) : 0.0;
+  __syncwarp();
+  double e = 0.0;
+  if (lane == 0) {
+    for (int b = 0; b < M; ++b)
+      if (p[b] > 0.0) e = __dsub_rn(e, tmp[b]);
+    e = __ddiv_rn(e < 0.0 ? 0.0 : e, kLn2);
+  }
+  __syncwarp();
+  return __shfl_sync(kFull, e, 0);
+}
+
+__device__ __forceinline__ double dclamp(double v, double hi) {
+  return v < 0.0 ? 0.0 : (hi < v ? hi : v);
+}
+
+// Final scores shared by shift and the ascent methods: entropy of p_score
+// (Epanechnikov), Bhattacharyya of p_step vs q, pdf_difference (identity).
+// p_step must already be in s.p. Returns false if a histogram is degenerate.
+__device__ bool warp_final_scores(const SeekParams& P, WarpScratch& s, const double c[3],
+                                  const ScaleGeom& sg, int lane, bool have_pstep,
+                                  salvox_detection& d, unsigned long long& visits,
+                                  bool pstep_from_shift) {
+  const int M = P.bins;
+  unsigned sup;
+  long long vis;
+  bool ok_step = have_pstep;
+  // bhattacharyya(p_step, q) before s.p is overwritten
+  double rho = 0.0;
+  if (ok_step && lane == 0) {
+    for (int b = 0; b < M; ++b) rho = __dadd_rn(rho, __dsqrt_rn(__dmul_rn(s.p[b], P.q[b])));
+    rho = rho < 1.0 ? rho : 1.0;
+  }
+  rho = __shfl_sync(kFull, rho, 0);
+  const bool ok_score = warp_candidate_hist(P, s, c, sg.main, 1, lane, &sup, &vis);
+  visits += (unsigned long long)vis;
+  if (pstep_from_shift) visits += (unsigned long long)vis;  // reference recomputes p_step
+  bool ok = true;
+  if (ok_score && ok_step) {
+    d.entropy_bits = warp_entropy_bits(s.p, M, lane, s.w);
+    d.bhattacharyya = rho;
+  } else {
+    ok = false;
+  }
+  // pdf_difference: both flanks are evaluated before the check (window.cpp:37-39)
+  double pdf = 0.0;
+  if (sg.pdf_ok) {
+    const bool ok_lo = warp_candidate_hist(P, s, c, sg.lo, 0, lane, &sup, &vis);
+    visits += (unsigned long long)vis;
+    for (int b = lane; b < M; b += 32) s.w[b] = s.p[b];
+    __syncwarp();
+    const bool ok_hi = warp_candidate_hist(P, s, c, sg.hi, 0, lane, &sup, &vis);
+    visits += (unsigned long long)vis;
+    if (ok_lo && ok_hi) {
+      double l1 = 0.0;
+      if (lane == 0) {
+        for (int b = 0; b < M; ++b) l1 = __dadd_rn(l1, fabs(__dsub_rn(s.p[b], s.w[b])));
+        pdf = __dmul_rn(sg.pdf_fac, l1);
+      }
+      pdf = __shfl_sync(kFull, pdf, 0);
+    }
+  }
+  d.pdf_diff = pdf;
+  return ok;
+}
+
+// ------------------------------------------------------------------- shift
+__global__ void __launch_bounds__(256) shift_kernel(const SeekParams P) {
+  __shared__ WarpScratch scratch[8];
+  const int lane = threadIdx.x & 31;
+  const int wid = threadIdx.x >> 5;
+  const int seed = blockIdx.x * 8 + wid;
+  if (seed >= P.n_seeds) return;
+  WarpScratch& s = scratch[wid];
+  const SeedIn si = P.seeds[seed];
+  const ScaleGeom& sg = P.geoms[si.geom];
+  const int M = P.bins;
+  const double lim[3] = {(double)(P.nx - 1), (double)(P.ny - 1), (double)(P.nz - 1)};
+  salvox_detection d;
+  memset(&d, 0, sizeof d);
+  d.seed_index = si.seed_index;
+  for (int i = 0; i < 9; ++i) d.H[i] = sg.H[i];
+  unsigned long long visits = 0;
+  double c[3] = {dclamp(si.pos[0], lim[0]), dclamp(si.pos[1], lim[1]), dclamp(si.pos[2], lim[2])};
+
+  unsigned support;
+  long long vis;
+  bool ok = warp_candidate_hist(P, s, c, sg.main, P.hist_kernel, lane, &support, &vis);
+  // inbounds_support_fraction at the clamped seed (shift.cpp:53-57)
+  auto frac_bad = [&](unsigned sup) {
+    if (sg.main.support_volume <= 0.0) return 0.0 < P.min_frac;
+    double f = __ddiv_rn((double)sup, sg.main.support_volume);
+    f = f < 1.0 ? f : 1.0;
+    return f < P.min_frac;
+  };
+  bool degenerate = frac_bad(support);
+  if (!degenerate) {
+    for (int it = 0; it < P.max_iters; ++it) {
+      d.iterations = it + 1;
+      visits += (unsigned long long)vis;  // shift_step's histogram pass
+      if (!ok) {
+        degenerate = true;
+        break;
+      }
+      // weights sqrt(q_b / max(p_b, 1e-6)) (histogram.hpp:107-113)
+      for (int b = lane; b < M; b += 32) {
+        const double pb = s.p[b] > 1e-6 ? s.p[b] : 1e-6;
+        s.w[b] = __dsqrt_rn(__ddiv_rn(P.q[b], pb));
+      }
+      __syncwarp();
+      // centroid pass (shift.cpp:25-30)
+      double acc = 0.0;  // lane 0: num.x, 1: num.y, 2: num.z, 3: den
+      const Box bb = window_box(c, sg.main, P.nx, P.ny, P.nz);
+      visits += (unsigned long long)box_size(bb);
+      warp_box_iter(bb, lane, [&](bool act, int x, int y, int z) {
+        bool in = false;
+        double g = 0.0;
+        if (act) {
+          const double dd = maha(sg.main, c, x, y, z);
+          in = dd <= 1.0;
+          if (in) g = __dmul_rn(kernel_step_weight(P.step_kernel, dd), s.w[bin_at(P, x, y, z)]);
+        }
+        const unsigned m0 = __ballot_sync(kFull, in);
+        s.v[lane] = g;
+        s.xyz[0][lane] = x;
+        s.xyz[1][lane] = y;
+        s.xyz[2][lane] = z;
+        __syncwarp();
+        if (lane < 4) {
+          unsigned m = m0;
+          while (m) {
+            const int j = __ffs(m) - 1;
+            const double gj = s.v[j];
+            acc = lane == 3 ? __dadd_rn(acc, gj)
+                            : __dadd_rn(acc, __dmul_rn(gj, (double)s.xyz[lane][j]));
+            m &= m - 1u;
+          }
+        }
+        __syncwarp();
+      });
+      const double den = __shfl_sync(kFull, acc, 3);
+      const double nx_ = __shfl_sync(kFull, acc, 0);
+      const double ny_ = __shfl_sync(kFull, acc, 1);
+      const double nz_ = __shfl_sync(kFull, acc, 2);
+      if (den <= 0.0) {
+        degenerate = true;
+        break;
+      }
+      const double moved[3] = {__ddiv_rn(nx_, den), __ddiv_rn(ny_, den), __ddiv_rn(nz_, den)};
+      double cl[3], df[3];
+      for (int i = 0; i < 3; ++i) cl[i] = dclamp(moved[i], lim[i]);
+      for (int i = 0; i < 3; ++i) df[i] = __dsub_rn(cl[i], moved[i]);
+      if (__dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(df[0], df[0]), __dmul_rn(df[1], df[1])),
+                               __dmul_rn(df[2], df[2]))) > 0.0)
+        d.flags |= SALVOX_FLAG_BOUNDARY_CLAMPED;
+      for (int i = 0; i < 3; ++i) df[i] = __dsub_rn(cl[i], c[i]);
+      const double step = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(df[0], df[0]), __dmul_rn(df[1], df[1])),
+                                               __dmul_rn(df[2], df[2])));
+      c[0] = cl[0];
+      c[1] = cl[1];
+      c[2] = cl[2];
+      // histogram at the new centre: its support count is the in-bounds
+      // fraction check (shift.cpp:75) and its pmf the next step's p.
+      ok = warp_candidate_hist(P, s, c, sg.main, P.hist_kernel, lane, &support, &vis);
+      if (frac_bad(support)) {
+        degenerate = true;
+        break;
+      }
+      if (step < P.min_step) {
+        d.flags |= SALVOX_FLAG_CONVERGED;
+        break;
+      }
+    }
+  }
+  if (degenerate) d.flags |= SALVOX_FLAG_DEGENERATE;
+  d.center[0] = c[0];
+  d.center[1] = c[1];
+  d.center[2] = c[2];
+  if (!degenerate) {
+    if (!warp_final_scores(P, s, c, sg, lane, ok, d, visits, true))
+      d.flags |= SALVOX_FLAG_DEGENERATE;
+  }
+  if (lane == 0) {
+    P.out[seed] = d;
+    P.visits[seed] = visits;
+  }
+}
+
+// -------------------------------------------------------- quadrant / octant
+// NE, NW, SW, SE (quadrant.cpp:14); octants: the four at z=+1, then at z=-1.
+__constant__ int c_dirs[8][3] = {{+1, +1, +1}, {-1, +1, +1}, {-1, -1, +1}, {+1, -1, +1},
+                                 {+1, +1, -1}, {-1, +1, -1}, {-1, -1, -1}, {+1, -1, -1}};
+
+__device__ __forceinline__ void axis_range(double p, double dk, int n, int* lo, int* hi) {
+  const double a = p, b = __dadd_rn(p, dk);  // [min, max] of (p, p + dir*k)
+  *lo = max(0, (int)ceil(a < b ? a : b));
+  *hi = min(n - 1, (int)floor(a < b ? b : a));
+}
+
+// Adds the voxels of box B that are not in box A (A subset of B, or A empty)
+// to the per-octant counts.
+__device__ void warp_count_shell(const SeekParams& P, unsigned* cnt, const Box& A, const Box& B,
+                                 bool a_empty, int lane) {
+  auto count_box = [&](const Box& bx) {
+    warp_box_iter(bx, lane, [&](bool act, int x, int y, int z) {
+      if (act) atomicAdd(&cnt[bin_at(P, x, y, z)], 1u);
+    });
+  };
+  if (a_empty) {
+    count_box(B);
+    return;
+  }
+  // x outside A.x
+  if (B.x0 < A.x0) count_box(Box{B.x0, A.x0 - 1, B.y0, B.y1, B.z0, B.z1});
+  if (B.x1 > A.x1) count_box(Box{A.x1 + 1, B.x1, B.y0, B.y1, B.z0, B.z1});
+  // x inside, y outside
+  if (B.y0 < A.y0) count_box(Box{A.x0, A.x1, B.y0, A.y0 - 1, B.z0, B.z1});
+  if (B.y1 > A.y1) count_box(Box{A.x0, A.x1, A.y1 + 1, B.y1, B.z0, B.z1});
+  // x, y inside, z outside
+  if (B.z0 < A.z0) count_box(Box{A.x0, A.x1, A.y0, A.y1, B.z0, A.z0 - 1});
+  if (B.z1 > A.z1) count_box(Box{A.x0, A.x1, A.y0, A.y1, A.z1 + 1, B.z1});
+}
+
+__global__ void __launch_bounds__(256) ascent_kernel(const SeekParams P) {
+  __shared__ WarpScratch scratch[8];
+  const int lane = threadIdx.x & 31;
+  const int wid = threadIdx.x >> 5;
+  const int seed = blockIdx.x * 8 + wid;
+  if (seed >= P.n_seeds) return;
+  WarpScratch& s = scratch[wid];
+  const SeedIn si = P.seeds[seed];
+  const int M = P.bins;
+  const bool two_d = P.method == SALVOX_METHOD_QUADRANT;
+  const int nq = two_d ? 4 : 8;
+  const int min_vox = two_d ? 4 : 8;
+  const double lim[3] = {(double)(P.nx - 1), (double)(P.ny - 1), (double)(P.nz - 1)};
+  double p[3] = {si.pos[0], si.pos[1], si.pos[2]};
+  unsigned long long visits = 0;
+  salvox_detection d;
+  memset(&d, 0, sizeof d);
+  d.seed_index = si.seed_index;
+  d.H[0] = d.H[4] = d.H[8] = 1.0;
+  double last_e[8];
+  int last_k[8];
+  bool degenerate = false, converged = false;
+  int iters = 0;
+  for (int it = 0; it < P.max_iters; ++it) {
+    double ent[8];
+    int bk[8];
+    for (int q = 0; q < nq; ++q) {
+      double best_e = 0.0;
+      int best_k = P.ascent_scales[0];
+      for (int b = lane; b < M; b += 32) s.cnt[0][b] = 0u;
+      __syncwarp();
+      Box prev{0, -1, 0, -1, 0, -1};
+      bool prev_empty = true;
+      for (int i = 0; i < P.n_ascent; ++i) {
+        const int k = P.ascent_scales[i];
+        Box B;
+        axis_range(p[0], (double)c_dirs[q][0] * (double)k, P.nx, &B.x0, &B.x1);
+        axis_range(p[1], (double)c_dirs[q][1] * (double)k, P.ny, &B.y0, &B.y1);
+        if (two_d) {
+          axis_range(p[2], 0.0, P.nz, &B.z0, &B.z1);
+        } else {
+          axis_range(p[2], (double)c_dirs[q][2] * (double)k, P.nz, &B.z0, &B.z1);
+        }
+        const long long count = box_size(B);
+        if (count > 0) {
+          warp_count_shell(P, s.cnt[0], prev, B, prev_empty, lane);
+          prev = B;
+          prev_empty = false;
+        }
+        __syncwarp();
+        double e = 0.0;
+        if (count > 0 && count >= min_vox) {  // quadrant.cpp:24-26
+          visits += (unsigned long long)count;
+          const double mass = (double)count;  // exact integer mass
+          for (int b = lane; b < M; b += 32) s.p[b] = __ddiv_rn((double)s.cnt[0][b], mass);
+          __syncwarp();
+          e = warp_entropy_bits(s.p, M, lane, s.w);
+        }
+        if (e > best_e) {  // strict: smallest scale wins ties (quadrant.cpp:52)
+          best_e = e;
+          best_k = k;
+        }
+      }
+      ent[q] = best_e;
+      bk[q] = best_k;
+    }
+    iters = it + 1;
+    for (int q = 0; q < nq; ++q) {
+      last_e[q] = ent[q];
+      last_k[q] = bk[q];
+    }
+    double total = 0.0;
+    for (int q = 0; q < nq; ++q) total = __dadd_rn(total, ent[q]);
+    if (total <= 0.0) {
+      degenerate = true;
+      break;
+    }
+    double ed[3] = {0.0, 0.0, 0.0};
+    for (int q = 0; q < nq; ++q) {
+      const double ne = __ddiv_rn(ent[q], total);
+      for (int a = 0; a < (two_d ? 2 : 3); ++a)
+        ed[a] = __dadd_rn(ed[a], __dmul_rn(__dmul_rn(ne, (double)c_dirs[q][a]), (double)bk[q]));
+    }
+    for (int a = 0; a < (two_d ? 2 : 3); ++a) p[a] = dclamp(__dadd_rn(p[a], ed[a]), lim[a]);
+    const double nrm =
+        two_d ? __dsqrt_rn(__dadd_rn(__dmul_rn(ed[0], ed[0]), __dmul_rn(ed[1], ed[1])))
+              : __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(ed[0], ed[0]), __dmul_rn(ed[1], ed[1])),
+                                     __dmul_rn(ed[2], ed[2])));
+    if (nrm < P.eta) {
+      converged = true;
+      break;
+    }
+  }
+  d.iterations = iters;
+  if (converged) d.flags |= SALVOX_FLAG_CONVERGED;
+  d.center[0] = p[0];
+  d.center[1] = p[1];
+  d.center[2] = two_d ? 0.0 : p[2];
+  if (degenerate) {
+    d.flags |= SALVOX_FLAG_DEGENERATE;
+  } else {
+    int bq = 0;
+    for (int q = 1; q < nq; ++q)
+      if (last_e[q] > last_e[bq]) bq = q;
+    const int k = max(2, last_k[bq]);  // pipeline.cpp:343
+    const ScaleGeom& sg = P.geoms[P.geom_of_k[k]];
+    for (int i = 0; i < 9; ++i) d.H[i] = sg.H[i];
+    const double c[3] = {d.center[0], d.center[1], d.center[2]};
+    unsigned sup;
+    long long vis;
+    // Epanechnikov histogram: entropy + Bhattacharyya vs uniform (pipeline.cpp:346-350)
+    const bool okp = warp_candidate_hist(P, s, c, sg.main, 1, lane, &sup, &vis);
+    visits += (unsigned long long)vis;
+    if (okp) {
+      double rho = 0.0;
+      if (lane == 0) {
+        for (int b = 0; b < M; ++b) rho = __dadd_rn(rho, __dsqrt_rn(__dmul_rn(s.p[b], P.q[b])));
+        rho = rho < 1.0 ? rho : 1.0;
+      }
+      d.bhattacharyya = __shfl_sync(kFull, rho, 0);
+      d.entropy_bits = warp_entropy_bits(s.p, M, lane, s.w);
+    }
+    double pdf = 0.0;
+    if (sg.pdf_ok) {
+      const bool ok_lo = warp_candidate_hist(P, s, c, sg.lo, 0, lane, &sup, &vis);
+      visits += (unsigned long long)vis;
+      for (int b = lane; b < M; b += 32) s.w[b] = s.p[b];
+      __syncwarp();
+      const bool ok_hi = warp_candidate_hist(P, s, c, sg.hi, 0, lane, &sup, &vis);
+      visits += (unsigned long long)vis;
+      if (ok_lo && ok_hi && lane == 0) {
+        double l1 = 0.0;
+        for (int b = 0; b < M; ++b) l1 = __dadd_rn(l1, fabs(__dsub_rn(s.p[b], s.w[b])));
+        pdf = __dmul_rn(sg.pdf_fac, l1);
+      }
+      pdf = __shfl_sync(kFull, pdf, 0);
+    }
+    d.pdf_diff = pdf;
+  }
+  if (lane == 0) {
+    P.out[seed] = d;
+    P.visits[seed] = visits;
+  }
+}
+
+// ------------------------------------------------------------------ selection
+__global__ void alive_kernel(const salvox_detection* __restrict__ d, int n, double* e, double* pd,
+                             unsigned char* alive) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const bool a = !(d[i].flags & SALVOX_FLAG_DEGENERATE) && d[i].entropy_bits > 0.0;
+    alive[i] = a;
+    e[i] = d[i].entropy_bits;
+    pd[i] = d[i].pdf_diff;
+  }
+}
+
+__global__ void passed_kernel(const salvox_detection* __restrict__ d, int n,
+                              const unsigned char* alive, double et, double pt, double* key,
+                              int* idx, unsigned char* pass) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const bool p = alive[i] && d[i].entropy_bits >= et && d[i].pdf_diff >= pt;  // pipeline.cpp:399
+    pass[i] = p;
+    key[i] = d[i].pdf_diff;
+    idx[i] = i;
+  }
+}
+
+// Greedy radius suppression over pdf-descending candidates (pipeline.cpp:168-183).
+// One warp: lanes test the candidate against the kept list in parallel.
+__global__ void dedupe_kernel(const salvox_detection* __restrict__ d, const int* order, int n,
+                              int k, double radius, salvox_detection* out, int* n_out) {
+  const int lane = threadIdx.x;
+  int kept_n = 0;
+  for (int i = 0; i < n && kept_n < k; ++i) {
+    const salvox_detection& c = d[order[i]];
+    bool clash = false;
+    for (int a = lane; a < kept_n; a += 32) {
+      const double dx = __dsub_rn(out[a].center[0], c.center[0]);
+      const double dy = __dsub_rn(out[a].center[1], c.center[1]);
+      const double dz = __dsub_rn(out[a].center[2], c.center[2]);
+      const double nrm =
+          __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
+      if (nrm <= radius) clash = true;
+    }
+    clash = __any_sync(kFull, clash);
+    if (!clash) {
+      if (lane == 0) out[kept_n] = c;
+      ++kept_n;
+      __syncwarp();
+    }
+  }
+  if (lane == 0) *n_out = kept_n;
+}
+
+// ------------------------------------------------------------------ host side
+namespace {
+
+WinGeom make_geom(const Mat3& H, bool two_d) {
+  WinGeom g{};
+  const Mat3 Hi = eigen_inverse(H);
+  std::memcpy(g.Hinv, Hi.m, sizeof g.Hinv);
+  for (int i = 0; i < 3; ++i) g.ext[i] = std::sqrt(std::max(H.m[i * 4], 0.0));
+  g.det_fac = 1.0 / std::sqrt(std::max(eigen_det(H), 1e-300));
+  g.support_volume = support_volume(H, two_d);
+  return g;
+}
+
+ScaleGeom make_scale_geom(const Mat3& H, bool two_d) {
+  ScaleGeom sg{};
+  sg.main = make_geom(H, two_d);
+  std::memcpy(sg.H, H.m, sizeof sg.H);
+  const double s = window_scale(H, two_d);
+  const double ds = 1.0;
+  sg.pdf_ok = !(s - ds < 1.0);
+  if (sg.pdf_ok) {
+    sg.lo = make_geom(window_scaled_to(H, s - ds, two_d), two_d);
+    sg.hi = make_geom(window_scaled_to(H, s + ds, two_d), two_d);
+    sg.pdf_fac = s * s / (2.0 * ds);
+  }
+  return sg;
+}
+
+struct SeekJob {
+  std::vector<SeedIn> seeds;
+  std::vector<ScaleGeom> geoms;
+  SeekParams P{};
+};
+
+void check_window(const salvox_window* iw) {
+  if (!iw) fail(SALVOX_EINVAL, "IntensityWindow: missing");
+  if (!iw->full_range && !(iw->low < iw->high))
+    fail(SALVOX_EINVAL, "IntensityWindow: low must be < high");
+  if (iw->bins < 2) fail(SALVOX_EINVAL, "IntensityWindow: bins must be >= 2");
+  if (iw->bins > kMaxBins) fail(SALVOX_EUNSUPPORTED, "seek (device): bins must be <= 64");
+}
+
+// Builds seeds + geometry for `method` (shift: one geometry per distinct scale;
+// ascent: one per post-scoring half-size k).
+void build_job(int nx, int ny, int nz, const salvox_detect_params* prm,
+               const std::vector<SeedRec>& recs, const std::vector<int>& index, SeekJob& job) {
+  const bool two_d = nz == 1;
+  const int method = prm->method;
+  SeekParams& P = job.P;
+  P.nx = nx;
+  P.ny = ny;
+  P.nz = nz;
+  P.method = method;
+  P.two_d = two_d;
+  if (method == SALVOX_METHOD_SHIFT) {
+    if (prm->shift_min_step <= 0.0) fail(SALVOX_EINVAL, "shift: min_step must be > 0");
+    if (prm->shift_max_iters < 1) fail(SALVOX_EINVAL, "shift: max_iters must be >= 1");
+    P.max_iters = prm->shift_max_iters;
+    P.min_step = prm->shift_min_step;
+    P.step_kernel = prm->shift_step_kernel;
+    P.hist_kernel = prm->shift_hist_kernel;
+    P.min_frac = prm->shift_min_inbounds_fraction;
+    std::map<std::array<double, 3>, int> gi;
+    for (size_t i = 0; i < recs.size(); ++i) {
+      const double s = recs[i].scale;
+      // pipeline.cpp:365 half = (s, s, 2D ? 1 : s); shift.cpp:9 pins z to 1 in 2D
+      std::array<double, 3> half = {s, s, s};
+      if (recs[i].half[0] != 0.0 || recs[i].half[1] != 0.0 || recs[i].half[2] != 0.0)
+        half = {recs[i].half[0], recs[i].half[1], recs[i].half[2]};
+      if (!(half[0] > 0.0 && half[1] > 0.0 && half[2] > 0.0))
+        fail(SALVOX_EINVAL, "shift: half extents must be > 0");  // shift.hpp:28-29
+      if (two_d) half[2] = 1.0;
+      auto it = gi.find(half);
+      if (it == gi.end()) {
+        it = gi.emplace(half, (int)job.geoms.size()).first;
+        job.geoms.push_back(make_scale_geom(diag_from_half(half[0], half[1], half[2]), two_d));
+      }
+      SeedIn si{};
+      std::memcpy(si.pos, recs[i].pos, sizeof si.pos);
+      si.geom = it->second;
+      si.seed_index = index[i];
+      job.seeds.push_back(si);
+    }
+  } else {
+    std::vector<int> ks;
+    if (prm->n_quadrant_scales > 0) {
+      ks.assign(prm->quadrant_scales, prm->quadrant_scales + prm->n_quadrant_scales);
+    } else {
+      for (int i = 0; i < prm->n_scales; ++i) ks.push_back((int)std::lround(prm->scales[i]));
+    }
+    if (ks.empty()) fail(SALVOX_EINVAL, "quadrant: empty scale range");
+    for (size_t i = 1; i < ks.size(); ++i)
+      if (ks[i] <= ks[i - 1]) fail(SALVOX_EINVAL, "quadrant: scale range must be strictly increasing");
+    if (prm->quadrant_eta <= 0.0) fail(SALVOX_EINVAL, "quadrant: eta must be > 0");
+    if (prm->quadrant_max_iters < 1) fail(SALVOX_EINVAL, "quadrant: max_iters must be >= 1");
+    if ((int)ks.size() > 64 || ks.back() > 128 || ks.front() < 0)
+      fail(SALVOX_EUNSUPPORTED, "ascent (device): at most 64 scales in [0, 128]");
+    P.max_iters = prm->quadrant_max_iters;
+    P.eta = prm->quadrant_eta;
+    P.n_ascent = (int)ks.size();
+    for (size_t i = 0; i < ks.size(); ++i) P.ascent_scales[i] = ks[i];
+    for (int k = 0; k <= 128; ++k) P.geom_of_k[k] = 0;
+    std::vector<int> post = {2};
+    for (int k : ks) post.push_back(std::max(2, k));
+    for (int k : post) {
+      if (P.geom_of_k[k] != 0 || (k == 2 && !job.geoms.empty())) continue;
+      P.geom_of_k[k] = (int)job.geoms.size();
+      const double kd = (double)k;
+      job.geoms.push_back(make_scale_geom(diag_from_half(kd, kd, two_d ? 1.0 : kd), two_d));
+    }
+    for (size_t i = 0; i < recs.size(); ++i) {
+      SeedIn si{};
+      std::memcpy(si.pos, recs[i].pos, sizeof si.pos);
+      si.geom = 0;
+      si.seed_index = index[i];
+      job.seeds.push_back(si);
+    }
+  }
+}
+
+// Runs the seek kernel for one volume whose bins are already on the device.
+void run_seek(salvox_ctx* ctx, SeekJob& job, const uint8_t* d_bins, int bins, const double* d_q,
+              salvox_detection* d_out, unsigned long long* d_visits) {
+  SeekParams& P = job.P;
+  P.bins = bins;
+  P.binvol = d_bins;
+  P.q = d_q;
+  P.n_seeds = (int)job.seeds.size();
+  P.out = d_out;
+  P.visits = d_visits;
+  if (P.n_seeds == 0) return;
+  const size_t gbytes = job.geoms.size() * sizeof(ScaleGeom);
+  const size_t sbytes = job.seeds.size() * sizeof(SeedIn);
+  char* d_geo = static_cast<char*>(ctx->d_geom.ensure(gbytes + sbytes + 256));
+  SX_CUDA(cudaMemcpyAsync(d_geo, job.geoms.data(), gbytes, cudaMemcpyHostToDevice, ctx->stream));
+  char* d_sd = d_geo + ((gbytes + 255) / 256) * 256;
+  SX_CUDA(cudaMemcpyAsync(d_sd, job.seeds.data(), sbytes, cudaMemcpyHostToDevice, ctx->stream));
+  P.geoms = reinterpret_cast<const ScaleGeom*>(d_geo);
+  P.seeds = reinterpret_cast<const SeedIn*>(d_sd);
+  const int grid = (P.n_seeds + 7) / 8;
+  if (P.method == SALVOX_METHOD_SHIFT)
+    shift_kernel<<<grid, 256, 0, ctx->stream>>>(P);
+  else
+    ascent_kernel<<<grid, 256, 0, ctx->stream>>>(P);
+  SX_LAUNCH_CHECK(ctx);
+}
+
+// Uploads the volume, bins it (K1, pitch nx) and the target pmf.
+const uint8_t* prepare_volume(salvox_ctx* ctx, const float* d_vol, int nx, int ny, int nz,
+                              const salvox_window* iw, double* d_q_out_host_unused,
+                              const double* target, double** d_q) {
+  (void)d_q_out_host_unused;
+  double low = iw->low, high = iw->high;
+  const size_t n = (size_t)nx * ny * nz;
+  if (iw->full_range) device_full_range(ctx, d_vol, n, &low, &high);
+  uint8_t* d_bins = static_cast<uint8_t*>(ctx->d_seek_bins.ensure(n));
+  launch_bin_volume(ctx, d_vol, d_bins, nx, ny, nz, nx, low, high, iw->bins);
+  std::vector<double> q(iw->bins);
+  if (target) {  // histogram_from_array normalizes (bindings/py_module.cpp:48-55)
+    double s = 0.0;
+    for (int b = 0; b < iw->bins; ++b) s += target[b];
+    if (s <= 0.0) fail(SALVOX_EINVAL, "Histogram::normalize: zero total mass");
+    for (int b = 0; b < iw->bins; ++b) q[b] = target[b] / s;
+  } else {
+    for (int b = 0; b < iw->bins; ++b) q[b] = 1.0 / iw->bins;  // Histogram::uniform
+  }
+  *d_q = static_cast<double*>(ctx->d_target.ensure(q.size() * 8));
+  SX_CUDA(cudaMemcpyAsync(*d_q, q.data(), q.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+  SX_CUDA(cudaStreamSynchronize(ctx->stream));  // q lives on this stack frame
+  return d_bins;
+}
+
+// Device selection: thresholds + dedupe over n detections at d_dets. Returns
+// the number kept, written to d_kept (device).
+int device_select(salvox_ctx* ctx, const salvox_detection* d_dets, int n, double qe, double qp,
+                  int k, double radius, bool thresholds, salvox_detection* d_kept) {
+  if (n <= 0 || k <= 0) return 0;
+  cudaStream_t st = ctx->stream;
+  const int blocks = std::min((n + 255) / 256, ctx->sm_count * 8);
+  // scratch: 4 double arrays + 2 int arrays + 2 flag arrays
+  char* base = static_cast<char*>(ctx->d_sel_a.ensure((size_t)n * (8 * 4 + 4 * 2 + 2) + 4096));
+  double* e = reinterpret_cast<double*>(base);
+  double* pd = e + n;
+  double* e2 = pd + n;
+  double* pd2 = e2 + n;
+  int* idx = reinterpret_cast<int*>(pd2 + n);
+  int* idx2 = idx + n;
+  unsigned char* alive = reinterpret_cast<unsigned char*>(idx2 + n);
+  unsigned char* pass = alive + n;
+  int* d_cnt = static_cast<int*>(ctx->d_sel_b.ensure(64));
+  double et = -INFINITY, pt = -INFINITY;
+  alive_kernel<<<blocks, 256, 0, st>>>(d_dets, n, e, pd, alive);
+  SX_LAUNCH_CHECK(ctx);
+  if (thresholds) {
+    size_t t1 = 0, t2 = 0;
+    SX_CUDA(cub::DeviceSelect::Flagged(nullptr, t1, e, alive, e2, d_cnt, n, st));
+    SX_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, t2, e2, e, n, 0, 64, st));
+    void* tmp = ctx->d_cub.ensure(std::max(t1, t2));
+    SX_CUDA(cub::DeviceSelect::Flagged(tmp, t1, e, alive, e2, d_cnt, n, st));
+    SX_CUDA(cub::DeviceSelect::Flagged(tmp, t1, pd, alive, pd2, d_cnt + 1, n, st));
+    int na = 0;
+    SX_CUDA(cudaMemcpyAsync(&na, d_cnt, 4, cudaMemcpyDeviceToHost, st));
+    SX_CUDA(cudaStreamSynchronize(st));
+    if (na == 0) return 0;  // pipeline.cpp:387
+    SX_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, t2, e2, e, na, 0, 64, st));
+    tmp = ctx->d_cub.ensure(t2);
+    SX_CUDA(cub::DeviceRadixSort::SortKeys(tmp, t2, e2, e, na, 0, 64, st));
+    SX_CUDA(cub::DeviceRadixSort::SortKeys(tmp, t2, pd2, pd, na, 0, 64, st));
+    ctx->launches += 10;
+    // quantile_threshold (pipeline.cpp:54-59)
+    const size_t ie = (size_t)std::floor(qe * double(na - 1));
+    const size_t ip = (size_t)std::floor(qp * double(na - 1));
+    SX_CUDA(cudaMemcpyAsync(&et, e + ie, 8, cudaMemcpyDeviceToHost, st));
+    SX_CUDA(cudaMemcpyAsync(&pt, pd + ip, 8, cudaMemcpyDeviceToHost, st));
+    SX_CUDA(cudaStreamSynchronize(st));
+  } else {
+    SX_CUDA(cudaMemsetAsync(alive, 1, n, st));
+  }
+  passed_kernel<<<blocks, 256, 0, st>>>(d_dets, n, alive, et, pt, e, idx, pass);
+  SX_LAUNCH_CHECK(ctx);
+  size_t t1 = 0, t2 = 0;
+  SX_CUDA(cub::DeviceSelect::Flagged(nullptr, t1, e, pass, e2, d_cnt, n, st));
+  SX_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, t2, e2, pd2, idx2, idx, n, 0, 64, st));
+  void* tmp = ctx->d_cub.ensure(std::max(t1, t2));
+  SX_CUDA(cub::DeviceSelect::Flagged(tmp, t1, e, pass, e2, d_cnt, n, st));
+  SX_CUDA(cub::DeviceSelect::Flagged(tmp, t1, idx, pass, idx2, d_cnt + 1, n, st));
+  int np = 0;
+  SX_CUDA(cudaMemcpyAsync(&np, d_cnt, 4, cudaMemcpyDeviceToHost, st));
+  SX_CUDA(cudaStreamSynchronize(st));
+  if (np == 0) return 0;
+  // stable sort by pdf_diff descending (pipeline.cpp:169-170): radix sort is stable
+  SX_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, t2, e2, pd2, idx2, idx, np, 0, 64, st));
+  tmp = ctx->d_cub.ensure(t2);
+  SX_CUDA(cub::DeviceRadixSort::SortPairsDescending(tmp, t2, e2, pd2, idx2, idx, np, 0, 64, st));
+  ctx->launches += 8;
+  dedupe_kernel<<<1, 32, 0, st>>>(d_dets, idx, np, k, radius, d_kept, d_cnt + 2);
+  SX_LAUNCH_CHECK(ctx);
+  int kept = 0;
+  SX_CUDA(cudaMemcpyAsync(&kept, d_cnt + 2, 4, cudaMemcpyDeviceToHost, st));
+  SX_CUDA(cudaStreamSynchronize(st));
+  return kept;
+}
+
+void plan_and_dedupe(int nx, int ny, int nz, const salvox_detect_params* prm,
+                     std::vector<SeedRec>& recs, std::vector<int>& index) {
+  std::vector<SeedRec> all;
+  plan_seeds(nx, ny, nz, prm->seed_mode, prm->seed_spacing, prm->seed_count, prm->scales,
+             prm->n_scales, prm->rng_seed, all);
+  recs.clear();
+  index.clear();
+  if (prm->method == SALVOX_METHOD_SHIFT) {
+    recs = all;
+    for (size_t i = 0; i < all.size(); ++i) index.push_back((int)i);
+    return;
+  }
+  // one trajectory per distinct consecutive position (pipeline.cpp:325-331)
+  for (size_t i = 0; i < all.size(); ++i) {
+    if (!recs.empty() && recs.back().pos[0] == all[i].pos[0] && recs.back().pos[1] == all[i].pos[1] &&
+        (prm->method == SALVOX_METHOD_QUADRANT || recs.back().pos[2] == all[i].pos[2]))
+      continue;
+    recs.push_back(all[i]);
+    index.push_back((int)i);
+  }
+}
+
+void check_method(const salvox_detect_params* prm, int nz) {
+  if (!prm) fail(SALVOX_EINVAL, "null params");
+  if (prm->method == SALVOX_METHOD_QUADRANT && nz != 1)
+    fail(SALVOX_EINVAL, "detect: quadrant method requires a 2D volume (nz == 1)");
+  if (prm->method == SALVOX_METHOD_ABMSOD)
+    fail(SALVOX_EUNSUPPORTED, "detect (device): abmsod is outside the accelerated path");
+  if (prm->method != SALVOX_METHOD_QUADRANT && prm->method != SALVOX_METHOD_SHIFT &&
+      prm->method != SALVOX_METHOD_OCTANT)
+    fail(SALVOX_EINVAL, "unknown method");
+  for (int k : {prm->shift_step_kernel, prm->shift_hist_kernel})
+    if (prm->method == SALVOX_METHOD_SHIFT && (k < 0 || k > 2)) fail(SALVOX_EINVAL, "unknown kernel");
+}
+
+unsigned long long sum_visits(salvox_ctx* ctx, const unsigned long long* d_v, int n) {
+  if (n <= 0) return 0;
+  std::vector<unsigned long long> h((size_t)n);
+  SX_CUDA(cudaMemcpyAsync(h.data(), d_v, (size_t)n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  SX_CUDA(cudaStreamSynchronize(ctx->stream));
+  unsigned long long s = 0;
+  for (auto v : h) s += v;
+  return s;
+}
+
+}  // namespace
+}  // namespace sx
+
+using namespace sx;
+
+extern "C" int salvox_detect(salvox_ctx* ctx, const float* volume, int32_t nx, int32_t ny,
+                             int32_t nz, const salvox_window* iw, const salvox_detect_params* prm,
+                             salvox_detection* out, int64_t cap, int64_t* n_out,
+                             salvox_detection* per_seed, int64_t cap_seed, int64_t* n_seed,
+                             uint64_t* visits) {
+  return guarded([&] {
+    if (!ctx) fail(SALVOX_EINVAL, "null context");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (nx < 1 || ny < 1 || nz < 1) fail(SALVOX_EINVAL, "Volume: dims must be >= 1");
+    if (!volume) fail(SALVOX_EINVAL, "null volume");
+    check_method(prm, nz);
+    check_window(iw);
+    std::vector<SeedRec> recs;
+    std::vector<int> index;
+    plan_and_dedupe(nx, ny, nz, prm, recs, index);
+    SeekJob job;
+    build_job(nx, ny, nz, prm, recs, index, job);
+    SX_CUDA(cudaSetDevice(ctx->device));
+    const size_t n = (size_t)nx * ny * nz;
+    float* d_vol = static_cast<float*>(ctx->d_seek_vol.ensure(n * 4));
+    SX_CUDA(cudaMemcpyAsync(d_vol, volume, n * 4, cudaMemcpyHostToDevice, ctx->stream));
+    double* d_q = nullptr;
+    const uint8_t* d_bins = prepare_volume(ctx, d_vol, nx, ny, nz, iw, nullptr, prm->shift_target, &d_q);
+    const int ns = (int)job.seeds.size();
+    char* d_dets = static_cast<char*>(ctx->d_dets.ensure((size_t)(ns + 1) * (sizeof(salvox_detection) + 8) * 2 + 512));
+    salvox_detection* d_all = reinterpret_cast<salvox_detection*>(d_dets);
+    salvox_detection* d_kept = d_all + (ns + 1);
+    unsigned long long* d_vis = reinterpret_cast<unsigned long long*>(d_kept + (ns + 1));
+    run_seek(ctx, job, d_bins, iw->bins, d_q, d_all, d_vis);
+    const int kept = device_select(ctx, d_all, ns, prm->entropy_quantile, prm->pdf_quantile,
+                                   prm->top_k, prm->dedupe_radius, true, d_kept);
+    if (out && cap > 0 && kept > 0)
+      SX_CUDA(cudaMemcpyAsync(out, d_kept, (size_t)std::min<int64_t>(kept, cap) * sizeof(salvox_detection),
+                              cudaMemcpyDeviceToHost, ctx->stream));
+    if (per_seed && cap_seed > 0 && ns > 0)
+      SX_CUDA(cudaMemcpyAsync(per_seed, d_all, (size_t)std::min<int64_t>(ns, cap_seed) * sizeof(salvox_detection),
+                              cudaMemcpyDeviceToHost, ctx->stream));
+    const unsigned long long v = sum_visits(ctx, d_vis, ns);
+    if (visits) *visits += v;
+    if (n_out) *n_out = kept;
+    if (n_seed) *n_seed = ns;
+  });
+}
+
+extern "C" int salvox_detect_batch_device(salvox_ctx* ctx, const float* d_volumes, int32_t batch,
+                                          int32_t nx, int32_t ny, int32_t nz,
+                                          const salvox_window* iw,
+                                          const salvox_detect_params* prm, salvox_detection* out,
+                                          int64_t cap, int64_t* n_out, uint64_t* visits) {
+  return guarded([&] {
+    if (!ctx) fail(SALVOX_EINVAL, "null context");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (nx < 1 || ny < 1 || nz < 1 || batch < 0) fail(SALVOX_EINVAL, "Volume: dims must be >= 1");
+    check_method(prm, nz);
+    check_window(iw);
+    std::vector<SeedRec> recs;
+    std::vector<int> index;
+    plan_and_dedupe(nx, ny, nz, prm, recs, index);
+    SeekJob job;
+    build_job(nx, ny, nz, prm, recs, index, job);
+    SX_CUDA(cudaSetDevice(ctx->device));
+    const size_t n = (size_t)nx * ny * nz;
+    const int ns = (int)job.seeds.size();
+    char* d_dets = static_cast<char*>(ctx->d_dets.ensure((size_t)(ns + 1) * (sizeof(salvox_detection) + 8) * 2 + 512));
+    salvox_detection* d_all = reinterpret_cast<salvox_detection*>(d_dets);
+    salvox_detection* d_kept = d_all + (ns + 1);
+    unsigned long long* d_vis = reinterpret_cast<unsigned long long*>(d_kept + (ns + 1));
+    for (int v = 0; v < batch; ++v) {
+      double* d_q = nullptr;
+      const uint8_t* d_bins =
+          prepare_volume(ctx, d_volumes + (size_t)v * n, nx, ny, nz, iw, nullptr, prm->shift_target, &d_q);
+      run_seek(ctx, job, d_bins, iw->bins, d_q, d_all, d_vis);
+      const int kept = device_select(ctx, d_all, ns, prm->entropy_quantile, prm->pdf_quantile,
+                                     prm->top_k, prm->dedupe_radius, true, d_kept);
+      if (out && cap > 0 && kept > 0)
+        SX_CUDA(cudaMemcpyAsync(out + (size_t)v * cap, d_kept,
+                                (size_t)std::min<int64_t>(kept, cap) * sizeof(salvox_detection),
+                                cudaMemcpyDeviceToHost, ctx->stream));
+      if (n_out) n_out[v] = kept;
+      const unsigned long long vs = sum_visits(ctx, d_vis, ns);
+      if (visits) *visits += vs;
+    }
+    SX_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+extern "C" int salvox_seek(salvox_ctx* ctx, const float* volume, int32_t nx, int32_t ny,
+                           int32_t nz, const salvox_window* iw, const salvox_detect_params* prm,
+                           const double* seed_positions, const double* seed_scales,
+                           const double* seed_half_extents, const int32_t* seed_index, int64_t n,
+                           salvox_detection* out, uint64_t* visits) {
+  return guarded([&] {
+    if (!ctx) fail(SALVOX_EINVAL, "null context");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (nx < 1 || ny < 1 || nz < 1) fail(SALVOX_EINVAL, "Volume: dims must be >= 1");
+    check_method(prm, nz);
+    check_window(iw);
+    if (n < 0 || (n > 0 && (!seed_positions || !out))) fail(SALVOX_EINVAL, "bad seed arrays");
+    std::vector<SeedRec> recs((size_t)n);
+    std::vector<int> index((size_t)n);
+    for (int64_t i = 0; i < n; ++i) {
+      std::memcpy(recs[i].pos, seed_positions + 3 * i, 3 * sizeof(double));
+      recs[i].scale = seed_scales ? seed_scales[i] : 8.0;
+      if (seed_half_extents) std::memcpy(recs[i].half, seed_half_extents + 3 * i, 3 * sizeof(double));
+      index[i] = seed_index ? seed_index[i] : (int)i;
+    }
+    SeekJob job;
+    build_job(nx, ny, nz, prm, recs, index, job);
+    if (n == 0) return;
+    SX_CUDA(cudaSetDevice(ctx->device));
+    const size_t nv = (size_t)nx * ny * nz;
+    float* d_vol = static_cast<float*>(ctx->d_seek_vol.ensure(nv * 4));
+    SX_CUDA(cudaMemcpyAsync(d_vol, volume, nv * 4, cudaMemcpyHostToDevice, ctx->stream));
+    double* d_q = nullptr;
+    const uint8_t* d_bins = prepare_volume(ctx, d_vol, nx, ny, nz, iw, nullptr, prm->shift_target, &d_q);
+    char* d_dets = static_cast<char*>(ctx->d_dets.ensure((size_t)(n + 1) * (sizeof(salvox_detection) + 8) * 2 + 512));
+    salvox_detection* d_all = reinterpret_cast<salvox_detection*>(d_dets);
+    unsigned long long* d_vis = reinterpret_cast<unsigned long long*>(d_all + 2 * (n + 1));
+    run_seek(ctx, job, d_bins, iw->bins, d_q, d_all, d_vis);
+    SX_CUDA(cudaMemcpyAsync(out, d_all, (size_t)n * sizeof(salvox_detection), cudaMemcpyDeviceToHost,
+                            ctx->stream));
+    const unsigned long long v = sum_visits(ctx, d_vis, (int)n);
+    if (visits) *visits += v;
+  });
+}
+
+static int select_host(salvox_ctx* ctx, const salvox_detection* dets, int64_t n, double qe,
+                       double qp, int32_t k, double radius, bool thresholds,
+                       salvox_detection* out, int64_t* n_out) {
+  return guarded([&] {
+    if (!ctx) fail(SALVOX_EINVAL, "null context");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (n < 0 || (n > 0 && !dets)) fail(SALVOX_EINVAL, "bad detection array");
+    SX_CUDA(cudaSetDevice(ctx->device));
+    char* d = static_cast<char*>(ctx->d_sel_c.ensure((size_t)(n + 1) * sizeof(salvox_detection) * 2));
+    salvox_detection* d_in = reinterpret_cast<salvox_detection*>(d);
+    salvox_detection* d_out = d_in + (n + 1);
+    if (n > 0)
+      SX_CUDA(cudaMemcpyAsync(d_in, dets, (size_t)n * sizeof(salvox_detection), cudaMemcpyHostToDevice,
+                              ctx->stream));
+    const int kept = device_select(ctx, d_in, (int)n, qe, qp, k, radius, thresholds, d_out);
+    if (kept > 0 && out)
+      SX_CUDA(cudaMemcpyAsync(out, d_out, (size_t)kept * sizeof(salvox_detection), cudaMemcpyDeviceToHost,
+                              ctx->stream));
+    SX_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (n_out) *n_out = kept;
+  });
+}
+
+extern "C" int salvox_select(salvox_ctx* ctx, const salvox_detection* dets, int64_t n,
+                             double q_entropy, double q_pdf, int32_t k, double radius,
+                             salvox_detection* out, int64_t* n_out) {
+  return select_host(ctx, dets, n, q_entropy, q_pdf, k, radius, true, out, n_out);
+}
+
+extern "C" int salvox_dedupe_top_k(salvox_ctx* ctx, const salvox_detection* dets, int64_t n,
+                                   int32_t k, double radius, salvox_detection* out,
+                                   int64_t* n_out) {
+  return select_host(ctx, dets, n, 0.0, 0.0, k, radius, false, out, n_out);
+}

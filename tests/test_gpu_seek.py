@@ -1,0 +1,133 @@
+"""GPU parity of the seed-grid detector (shift / quadrant / octant) vs the oracle.
+
+Contract: converged positions, iteration counts, flags, seed indices, window H
+are bit-exact; with the oracle in shared-log mode (sx_log on both sides) the
+scores (entropy, Bhattacharyya, pdf_diff) are bit-exact too, and the selected
+detections (thresholds + dedupe) are identical. Against the glibc-log oracle the
+scores agree to 1e-12 relative.
+"""
+import numpy as np
+import pytest
+
+from tests import phantoms
+
+pytestmark = pytest.mark.gpu
+
+FIELDS_EXACT = ["center", "H", "iterations", "flags", "seed_index"]
+FIELDS_SCORE = ["entropy_bits", "pdf_diff", "bhattacharyya"]
+
+
+def _same(gpu, ref, scores_exact=True):
+    assert len(gpu) == len(ref)
+    for f in FIELDS_EXACT:
+        assert np.array_equal(gpu[f], ref[f]), f
+    for f in FIELDS_SCORE:
+        if scores_exact:
+            assert np.array_equal(gpu[f], ref[f]), f
+        else:
+            assert np.allclose(gpu[f], ref[f], rtol=1e-12, atol=1e-14), f
+
+
+def _both(sx, oracle, vol, low, high, bins, **kw):
+    sel, seeds, visits = sx.detect_records(vol, window_low=low, window_high=high, bins=bins,
+                                           per_seed=True, **kw)
+    okw = dict(kw)
+    okw["top_k"] = okw.pop("k", 20)
+    oracle.set_log_mode(1)
+    try:
+        rsel, rseeds, rvis = oracle.detect(vol, low, high, bins, **okw)
+    finally:
+        oracle.set_log_mode(0)
+    return sel, seeds, visits, rsel, rseeds, rvis
+
+
+def test_shift_finds_ball_center(sx, oracle):  # test_pipeline.cpp:296-319
+    vol, cent = oracle.make_phantom(phantoms.ball_3d(64, (36.0, 30.0, 28.0), 9.0, 101))
+    sel, seeds, visits, rsel, rseeds, rvis = _both(
+        sx, oracle, vol, 0, 64, 64, method="shift", seed_spacing=16.0, scales=[6.0, 9.0], k=5,
+        dedupe_radius=6.0)
+    _same(seeds, rseeds)
+    _same(sel, rsel)
+    assert visits == rvis
+    assert len(sel) > 0 and np.linalg.norm(sel[0]["center"] - cent[0]) <= 2.0
+
+
+def test_shift_2d_and_anisotropic(sx, oracle):
+    vol, _ = oracle.make_phantom(phantoms.cube_3d(48, 7, 83))
+    rng = np.random.default_rng(13)
+    seeds = rng.uniform(0, 47, size=(10, 3))
+    gpu, _ = sx.seek_records(vol, seeds, half_extents=[6.0, 5.0, 4.0], method="shift",
+                             window_low=0, window_high=64, bins=64)
+    oracle.set_log_mode(1)
+    try:
+        for i, s in enumerate(seeds):  # test_seek.cpp:360-375
+            ref, _ = oracle.saliency_shift(vol, 0, 64, 64, s, [6.0, 5.0, 4.0])
+            for f in FIELDS_EXACT[:4] + FIELDS_SCORE:
+                assert np.array_equal(gpu[i][f], ref[f]), (i, f)
+    finally:
+        oracle.set_log_mode(0)
+    vol2, _ = oracle.make_phantom(phantoms.square_2d(96, 45.0, 49.0, 9, 64, 303))
+    sel, seeds2, visits, rsel, rseeds, rvis = _both(
+        sx, oracle, vol2, 0, 64, 64, method="shift", seed_spacing=12.0, scales=[6.0, 10.0], k=3,
+        dedupe_radius=8.0)
+    _same(seeds2, rseeds)
+    _same(sel, rsel)
+
+
+def test_shift_constant_volume_empty(sx, oracle):  # test_pipeline.cpp:381-392
+    vol = np.ones((48, 48, 48), np.float32)
+    assert sx.detect(vol, method="shift", seed_spacing=16.0, scales=[6.0], window_low=0,
+                     window_high=64, bins=64) == []
+
+
+def test_quadrant_matches_oracle(sx, oracle):  # test_pipeline.cpp:356-379 + test_seek.cpp:148-166
+    vol, _ = oracle.make_phantom(phantoms.square_2d(128, 63.0, 63.0, 12, 64, 23))
+    sel, seeds, visits, rsel, rseeds, rvis = _both(
+        sx, oracle, vol, 0, 64, 64, method="quadrant", seed_spacing=16.0,
+        scales=[4.0, 8.0, 12.0, 16.0], k=3, dedupe_radius=8.0)
+    _same(seeds, rseeds)
+    _same(sel, rsel)
+    assert visits == rvis
+    assert any(np.linalg.norm(d["center"][:2] - [63, 63]) <= 3 for d in seeds
+               if not d["flags"] & 2)
+
+
+def test_quadrant_requires_2d(sx):  # test_pipeline.cpp:394-400
+    with pytest.raises(ValueError, match="requires a 2D volume"):
+        sx.detect(np.zeros((16, 16, 16), np.float32), method="quadrant", window_low=0,
+                  window_high=64, bins=64)
+
+
+def test_octant_matches_oracle(sx, oracle):
+    spec = phantoms.ball_3d(48, (26.0, 22.0, 24.0), 8.0, 55, levels=16,
+                            background={"type": "gaussian", "mean": 4.0, "sigma": 1.5})
+    vol, cent = oracle.make_phantom(spec)
+    sel, seeds, visits, rsel, rseeds, rvis = _both(
+        sx, oracle, vol, 0, 16, 16, method="octant", seed_spacing=12.0, scales=[3.0, 5.0, 7.0, 9.0],
+        k=5, dedupe_radius=6.0)
+    _same(seeds, rseeds)
+    _same(sel, rsel)
+    assert visits == rvis
+
+
+def test_select_matches_oracle(sx, oracle):
+    rng = np.random.default_rng(4)
+    d = np.zeros(400, sx.DET_DTYPE)
+    d["center"][:, 0] = rng.uniform(0, 500, 400)
+    d["pdf_diff"] = rng.random(400)
+    d["entropy_bits"] = rng.random(400) * 5
+    d["flags"] = np.where(rng.random(400) < 0.1, 2, 1)
+    d["entropy_bits"][::37] = 0.0
+    d["seed_index"] = np.arange(400)
+    got = sx.select(d, 0.9, 0.2, 20, 5.0)
+    ref = oracle.select(d.view(oracle.DET_DTYPE), 0.9, 0.2, 20, 5.0)
+    assert np.array_equal(got["seed_index"], ref["seed_index"])
+    got2 = sx.dedupe_top_k(d, 20, 5.0)  # test_pipeline.cpp:55-83
+    ref2 = oracle.dedupe_top_k(d.view(oracle.DET_DTYPE), 20, 5.0)
+    assert np.array_equal(got2["seed_index"], ref2["seed_index"])
+    assert len(sx.dedupe_top_k(d[:0], 20, 5.0)) == 0
+    pair = np.zeros(2, sx.DET_DTYPE)
+    pair["center"][:, 0] = [10, 11]
+    pair["pdf_diff"] = [1.0, 2.0]
+    out = sx.dedupe_top_k(pair, 20, 5.0)
+    assert len(out) == 1 and out[0]["pdf_diff"] == 2.0
