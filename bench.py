@@ -1,0 +1,380 @@
+#!/usr/bin/env python3
+"""bench.py -- headline benchmark of the B200 hot path (BASELINE.json configs[1]).
+
+Workload: exhaustive Kadir-Brady saliency on the 256^3 synthetic C2 phantom
+(gaussian background + 3 balls + 1 box, uniform fills, 32 bins),
+13 scales 3..15, per-voxel best scale + strict-maxima selection. One step = one
+full pass (bin pre-pass, kb_kernel, maxima, sort). Metric: voxel-scale entropy
+evaluations per second (nx*ny*nz*13 per pass).
+
+  python bench.py [--gpus N --steps K --warmup W]            # B200 arm
+  python bench.py --impl reference [--steps K --warmup W]     # CPU reference arm
+
+N > 1 runs under torchrun: the volume is z-slab sharded (strong scaling), the
+per-slab maxima meet in one NCCL all-gather (paper_1310_6736_b200/sharding.py).
+`value` times the device-resident pass (CUDA events on the launching stream,
+L2 flushed between steps, max over ranks); `e2e` times the public API call with
+the pinned host volume in and the maps + maxima out. The roofline denominator is
+the shared-memory update peak measured live by salvox_probe_smem_peak (the pass
+is bound by shared-memory atomics, not HBM or tensor cores -- DESIGN.md).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+SCALES = [float(s) for s in range(3, 16)]
+BINS = 32
+LOW, HIGH = 0.0, 32.0  # window [0, 32), SURVEY.md 8(d) C2
+METRIC = "voxel-scale entropy evals/sec (exhaustive); 256³ seed-grid volumes/sec"
+UNIT = "voxel-scale evals/s"
+
+
+def c2_spec():
+    from tests import phantoms
+    return phantoms.config_c2()
+
+
+def c3_spec():
+    from tests import phantoms
+    return phantoms.config_c3()
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ reference arm
+def cpu_sample_run(vol, threads, planes):
+    """The oracle's literal restatement of pipeline.cpp:63-166 (fp64, the reference's loop
+    order) on a bounded sample: `planes` full central z-planes of the same volume, split
+    row-wise over `threads` host threads."""
+    from oracle import oracle as O
+    nz, ny, nx = vol.shape
+    z0 = nz // 2 - planes // 2
+    t0 = time.perf_counter()
+    O.exhaustive(vol, LOW, HIGH, BINS, SCALES, budget=10**15, mode="literal", threads=threads,
+                 z_range=(z0, z0 + planes))
+    dt = time.perf_counter() - t0
+    evals = nx * ny * planes * len(SCALES)
+    return evals / dt, (f"C2 volume, planes z={z0}..{z0 + planes - 1} "
+                        f"({nx * ny * planes} voxels x 13 scales, {dt:.1f} s)")
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    from paper_1310_6736_b200 import api
+    vol, _ = api.make_phantom(c2_spec())
+    threads = os.cpu_count() or 1
+    planes = max(1, threads // 2)  # ~5-10 s per step on the box's cores
+    for _ in range(min(args.warmup, 1)):
+        cpu_sample_run(vol, threads, 1)
+    vals = []
+    for _ in range(args.steps):
+        v, sample = cpu_sample_run(vol, threads, planes)
+        vals.append(v)
+    value = float(np.mean(vals))
+    total_evals = float(np.prod(vol.shape)) * len(SCALES)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": total_evals / value * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "exhaustive Kadir-Brady, 256^3 C2 phantom, 32 bins, scales 3..15",
+                   "sample_per_step": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "reference C++ is unbuildable here (Eigen3/vendor absent); the literal oracle "
+                "restatement (oracle/salvox_oracle.c, fp64, reference loop order) is timed; "
+                "ms_per_step extrapolates the sample to one full 256^3 pass",
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ B200 arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-seed-grid", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    import torch
+    import torch.distributed as dist
+
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        if args.impl == "b200":
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    import paper_1310_6736_b200 as sx
+    from paper_1310_6736_b200 import api, sharding
+    from paper_1310_6736_b200._lib import Context
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    ctx = Context(local)
+    ctx.set_stream(stream.cuda_stream)
+
+    vol, _ = api.make_phantom(c2_spec())
+    nz, ny, nx = vol.shape
+    R = sharding.halo_radius(SCALES)
+    z0, z1, zs0, zs1 = sharding.slab_bounds(nz, world, rank, R)
+    total_evals = float(nx * ny * nz * len(SCALES))
+    budget = 10**15
+
+    # live roofline denominator (same GPU, same run)
+    peak_atoms, peak_lds = ctx.probe_smem_peak(64)
+
+    # ---- value: device-resident slab, events on the launching stream
+    slab_host = torch.from_numpy(np.ascontiguousarray(vol[zs0:zs1])).pin_memory()
+    d_slab = slab_host.to(dev, non_blocking=True)
+    d_score = torch.empty((z1 - z0, ny, nx), dtype=torch.float32, device=dev)
+    d_best = torch.empty_like(d_score)
+    flush = torch.empty(int(256 * 2**20), dtype=torch.uint8, device=dev)  # > 126 MB L2
+    from paper_1310_6736_b200 import _lib
+    import ctypes as C
+    sc = np.asarray(SCALES, np.float64)
+    iw = _lib.Window(LOW, HIGH, BINS, 0)
+    nmax = C.c_int64(0)
+
+    def device_pass():
+        _lib.check(_lib.load().salvox_exhaustive_slab_device(
+            ctx.handle, C.c_void_p(d_slab.data_ptr()), nx, ny, nz, zs0, zs1, z0, z1, C.byref(iw),
+            sc.ctypes.data_as(C.c_void_p), len(sc), 0, budget, C.c_void_p(d_score.data_ptr()),
+            C.c_void_p(d_best.data_ptr()), C.byref(nmax)))
+
+    for _ in range(args.warmup):
+        device_pass()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    ctx.set_profiling(True)
+    launches0 = ctx.launch_count()
+    times = []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.fill_(1)  # L2 flush between timed steps (outside the events)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            device_pass()
+            e1.record(stream)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1))
+    torch.cuda.synchronize(dev)
+    launches = ctx.launch_count() - launches0
+    kb_ms, kb_n, kb_updates = ctx.kernel_time()
+    ctx.set_profiling(False)
+    ms_local = float(np.mean(times))
+    ms = ms_local
+    if world > 1:
+        t = torch.tensor([ms_local], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    value = total_evals / (ms * 1e-3)
+
+    # ---- e2e: public API (host pinned volume in, maps + maxima out), sharded over ranks
+    vol_pinned = torch.from_numpy(vol).pin_memory().numpy()
+    h2d = (zs1 - zs0) * ny * nx * 4
+    e2e_times, d2h = [], 0
+    for i in range(args.warmup + args.steps):
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        score, best, (oz0, oz1), merged, _ = sharding.exhaustive_sharded(
+            vol_pinned, SCALES, LOW, HIGH, BINS, budget=budget, device=dev if world > 1 else None,
+            ctx=ctx)
+        t1 = time.perf_counter()
+        if i >= args.warmup:
+            e2e_times.append((t1 - t0) * 1e3)
+            d2h = score.nbytes + best.nbytes + len(merged) * sx.MAX_DTYPE.itemsize
+    e2e_ms = float(np.mean(e2e_times))
+    if world > 1:
+        t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+
+    # ---- secondary: 256x256x160 seed-grid (shift, 64 bins) volumes/s, device-resident
+    seed_grid = None
+    if not args.no_seed_grid and rank == 0:
+        seed_grid = bench_seed_grid(ctx, dev, stream, flush)
+
+    # ---- cpu baseline (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        val, sample = cpu_sample_run(vol, threads, threads)
+        cpu = {"value": val, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample}
+
+    if rank == 0:
+        achieved = kb_updates / (kb_ms * 1e-3) if kb_ms > 0 else None
+        traffic = None
+        prof = os.path.join(ROOT, "profiles", "kb_kernel_ncu.json")
+        if os.path.exists(prof):
+            try:
+                traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+            except Exception:
+                traffic = None
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic",
+            "config": {"workload": "exhaustive Kadir-Brady saliency, 256^3 C2 phantom "
+                                   "(BASELINE.json configs[1]), 32 bins, scales 3..15, "
+                                   "per-voxel best scale + strict maxima",
+                       "voxels": nx * ny * nz, "scales": len(SCALES),
+                       "evals_per_pass": total_evals, "parallelism": f"z-slab x{world}",
+                       "l2": "flushed between timed steps (256 MiB write)"},
+            "e2e": {"value": total_evals / (e2e_ms * 1e-3), "unit": UNIT,
+                    "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world,
+                    "ms_per_step": e2e_ms},
+            "roofline": {"bound": "smem", "achieved": achieved, "peak": peak_atoms,
+                         "unit": "histogram updates/s", "frac": (achieved / peak_atoms)
+                         if achieved else None, "traffic": traffic,
+                         "kernel": "kb_kernel", "kb_ms_per_launch": kb_ms / max(kb_n, 1),
+                         "updates_per_launch": kb_updates / max(kb_n, 1),
+                         "peak_source": "live: salvox_probe_smem_peak (kb_kernel inner loop, "
+                                        "LDS.U8 + ATOMS.ADD), not in MEASURED_PEAKS.json",
+                         "lds_only_peak": peak_lds},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        if cpu is not None:
+            line["cpu_baseline"] = cpu
+        if seed_grid is not None:
+            line["seed_grid"] = seed_grid
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def bench_seed_grid(ctx, dev, stream, flush, steps=3):
+    """C3 (256x256x160 MR phantom, 64 bins, shift, lattice 16 x scales {8, 12}) volumes/s."""
+    import ctypes as C
+
+    import torch
+
+    from paper_1310_6736_b200 import _lib, api
+
+    vol, _ = api.make_phantom(c3_spec())
+    d_vol = torch.from_numpy(vol).to(dev)
+    iw = _lib.Window(0.0, 64.0, 64, 0)
+    P, keep = api._detect_params("shift", seed_spacing=16.0, scales=(8.0, 12.0), k=20,
+                                 dedupe_radius=5.0)
+    out = np.empty(20, _lib.DET_DTYPE)
+    n_out = np.zeros(1, np.int64)
+    visits = C.c_uint64(0)
+    nz, ny, nx = vol.shape
+
+    def run():
+        _lib.check(_lib.load().salvox_detect_batch_device(
+            ctx.handle, C.c_void_p(d_vol.data_ptr()), 1, nx, ny, nz, C.byref(iw), C.byref(P),
+            out.ctypes.data_as(C.c_void_p), 20, n_out.ctypes.data_as(C.c_void_p),
+            C.byref(visits)))
+
+    run()
+    times = []
+    for _ in range(steps):
+        flush.fill_(1)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        run()
+        e1.record(stream)
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1))
+    ms = float(np.mean(times))
+    del keep
+    return {"metric": "seed-grid volumes/sec", "value": 1e3 / ms, "unit": "volumes/s",
+            "ms_per_volume": ms,
+            "config": {"workload": "C3 256x256x160 MR phantom, shift mean-shift, 64 bins, "
+                                   "lattice 16 x scales {8, 12} = 5120 seeds",
+                       "selected": int(n_out[0])}}
+
+
+if __name__ == "__main__":
+    main()

@@ -160,6 +160,17 @@ SALVOX_API int salvox_exhaustive_device(salvox_ctx* ctx, const float* d_volume, 
                              int32_t n_scales, int32_t kernel, uint64_t budget, float* d_score,
                              float* d_best_scale, int64_t* n_maxima);
 
+/* Device-resident z-slab form: d_slab (device) holds planes [zs0, zs1) of the
+ * volume; scores the owned planes [z0, z1) (same halo rule as
+ * salvox_exhaustive_slab). d_score / d_best_scale (device, nullable) receive the
+ * owned-plane maps. */
+SALVOX_API int salvox_exhaustive_slab_device(salvox_ctx* ctx, const float* d_slab, int32_t nx,
+                                             int32_t ny, int32_t nz, int32_t zs0, int32_t zs1,
+                                             int32_t z0, int32_t z1, const salvox_window* iw,
+                                             const double* scales, int32_t n_scales,
+                                             int32_t kernel, uint64_t budget, float* d_score,
+                                             float* d_best_scale, int64_t* n_maxima);
+
 /* Copies the maxima of the last exhaustive call on ctx. */
 SALVOX_API int salvox_last_maxima(salvox_ctx* ctx, salvox_maximum* out, int64_t cap, int64_t* n_out);
 

@@ -123,7 +123,8 @@ def _declare(L):
     L.sxo_exhaustive.restype = C.c_int
     L.sxo_exhaustive.argtypes = [_f32p, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_int,
                                  _f64p, C.c_int, C.c_int, C.c_uint64, C.c_int, C.c_int, C.c_int,
-                                 C.c_int, _f32p, _f32p, _u64p, C.c_char_p, C.c_int]
+                                 C.c_int, C.c_int, C.c_int, _f32p, _f32p, _u64p, C.c_char_p,
+                                 C.c_int]
     L.sxo_voxel_shell_hist.restype = C.c_int
     L.sxo_voxel_shell_hist.argtypes = [_f32p, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
                                        C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, _u64p]
@@ -232,7 +233,7 @@ def bin_of(low, high, bins, intensity):
 
 # ------------------------------------------------------------- pipeline.cpp exhaustive
 def exhaustive(vol, low, high, bins, scales, kernel="identity", budget=2_000_000, mode="literal",
-               threads=1, z_range=None):
+               threads=1, z_range=None, y_range=None):
     """pipeline.cpp:63-141. Returns (score, best_scale, visits) as (nz,ny,nx) float32."""
     v, nx, ny, nz = _vol(vol)
     sc = np.ascontiguousarray(scales, np.float64)
@@ -241,9 +242,10 @@ def exhaustive(vol, low, high, bins, scales, kernel="identity", budget=2_000_000
     visits = np.zeros(1, np.uint64)
     err = C.create_string_buffer(256)
     z0, z1 = z_range if z_range is not None else (0, nz)
+    y0, y1 = y_range if y_range is not None else (0, ny)
     rc = lib().sxo_exhaustive(v, nx, ny, nz, low, high, bins, sc, len(sc), KERNELS[kernel],
                               int(budget), 0 if mode == "literal" else 1, int(threads), int(z0),
-                              int(z1), score, best, visits, err, 256)
+                              int(z1), int(y0), int(y1), score, best, visits, err, 256)
     if rc != 0:
         raise OracleError(err.value.decode())
     return score, best, int(visits[0])

@@ -285,7 +285,8 @@ typedef struct {
   const double* radii;
   int n_radii;
   sphere_offsets* offs;
-  int z0, z1; /* planes of this worker */
+  int64_t r0, r1; /* rows (z,y) of this worker, as z*ny+y in [r0, r1) */
+  int ry0, ry1;    /* row window inside each plane */
   float* score;
   float* best_scale;
   uint8_t* binvol; /* exact mode: precomputed bin_of */
@@ -309,8 +310,9 @@ static void* exh_worker(void* arg) {
   double* hists = (double*)malloc(sizeof(double) * (size_t)NR * M);
   int* normalized = (int*)malloc(sizeof(int) * (size_t)NR);
   uint64_t* S = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)NR * M);
-  for (int z = j->z0; z < j->z1; ++z)
-    for (int y = 0; y < ny; ++y)
+  const int nry = j->ry1 - j->ry0;
+  for (int64_t row = j->r0; row < j->r1; ++row) {
+    const int z = (int)(row / nry), y = j->ry0 + (int)(row % nry);
       for (int x = 0; x < nx; ++x) {
         for (int ri = 0; ri < NR; ++ri) {
           double* h = hists + (size_t)ri * M;
@@ -368,6 +370,7 @@ static void* exh_worker(void* arg) {
         j->score[idx] = (float)best;
         j->best_scale[idx] = (float)best_s;
       }
+  }
   free(hists);
   free(normalized);
   free(S);
@@ -376,8 +379,8 @@ static void* exh_worker(void* arg) {
 
 int sxo_exhaustive(const float* vol, int nx, int ny, int nz, double low, double high, int bins,
                    const double* scales, int n_scales, int kernel, uint64_t budget, int mode,
-                   int threads, int z_begin, int z_end, float* score, float* best_scale,
-                   uint64_t* visits, char* err, int err_len) {
+                   int threads, int z_begin, int z_end, int y_begin, int y_end, float* score,
+                   float* best_scale, uint64_t* visits, char* err, int err_len) {
   if (n_scales < 1) {
     set_err(err, err_len, "exhaustive scan: no scales");
     return -1;
@@ -422,9 +425,12 @@ int sxo_exhaustive(const float* vol, int nx, int ny, int nz, double low, double 
   }
   if (z_end <= 0 || z_end > nz) z_end = nz;
   if (z_begin < 0) z_begin = 0;
+  if (y_end <= 0 || y_end > ny) y_end = ny;
+  if (y_begin < 0) y_begin = 0;
   if (threads < 1) threads = 1;
   const int planes = z_end - z_begin;
-  if (threads > planes) threads = planes > 0 ? planes : 1;
+  const int64_t rows = (int64_t)planes * (y_end - y_begin);
+  if (threads > rows) threads = rows > 0 ? (int)rows : 1;
   exh_job* jobs = (exh_job*)calloc((size_t)threads, sizeof(exh_job));
   pthread_t* tids = (pthread_t*)calloc((size_t)threads, sizeof(pthread_t));
   for (int t = 0; t < threads; ++t) {
@@ -443,8 +449,11 @@ int sxo_exhaustive(const float* vol, int nx, int ny, int nz, double low, double 
     j->radii = radii;
     j->n_radii = nr;
     j->offs = offs;
-    j->z0 = z_begin + (int)((int64_t)planes * t / threads);
-    j->z1 = z_begin + (int)((int64_t)planes * (t + 1) / threads);
+    /* rows are numbered (z - z_begin) * nry + (y - y_begin); offset z by z_begin */
+    j->ry0 = y_begin;
+    j->ry1 = y_end;
+    j->r0 = (int64_t)z_begin * (y_end - y_begin) + rows * t / threads;
+    j->r1 = (int64_t)z_begin * (y_end - y_begin) + rows * (t + 1) / threads;
     j->score = score;
     j->best_scale = best_scale;
     j->binvol = binvol;
@@ -458,7 +467,7 @@ int sxo_exhaustive(const float* vol, int nx, int ny, int nz, double low, double 
   if (visits) { /* pipeline.cpp:118,141: every offset of every radius, OOB included */
     uint64_t per = 0;
     for (int i = 0; i < nr; ++i) per += (uint64_t)offs[i].n;
-    *visits += per * (uint64_t)nx * ny * (uint64_t)planes;
+    *visits += per * (uint64_t)nx * (uint64_t)rows;
   }
   for (int i = 0; i < nr; ++i) free_offsets(&offs[i]);
   free(offs);

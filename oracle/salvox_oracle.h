@@ -55,13 +55,14 @@ int sxo_bin_of(double low, double high, int bins, double intensity);
  * mode 0 = literal (reference loop order, fp64 fl(n/r^2) sums);
  * mode 1 = exact (integer shell sums S_b(r), p_b = S_b/T in fp64).
  * kernel: 0 identity, 1 epanechnikov, 2 gaussian (literal mode only for 2).
- * z_begin/z_end restrict the scored planes (bounded CPU-baseline samples);
- * pass 0, nz for the whole volume. threads >= 1 splits z planes over pthreads.
+ * z_begin/z_end and y_begin/y_end restrict the scored rows (bounded
+ * CPU-baseline samples); pass 0, 0 for the whole range. threads >= 1 splits the
+ * (z, y) rows over pthreads (each voxel is independent: results are identical).
  * Returns 0, or -1 with err (invalid_argument semantics). */
 int sxo_exhaustive(const float* vol, int nx, int ny, int nz, double low, double high, int bins,
                    const double* scales, int n_scales, int kernel, uint64_t budget, int mode,
-                   int threads, int z_begin, int z_end, float* score, float* best_scale,
-                   uint64_t* visits, char* err, int err_len);
+                   int threads, int z_begin, int z_end, int y_begin, int y_end, float* score,
+                   float* best_scale, uint64_t* visits, char* err, int err_len);
 
 /* Exact integer histograms S_b(r) (b = 0..bins-1) and T(r) around one voxel
  * for the identity kernel: S_b(r) = sum over in-bounds offsets o with

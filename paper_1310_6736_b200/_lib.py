@@ -86,10 +86,13 @@ class DetectParams(C.Structure):
 EXPORTS = [
     "salvox_last_error", "salvox_version", "salvox_ctx_create", "salvox_ctx_destroy",
     "salvox_ctx_set_stream", "salvox_ctx_launch_count", "salvox_exhaustive",
-    "salvox_exhaustive_slab", "salvox_exhaustive_device", "salvox_last_maxima",
+    "salvox_exhaustive_slab", "salvox_exhaustive_device", "salvox_exhaustive_slab_device",
+    "salvox_last_maxima",
     "salvox_exhaustive_debug_hist", "salvox_detect", "salvox_detect_batch_device", "salvox_seek",
     "salvox_select", "salvox_dedupe_top_k", "salvox_plan_seeds", "salvox_make_phantom",
 ]
+# include/salvox_bench.h
+BENCH_EXPORTS = ["salvox_probe_smem_peak", "salvox_ctx_set_profiling", "salvox_ctx_kernel_time"]
 
 _lib = None
 _lock = threading.Lock()
@@ -130,6 +133,9 @@ def _declare(L):
                                          _i64, _pi64, _pu64]
     L.salvox_exhaustive_device.argtypes = [_vp, _vp, _i32, _i32, _i32, C.POINTER(Window), _vp,
                                            _i32, _i32, _u64, _vp, _vp, _pi64]
+    L.salvox_exhaustive_slab_device.argtypes = [_vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32,
+                                                _i32, C.POINTER(Window), _vp, _i32, _i32, _u64,
+                                                _vp, _vp, _pi64]
     L.salvox_last_maxima.argtypes = [_vp, _vp, _i64, _pi64]
     L.salvox_exhaustive_debug_hist.argtypes = [_vp, _vp, _i32, _vp, _vp, C.POINTER(_i32)]
     L.salvox_detect.argtypes = [_vp, _vp, _i32, _i32, _i32, C.POINTER(Window),
@@ -144,7 +150,10 @@ def _declare(L):
                                     _i64, _pi64]
     L.salvox_make_phantom.argtypes = [_i32, _i32, _i32, _i32, _dbl, _dbl, _dbl, _i32, _vp, _vp,
                                       _vp, _vp, _vp, _vp, _vp, _vp, _u64, _vp, _vp]
-    for name in EXPORTS:
+    L.salvox_probe_smem_peak.argtypes = [_vp, C.c_int, C.POINTER(_dbl), C.POINTER(_dbl)]
+    L.salvox_ctx_set_profiling.argtypes = [_vp, C.c_int]
+    L.salvox_ctx_kernel_time.argtypes = [_vp, C.POINTER(_dbl), _pi64, C.POINTER(_dbl)]
+    for name in EXPORTS + BENCH_EXPORTS:
         if name not in ("salvox_last_error",):
             getattr(L, name).restype = C.c_int
 
@@ -182,6 +191,21 @@ class Context:
         out = C.c_uint64(0)
         check(load().salvox_ctx_launch_count(self._h, C.byref(out)))
         return int(out.value)
+
+    def set_profiling(self, on: bool):
+        check(load().salvox_ctx_set_profiling(self._h, 1 if on else 0))
+
+    def kernel_time(self):
+        """(kb_kernel ms total, launches, algorithmic updates) since set_profiling(True)."""
+        ms, n, u = C.c_double(0), C.c_int64(0), C.c_double(0)
+        check(load().salvox_ctx_kernel_time(self._h, C.byref(ms), C.byref(n), C.byref(u)))
+        return ms.value, n.value, u.value
+
+    def probe_smem_peak(self, iters: int = 64):
+        """(ATOMS update rate, LDS-only fetch rate) of kb_kernel's inner loop, per second."""
+        a, b = C.c_double(0), C.c_double(0)
+        check(load().salvox_probe_smem_peak(self._h, int(iters), C.byref(a), C.byref(b)))
+        return a.value, b.value
 
     def close(self):
         if self._h:

@@ -113,6 +113,11 @@ struct salvox_ctx {
   cudaStream_t stream = nullptr;
   std::mutex mu;
   uint64_t launches = 0;
+  // kb_kernel timing (salvox_ctx_set_profiling)
+  bool profiling = false;
+  double kb_ms_total = 0.0;
+  int64_t kb_launches = 0;
+  double kb_updates_total = 0.0;
   // exhaustive path
   sx::DevBuf d_vol, d_bins, d_score, d_best, d_keys, d_keys_alt, d_cub, d_counter, d_maxima,
       d_minmax, d_dbg;

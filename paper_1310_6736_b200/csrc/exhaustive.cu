@@ -626,7 +626,25 @@ long long run_exhaustive(salvox_ctx* ctx, const float* d_slab, int nx, int ny, i
   {
     std::lock_guard<std::mutex> lk(g_const_mu);
     upload_tables(ctx, run.pl);
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    if (ctx->profiling) {
+      SX_CUDA(cudaEventCreate(&ev0));
+      SX_CUDA(cudaEventCreate(&ev1));
+      SX_CUDA(cudaEventRecord(ev0, ctx->stream));
+    }
     dispatch_kb<false>(ctx, run.tc, run.map, kp, run.grid, run.smem);
+    if (ctx->profiling) {
+      SX_CUDA(cudaEventRecord(ev1, ctx->stream));
+      SX_CUDA(cudaEventSynchronize(ev1));
+      float ms = 0.f;
+      SX_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
+      cudaEventDestroy(ev0);
+      cudaEventDestroy(ev1);
+      ctx->kb_ms_total += ms;
+      ctx->kb_launches += 1;
+      ctx->kb_updates_total +=
+          (double)nx * ny * (zc1 - zc0) * (double)(run.pl.ball_size.back() - 1);
+    }
     SX_CUDA(cudaEventRecord(g_const_done, ctx->stream));
   }
 
@@ -758,35 +776,56 @@ extern "C" int salvox_exhaustive_slab(salvox_ctx* ctx, const float* slab, int32_
                          budget, score_out, best_scale_out, maxima, cap, n_maxima, visits, true);
 }
 
+static int exhaustive_device_impl(salvox_ctx* ctx, const float* d_slab, int32_t nx, int32_t ny,
+                                  int32_t nz, int32_t zs0, int32_t zs1, int32_t z0, int32_t z1,
+                                  const salvox_window* iw, const double* scales, int32_t n_scales,
+                                  int32_t kernel, uint64_t budget, float* d_score,
+                                  float* d_best_scale, int64_t* n_maxima, bool slab_form) {
+  return guarded([&] {
+    if (!ctx) fail(SALVOX_EINVAL, "null context");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    validate_exhaustive(nx, ny, nz, iw, scales, n_scales, kernel, budget);
+    if (!d_slab) fail(SALVOX_EINVAL, "null volume");
+    if (!(0 <= zs0 && zs0 <= z0 && z0 < z1 && z1 <= zs1 && zs1 <= nz))
+      fail(SALVOX_EINVAL, "exhaustive slab: need 0 <= zs0 <= z0 < z1 <= zs1 <= nz");
+    if (slab_form && iw->full_range)
+      fail(SALVOX_EINVAL, "exhaustive slab: pass an explicit (global) intensity window");
+    SX_CUDA(cudaSetDevice(ctx->device));
+    double low = iw->low, high = iw->high;
+    if (iw->full_range) device_full_range(ctx, d_slab, (size_t)nx * ny * (zs1 - zs0), &low, &high);
+    ExhRun run;
+    const long long cnt = run_exhaustive(ctx, d_slab, nx, ny, nz, zs0, zs1, z0, z1, low, high,
+                                         iw->bins, scales, n_scales, &run);
+    const size_t nown = (size_t)nx * ny * (z1 - z0);
+    const size_t off = (size_t)nx * ny * (z0 - run.kp.zc0);
+    if (d_score)
+      SX_CUDA(cudaMemcpyAsync(d_score, ctx->d_score.as<float>() + off, nown * 4,
+                              cudaMemcpyDeviceToDevice, ctx->stream));
+    if (d_best_scale)
+      SX_CUDA(cudaMemcpyAsync(d_best_scale, ctx->d_best.as<float>() + off, nown * 4,
+                              cudaMemcpyDeviceToDevice, ctx->stream));
+    fetch_maxima(ctx, cnt, nullptr, 0);
+    if (n_maxima) *n_maxima = cnt;
+  });
+}
+
 extern "C" int salvox_exhaustive_device(salvox_ctx* ctx, const float* d_volume, int32_t nx,
                                         int32_t ny, int32_t nz, const salvox_window* iw,
                                         const double* scales, int32_t n_scales, int32_t kernel,
                                         uint64_t budget, float* d_score, float* d_best_scale,
                                         int64_t* n_maxima) {
-  return guarded([&] {
-    if (!ctx) fail(SALVOX_EINVAL, "null context");
-    std::lock_guard<std::mutex> lk(ctx->mu);
-    validate_exhaustive(nx, ny, nz, iw, scales, n_scales, kernel, budget);
-    SX_CUDA(cudaSetDevice(ctx->device));
-    double low = iw->low, high = iw->high;
-    const size_t n = (size_t)nx * ny * nz;
-    if (iw->full_range) device_full_range(ctx, d_volume, n, &low, &high);
-    ExhRun run;
-    const long long cnt = run_exhaustive(ctx, d_volume, nx, ny, nz, 0, nz, 0, nz, low, high,
-                                         iw->bins, scales, n_scales, &run);
-    if (d_score)
-      SX_CUDA(cudaMemcpyAsync(d_score, ctx->d_score.p, n * 4, cudaMemcpyDeviceToDevice, ctx->stream));
-    if (d_best_scale)
-      SX_CUDA(cudaMemcpyAsync(d_best_scale, ctx->d_best.p, n * 4, cudaMemcpyDeviceToDevice,
-                              ctx->stream));
-    SX_CUDA(cudaStreamSynchronize(ctx->stream));
-    ctx->last_maxima.clear();
-    ctx->last_maxima.resize((size_t)cnt);
-    if (cnt > 0)
-      SX_CUDA(cudaMemcpy(ctx->last_maxima.data(), ctx->d_maxima.p, cnt * sizeof(salvox_maximum),
-                         cudaMemcpyDeviceToHost));
-    if (n_maxima) *n_maxima = cnt;
-  });
+  return exhaustive_device_impl(ctx, d_volume, nx, ny, nz, 0, nz, 0, nz, iw, scales, n_scales,
+                                kernel, budget, d_score, d_best_scale, n_maxima, false);
+}
+
+extern "C" int salvox_exhaustive_slab_device(salvox_ctx* ctx, const float* d_slab, int32_t nx,
+                                             int32_t ny, int32_t nz, int32_t zs0, int32_t zs1,
+                                             int32_t z0, int32_t z1, const salvox_window* iw,
+                                             const double* scales, int32_t n_scales,
+                                             int32_t kernel, uint64_t budget, float* d_score,
+                                             float* d_best_scale, int64_t* n_maxima) {
+  return exhaustive_device_impl(ctx, d_slab, nx, ny, nz, zs0, zs1, z0, z1, iw, scales, n_scales,
+                                kernel, budget, d_score, d_best_scale, n_maxima, true);
 }
 
 extern "C" int salvox_last_maxima(salvox_ctx* ctx, salvox_maximum* out, int64_t cap,

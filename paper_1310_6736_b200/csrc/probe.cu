@@ -1,0 +1,138 @@
+// probe.cu -- live roofline denominator for the exhaustive kernel.
+//
+// The exhaustive pass is bound by shared-memory traffic, not HBM or tensor
+// cores, and MEASURED_PEAKS.json has no shared-memory figure,
+// so bench.py measures it here on the same GPU in the same run. The probe runs
+// kb_kernel's inner-loop instruction mix with nothing else: a u8 bin fetched
+// from a shared-memory tile at a warp-uniform constant-table offset (+-o pair)
+// and one ATOMS.ADD into a lane-private column hist[bin][thread]
+// (conflict-free), one 512-thread CTA per SM, 2x33-bin columns like kb_kernel.
+#include "../../include/salvox_bench.h"
+#include "common.cuh"
+
+namespace sx {
+
+constexpr int kProbeTable = 2048;
+__constant__ int4 c_probe[kProbeTable / 4];
+
+template <int NT, int NB, bool ATOMIC>
+__global__ void __launch_bounds__(NT, 1) smem_probe_kernel(int iters, uint32_t* out) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint32_t* hist = reinterpret_cast<uint32_t*>(smem);
+  uint8_t* tile = smem + NB * NT * 4;
+  constexpr int kTile = 76800;  // 48 x 40 x 40, kb_kernel's 3D tile at R = 16
+  const int tid = threadIdx.x;
+  for (int i = tid; i < kTile; i += NT) {
+    uint32_t h = uint32_t(i) * 2654435761u + blockIdx.x;
+    h ^= h >> 15;
+    tile[i] = uint8_t(h % NB);
+  }
+  for (int i = tid; i < NB * NT; i += NT) hist[i] = 0;
+  __syncthreads();
+  const int lx = tid & 7, ly = (tid >> 3) & 7, lz = tid >> 6;
+  const uint8_t* tb = tile + (lz + 16) * 1920 + (ly + 16) * 48 + (lx + 16);
+  uint32_t* hc = hist + tid;
+  uint32_t acc = 0;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll 2
+    for (int e4 = 0; e4 < kProbeTable / 4; ++e4) {
+      const int4 w = c_probe[e4];
+      const int o0 = w.x >> 9, o1 = w.y >> 9, o2 = w.z >> 9, o3 = w.w >> 9;
+      const uint32_t b0 = tb[o0], b1 = tb[-o0], b2 = tb[o1], b3 = tb[-o1];
+      const uint32_t b4 = tb[o2], b5 = tb[-o2], b6 = tb[o3], b7 = tb[-o3];
+      const uint32_t n0 = (uint32_t)w.x & 511u, n1 = (uint32_t)w.y & 511u;
+      const uint32_t n2 = (uint32_t)w.z & 511u, n3 = (uint32_t)w.w & 511u;
+      if (ATOMIC) {
+        atomicAdd(hc + b0 * NT, n0);
+        atomicAdd(hc + b1 * NT, n0);
+        atomicAdd(hc + b2 * NT, n1);
+        atomicAdd(hc + b3 * NT, n1);
+        atomicAdd(hc + b4 * NT, n2);
+        atomicAdd(hc + b5 * NT, n2);
+        atomicAdd(hc + b6 * NT, n3);
+        atomicAdd(hc + b7 * NT, n3);
+      } else {
+        acc += (b0 + b1) * n0 + (b2 + b3) * n1 + (b4 + b5) * n2 + (b6 + b7) * n3;
+      }
+    }
+  }
+  __syncthreads();
+  uint32_t s = acc;
+  for (int b = 0; b < NB; ++b) s += hist[b * NT + tid];
+  out[blockIdx.x * NT + tid] = s;
+}
+
+}  // namespace sx
+
+using namespace sx;
+
+extern "C" int salvox_probe_smem_peak(salvox_ctx* ctx, int iters, double* atoms_updates_per_s,
+                                      double* lds_fetches_per_s) {
+  return guarded([&] {
+    if (!ctx) fail(SALVOX_EINVAL, "null context");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    SX_CUDA(cudaSetDevice(ctx->device));
+    // the same +-o pair encoding as kb_kernel (48 x 40 pitch, R = 16 ball offsets)
+    std::vector<int32_t> tab(kProbeTable);
+    uint32_t s = 12345;
+    for (int k = 0; k < kProbeTable; ++k) {
+      int dx, dy, dz, n;
+      do {
+        s = s * 1664525u + 1013904223u;
+        dx = int((s >> 8) % 33) - 16;
+        dy = int((s >> 16) % 33) - 16;
+        dz = int((s >> 24) % 33) - 16;
+        n = dx * dx + dy * dy + dz * dz;
+      } while (n > 256 || n == 0);
+      const int off = dz * 1920 + dy * 48 + dx;
+      tab[k] = (int32_t)((uint32_t)off << 9 | (uint32_t)n);
+    }
+    SX_CUDA(cudaMemcpyToSymbolAsync(c_probe, tab.data(), tab.size() * 4, 0, cudaMemcpyHostToDevice,
+                                    ctx->stream));
+    constexpr int NT = 512, NB = 33;
+    const size_t smem = (size_t)NB * NT * 4 + 76800;
+    uint32_t* d_out = static_cast<uint32_t*>(ctx->d_dbg.ensure((size_t)ctx->sm_count * 2 * NT * 4));
+    auto run = [&](auto kern, double* rate, double per_iter) {
+      SX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      const int grid = ctx->sm_count * 2;
+      kern<<<grid, NT, smem, ctx->stream>>>(1, d_out);  // warm-up
+      SX_LAUNCH_CHECK(ctx);
+      cudaEvent_t a, b;
+      SX_CUDA(cudaEventCreate(&a));
+      SX_CUDA(cudaEventCreate(&b));
+      SX_CUDA(cudaEventRecord(a, ctx->stream));
+      kern<<<grid, NT, smem, ctx->stream>>>(iters, d_out);
+      SX_LAUNCH_CHECK(ctx);
+      SX_CUDA(cudaEventRecord(b, ctx->stream));
+      SX_CUDA(cudaEventSynchronize(b));
+      float ms = 0.f;
+      SX_CUDA(cudaEventElapsedTime(&ms, a, b));
+      cudaEventDestroy(a);
+      cudaEventDestroy(b);
+      if (rate) *rate = (double)grid * NT * iters * per_iter / (ms * 1e-3);
+    };
+    run(smem_probe_kernel<NT, NB, true>, atoms_updates_per_s, 2.0 * kProbeTable);
+    run(smem_probe_kernel<NT, NB, false>, lds_fetches_per_s, 2.0 * kProbeTable);
+  });
+}
+
+extern "C" int salvox_ctx_set_profiling(salvox_ctx* ctx, int on) {
+  return guarded([&] {
+    if (!ctx) fail(SALVOX_EINVAL, "null context");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    ctx->profiling = on != 0;
+    ctx->kb_ms_total = 0.0;
+    ctx->kb_launches = 0;
+  });
+}
+
+extern "C" int salvox_ctx_kernel_time(salvox_ctx* ctx, double* kb_ms_total, int64_t* kb_launches,
+                                      double* kb_updates_total) {
+  return guarded([&] {
+    if (!ctx) fail(SALVOX_EINVAL, "null context");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (kb_ms_total) *kb_ms_total = ctx->kb_ms_total;
+    if (kb_launches) *kb_launches = ctx->kb_launches;
+    if (kb_updates_total) *kb_updates_total = ctx->kb_updates_total;
+  });
+}
