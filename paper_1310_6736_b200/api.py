@@ -108,7 +108,8 @@ def kadir_brady_exhaustive(volume, scales, window_low=None, window_high=None, bi
 
 
 def kadir_brady_exhaustive_slab(slab, nz_total, zs0, z0, z1, scales, window_low, window_high,
-                                bins=64, kernel="identity", budget=DEFAULT_BUDGET, ctx=None):
+                                bins=64, kernel="identity", budget=DEFAULT_BUDGET, ctx=None,
+                                out=None):
     """z-slab form (salvox_exhaustive_slab): `slab` holds planes [zs0, zs0+len) of a volume
     with nz_total planes; returns owned-plane maps [z0, z1) and global maxima."""
     s = np.ascontiguousarray(slab, dtype=np.float32)
@@ -118,8 +119,13 @@ def kadir_brady_exhaustive_slab(slab, nz_total, zs0, z0, z1, scales, window_low,
     if iw.full_range:
         raise ValueError("exhaustive slab: pass an explicit (global) intensity window")
     c = _ctx(ctx)
-    score = np.empty((z1 - z0, ny, nx), np.float32)
-    best = np.empty((z1 - z0, ny, nx), np.float32)
+    if out is not None:  # caller-provided (e.g. pinned) output planes
+        score, best = out
+        assert score.shape == best.shape == (z1 - z0, ny, nx)
+        assert score.dtype == best.dtype == np.float32 and score.flags.c_contiguous
+    else:
+        score = np.empty((z1 - z0, ny, nx), np.float32)
+        best = np.empty((z1 - z0, ny, nx), np.float32)
     cap = 4096
     maxima = np.empty(cap, MAX_DTYPE)
     n = C.c_int64(0)

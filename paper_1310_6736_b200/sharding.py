@@ -84,12 +84,13 @@ def allgather_maxima(local: np.ndarray, group=None, device=None) -> np.ndarray:
 
 
 def exhaustive_sharded(volume: np.ndarray, scales, window_low, window_high, bins=64,
-                       budget=None, group=None, device=None, compute=None, ctx=None):
+                       budget=None, group=None, device=None, compute=None, ctx=None, out=None):
     """kadir_brady_exhaustive over z-slabs, one per rank.
 
     Returns (owned score planes, owned best_scale planes, (z0, z1), merged maxima,
     visits of this rank). `compute(slab, nz, zs0, z0, z1)` may replace the
-    device call (the CPU multi-process tests inject the oracle there).
+    device call (the CPU multi-process tests inject the oracle there). `out`
+    optionally supplies (score, best) host buffers for the owned planes (e.g. pinned).
     """
     import torch.distributed as dist
 
@@ -111,6 +112,7 @@ def exhaustive_sharded(volume: np.ndarray, scales, window_low, window_high, bins
     else:
         score, best, local, visits = api.kadir_brady_exhaustive_slab(
             vol[zs0:zs1], nz, zs0, z0, z1, scales, window_low, window_high, bins,
-            budget=budget if budget is not None else api.DEFAULT_BUDGET, ctx=ctx)
-    merged = allgather_maxima(local, group, device) if world > 1 else merge_maxima([local])
+            budget=budget if budget is not None else api.DEFAULT_BUDGET, ctx=ctx, out=out)
+    # one rank: the slab call already returns the reference's stable order
+    merged = allgather_maxima(local, group, device) if world > 1 else local
     return score, best, (z0, z1), merged, visits

@@ -1,0 +1,116 @@
+"""Multi-process (world_size 2, gloo, CPU) test of the z-slab sharding host logic:
+slab bounds + halo, the one all-gather of per-slab maxima and the stable merge.
+The per-slab compute is injected (the oracle stands in for the device kernel,
+which cannot run here); the merged result must equal the single-process one."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+from tests import phantoms
+
+SCALES = [2.0, 3.0, 4.0]
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _oracle_slab(vol_full, bins):
+    from oracle import oracle as O
+    from paper_1310_6736_b200 import sharding
+
+    def compute(slab, nz, zs0, z0, z1):
+        # score the planes [z0-1, z1+1) of the slab with the oracle, select maxima of [z0, z1)
+        zc0, zc1 = max(0, z0 - 1), min(nz, z1 + 1)
+        s, b, v = O.exhaustive(slab, 0, bins, bins, SCALES, budget=10**12, mode="exact",
+                               threads=2, z_range=(zc0 - zs0, zc1 - zs0))
+        pos, sc, scale, lin = O.local_maxima(s, b)
+        keep = (pos[:, 2] + zs0 >= z0) & (pos[:, 2] + zs0 < z1)
+        m = np.zeros(int(keep.sum()), sharding.MAX_DTYPE)
+        m["position"] = pos[keep] + [0, 0, zs0]
+        m["score"] = sc[keep]
+        m["scale"] = scale[keep]
+        ny, nx = slab.shape[1:]
+        m["linear_index"] = lin[keep] + zs0 * ny * nx
+        return s[z0 - zs0:z1 - zs0], b[z0 - zs0:z1 - zs0], m, v
+    return compute
+
+
+def _worker(rank, world, port, vol, bins, out):
+    import torch.distributed as dist
+
+    from paper_1310_6736_b200 import sharding
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        s, b, (z0, z1), merged, _ = sharding.exhaustive_sharded(
+            vol, SCALES, 0, bins, bins, compute=_oracle_slab(vol, bins))
+        out[rank] = (z0, z1, s, merged)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_slab_bounds_cover_and_halo():
+    from paper_1310_6736_b200 import sharding
+
+    for nz, world in [(256, 8), (34, 4), (5, 8), (1, 2)]:
+        R = sharding.halo_radius([3.0, 15.0])
+        owned = []
+        for r in range(world):
+            z0, z1, zs0, zs1 = sharding.slab_bounds(nz, world, r, R)
+            owned += list(range(z0, z1))
+            assert zs0 == max(0, z0 - R - 1) and zs1 == min(nz, z1 + R + 1)
+        assert owned == list(range(nz))
+
+
+def test_two_rank_gloo_matches_single_process(oracle):
+    from paper_1310_6736_b200 import sharding
+
+    bins = 16
+    vol, _ = oracle.make_phantom(phantoms.ball_3d(18, (9.0, 8.0, 9.0), 4.0, 21, levels=bins,
+                                                 background={"type": "gaussian", "mean": 4.0,
+                                                             "sigma": 1.5}))
+    s_ref, b_ref, _ = oracle.exhaustive(vol, 0, bins, bins, SCALES, budget=10**12, mode="exact",
+                                        threads=4)
+    pos, sc, scale, lin = oracle.local_maxima(s_ref, b_ref)
+    mgr = mp.Manager()
+    out = mgr.dict()
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, vol, bins, out)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    planes = []
+    for r in range(2):
+        z0, z1, s, merged = out[r]
+        planes.append((z0, s))
+        assert np.array_equal(merged["linear_index"], lin)  # identical on every rank
+        assert np.array_equal(merged["score"], sc)
+        assert np.array_equal(merged["scale"], scale)
+    full = np.concatenate([s for _, s in sorted(planes, key=lambda t: t[0])])
+    assert np.array_equal(full, s_ref)
+
+
+def test_merge_is_stable_order():
+    from paper_1310_6736_b200 import sharding
+
+    a = np.zeros(3, sharding.MAX_DTYPE)
+    a["score"] = [5.0, 3.0, 3.0]
+    a["linear_index"] = [10, 4, 20]
+    b = np.zeros(2, sharding.MAX_DTYPE)
+    b["score"] = [5.0, 3.0]
+    b["linear_index"] = [2, 11]
+    m = sharding.merge_maxima([a, b])
+    assert list(m["linear_index"]) == [2, 10, 4, 11, 20]
