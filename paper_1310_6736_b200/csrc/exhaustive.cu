@@ -109,16 +109,26 @@ void device_full_range(salvox_ctx* ctx, const float* d_vol, size_t n, double* lo
 
 // ----------------------------------------------------------------------------- K2
 struct KbBound {
-  int32_t end;    // end of this radius' segment in the pair table (multiple of 4)
+  int32_t lend;   // end of this radius' run of |o|^2 levels
   int32_t flags;  // bit0: r_i is a scale (entropy); bit1: evaluate scale r_{i-1}
   int32_t rank;   // first position of scale r_{i-1} in the caller's list
-  float scale;    // (float) r_{i-1}
+  uint32_t W;     // sum of |o|^2 over B(r_i) \ {0}: T(r_i) = W - S_0 (bin 0 = outside)
   double fac;     // s * s / 2.0 (pipeline.cpp:131)
+  float scale;    // (float) r_{i-1}
+  int32_t pad_;
 };
 
-constexpr int kMaxPairs = 12288;  // 48 KB of constant memory
+// One |o|^2 level: the +-o representatives with that squared norm are
+// c_offs[start, start + count) (start is a multiple of 4), weight n.
+struct KbLevel {
+  int32_t start, count, n, pad_;
+};
+
+constexpr int kMaxOffs = 12288;   // 48 KB of constant memory
+constexpr int kMaxLevels = 640;
 constexpr int kMaxRadii = 192;
-__constant__ int4 c_pairs[kMaxPairs / 4];
+__constant__ int4 c_offs[kMaxOffs / 4];
+__constant__ KbLevel c_levels[kMaxLevels];
 __constant__ KbBound c_bounds[kMaxRadii];
 
 struct KbParams {
@@ -220,31 +230,44 @@ __global__ void __launch_bounds__(TX* TY* TZ, 1)
   float best_s = 0.f;
   int best_rank = INT_MAX;
 
-  int e4 = 0;  // index into c_pairs (int4 units)
+  // Walk the |o|^2 levels in order; within a level the weight n is loop-invariant
+  // (one register), each table entry is a raw tile offset o giving two updates
+  // (+o and -o): per update one address add, one LDS.U8, one IMAD, one ATOMS.
+  const int4* offs4 = c_offs;
+  int lvl = 0;
   for (int i = 0; i < p.n_radii; ++i) {
     const KbBound bd = c_bounds[i];
-    const int end4 = bd.end >> 2;
+    for (; lvl < bd.lend; ++lvl) {
+      const KbLevel L = c_levels[lvl];
+      const uint32_t n = (uint32_t)L.n;
+      const int g0 = L.start >> 2, g1 = (L.start + L.count) >> 2;
 #pragma unroll 2
-    for (; e4 < end4; ++e4) {
-      const int4 w = c_pairs[e4];
-      const int o0 = w.x >> 9, o1 = w.y >> 9, o2 = w.z >> 9, o3 = w.w >> 9;
-      const uint32_t b0 = tb[o0], b1 = tb[-o0], b2 = tb[o1], b3 = tb[-o1];
-      const uint32_t b4 = tb[o2], b5 = tb[-o2], b6 = tb[o3], b7 = tb[-o3];
-      const uint32_t n0 = (uint32_t)w.x & 511u, n1 = (uint32_t)w.y & 511u;
-      const uint32_t n2 = (uint32_t)w.z & 511u, n3 = (uint32_t)w.w & 511u;
-      atomicAdd(hc + b0 * NT, n0);
-      atomicAdd(hc + b1 * NT, n0);
-      atomicAdd(hc + b2 * NT, n1);
-      atomicAdd(hc + b3 * NT, n1);
-      atomicAdd(hc + b4 * NT, n2);
-      atomicAdd(hc + b5 * NT, n2);
-      atomicAdd(hc + b6 * NT, n3);
-      atomicAdd(hc + b7 * NT, n3);
+      for (int g = g0; g < g1; ++g) {
+        const int4 w = offs4[g];
+        const uint32_t b0 = tb[w.x], b1 = tb[-w.x], b2 = tb[w.y], b3 = tb[-w.y];
+        const uint32_t b4 = tb[w.z], b5 = tb[-w.z], b6 = tb[w.w], b7 = tb[-w.w];
+        atomicAdd(hc + b0 * NT, n);
+        atomicAdd(hc + b1 * NT, n);
+        atomicAdd(hc + b2 * NT, n);
+        atomicAdd(hc + b3 * NT, n);
+        atomicAdd(hc + b4 * NT, n);
+        atomicAdd(hc + b5 * NT, n);
+        atomicAdd(hc + b6 * NT, n);
+        atomicAdd(hc + b7 * NT, n);
+      }
+      const int rem = (L.count & 3);
+      if (rem) {  // tail of the level (entries of the last group, in order)
+        const int4 w = offs4[g1];
+        const int o[3] = {w.x, w.y, w.z};
+        for (int j = 0; j < rem; ++j) {
+          const uint32_t bp = tb[o[j]], bm = tb[-o[j]];
+          atomicAdd(hc + bp * NT, n);
+          atomicAdd(hc + bm * NT, n);
+        }
+      }
     }
-    // ---- boundary: the column now holds S_b(r_i) for b = 1..NB-1 (0 = outside)
-    uint32_t T = 0u;
-#pragma unroll
-    for (int b = 1; b < NB; ++b) T += hc[b * NT];
+    // ---- boundary: the column now holds S_b(r_i) for b = 0..NB-1 (0 = outside)
+    const uint32_t T = bd.W - hc[0];
     const bool doH = (bd.flags & 1) && T > 0u;
     const bool doE = (bd.flags & 2) && T > 0u && TA > 0u && TB > 0u;
     const float invT = doH ? 1.0f / (float)T : 0.f;
@@ -386,7 +409,8 @@ TileCfg pick_tile(int bins, bool two_d) {
 struct Plan {
   std::vector<double> radii;
   std::vector<KbBound> bounds;
-  std::vector<int32_t> pairs;  // packed (tile offset << 9) | n, padded per radius to 4
+  std::vector<int32_t> offs;    // +-o representatives (tile offsets), grouped by level
+  std::vector<KbLevel> levels;  // |o|^2 levels in increasing order
   std::vector<uint64_t> ball_size;  // |B(r_i)| incl. centre (EvalCounter, :118)
   int R = 0;
 };
@@ -465,23 +489,28 @@ Plan make_plan(const double* scales, int n_scales, bool two_d, const TileCfg& tc
     is_scale[ic] = true;
     eval_rank[ih] = std::min(eval_rank[ih], k);
   }
-  int p_at = 0;
   size_t c = 0;
+  uint32_t W = 0;  // running sum of |o|^2 over all members (both signs)
   for (int i = 0; i < NR; ++i) {
-    for (; c < cand.size() && cand[c].n <= Nmax[i]; ++c) {
-      const Off& o = cand[c];
-      const bool rep = o.z > 0 || (o.z == 0 && (o.y > 0 || (o.y == 0 && o.x > 0)));
-      if (!rep) continue;
-      const int off = o.z * SZ + o.y * SY + o.x;
-      pl.pairs.push_back((int32_t)((uint32_t)off << 9 | (uint32_t)o.n));
-      ++p_at;
-    }
-    while (p_at % 4) {  // pad with zero-weight entries (harmless adds of 0)
-      pl.pairs.push_back(0);
-      ++p_at;
+    while (c < cand.size() && cand[c].n <= Nmax[i]) {  // one |o|^2 level
+      const int n = cand[c].n;
+      KbLevel L{};
+      L.start = (int)pl.offs.size();
+      L.n = n;
+      for (; c < cand.size() && cand[c].n == n; ++c) {
+        const Off& o = cand[c];
+        W += (uint32_t)o.n;
+        const bool rep = o.z > 0 || (o.z == 0 && (o.y > 0 || (o.y == 0 && o.x > 0)));
+        if (!rep) continue;
+        pl.offs.push_back(o.z * SZ + o.y * SY + o.x);
+      }
+      L.count = (int)pl.offs.size() - L.start;
+      while (pl.offs.size() % 4) pl.offs.push_back(0);  // next level starts 16-byte aligned
+      pl.levels.push_back(L);
     }
     KbBound b{};
-    b.end = p_at;
+    b.lend = (int)pl.levels.size();
+    b.W = W;
     b.flags = (is_scale[i] ? 1 : 0) | (eval_rank[i] != INT_MAX ? 2 : 0);
     if (eval_rank[i] != INT_MAX) {
       const double s = pl.radii[i - 1];
@@ -491,7 +520,8 @@ Plan make_plan(const double* scales, int n_scales, bool two_d, const TileCfg& tc
     }
     pl.bounds.push_back(b);
   }
-  if ((int)pl.pairs.size() > kMaxPairs) fail(SALVOX_EUNSUPPORTED, "exhaustive (device): table too large");
+  if ((int)pl.offs.size() > kMaxOffs || (int)pl.levels.size() > kMaxLevels)
+    fail(SALVOX_EUNSUPPORTED, "exhaustive (device): offset table too large");
   return pl;
 }
 
@@ -539,8 +569,10 @@ struct ExhRun {
 void upload_tables(salvox_ctx* ctx, const Plan& pl) {
   if (!g_const_done) SX_CUDA(cudaEventCreateWithFlags(&g_const_done, cudaEventDisableTiming));
   SX_CUDA(cudaStreamWaitEvent(ctx->stream, g_const_done, 0));
-  SX_CUDA(cudaMemcpyToSymbolAsync(c_pairs, pl.pairs.data(), pl.pairs.size() * 4, 0,
+  SX_CUDA(cudaMemcpyToSymbolAsync(c_offs, pl.offs.data(), pl.offs.size() * 4, 0,
                                   cudaMemcpyHostToDevice, ctx->stream));
+  SX_CUDA(cudaMemcpyToSymbolAsync(c_levels, pl.levels.data(), pl.levels.size() * sizeof(KbLevel),
+                                  0, cudaMemcpyHostToDevice, ctx->stream));
   SX_CUDA(cudaMemcpyToSymbolAsync(c_bounds, pl.bounds.data(), pl.bounds.size() * sizeof(KbBound),
                                   0, cudaMemcpyHostToDevice, ctx->stream));
 }
