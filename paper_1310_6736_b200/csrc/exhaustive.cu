@@ -29,6 +29,7 @@
 #include <array>
 #include <climits>
 #include <cmath>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -119,12 +120,15 @@ struct KbBound {
 };
 
 // One |o|^2 level: the +-o representatives with that squared norm are
-// c_offs[start, start + count) (start is a multiple of 4), weight n.
+// c_offs[start, start + count) (start is a multiple of 4), weight n. The pair
+// kernel splits a level by the parity of o.x: list 0 (even) and list 1 (odd).
 struct KbLevel {
-  int32_t start, count, n, pad_;
+  int32_t start0, start1;
+  int16_t count0, count1;
+  int32_t n;
 };
 
-constexpr int kMaxOffs = 12288;   // 48 KB of constant memory
+constexpr int kMaxOffs = 10240;   // 40 KB of constant memory
 constexpr int kMaxLevels = 640;
 constexpr int kMaxRadii = 192;
 __constant__ int4 c_offs[kMaxOffs / 4];
@@ -240,7 +244,7 @@ __global__ void __launch_bounds__(TX* TY* TZ, 1)
     for (; lvl < bd.lend; ++lvl) {
       const KbLevel L = c_levels[lvl];
       const uint32_t n = (uint32_t)L.n;
-      const int g0 = L.start >> 2, g1 = (L.start + L.count) >> 2;
+      const int g0 = L.start0 >> 2, g1 = (L.start0 + L.count0) >> 2;
 #pragma unroll 2
       for (int g = g0; g < g1; ++g) {
         const int4 w = offs4[g];
@@ -255,7 +259,7 @@ __global__ void __launch_bounds__(TX* TY* TZ, 1)
         atomicAdd(hc + b6 * NT, n);
         atomicAdd(hc + b7 * NT, n);
       }
-      const int rem = (L.count & 3);
+      const int rem = (L.count0 & 3);
       if (rem) {  // tail of the level (entries of the last group, in order)
         const int4 w = offs4[g1];
         const int o[3] = {w.x, w.y, w.z};
@@ -313,6 +317,235 @@ __global__ void __launch_bounds__(TX* TY* TZ, 1)
     const size_t o = ((size_t)(gz - p.zc0) * p.ny + gy) * p.nx + gx;
     p.score[o] = (float)best;
     p.best[o] = best_s;
+  }
+}
+
+__device__ __forceinline__ void pair_atom(uint32_t saddr, uint32_t n) {
+  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(saddr), "r"(n) : "memory");
+}
+
+// K2' (NB <= 33): two x-adjacent voxels per thread. One LDS.U16 fetches both
+// voxels' bins for an offset: even x-offsets read the TMA tile (A), odd ones a
+// one-byte-shifted copy (B[k] = A[k+1], built in shared memory after the TMA
+// load), so every fetch is 2-byte aligned and bin fetches cost 0.5 wavefront
+// per update instead of 1 (the ATOMS.ADD per update is the irreducible part).
+// Each |o|^2 level is split by o.x parity so the copy choice is loop-invariant.
+// Warp footprint 8 voxels (4 threads) x 8 rows at a 48-byte row pitch: the 8
+// rows' 2-3-word spans fall in disjoint banks.
+template <int NB, int TY, int TZ, bool DBG>
+__global__ void __launch_bounds__(4 * TY * TZ, 1)
+    kb_pair_kernel(const __grid_constant__ CUtensorMap tmap, const KbParams p) {
+  constexpr int TX = 8;
+  constexpr int NT = 4 * TY * TZ;  // threads
+  constexpr int NC = 2 * NT;       // histogram columns (voxels)
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint32_t* hist = reinterpret_cast<uint32_t*>(smem);
+  uint8_t* tileA = smem + NB * NC * 4;
+  const uint32_t tstride = (p.tile_bytes + 127u) & ~127u;
+  uint8_t* tileB = tileA + tstride;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(tileB + tstride);
+  const int tid = threadIdx.x;
+
+  int tx0, ty0, tz0;
+  long long dbg_lin = -1;
+  if (DBG) {
+    dbg_lin = p.dbg_vox[blockIdx.x];
+    const int vx = (int)(dbg_lin % p.nx);
+    const int vy = (int)((dbg_lin / p.nx) % p.ny);
+    const int vz = (int)(dbg_lin / ((long long)p.nx * p.ny));
+    tx0 = vx / TX * TX;
+    ty0 = vy / TY * TY;
+    tz0 = p.zc0 + (vz - p.zc0) / TZ * TZ;
+  } else {
+    tx0 = blockIdx.x * TX;
+    ty0 = blockIdx.y * TY;
+    tz0 = p.zc0 + blockIdx.z * TZ;
+  }
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int xs = tx0 - p.R;
+  const int xa = xs - (((xs % 16) + 16) % 16);
+  const int delta = xs - xa;
+  if (tid == 0) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(p.tile_bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(tileA)),
+        "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(xa), "r"(ty0 - p.R),
+        "r"(tz0 - p.Rz - p.zs0), "r"(smem_u32(bar))
+        : "memory");
+  }
+  {
+    uint4* h4 = reinterpret_cast<uint4*>(hist);
+    for (int i = tid; i < NB * NC / 4; i += NT) h4[i] = make_uint4(0u, 0u, 0u, 0u);
+  }
+  {
+    uint32_t done = 0;
+    while (!done) {
+      asm volatile(
+          "{ .reg .pred q; mbarrier.try_wait.parity.shared::cta.b64 q, [%1], 0; selp.u32 %0, 1, 0, q; }"
+          : "=r"(done)
+          : "r"(smem_u32(bar))
+          : "memory");
+    }
+  }
+  {  // B[k] = A[k + 1]: funnel-shift 16-byte chunks
+    const uint32_t* a32 = reinterpret_cast<const uint32_t*>(tileA);
+    uint4* b4 = reinterpret_cast<uint4*>(tileB);
+    const int nchunk = (int)(p.tile_bytes + 15u) / 16;
+    for (int i = tid; i < nchunk; i += NT) {
+      const uint4 v = reinterpret_cast<const uint4*>(tileA)[i];
+      const uint32_t nx4 = (4 * i + 4) * 4 < (int)tstride ? a32[4 * i + 4] : 0u;
+      b4[i] = make_uint4(__funnelshift_r(v.x, v.y, 8), __funnelshift_r(v.y, v.z, 8),
+                         __funnelshift_r(v.z, v.w, 8), __funnelshift_r(v.w, nx4, 8));
+    }
+  }
+  __syncthreads();
+  const int lxp = tid & 3, ly = (tid >> 2) % TY, lz = tid / (4 * TY);
+  const int gx = tx0 + 2 * lxp, gy = ty0 + ly, gz = tz0 + lz;
+  const bool valid0 = gx < p.nx && gy < p.ny && gz < p.zc1;
+  const bool valid1 = valid0 && gx + 1 < p.nx;
+  if (!valid0) return;
+  const long long lin0 = (long long)gx + (long long)p.nx * ((long long)gy + (long long)p.ny * gz);
+  const int dbg_which = DBG ? (lin0 == dbg_lin ? 0 : (valid1 && lin0 + 1 == dbg_lin ? 1 : -1)) : 0;
+  if (DBG && dbg_which < 0) return;
+  const uint8_t* tbA = tileA + (lz + p.Rz) * p.SZ + (ly + p.R) * p.SY + (2 * lxp + p.R + delta);
+  const uint8_t* tbB = tbA + (tstride - 1);  // odd x-offset s: B[s - 1] = (A[s], A[s + 1])
+  uint32_t* h0 = hist + tid;
+  uint32_t* h1 = hist + NT + tid;
+  // shared-window byte addresses: column c of bin b lives at hbase + b * NC * 4 + c * 4
+  // (NC * 4 = 2^11 and the column offset < 2^11, so the bin field can be OR-ed in)
+  static_assert(NC * 4 == 2048, "pair kernel assumes 512 columns");
+  const uint32_t hs0 = smem_u32(h0), hs1 = smem_u32(h1);
+
+  uint32_t A0[NB], B0[NB], A1[NB], B1[NB];
+#pragma unroll
+  for (int b = 0; b < NB; ++b) A0[b] = B0[b] = A1[b] = B1[b] = 0u;
+  uint32_t TA0 = 0u, TB0 = 0u, TA1 = 0u, TB1 = 0u;
+  float Hb0 = 0.f, Hb1 = 0.f;
+  double best0 = 0.0, best1 = 0.0;
+  float bs0 = 0.f, bs1 = 0.f;
+  int br0 = INT_MAX, br1 = INT_MAX;
+
+  const int4* offs4 = c_offs;
+  auto run_list = [&](const uint8_t* tb, int start, int count, uint32_t n) {
+    const int g0 = start >> 2, g1 = (start + count) >> 2;
+#pragma unroll 2
+    for (int g = g0; g < g1; ++g) {
+      const int4 w = offs4[g];
+      const uint32_t vs[8] = {*reinterpret_cast<const uint16_t*>(tb + w.x),
+                              *reinterpret_cast<const uint16_t*>(tb - w.x),
+                              *reinterpret_cast<const uint16_t*>(tb + w.y),
+                              *reinterpret_cast<const uint16_t*>(tb - w.y),
+                              *reinterpret_cast<const uint16_t*>(tb + w.z),
+                              *reinterpret_cast<const uint16_t*>(tb - w.z),
+                              *reinterpret_cast<const uint16_t*>(tb + w.w),
+                              *reinterpret_cast<const uint16_t*>(tb - w.w)};
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        pair_atom(hs0 + (__byte_perm(vs[j], 0u, 0x4440) << 11), n);
+        pair_atom(hs1 + (__byte_perm(vs[j], 0u, 0x4441) << 11), n);
+      }
+    }
+    const int rem = count & 3;
+    if (rem) {
+      const int4 w = offs4[g1];
+      const int o[3] = {w.x, w.y, w.z};
+      for (int j = 0; j < rem; ++j) {
+        const uint32_t vp = *reinterpret_cast<const uint16_t*>(tb + o[j]);
+        const uint32_t vm = *reinterpret_cast<const uint16_t*>(tb - o[j]);
+        pair_atom(hs0 + (__byte_perm(vp, 0u, 0x4440) << 11), n);
+        pair_atom(hs1 + (__byte_perm(vp, 0u, 0x4441) << 11), n);
+        pair_atom(hs0 + (__byte_perm(vm, 0u, 0x4440) << 11), n);
+        pair_atom(hs1 + (__byte_perm(vm, 0u, 0x4441) << 11), n);
+      }
+    }
+  };
+
+  int lvl = 0;
+  for (int i = 0; i < p.n_radii; ++i) {
+    const KbBound bd = c_bounds[i];
+    for (; lvl < bd.lend; ++lvl) {
+      const KbLevel L = c_levels[lvl];
+      run_list(tbA, L.start0, L.count0, (uint32_t)L.n);
+      run_list(tbB, L.start1, L.count1, (uint32_t)L.n);
+    }
+    // ---- boundary: both columns hold S_b(r_i)
+    const uint32_t T0 = bd.W - h0[0], T1 = bd.W - h1[0];
+    const bool doH0 = (bd.flags & 1) && T0 > 0u, doH1 = (bd.flags & 1) && T1 > 0u;
+    const bool doE0 = (bd.flags & 2) && T0 > 0u && TA0 > 0u && TB0 > 0u;
+    const bool doE1 = (bd.flags & 2) && T1 > 0u && TA1 > 0u && TB1 > 0u;
+    const float invT0 = doH0 ? 1.0f / (float)T0 : 0.f;
+    const float invT1 = doH1 ? 1.0f / (float)T1 : 0.f;
+    float hacc0 = 0.f, hacc1 = 0.f;
+    unsigned long long num0 = 0ull, num1 = 0ull;
+#pragma unroll
+    for (int b = 1; b < NB; ++b) {
+      const uint32_t c0 = h0[b * NC], c1 = h1[b * NC];
+      if (doH0 && c0) {
+        const float pb = (float)c0 * invT0;
+        const float lg = (2u * c0 > T0) ? log1pf(-(float)(T0 - c0) * invT0) * 1.4426950408889634f
+                                        : __log2f(pb);
+        hacc0 -= pb * lg;
+      }
+      if (doH1 && c1) {
+        const float pb = (float)c1 * invT1;
+        const float lg = (2u * c1 > T1) ? log1pf(-(float)(T1 - c1) * invT1) * 1.4426950408889634f
+                                        : __log2f(pb);
+        hacc1 -= pb * lg;
+      }
+      if (doE0) {
+        const unsigned long long x = (unsigned long long)c0 * TA0, y = (unsigned long long)A0[b] * T0;
+        num0 += x > y ? x - y : y - x;
+      }
+      if (doE1) {
+        const unsigned long long x = (unsigned long long)c1 * TA1, y = (unsigned long long)A1[b] * T1;
+        num1 += x > y ? x - y : y - x;
+      }
+      if (DBG && b - 1 < p.bins)
+        p.dbg_out[(size_t)i * (p.bins + 1) + (b - 1)] = dbg_which == 0 ? c0 : c1;
+      A0[b] = B0[b];
+      B0[b] = c0;
+      A1[b] = B1[b];
+      B1[b] = c1;
+    }
+    if (DBG) p.dbg_out[(size_t)i * (p.bins + 1) + p.bins] = dbg_which == 0 ? T0 : T1;
+    if (doE0) {
+      const double y = ((double)Hb0 * bd.fac) * ((double)num0 / ((double)T0 * (double)TA0));
+      if (y > best0 || (y == best0 && y > 0.0 && bd.rank < br0)) {
+        best0 = y;
+        bs0 = bd.scale;
+        br0 = bd.rank;
+      }
+    }
+    if (doE1) {
+      const double y = ((double)Hb1 * bd.fac) * ((double)num1 / ((double)T1 * (double)TA1));
+      if (y > best1 || (y == best1 && y > 0.0 && bd.rank < br1)) {
+        best1 = y;
+        bs1 = bd.scale;
+        br1 = bd.rank;
+      }
+    }
+    TA0 = TB0;
+    TB0 = T0;
+    TA1 = TB1;
+    TB1 = T1;
+    Hb0 = doH0 ? fmaxf(hacc0, 0.f) : 0.f;
+    Hb1 = doH1 ? fmaxf(hacc1, 0.f) : 0.f;
+  }
+  if (!DBG) {
+    const size_t o = ((size_t)(gz - p.zc0) * p.ny + gy) * p.nx + gx;
+    p.score[o] = (float)best0;
+    p.best[o] = bs0;
+    if (valid1) {
+      p.score[o + 1] = (float)best1;
+      p.best[o + 1] = bs1;
+    }
   }
 }
 
@@ -396,12 +629,29 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 struct TileCfg {
   int nb, tx, ty, tz;
+  bool pair;  // kb_pair_kernel (two voxels per thread, tx = 8)
 };
 
 TileCfg pick_tile(int bins, bool two_d) {
   const int nb = bins <= 16 ? 17 : (bins <= 32 ? 33 : 65);
-  if (two_d) return nb == 65 ? TileCfg{65, 32, 8, 1} : TileCfg{nb, 32, 16, 1};
-  return nb == 65 ? TileCfg{65, 8, 8, 4} : TileCfg{nb, 8, 8, 8};
+  if (nb == 65) return two_d ? TileCfg{65, 32, 8, 1, false} : TileCfg{65, 8, 8, 4, false};
+  // Default: one voxel per thread (kb_kernel, 16 warps/SM, 79-80 ms at C2).
+  // SALVOX_KB_PAIR=1 selects kb_pair_kernel: 25% fewer shared-memory wavefronts
+  // per update but 247 registers -> 8 warps/SM, latency-bound (86 ms at C2, r01).
+  static const int mode = [] {
+    const char* e = std::getenv("SALVOX_KB_PAIR");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (mode == 0) return two_d ? TileCfg{nb, 32, 16, 1, false} : TileCfg{nb, 8, 8, 8, false};
+  return two_d ? TileCfg{nb, 8, 64, 1, true} : TileCfg{nb, 8, 8, 8, true};
+}
+
+// Dynamic shared memory of one CTA: histogram columns, tile(s), mbarrier.
+size_t kb_smem(const TileCfg& tc, uint32_t tile_bytes) {
+  const size_t voxels = (size_t)tc.tx * tc.ty * tc.tz;
+  if (tc.pair)
+    return (size_t)tc.nb * voxels * 4 + 2 * (((size_t)tile_bytes + 127) & ~(size_t)127) + 16;
+  return (size_t)tc.nb * voxels * 4 + (((size_t)tile_bytes + 15) & ~(size_t)15) + 16;
 }
 
 // Offsets of make_sphere_offsets (pipeline.cpp:37-52) for every needed radius,
@@ -442,7 +692,9 @@ Plan make_plan(const double* scales, int n_scales, bool two_d, const TileCfg& tc
   const int R = pl.R;
   int dmax = 0;  // worst shift of the 16-byte-aligned box start (see kb_kernel)
   for (int k = 0; k < 16; ++k) dmax = std::max(dmax, (((tc.tx * k - R) % 16) + 16) % 16);
-  const int BX = ((tc.tx + 2 * R + dmax) + 15) / 16 * 16;
+  int BX = ((tc.tx + 2 * R + dmax) + 15) / 16 * 16;
+  if (tc.pair) BX = 48;  // 12-word pitch: conflict-free 8-row warp footprint (kb_pair_kernel)
+  if (tc.tx + 2 * R + dmax > BX) fail(SALVOX_EUNSUPPORTED, "exhaustive (device): halo too wide");
   const int BY = tc.ty + 2 * R;
   const int SY = BX, SZ = BX * BY;
   *SYo = SY;
@@ -494,18 +746,28 @@ Plan make_plan(const double* scales, int n_scales, bool two_d, const TileCfg& tc
   for (int i = 0; i < NR; ++i) {
     while (c < cand.size() && cand[c].n <= Nmax[i]) {  // one |o|^2 level
       const int n = cand[c].n;
-      KbLevel L{};
-      L.start = (int)pl.offs.size();
-      L.n = n;
+      std::vector<int> lists[2];
       for (; c < cand.size() && cand[c].n == n; ++c) {
         const Off& o = cand[c];
         W += (uint32_t)o.n;
         const bool rep = o.z > 0 || (o.z == 0 && (o.y > 0 || (o.y == 0 && o.x > 0)));
         if (!rep) continue;
-        pl.offs.push_back(o.z * SZ + o.y * SY + o.x);
+        lists[tc.pair ? (o.x & 1) : 0].push_back(o.z * SZ + o.y * SY + o.x);
       }
-      L.count = (int)pl.offs.size() - L.start;
-      while (pl.offs.size() % 4) pl.offs.push_back(0);  // next level starts 16-byte aligned
+      KbLevel L{};
+      L.n = n;
+      for (int k = 0; k < 2; ++k) {
+        const int st = (int)pl.offs.size();
+        for (int v : lists[k]) pl.offs.push_back(v);
+        while (pl.offs.size() % 4) pl.offs.push_back(0);  // next list starts 16-byte aligned
+        if (k == 0) {
+          L.start0 = st;
+          L.count0 = (int16_t)lists[0].size();
+        } else {
+          L.start1 = st;
+          L.count1 = (int16_t)lists[1].size();
+        }
+      }
       pl.levels.push_back(L);
     }
     KbBound b{};
@@ -543,7 +805,7 @@ template <bool DBG>
 void dispatch_kb(salvox_ctx* ctx, const TileCfg& tc, const CUtensorMap& map, const KbParams& kp,
                  dim3 grid, size_t smem) {
 #define SX_KB(NB, TX, TY, TZ)                                             \
-  if (tc.nb == NB && tc.tx == TX && tc.ty == TY && tc.tz == TZ) {         \
+  if (!tc.pair && tc.nb == NB && tc.tx == TX && tc.ty == TY && tc.tz == TZ) { \
     launch_kb<NB, TX, TY, TZ, DBG>(ctx, map, kp, grid, smem);             \
     return;                                                               \
   }
@@ -554,6 +816,19 @@ void dispatch_kb(salvox_ctx* ctx, const TileCfg& tc, const CUtensorMap& map, con
   SX_KB(33, 32, 16, 1)
   SX_KB(65, 32, 8, 1)
 #undef SX_KB
+#define SX_KP(NB, TY, TZ)                                                                    \
+  if (tc.pair && tc.nb == NB && tc.ty == TY && tc.tz == TZ) {                                \
+    auto k = kb_pair_kernel<NB, TY, TZ, DBG>;                                                \
+    SX_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    k<<<grid, 4 * TY * TZ, smem, ctx->stream>>>(map, kp);                                    \
+    SX_LAUNCH_CHECK(ctx);                                                                    \
+    return;                                                                                  \
+  }
+  SX_KP(17, 8, 8)
+  SX_KP(33, 8, 8)
+  SX_KP(17, 64, 1)
+  SX_KP(33, 64, 1)
+#undef SX_KP
   fail(SALVOX_EUNSUPPORTED, "exhaustive (device): no kernel for this tile configuration");
 }
 
@@ -651,8 +926,7 @@ long long run_exhaustive(salvox_ctx* ctx, const float* d_slab, int nx, int ny, i
   kp.best = d_best;
   kp.dbg_vox = nullptr;
   kp.dbg_out = nullptr;
-  const int NT = run.tc.tx * run.tc.ty * run.tc.tz;
-  run.smem = (size_t)run.tc.nb * NT * 4 + ((kp.tile_bytes + 15u) & ~15u) + 16;
+  run.smem = kb_smem(run.tc, kp.tile_bytes);
   run.grid = dim3((nx + run.tc.tx - 1) / run.tc.tx, (ny + run.tc.ty - 1) / run.tc.ty,
                   (zc1 - zc0 + run.tc.tz - 1) / run.tc.tz);
   {
@@ -922,8 +1196,7 @@ extern "C" int salvox_exhaustive_debug_hist(salvox_ctx* ctx, const int64_t* voxe
     uint32_t* d_out = reinterpret_cast<uint32_t*>(d_vox + n);
     SX_CUDA(cudaMemcpyAsync(d_vox, voxels, (size_t)n * 8, cudaMemcpyHostToDevice, ctx->stream));
     SX_CUDA(cudaMemsetAsync(d_out, 0, (size_t)n * NR * (st.bins + 1) * 4, ctx->stream));
-    const int NT = run.tc.tx * run.tc.ty * run.tc.tz;
-    const size_t smem = (size_t)run.tc.nb * NT * 4 + ((kp.tile_bytes + 15u) & ~15u) + 16;
+    const size_t smem = kb_smem(run.tc, kp.tile_bytes);
     std::lock_guard<std::mutex> lk2(g_const_mu);
     upload_tables(ctx, run.pl);
     for (int i = 0; i < n; ++i) {  // one block per voxel, each writes its own slice
