@@ -1,0 +1,163 @@
+// The hot-path entry points of the C++ API, forwarded to the B200 C-ABI
+// (reference src/pipeline.cpp:63-183, :311-402; src/seeds.cpp:7-45).
+#include "salvox/pipeline.hpp"
+
+#include <algorithm>
+
+#include "salvox/device.hpp"
+#include "salvox_capi.h"
+
+namespace salvox {
+
+namespace {
+salvox_ctx* ctx() { return device_context(current_device()); }
+
+salvox_detection to_c(const Detection& d) {
+  salvox_detection c{};
+  for (int i = 0; i < 3; ++i) c.center[i] = d.center[i];
+  for (int r = 0; r < 3; ++r)
+    for (int k = 0; k < 3; ++k) c.H[r * 3 + k] = d.H(r, k);
+  c.entropy_bits = d.entropy_bits;
+  c.pdf_diff = d.pdf_diff;
+  c.bhattacharyya = d.bhattacharyya;
+  c.iterations = d.iterations;
+  c.flags = d.flags;
+  c.seed_index = d.seed_index;
+  return c;
+}
+}  // namespace
+
+Detection from_c(const salvox_detection& c) {
+  Detection d;
+  d.center = Eigen::Vector3d(c.center[0], c.center[1], c.center[2]);
+  for (int r = 0; r < 3; ++r)
+    for (int k = 0; k < 3; ++k) d.H(r, k) = c.H[r * 3 + k];
+  d.entropy_bits = c.entropy_bits;
+  d.pdf_diff = c.pdf_diff;
+  d.bhattacharyya = c.bhattacharyya;
+  d.iterations = c.iterations;
+  d.flags = c.flags;
+  d.seed_index = c.seed_index;
+  return d;
+}
+
+Method method_from_name(const std::string& name) {
+  if (name == "quadrant") return Method::Quadrant;
+  if (name == "shift") return Method::Shift;
+  if (name == "abmsod") return Method::Abmsod;
+  if (name == "octant") return Method::Octant;
+  throw std::invalid_argument("unknown method '" + name + "'");
+}
+
+const char* method_name(Method m) {
+  switch (m) {
+    case Method::Quadrant: return "quadrant";
+    case Method::Shift: return "shift";
+    case Method::Abmsod: return "abmsod";
+    case Method::Octant: return "octant";
+  }
+  return "?";
+}
+
+std::vector<Seed> plan_seeds(const Volume& v, const SeedPlan& plan) {
+  plan.validate();
+  const int mode = plan.mode == SeedPlan::Mode::Lattice ? 0 : 1;
+  int64_t n = 0;
+  check_status(salvox_plan_seeds(v.nx(), v.ny(), v.nz(), mode, plan.spacing, plan.count,
+                                 plan.scales.data(), int(plan.scales.size()), plan.rng_seed,
+                                 nullptr, nullptr, 0, &n));
+  std::vector<double> pos(static_cast<size_t>(n) * 3), sc(static_cast<size_t>(n));
+  check_status(salvox_plan_seeds(v.nx(), v.ny(), v.nz(), mode, plan.spacing, plan.count,
+                                 plan.scales.data(), int(plan.scales.size()), plan.rng_seed,
+                                 pos.data(), sc.data(), n, &n));
+  std::vector<Seed> out(static_cast<size_t>(n));
+  for (int64_t i = 0; i < n; ++i)
+    out[size_t(i)] = {Eigen::Vector3d(pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]), sc[size_t(i)],
+                      int(i)};
+  return out;
+}
+
+ExhaustiveResult kadir_brady_exhaustive(const Volume& v, const IntensityWindow& iw,
+                                        const std::vector<double>& scales, Kernel kernel,
+                                        EvalCounter* counter, uint64_t budget) {
+  ExhaustiveResult res;
+  res.map.dims = Eigen::Vector3i(v.nx(), v.ny(), v.nz());
+  res.map.score.resize(v.size());
+  res.map.best_scale.resize(v.size());
+  const salvox_window w{iw.low, iw.high, iw.bins, 0};
+  int64_t n = 0;
+  uint64_t visits = 0;
+  salvox_ctx* c = ctx();
+  check_status(salvox_exhaustive(c, v.data().data(), v.nx(), v.ny(), v.nz(), &w, scales.data(),
+                                 int(scales.size()), int(kernel), budget, res.map.score.data(),
+                                 res.map.best_scale.data(), nullptr, 0, &n, &visits));
+  std::vector<salvox_maximum> mx(static_cast<size_t>(n));
+  if (n > 0) check_status(salvox_last_maxima(c, mx.data(), n, &n));
+  res.maxima.reserve(size_t(n));
+  for (const salvox_maximum& m : mx)
+    res.maxima.push_back(
+        {Eigen::Vector3d(m.position[0], m.position[1], m.position[2]), m.score, m.scale});
+  if (counter) counter->add(visits);
+  return res;
+}
+
+std::vector<Detection> dedupe_top_k(std::vector<Detection> dets, int k, double radius) {
+  std::vector<salvox_detection> in(dets.size()), out(dets.size() + 1);
+  std::transform(dets.begin(), dets.end(), in.begin(), to_c);
+  int64_t n = 0;
+  check_status(salvox_dedupe_top_k(ctx(), in.data(), int64_t(in.size()), k, radius, out.data(), &n));
+  std::vector<Detection> kept;
+  for (int64_t i = 0; i < n; ++i) kept.push_back(from_c(out[size_t(i)]));
+  return kept;
+}
+
+std::vector<Detection> detect(const Volume& v, const IntensityWindow& iw, DetectParams params,
+                              EvalCounter* counter) {
+  if (params.method == Method::Quadrant && !v.is_2d())
+    throw std::invalid_argument("detect: quadrant method requires a 2D volume (nz == 1)");
+  params.seeds.validate();
+  if (params.method == Method::Abmsod)
+    throw unsupported_error("detect (device): abmsod is outside the accelerated path");
+  if (params.method == Method::Shift) params.shift.validate();
+  salvox_detect_params p{};
+  p.method = params.method == Method::Quadrant ? SALVOX_METHOD_QUADRANT
+             : params.method == Method::Shift  ? SALVOX_METHOD_SHIFT
+                                               : SALVOX_METHOD_OCTANT;
+  p.seed_mode = params.seeds.mode == SeedPlan::Mode::Lattice ? 0 : 1;
+  p.seed_spacing = params.seeds.spacing;
+  p.seed_count = params.seeds.count;
+  p.top_k = params.top_k;
+  p.rng_seed = params.seeds.rng_seed;
+  p.scales = params.seeds.scales.data();
+  p.n_scales = int(params.seeds.scales.size());
+  p.workers = int(params.workers);
+  p.dedupe_radius = params.dedupe_radius;
+  p.entropy_quantile = params.entropy_quantile;
+  p.pdf_quantile = params.pdf_quantile;
+  p.quadrant_eta = params.quadrant.eta;
+  p.quadrant_max_iters = params.quadrant.max_iters;
+  p.n_quadrant_scales = int(params.quadrant.scale_range.size());
+  p.quadrant_scales = params.quadrant.scale_range.data();
+  p.shift_min_step = params.shift.min_step;
+  p.shift_max_iters = params.shift.max_iters;
+  p.shift_step_kernel = int(params.shift.step_kernel);
+  p.shift_hist_kernel = int(params.shift.hist_kernel);
+  p.shift_min_inbounds_fraction = params.shift.min_inbounds_fraction;
+  std::vector<double> target;
+  if (params.shift.target) {
+    target = params.shift.target->p;
+    p.shift_target = target.data();
+  }
+  const salvox_window w{iw.low, iw.high, iw.bins, 0};
+  std::vector<salvox_detection> out(size_t(std::max(params.top_k, 1)));
+  int64_t n_out = 0, n_seed = 0;
+  uint64_t visits = 0;
+  check_status(salvox_detect(ctx(), v.data().data(), v.nx(), v.ny(), v.nz(), &w, &p, out.data(),
+                             int64_t(out.size()), &n_out, nullptr, 0, &n_seed, &visits));
+  if (counter) counter->add(visits);
+  std::vector<Detection> dets;
+  for (int64_t i = 0; i < n_out; ++i) dets.push_back(from_c(out[size_t(i)]));
+  return dets;
+}
+
+}  // namespace salvox

@@ -1,0 +1,166 @@
+// salvox-b200: command-line driver of the B200 drop-in (mirrors the reference's
+// tools/main.cpp "detect" and "phantom" subcommands, plus "exhaustive").
+//   salvox-b200 detect --volume V.mhd --out R.json [--config C.json] [--method M]
+//                      [--window LOW:HIGH] [--bins N] [--seeds lattice:S|random:N]
+//                      [--scales a,b,c] [--k K] [--dedupe-radius R] [--workers W]
+//                      [--rng-seed S] [--entropy-quantile Q] [--pdf-quantile Q]
+//   salvox-b200 phantom SPEC.json OUT.mhd
+//   salvox-b200 exhaustive --volume V.mhd --scales a,b --out MAXIMA.json [--window L:H]
+//                          [--bins N] [--budget B]
+// Exit codes: 0 success, 1 config/IO/device error, 2 detect found nothing.
+#include <chrono>
+#include <cstdio>
+#include <iostream>
+#include <map>
+#include <string>
+
+#include "../src/json_min.hpp"
+#include "salvox/config.hpp"
+#include "salvox/meta_io.hpp"
+#include "salvox/phantom.hpp"
+#include "salvox/pipeline.hpp"
+#include "salvox/report.hpp"
+
+using namespace salvox;
+
+namespace {
+
+std::map<std::string, std::string> parse_flags(int argc, char** argv, int first) {
+  std::map<std::string, std::string> f;
+  for (int i = first; i < argc; ++i) {
+    std::string a = argv[i];
+    if (a.rfind("--", 0) != 0) throw std::invalid_argument("unexpected argument '" + a + "'");
+    if (i + 1 >= argc) throw std::invalid_argument("flag " + a + " needs a value");
+    f[a.substr(2)] = argv[++i];
+  }
+  return f;
+}
+
+std::vector<double> parse_list(const std::string& s) {
+  std::vector<double> out;
+  size_t p = 0;
+  while (p <= s.size()) {
+    const size_t c = s.find(',', p);
+    out.push_back(std::stod(s.substr(p, c == std::string::npos ? std::string::npos : c - p)));
+    if (c == std::string::npos) break;
+    p = c + 1;
+  }
+  return out;
+}
+
+RunConfig resolve(const std::map<std::string, std::string>& f) {
+  RunConfig cfg;
+  auto has = [&](const char* k) { return f.count(k) > 0; };
+  if (has("config")) cfg = RunConfig::from_json_text(read_file(f.at("config")));
+  if (has("method")) cfg.method = f.at("method");
+  if (has("volume")) cfg.volume_path = f.at("volume");
+  if (has("window")) {
+    const std::string w = f.at("window");
+    const auto c = w.find(':');
+    if (c == std::string::npos) throw std::invalid_argument("--window expects LOW:HIGH");
+    cfg.window_low = std::stod(w.substr(0, c));
+    cfg.window_high = std::stod(w.substr(c + 1));
+  }
+  if (has("bins")) cfg.bins = std::stoi(f.at("bins"));
+  if (has("seeds")) {
+    const std::string s = f.at("seeds");
+    const auto c = s.find(':');
+    if (c == std::string::npos)
+      throw std::invalid_argument("--seeds expects lattice:SPACING or random:COUNT");
+    if (s.substr(0, c) == "lattice") {
+      cfg.seed_mode = "lattice";
+      cfg.seed_spacing = std::stod(s.substr(c + 1));
+    } else if (s.substr(0, c) == "random") {
+      cfg.seed_mode = "random";
+      cfg.seed_count = std::stoi(s.substr(c + 1));
+    } else {
+      throw std::invalid_argument("--seeds mode must be lattice or random");
+    }
+  }
+  if (has("scales")) cfg.scales = parse_list(f.at("scales"));
+  if (has("k")) cfg.top_k = std::stoi(f.at("k"));
+  if (has("dedupe-radius")) cfg.dedupe_radius = std::stod(f.at("dedupe-radius"));
+  if (has("workers")) cfg.workers = unsigned(std::stoi(f.at("workers")));
+  if (has("rng-seed")) cfg.rng_seed = std::stoull(f.at("rng-seed"));
+  if (has("out")) cfg.out_path = f.at("out");
+  if (has("entropy-quantile")) cfg.entropy_quantile = std::stod(f.at("entropy-quantile"));
+  if (has("pdf-quantile")) cfg.pdf_quantile = std::stod(f.at("pdf-quantile"));
+  cfg.validate();
+  return cfg;
+}
+
+int cmd_detect(const std::map<std::string, std::string>& f) {
+  const RunConfig cfg = resolve(f);
+  if (cfg.volume_path.empty()) throw std::invalid_argument("detect: --volume is required");
+  if (cfg.out_path.empty()) throw std::invalid_argument("detect: --out is required");
+  const Volume v = load_volume(cfg.volume_path);
+  const auto t0 = std::chrono::steady_clock::now();
+  const auto dets = detect(v, cfg.intensity_window(v), cfg.detect_params());
+  const double ms =
+      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  write_file_atomic(cfg.out_path, detection_report_json(cfg, v, dets, ms));
+  size_t usable = 0;
+  for (const auto& d : dets) usable += d.has(kFlagDegenerate) ? 0 : 1;
+  std::cerr << "detect: " << usable << " detection(s) written to " << cfg.out_path << "\n";
+  return usable > 0 ? 0 : 2;
+}
+
+int cmd_exhaustive(const std::map<std::string, std::string>& f) {
+  RunConfig cfg = resolve(f);
+  if (cfg.volume_path.empty() || cfg.out_path.empty())
+    throw std::invalid_argument("exhaustive: --volume and --out are required");
+  const Volume v = load_volume(cfg.volume_path);
+  const uint64_t budget = f.count("budget") ? std::stoull(f.at("budget")) : 2'000'000ull;
+  EvalCounter counter;
+  const auto res = kadir_brady_exhaustive(v, cfg.intensity_window(v), cfg.scales,
+                                          Kernel::Identity, &counter, budget);
+  json::Value j = json::Value::object();
+  j.set("visits", json::Value::number(double(counter.count())));
+  json::Value arr = json::Value::array();
+  for (const auto& m : res.maxima) {
+    json::Value mj = json::Value::object();
+    json::Value p = json::Value::array();
+    for (int i = 0; i < 3; ++i) p.push(json::Value::number(m.position[i]));
+    mj.set("position", p);
+    mj.set("score", json::Value::number(m.score));
+    mj.set("scale", json::Value::number(m.scale));
+    arr.push(mj);
+  }
+  j.set("maxima", arr);
+  write_file_atomic(cfg.out_path, json::dump(j, 1) + "\n");
+  std::cerr << "exhaustive: " << res.maxima.size() << " maxima written to " << cfg.out_path << "\n";
+  return 0;
+}
+
+int cmd_phantom(const std::string& spec_path, const std::string& out_path) {
+  const auto [v, gt] = make_phantom(PhantomSpec::from_json_text(read_file(spec_path)));
+  save_volume(v, out_path);
+  std::filesystem::path gt_path(out_path);
+  gt_path.replace_extension(".gt.json");
+  write_file_atomic(gt_path, gt.to_json_text());
+  std::cerr << "phantom: wrote " << out_path << " and " << gt_path.string() << "\n";
+  return 0;
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+  if (argc < 2) {
+    std::cerr << "usage: salvox-b200 {detect|exhaustive|phantom} ...\n";
+    return 1;
+  }
+  const std::string cmd = argv[1];
+  try {
+    if (cmd == "detect") return cmd_detect(parse_flags(argc, argv, 2));
+    if (cmd == "exhaustive") return cmd_exhaustive(parse_flags(argc, argv, 2));
+    if (cmd == "phantom") {
+      if (argc != 4) throw std::invalid_argument("usage: salvox-b200 phantom SPEC.json OUT.mhd");
+      return cmd_phantom(argv[2], argv[3]);
+    }
+    std::cerr << "unknown subcommand '" << cmd << "'\n";
+    return 1;
+  } catch (const std::exception& e) {
+    std::cerr << "error: " << e.what() << "\n";
+    return 1;
+  }
+}

@@ -216,6 +216,25 @@ SALVOX_API int salvox_seek(salvox_ctx* ctx, const float* volume, int32_t nx, int
                 const double* seed_half_extents, const int32_t* seed_index, int64_t n,
                 salvox_detection* out, uint64_t* visits);
 
+/* Raw ascent trajectories: quadrant_seek / quadrant_seek_one (quadrant.hpp:64-76,
+ * src/quadrant.cpp:83-125; dims = 2, nz must be 1) or the NEW octant ascent
+ * (dims = 3). scales = QuadrantParams::scale_range (strictly increasing);
+ * seeds hold 3 doubles each. No post-scoring (unlike salvox_detect). */
+typedef struct {
+  double position[3];
+  double entropy_bits; /* entropy of the highest-entropy quadrant/octant window */
+  int32_t best_scale;  /* its argmax scale */
+  int32_t iterations;
+  int32_t converged;
+  int32_t degenerate;
+} salvox_ascent_result;
+
+SALVOX_API int salvox_ascent_seek(salvox_ctx* ctx, const float* volume, int32_t nx, int32_t ny,
+                                  int32_t nz, const salvox_window* iw, int32_t dims,
+                                  const int32_t* scales, int32_t n_scales, double eta,
+                                  int32_t max_iters, const double* seeds, int64_t n,
+                                  salvox_ascent_result* out, uint64_t* visits);
+
 /* Thresholds + dedupe (pipeline.cpp:383-401, :54-59, :168-183) on the device. */
 SALVOX_API int salvox_select(salvox_ctx* ctx, const salvox_detection* dets, int64_t n, double q_entropy,
                   double q_pdf, int32_t k, double radius, salvox_detection* out,

@@ -35,6 +35,10 @@ DET_DTYPE = np.dtype(
         ("reserved", "<i4"),
     ]
 )
+ASCENT_DTYPE = np.dtype(
+    [("position", "<f8", (3,)), ("entropy_bits", "<f8"), ("best_scale", "<i4"),
+     ("iterations", "<i4"), ("converged", "<i4"), ("degenerate", "<i4")]
+)
 MAX_DTYPE = np.dtype(
     [("position", "<f8", (3,)), ("score", "<f8"), ("scale", "<f8"), ("linear_index", "<i8")]
 )
@@ -90,6 +94,7 @@ EXPORTS = [
     "salvox_last_maxima",
     "salvox_exhaustive_debug_hist", "salvox_detect", "salvox_detect_batch_device", "salvox_seek",
     "salvox_select", "salvox_dedupe_top_k", "salvox_plan_seeds", "salvox_make_phantom",
+    "salvox_ascent_seek",
 ]
 # include/salvox_bench.h
 BENCH_EXPORTS = ["salvox_probe_smem_peak", "salvox_ctx_set_profiling", "salvox_ctx_kernel_time"]
@@ -144,6 +149,8 @@ def _declare(L):
                                              C.POINTER(DetectParams), _vp, _i64, _vp, _pu64]
     L.salvox_seek.argtypes = [_vp, _vp, _i32, _i32, _i32, C.POINTER(Window),
                               C.POINTER(DetectParams), _vp, _vp, _vp, _vp, _i64, _vp, _pu64]
+    L.salvox_ascent_seek.argtypes = [_vp, _vp, _i32, _i32, _i32, C.POINTER(Window), _i32, _vp,
+                                     _i32, _dbl, _i32, _vp, _i64, _vp, _pu64]
     L.salvox_select.argtypes = [_vp, _vp, _i64, _dbl, _dbl, _i32, _dbl, _vp, _pi64]
     L.salvox_dedupe_top_k.argtypes = [_vp, _vp, _i64, _i32, _dbl, _vp, _pi64]
     L.salvox_plan_seeds.argtypes = [_i32, _i32, _i32, _i32, _dbl, _i32, _vp, _i32, _u64, _vp, _vp,

@@ -268,17 +268,30 @@ def saliency_shift(volume, seed, half_extents, window_low=None, window_high=None
 
 def quadrant_seek(volume, seeds, scale_range, window_low=None, window_high=None, bins=64, eta=0.5,
                   max_iters=50, ctx=None, octant=False):
-    """quadrant_seek (quadrant.hpp:73-76); octant=True runs the 3D octant ascent.
-    Returns DET_DTYPE records: center, iterations, converged/degenerate flags,
-    post-scored entropy / Bhattacharyya / pdf_diff as detect() fills them."""
+    """quadrant_seek (quadrant.hpp:73-76, quadrant.cpp:83-125) on the device; octant=True
+    runs the 3D octant ascent. Returns ASCENT_DTYPE records (position, entropy_bits and
+    best_scale of the highest-entropy window, iterations, converged, degenerate) and the
+    EvalCounter visits."""
+    from ._lib import ASCENT_DTYPE
+
+    v, nx, ny, nz = _volume(volume)
     s = np.asarray(seeds, np.float64)
+    if s.ndim == 1:
+        s = s[None]
     if s.shape[-1] == 2:
         s = np.concatenate([s, np.zeros(s.shape[:-1] + (1,))], axis=-1)
-    d, visits = seek_records(volume, s, method="octant" if octant else "quadrant",
-                             window_low=window_low, window_high=window_high, bins=bins, ctx=ctx,
-                             quadrant_scales=list(scale_range), quadrant_eta=eta,
-                             quadrant_max_iters=max_iters)
-    return d
+    s = np.ascontiguousarray(s)
+    if len(s) == 0:
+        raise ValueError("quadrant_seek: no seeds")  # quadrant.cpp:290
+    iw = _window(window_low, window_high, bins)
+    sr = np.ascontiguousarray(scale_range, np.int32)
+    out = np.empty(len(s), ASCENT_DTYPE)
+    visits = C.c_uint64(0)
+    check(_lib.load().salvox_ascent_seek(_ctx(ctx).handle, ptr(v), nx, ny, nz, C.byref(iw),
+                                         3 if octant else 2, ptr(sr), len(sr), float(eta),
+                                         int(max_iters), ptr(s), len(s), ptr(out),
+                                         C.byref(visits)))
+    return out, int(visits.value)
 
 
 def select(dets, entropy_quantile=0.9, pdf_quantile=0.0, k=20, dedupe_radius=5.0, ctx=None):

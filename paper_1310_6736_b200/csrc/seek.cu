@@ -69,6 +69,8 @@ struct SeekParams {
   int n_seeds;
   salvox_detection* out;
   unsigned long long* visits;
+  salvox_ascent_result* ascent_out;  // raw ascent results (salvox_ascent_seek), nullable
+  int post_score;                    // ascent: score the converged window (detect)
 };
 
 struct WarpScratch {
@@ -521,9 +523,28 @@ __global__ void __launch_bounds__(256) ascent_kernel(const SeekParams P) {
   d.center[0] = p[0];
   d.center[1] = p[1];
   d.center[2] = two_d ? 0.0 : p[2];
+  if (P.ascent_out && lane == 0) {  // quadrant_seek_one's result (quadrant.cpp:276-282)
+    salvox_ascent_result r;
+    r.position[0] = p[0];
+    r.position[1] = p[1];
+    r.position[2] = p[2];
+    r.iterations = iters;
+    r.converged = converged;
+    r.degenerate = degenerate;
+    r.best_scale = 0;
+    r.entropy_bits = 0.0;
+    if (!degenerate) {
+      int bq = 0;
+      for (int q = 1; q < nq; ++q)
+        if (last_e[q] > last_e[bq]) bq = q;
+      r.best_scale = last_k[bq];
+      r.entropy_bits = last_e[bq];
+    }
+    P.ascent_out[seed] = r;
+  }
   if (degenerate) {
     d.flags |= SALVOX_FLAG_DEGENERATE;
-  } else {
+  } else if (P.post_score) {
     int bq = 0;
     for (int q = 1; q < nq; ++q)
       if (last_e[q] > last_e[bq]) bq = q;
@@ -716,6 +737,8 @@ void build_job(int nx, int ny, int nz, const salvox_detect_params* prm,
       fail(SALVOX_EUNSUPPORTED, "ascent (device): at most 64 scales in [0, 128]");
     P.max_iters = prm->quadrant_max_iters;
     P.eta = prm->quadrant_eta;
+    P.post_score = 1;
+    P.ascent_out = nullptr;
     P.n_ascent = (int)ks.size();
     for (size_t i = 0; i < ks.size(); ++i) P.ascent_scales[i] = ks[i];
     for (int k = 0; k <= 128; ++k) P.geom_of_k[k] = 0;
@@ -1031,6 +1054,58 @@ extern "C" int salvox_seek(salvox_ctx* ctx, const float* volume, int32_t nx, int
     run_seek(ctx, job, d_bins, iw->bins, d_q, d_all, d_vis);
     SX_CUDA(cudaMemcpyAsync(out, d_all, (size_t)n * sizeof(salvox_detection), cudaMemcpyDeviceToHost,
                             ctx->stream));
+    const unsigned long long v = sum_visits(ctx, d_vis, (int)n);
+    if (visits) *visits += v;
+  });
+}
+
+extern "C" int salvox_ascent_seek(salvox_ctx* ctx, const float* volume, int32_t nx, int32_t ny,
+                                  int32_t nz, const salvox_window* iw, int32_t dims,
+                                  const int32_t* scales, int32_t n_scales, double eta,
+                                  int32_t max_iters, const double* seeds, int64_t n,
+                                  salvox_ascent_result* out, uint64_t* visits) {
+  return guarded([&] {
+    if (!ctx) fail(SALVOX_EINVAL, "null context");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (nx < 1 || ny < 1 || nz < 1) fail(SALVOX_EINVAL, "Volume: dims must be >= 1");
+    if (dims != 2 && dims != 3) fail(SALVOX_EINVAL, "ascent: dims must be 2 or 3");
+    if (dims == 2 && nz != 1)
+      fail(SALVOX_EINVAL, "quadrant_step: volume must be 2D (nz == 1)");  // quadrant.cpp:42
+    check_window(iw);
+    if (n < 0 || (n > 0 && (!seeds || !out))) fail(SALVOX_EINVAL, "bad seed arrays");
+    salvox_detect_params prm{};
+    prm.method = dims == 2 ? SALVOX_METHOD_QUADRANT : SALVOX_METHOD_OCTANT;
+    prm.quadrant_scales = scales;
+    prm.n_quadrant_scales = n_scales;
+    prm.quadrant_eta = eta;
+    prm.quadrant_max_iters = max_iters;
+    if (n_scales < 1 || !scales) fail(SALVOX_EINVAL, "quadrant: empty scale range");
+    std::vector<SeedRec> recs((size_t)n);
+    std::vector<int> index((size_t)n);
+    for (int64_t i = 0; i < n; ++i) {
+      std::memcpy(recs[i].pos, seeds + 3 * i, 3 * sizeof(double));
+      recs[i].scale = 0.0;
+      index[i] = (int)i;
+    }
+    SeekJob job;
+    build_job(nx, ny, nz, &prm, recs, index, job);
+    if (n == 0) return;
+    SX_CUDA(cudaSetDevice(ctx->device));
+    const size_t nv = (size_t)nx * ny * nz;
+    float* d_vol = static_cast<float*>(ctx->d_seek_vol.ensure(nv * 4));
+    SX_CUDA(cudaMemcpyAsync(d_vol, volume, nv * 4, cudaMemcpyHostToDevice, ctx->stream));
+    double* d_q = nullptr;
+    const uint8_t* d_bins = prepare_volume(ctx, d_vol, nx, ny, nz, iw, nullptr, nullptr, &d_q);
+    char* d_dets = static_cast<char*>(ctx->d_dets.ensure(
+        (size_t)(n + 1) * (sizeof(salvox_detection) + 8 + sizeof(salvox_ascent_result)) + 1024));
+    salvox_detection* d_all = reinterpret_cast<salvox_detection*>(d_dets);
+    unsigned long long* d_vis = reinterpret_cast<unsigned long long*>(d_all + (n + 1));
+    salvox_ascent_result* d_res = reinterpret_cast<salvox_ascent_result*>(d_vis + (n + 1));
+    job.P.post_score = 0;
+    job.P.ascent_out = d_res;
+    run_seek(ctx, job, d_bins, iw->bins, d_q, d_all, d_vis);
+    SX_CUDA(cudaMemcpyAsync(out, d_res, (size_t)n * sizeof(salvox_ascent_result),
+                            cudaMemcpyDeviceToHost, ctx->stream));
     const unsigned long long v = sum_visits(ctx, d_vis, (int)n);
     if (visits) *visits += v;
   });

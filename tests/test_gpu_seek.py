@@ -131,3 +131,31 @@ def test_select_matches_oracle(sx, oracle):
     pair["pdf_diff"] = [1.0, 2.0]
     out = sx.dedupe_top_k(pair, 20, 5.0)
     assert len(out) == 1 and out[0]["pdf_diff"] == 2.0
+
+
+def test_raw_quadrant_and_octant_seek_match_oracle(sx, oracle):
+    """salvox_ascent_seek == quadrant_seek_one (quadrant.cpp:83-114), bit for bit."""
+    vol, _ = oracle.make_phantom(phantoms.square_2d(96, 40.0, 47.0, 10, 64, 57))
+    seeds = [[32.0, 44.0], [60.5, 50.25], [5.0, 90.0], [47.0, 47.0]]
+    res, visits = sx.quadrant_seek(vol, seeds, [4, 6, 10], 0, 64, 64, max_iters=8)
+    oracle.set_log_mode(1)
+    try:
+        rv = 0
+        for r, s in zip(res, seeds):
+            ref = oracle.ascent_seek_one(vol, 0, 64, 64, s, [4, 6, 10], max_iters=8)
+            assert np.array_equal(r["position"], ref["position"])
+            assert r["best_scale"] == ref["best_scale"] and r["iterations"] == ref["iterations"]
+            assert r["entropy_bits"] == ref["entropy_bits"]
+            assert bool(r["converged"]) == ref["converged"]
+            assert bool(r["degenerate"]) == ref["degenerate"]
+        vol3, _ = oracle.make_phantom(phantoms.cube_3d(48, 7, 71))
+        seeds3 = [[30.0, 28.0, 20.0], [10.0, 12.0, 40.0], [23.5, 23.5, 23.5]]
+        res3, _ = sx.quadrant_seek(vol3, seeds3, [3, 6, 9], 0, 64, 64, octant=True)
+        for r, s in zip(res3, seeds3):
+            ref = oracle.ascent_seek_one(vol3, 0, 64, 64, s, [3, 6, 9], dims=3)
+            assert np.array_equal(r["position"], ref["position"])
+            assert r["best_scale"] == ref["best_scale"] and r["entropy_bits"] == ref["entropy_bits"]
+    finally:
+        oracle.set_log_mode(0)
+    with pytest.raises(ValueError, match="must be 2D"):
+        sx.quadrant_seek(np.zeros((4, 8, 8), np.float32), [[2.0, 2.0]], [2], 0, 64, 64)
