@@ -12,10 +12,12 @@ extern "C" {
 /* Peak rate of kb_kernel's inner-loop pair (u8 bin fetch from a shared tile at
  * a warp-uniform offset + one ATOMS.ADD into a lane-private column), measured
  * by a microkernel with the identical instruction mix and occupancy:
- * *atoms_updates_per_s (the exhaustive roofline denominator) and
- * *lds_fetches_per_s (bin fetches alone, no histogram update). */
+ * *atoms_updates_per_s (the exhaustive roofline denominator),
+ * *lds_fetches_per_s (bin fetches alone, no histogram update) and
+ * *atoms_only_per_s (ATOMS.ADD alone with register-resident bins: the
+ * one-atomic-per-update floor of any shared-memory histogram design). */
 SALVOX_API int salvox_probe_smem_peak(salvox_ctx* ctx, int iters, double* atoms_updates_per_s,
-                                      double* lds_fetches_per_s);
+                                      double* lds_fetches_per_s, double* atoms_only_per_s);
 
 /* Times every exhaustive kb_kernel launch with CUDA events on the launching
  * stream while on (resets the accumulators). */

@@ -157,7 +157,8 @@ def _declare(L):
                                     _i64, _pi64]
     L.salvox_make_phantom.argtypes = [_i32, _i32, _i32, _i32, _dbl, _dbl, _dbl, _i32, _vp, _vp,
                                       _vp, _vp, _vp, _vp, _vp, _vp, _u64, _vp, _vp]
-    L.salvox_probe_smem_peak.argtypes = [_vp, C.c_int, C.POINTER(_dbl), C.POINTER(_dbl)]
+    L.salvox_probe_smem_peak.argtypes = [_vp, C.c_int, C.POINTER(_dbl), C.POINTER(_dbl),
+                                         C.POINTER(_dbl)]
     L.salvox_ctx_set_profiling.argtypes = [_vp, C.c_int]
     L.salvox_ctx_kernel_time.argtypes = [_vp, C.POINTER(_dbl), _pi64, C.POINTER(_dbl)]
     for name in EXPORTS + BENCH_EXPORTS:
@@ -209,10 +210,11 @@ class Context:
         return ms.value, n.value, u.value
 
     def probe_smem_peak(self, iters: int = 64):
-        """(ATOMS update rate, LDS-only fetch rate) of kb_kernel's inner loop, per second."""
-        a, b = C.c_double(0), C.c_double(0)
-        check(load().salvox_probe_smem_peak(self._h, int(iters), C.byref(a), C.byref(b)))
-        return a.value, b.value
+        """(LDS.U8+ATOMS pair rate, LDS-only rate, ATOMS-only rate) per second."""
+        a, b, c = C.c_double(0), C.c_double(0), C.c_double(0)
+        check(load().salvox_probe_smem_peak(self._h, int(iters), C.byref(a), C.byref(b),
+                                            C.byref(c)))
+        return a.value, b.value, c.value
 
     def close(self):
         if self._h:

@@ -549,6 +549,220 @@ __global__ void __launch_bounds__(4 * TY * TZ, 1)
   }
 }
 
+// K2'' (3D, NB <= 33): 1024 threads per CTA (32 warps/SM, twice kb_kernel's
+// latency hiding) with the two radius snapshots held in TENSOR MEMORY. At 1024
+// threads the register file allows 64 registers per thread, too few for the
+// 2 x 32 snapshot words, so each thread parks them in its TMEM lane: warp w
+// owns lanes 32*(w%4).. and the 64-column slice 64*(w/4); columns [0,32) and
+// [32,64) of the slice are the two ring slots (bins 1..32). At each radius the
+// older slot is streamed out with tcgen05.ld (8 columns at a time), combined
+// with the live shared-memory column (L1 term), and overwritten in place with
+// the live column by tcgen05.st -- it becomes the newest snapshot.
+__device__ __forceinline__ void tm_ld8(uint32_t taddr, uint32_t* r) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                 "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+}
+__device__ __forceinline__ void tm_st8(uint32_t taddr, const uint32_t* r) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
+               "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]),
+               "r"(r[7])
+               : "memory");
+}
+
+template <int NB, bool DBG>
+__global__ void __launch_bounds__(1024, 1)
+    kb_tmem_kernel(const __grid_constant__ CUtensorMap tmap, const KbParams p) {
+  constexpr int TX = 16, TY = 8, TZ = 8, NT = 1024;
+  constexpr int NS = NB - 1;  // snapshot bins (1..NB-1); multiple of 8
+  static_assert(NS % 8 == 0 && 2 * NS <= 64, "TMEM slice is 64 columns per thread");
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint32_t* hist = reinterpret_cast<uint32_t*>(smem);
+  uint8_t* tile = smem + NB * NT * 4;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(tile + ((p.tile_bytes + 15u) & ~15u));
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 1);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  int tx0, ty0, tz0;
+  long long dbg_lin = -1;
+  if (DBG) {
+    dbg_lin = p.dbg_vox[blockIdx.x];
+    const int vx = (int)(dbg_lin % p.nx);
+    const int vy = (int)((dbg_lin / p.nx) % p.ny);
+    const int vz = (int)(dbg_lin / ((long long)p.nx * p.ny));
+    tx0 = vx / TX * TX;
+    ty0 = vy / TY * TY;
+    tz0 = p.zc0 + (vz - p.zc0) / TZ * TZ;
+  } else {
+    tx0 = blockIdx.x * TX;
+    ty0 = blockIdx.y * TY;
+    tz0 = p.zc0 + blockIdx.z * TZ;
+  }
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {  // all 512 TMEM columns: one CTA per SM (shared memory bound)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     smem_u32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tbase = *tmem_slot;
+  const int xs = tx0 - p.R;
+  const int xa = xs - (((xs % 16) + 16) % 16);
+  const int delta = xs - xa;
+  if (tid == 0) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(p.tile_bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(tile)),
+        "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(xa), "r"(ty0 - p.R),
+        "r"(tz0 - p.Rz - p.zs0), "r"(smem_u32(bar))
+        : "memory");
+  }
+  {
+    uint4* h4 = reinterpret_cast<uint4*>(hist);
+    for (int i = tid; i < NB * NT / 4; i += NT) h4[i] = make_uint4(0u, 0u, 0u, 0u);
+  }
+  {
+    uint32_t done = 0;
+    while (!done) {
+      asm volatile(
+          "{ .reg .pred q; mbarrier.try_wait.parity.shared::cta.b64 q, [%1], 0; selp.u32 %0, 1, 0, q; }"
+          : "=r"(done)
+          : "r"(smem_u32(bar))
+          : "memory");
+    }
+  }
+  __syncthreads();
+  // warp footprint 8 (x) x 4 (y): lane -> (x, y); warps tile 2 (x) x 2 (y) x 8 (z)
+  const int lx = (lane & 7) + 8 * (warp & 1);
+  const int ly = (lane >> 3) + 4 * ((warp >> 1) & 1);
+  const int lz = warp >> 2;
+  const int gx = tx0 + lx, gy = ty0 + ly, gz = tz0 + lz;
+  const bool valid = gx < p.nx && gy < p.ny && gz < p.zc1;
+  const bool dbg_me =
+      DBG && valid && ((long long)gx + (long long)p.nx * ((long long)gy + (long long)p.ny * gz)) == dbg_lin;
+  // invalid threads keep walking (their tile bytes exist) so the warp-wide
+  // tcgen05.ld/st stay converged; they just never store a result
+  const uint8_t* tb = tile + (lz + p.Rz) * p.SZ + (ly + p.R) * p.SY + (lx + p.R + delta);
+  uint32_t* hc = hist + tid;
+  const uint32_t lane_base = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(64 * (warp >> 2));
+  uint32_t slotA = lane_base, slotB = lane_base + NS;  // A: older, B: newer
+
+  {  // zero both TMEM slots (snapshots of "radius 0")
+    uint32_t z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+    for (int c = 0; c < 2 * NS; c += 8) tm_st8(lane_base + c, z);
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  uint32_t TA = 0u, TB = 0u;
+  float Hb = 0.f;
+  double best = 0.0;
+  float best_s = 0.f;
+  int best_rank = INT_MAX;
+
+  const int4* offs4 = c_offs;
+  int lvl = 0;
+  for (int i = 0; i < p.n_radii; ++i) {
+    const KbBound bd = c_bounds[i];
+    for (; lvl < bd.lend; ++lvl) {
+      const KbLevel L = c_levels[lvl];
+      const uint32_t n = (uint32_t)L.n;
+      const int g0 = L.start0 >> 2, g1 = (L.start0 + L.count0) >> 2;
+#pragma unroll 2
+      for (int g = g0; g < g1; ++g) {
+        const int4 w = offs4[g];
+        const uint32_t b0 = tb[w.x], b1 = tb[-w.x], b2 = tb[w.y], b3 = tb[-w.y];
+        const uint32_t b4 = tb[w.z], b5 = tb[-w.z], b6 = tb[w.w], b7 = tb[-w.w];
+        atomicAdd(hc + b0 * NT, n);
+        atomicAdd(hc + b1 * NT, n);
+        atomicAdd(hc + b2 * NT, n);
+        atomicAdd(hc + b3 * NT, n);
+        atomicAdd(hc + b4 * NT, n);
+        atomicAdd(hc + b5 * NT, n);
+        atomicAdd(hc + b6 * NT, n);
+        atomicAdd(hc + b7 * NT, n);
+      }
+      const int rem = (L.count0 & 3);
+      if (rem) {
+        const int4 w = offs4[g1];
+        const int o[3] = {w.x, w.y, w.z};
+        for (int j = 0; j < rem; ++j) {
+          const uint32_t bp = tb[o[j]], bm = tb[-o[j]];
+          atomicAdd(hc + bp * NT, n);
+          atomicAdd(hc + bm * NT, n);
+        }
+      }
+    }
+    // ---- boundary
+    const uint32_t T = bd.W - hc[0];
+    const bool doH = (bd.flags & 1) && T > 0u;
+    const bool doE = (bd.flags & 2) && T > 0u && TA > 0u && TB > 0u;
+    const float invT = doH ? 1.0f / (float)T : 0.f;
+    float hacc = 0.f;
+    unsigned long long num = 0ull;
+#pragma unroll
+    for (int c = 0; c < NS; c += 8) {
+      uint32_t a[8], cur[8];
+      tm_ld8(slotA + c, a);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) cur[j] = hc[(1 + c + j) * NT];
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t cv = cur[j];
+        if (doH && cv) {
+          const float pb = (float)cv * invT;
+          const float lg = (2u * cv > T) ? log1pf(-(float)(T - cv) * invT) * 1.4426950408889634f
+                                         : __log2f(pb);
+          hacc -= pb * lg;
+        }
+        if (doE) {
+          const unsigned long long x = (unsigned long long)cv * TA, y = (unsigned long long)a[j] * T;
+          num += x > y ? x - y : y - x;
+        }
+        if (DBG && dbg_me && c + j < p.bins) p.dbg_out[(size_t)i * (p.bins + 1) + c + j] = cv;
+      }
+      tm_st8(slotA + c, cur);  // the older slot becomes the newest snapshot
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    if (DBG && dbg_me) p.dbg_out[(size_t)i * (p.bins + 1) + p.bins] = T;
+    if (doE) {
+      const double y = ((double)Hb * bd.fac) * ((double)num / ((double)T * (double)TA));
+      if (y > best || (y == best && y > 0.0 && bd.rank < best_rank)) {
+        best = y;
+        best_s = bd.scale;
+        best_rank = bd.rank;
+      }
+    }
+    const uint32_t t = slotA;
+    slotA = slotB;
+    slotB = t;
+    TA = TB;
+    TB = T;
+    Hb = doH ? fmaxf(hacc, 0.f) : 0.f;
+  }
+  if (!DBG && valid) {
+    const size_t o = ((size_t)(gz - p.zc0) * p.ny + gy) * p.nx + gx;
+    p.score[o] = (float)best;
+    p.best[o] = best_s;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tbase) : "memory");
+  }
+}
+
 // ----------------------------------------------------------------------------- K3
 __global__ void maxima_kernel(const float* __restrict__ score, int nx, int ny, int nz, int zc0,
                               int z0, int z1, unsigned long long* keys, unsigned int* counter) {
@@ -629,21 +843,25 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 struct TileCfg {
   int nb, tx, ty, tz;
-  bool pair;  // kb_pair_kernel (two voxels per thread, tx = 8)
+  bool pair;          // kb_pair_kernel (two voxels per thread, tx = 8)
+  bool tmem = false;  // kb_tmem_kernel (1024 threads, snapshots in TMEM)
 };
 
 TileCfg pick_tile(int bins, bool two_d) {
   const int nb = bins <= 16 ? 17 : (bins <= 32 ? 33 : 65);
   if (nb == 65) return two_d ? TileCfg{65, 32, 8, 1, false} : TileCfg{65, 8, 8, 4, false};
-  // Default: one voxel per thread (kb_kernel, 16 warps/SM, 79-80 ms at C2).
-  // SALVOX_KB_PAIR=1 selects kb_pair_kernel: 25% fewer shared-memory wavefronts
-  // per update but 247 registers -> 8 warps/SM, latency-bound (86 ms at C2, r01).
+  // Variants (A/B knob SALVOX_KB_VARIANT; measured at C2 on one B200, r01):
+  //   2 (default, 3D): kb_tmem_kernel -- 1024 threads, snapshots in TMEM, 71.2 ms
+  //   0: kb_kernel -- 512 threads, snapshots in registers, 80.2 ms (2D default)
+  //   1: kb_pair_kernel -- 2 voxels/thread, 25% fewer smem wavefronts but 247
+  //      registers -> 8 warps/SM, latency-bound, 85.9 ms
   static const int mode = [] {
-    const char* e = std::getenv("SALVOX_KB_PAIR");
-    return e ? std::atoi(e) : 0;
+    const char* e = std::getenv("SALVOX_KB_VARIANT");
+    return e ? std::atoi(e) : 2;
   }();
-  if (mode == 0) return two_d ? TileCfg{nb, 32, 16, 1, false} : TileCfg{nb, 8, 8, 8, false};
-  return two_d ? TileCfg{nb, 8, 64, 1, true} : TileCfg{nb, 8, 8, 8, true};
+  if (mode == 1) return two_d ? TileCfg{nb, 8, 64, 1, true} : TileCfg{nb, 8, 8, 8, true};
+  if (mode == 2 && !two_d) return TileCfg{nb, 16, 8, 8, false, true};
+  return two_d ? TileCfg{nb, 32, 16, 1, false} : TileCfg{nb, 8, 8, 8, false};
 }
 
 // Dynamic shared memory of one CTA: histogram columns, tile(s), mbarrier.
@@ -651,6 +869,7 @@ size_t kb_smem(const TileCfg& tc, uint32_t tile_bytes) {
   const size_t voxels = (size_t)tc.tx * tc.ty * tc.tz;
   if (tc.pair)
     return (size_t)tc.nb * voxels * 4 + 2 * (((size_t)tile_bytes + 127) & ~(size_t)127) + 16;
+  if (tc.tmem) return (size_t)tc.nb * voxels * 4 + (((size_t)tile_bytes + 15) & ~(size_t)15) + 32;
   return (size_t)tc.nb * voxels * 4 + (((size_t)tile_bytes + 15) & ~(size_t)15) + 16;
 }
 
@@ -805,7 +1024,7 @@ template <bool DBG>
 void dispatch_kb(salvox_ctx* ctx, const TileCfg& tc, const CUtensorMap& map, const KbParams& kp,
                  dim3 grid, size_t smem) {
 #define SX_KB(NB, TX, TY, TZ)                                             \
-  if (!tc.pair && tc.nb == NB && tc.tx == TX && tc.ty == TY && tc.tz == TZ) { \
+  if (!tc.pair && !tc.tmem && tc.nb == NB && tc.tx == TX && tc.ty == TY && tc.tz == TZ) { \
     launch_kb<NB, TX, TY, TZ, DBG>(ctx, map, kp, grid, smem);             \
     return;                                                               \
   }
@@ -823,6 +1042,13 @@ void dispatch_kb(salvox_ctx* ctx, const TileCfg& tc, const CUtensorMap& map, con
     k<<<grid, 4 * TY * TZ, smem, ctx->stream>>>(map, kp);                                    \
     SX_LAUNCH_CHECK(ctx);                                                                    \
     return;                                                                                  \
+  }
+  if (tc.tmem) {
+    auto k = tc.nb == 17 ? kb_tmem_kernel<17, DBG> : kb_tmem_kernel<33, DBG>;
+    SX_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k<<<grid, 1024, smem, ctx->stream>>>(map, kp);
+    SX_LAUNCH_CHECK(ctx);
+    return;
   }
   SX_KP(17, 8, 8)
   SX_KP(33, 8, 8)

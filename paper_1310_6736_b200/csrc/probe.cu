@@ -15,7 +15,9 @@ namespace sx {
 constexpr int kProbeTable = 2048;
 __constant__ int4 c_probe[kProbeTable / 4];
 
-template <int NT, int NB, bool ATOMIC>
+// MODE 0: LDS.U8 + ATOMS (kb_kernel's pair), 1: LDS.U8 only, 2: ATOMS only
+// (bins from a register hash: the one-atomic-per-update floor of any design).
+template <int NT, int NB, int MODE>
 __global__ void __launch_bounds__(NT, 1) smem_probe_kernel(int iters, uint32_t* out) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint32_t* hist = reinterpret_cast<uint32_t*>(smem);
@@ -38,11 +40,18 @@ __global__ void __launch_bounds__(NT, 1) smem_probe_kernel(int iters, uint32_t* 
     for (int e4 = 0; e4 < kProbeTable / 4; ++e4) {
       const int4 w = c_probe[e4];
       const int o0 = w.x >> 9, o1 = w.y >> 9, o2 = w.z >> 9, o3 = w.w >> 9;
-      const uint32_t b0 = tb[o0], b1 = tb[-o0], b2 = tb[o1], b3 = tb[-o1];
-      const uint32_t b4 = tb[o2], b5 = tb[-o2], b6 = tb[o3], b7 = tb[-o3];
+      uint32_t b0, b1, b2, b3, b4, b5, b6, b7;
+      if (MODE == 2) {
+        const uint32_t h = (uint32_t)(o0 ^ o1 ^ o2 ^ o3) * 2654435761u ^ (uint32_t)tid;
+        b0 = h & 31u, b1 = (h >> 5) & 31u, b2 = (h >> 10) & 31u, b3 = (h >> 15) & 31u;
+        b4 = (h >> 3) & 31u, b5 = (h >> 8) & 31u, b6 = (h >> 13) & 31u, b7 = (h >> 18) & 31u;
+      } else {
+        b0 = tb[o0], b1 = tb[-o0], b2 = tb[o1], b3 = tb[-o1];
+        b4 = tb[o2], b5 = tb[-o2], b6 = tb[o3], b7 = tb[-o3];
+      }
       const uint32_t n0 = (uint32_t)w.x & 511u, n1 = (uint32_t)w.y & 511u;
       const uint32_t n2 = (uint32_t)w.z & 511u, n3 = (uint32_t)w.w & 511u;
-      if (ATOMIC) {
+      if (MODE != 1) {
         atomicAdd(hc + b0 * NT, n0);
         atomicAdd(hc + b1 * NT, n0);
         atomicAdd(hc + b2 * NT, n1);
@@ -67,7 +76,7 @@ __global__ void __launch_bounds__(NT, 1) smem_probe_kernel(int iters, uint32_t* 
 using namespace sx;
 
 extern "C" int salvox_probe_smem_peak(salvox_ctx* ctx, int iters, double* atoms_updates_per_s,
-                                      double* lds_fetches_per_s) {
+                                      double* lds_fetches_per_s, double* atoms_only_per_s) {
   return guarded([&] {
     if (!ctx) fail(SALVOX_EINVAL, "null context");
     std::lock_guard<std::mutex> lk(ctx->mu);
@@ -111,8 +120,9 @@ extern "C" int salvox_probe_smem_peak(salvox_ctx* ctx, int iters, double* atoms_
       cudaEventDestroy(b);
       if (rate) *rate = (double)grid * NT * iters * per_iter / (ms * 1e-3);
     };
-    run(smem_probe_kernel<NT, NB, true>, atoms_updates_per_s, 2.0 * kProbeTable);
-    run(smem_probe_kernel<NT, NB, false>, lds_fetches_per_s, 2.0 * kProbeTable);
+    run(smem_probe_kernel<NT, NB, 0>, atoms_updates_per_s, 2.0 * kProbeTable);
+    run(smem_probe_kernel<NT, NB, 1>, lds_fetches_per_s, 2.0 * kProbeTable);
+    run(smem_probe_kernel<NT, NB, 2>, atoms_only_per_s, 2.0 * kProbeTable);
   });
 }
 
@@ -123,6 +133,7 @@ extern "C" int salvox_ctx_set_profiling(salvox_ctx* ctx, int on) {
     ctx->profiling = on != 0;
     ctx->kb_ms_total = 0.0;
     ctx->kb_launches = 0;
+    ctx->kb_updates_total = 0.0;
   });
 }
 
