@@ -77,8 +77,9 @@ struct WarpScratch {
   double h[kMaxBins];
   double p[kMaxBins];     // last normalized candidate histogram
   double w[kMaxBins];     // mean-shift weights / scratch pmf
-  double v[32];
-  int xyz[3][32];
+  double v[32];           // compacted per-chunk values (support voxels, in order)
+  double t[3][32];        // compacted centroid terms g*x, g*y, g*z
+  int bin[32];            // compacted bins
   unsigned cnt[1][kMaxBins];  // ascent box counts (one octant at a time)
 };
 
@@ -152,15 +153,18 @@ __device__ __forceinline__ int bin_at(const SeekParams& P, int x, int y, int z) 
 
 // try_candidate_histogram (window.cpp:5-19): sequential per-bin fp64 masses in
 // support order, normalized into s.p. Returns ok; *support, *visited.
+// Per 32-voxel chunk the support voxels are compacted (ballot + popc rank) into
+// shared memory in z->y->x order; lane l owns bins l and l+32 and walks the
+// compacted list with broadcast loads, adding the matching masses in order into
+// register accumulators. The only serial dependency is the fp64 add chain.
 __device__ bool warp_candidate_hist(const SeekParams& P, WarpScratch& s, const double c[3],
                                     const WinGeom& g, int kernel, int lane, unsigned* support_out,
                                     long long* visited) {
   const int M = P.bins;
-  for (int b = lane; b < M; b += 32) s.h[b] = 0.0;
-  __syncwarp();
   const Box bb = window_box(c, g, P.nx, P.ny, P.nz);
   *visited = box_size(bb);
   unsigned support = 0;
+  double a0 = 0.0, a1 = 0.0;  // bins lane, lane + 32
   warp_box_iter(bb, lane, [&](bool act, int x, int y, int z) {
     bool in = false;
     int bin = 0;
@@ -173,22 +177,27 @@ __device__ bool warp_candidate_hist(const SeekParams& P, WarpScratch& s, const d
         val = __dmul_rn(g.det_fac, kernel_value(kernel, d));
       }
     }
-    support += __popc(__ballot_sync(kFull, in));
-    const unsigned grp = __match_any_sync(kFull, in ? bin : -1 - lane);
-    s.v[lane] = val;
+    const unsigned m = __ballot_sync(kFull, in);
+    const int cnt = __popc(m);
+    support += (unsigned)cnt;
+    if (in) {
+      const int r = __popc(m & ((1u << lane) - 1u));
+      s.bin[r] = bin;
+      s.v[r] = val;
+    }
     __syncwarp();
-    if (in && (grp & ((1u << lane) - 1u)) == 0u) {  // group leader: members in lane order
-      double acc = s.h[bin];
-      unsigned m = grp;
-      while (m) {
-        const int j = __ffs(m) - 1;
-        acc = __dadd_rn(acc, s.v[j]);
-        m &= m - 1u;
-      }
-      s.h[bin] = acc;
+#pragma unroll 4
+    for (int k = 0; k < cnt; ++k) {
+      const int bk = s.bin[k];
+      const double vk = s.v[k];
+      if (bk == lane) a0 = __dadd_rn(a0, vk);
+      if (bk == lane + 32) a1 = __dadd_rn(a1, vk);
     }
     __syncwarp();
   });
+  if (lane < M) s.h[lane] = a0;
+  if (lane + 32 < M) s.h[lane + 32] = a1;
+  __syncwarp();
   double mass = 0.0;
   if (lane == 0)
     for (int b = 0; b < M; ++b) mass = __dadd_rn(mass, s.h[b]);  // Histogram::mass
@@ -312,7 +321,8 @@ __global__ void __launch_bounds__(256) shift_kernel(const SeekParams P) {
         s.w[b] = __dsqrt_rn(__ddiv_rn(P.q[b], pb));
       }
       __syncwarp();
-      // centroid pass (shift.cpp:25-30)
+      // centroid pass (shift.cpp:25-30): support voxels compacted per chunk; lanes
+      // 0..3 run the num.x / num.y / num.z / den chains in z->y->x order
       double acc = 0.0;  // lane 0: num.x, 1: num.y, 2: num.z, 3: den
       const Box bb = window_box(c, sg.main, P.nx, P.ny, P.nz);
       visits += (unsigned long long)box_size(bb);
@@ -325,20 +335,19 @@ __global__ void __launch_bounds__(256) shift_kernel(const SeekParams P) {
           if (in) g = __dmul_rn(kernel_step_weight(P.step_kernel, dd), s.w[bin_at(P, x, y, z)]);
         }
         const unsigned m0 = __ballot_sync(kFull, in);
-        s.v[lane] = g;
-        s.xyz[0][lane] = x;
-        s.xyz[1][lane] = y;
-        s.xyz[2][lane] = z;
+        const int cnt = __popc(m0);
+        if (in) {  // Eigen: num += g * Vector3d(sx, sy, sz) -> per-component products
+          const int r = __popc(m0 & ((1u << lane) - 1u));
+          s.v[r] = g;
+          s.t[0][r] = __dmul_rn(g, (double)x);
+          s.t[1][r] = __dmul_rn(g, (double)y);
+          s.t[2][r] = __dmul_rn(g, (double)z);
+        }
         __syncwarp();
         if (lane < 4) {
-          unsigned m = m0;
-          while (m) {
-            const int j = __ffs(m) - 1;
-            const double gj = s.v[j];
-            acc = lane == 3 ? __dadd_rn(acc, gj)
-                            : __dadd_rn(acc, __dmul_rn(gj, (double)s.xyz[lane][j]));
-            m &= m - 1u;
-          }
+          const double* src = lane == 3 ? s.v : s.t[lane];
+#pragma unroll 4
+          for (int k = 0; k < cnt; ++k) acc = __dadd_rn(acc, src[k]);
         }
         __syncwarp();
       });
