@@ -30,6 +30,8 @@
 namespace sx {
 
 constexpr int kMaxBins = 64;
+constexpr int kG = 4;            // bounding-box chunks of 32 voxels per warp step (ILP)
+constexpr int kStep = 32 * kG;
 constexpr unsigned kFull = 0xffffffffu;
 constexpr double kLn2 = 0.693147180559945309417232121458176568;  // std::numbers::ln2
 
@@ -77,9 +79,9 @@ struct WarpScratch {
   double h[kMaxBins];
   double p[kMaxBins];     // last normalized candidate histogram
   double w[kMaxBins];     // mean-shift weights / scratch pmf
-  double v[32];           // compacted per-chunk values (support voxels, in order)
-  double t[3][32];        // compacted centroid terms g*x, g*y, g*z
-  int bin[32];            // compacted bins
+  double v[kStep];        // compacted per-step values (support voxels, in order)
+  double t[3][kStep];     // compacted centroid terms g*x, g*y, g*z
+  int bin[kStep];         // compacted bins
   unsigned cnt[1][kMaxBins];  // ascent box counts (one octant at a time)
 };
 
@@ -111,6 +113,39 @@ __device__ __forceinline__ void warp_box_iter(const Box& b, int lane, F&& f) {
     }
     f(act, x, y, z);
   }
+}
+
+// kG consecutive 32-voxel chunks per step: lane l gets voxels base + 32 j + l,
+// j = 0..kG-1, so the kG independent per-voxel computations overlap (ILP), and
+// the step's support list is compacted in z->y->x order.
+template <class F>
+__device__ __forceinline__ void warp_box_iter_g(const Box& b, int lane, F&& f) {
+  const int Lx = b.x1 - b.x0 + 1, Ly = b.y1 - b.y0 + 1, Lz = b.z1 - b.z0 + 1;
+  if (Lx <= 0 || Ly <= 0 || Lz <= 0) return;
+  const int total = Lx * Ly * Lz;
+  for (int base = 0; base < total; base += kStep) {
+    bool act[kG];
+    int x[kG], y[kG], z[kG];
+#pragma unroll
+    for (int j = 0; j < kG; ++j) {
+      const int L = base + 32 * j + lane;
+      act[j] = L < total;
+      const int Lc = act[j] ? L : 0;
+      const int t = Lc / Lx;
+      x[j] = b.x0 + (Lc - t * Lx);
+      const int zz = t / Ly;
+      y[j] = b.y0 + (t - zz * Ly);
+      z[j] = b.z0 + zz;
+    }
+    f(act, x, y, z);
+  }
+}
+
+__device__ __forceinline__ void dadd_if(bool p, double& acc, double v) {
+  // predicated add: the chain waits on the add latency only (no select)
+  asm("{ .reg .pred q; setp.ne.b32 q, %2, 0; @q add.rn.f64 %0, %0, %1; }"
+      : "+d"(acc)
+      : "d"(v), "r"((int)p));
 }
 
 __device__ __forceinline__ Box window_box(const double c[3], const WinGeom& g, int nx, int ny,
@@ -165,33 +200,43 @@ __device__ bool warp_candidate_hist(const SeekParams& P, WarpScratch& s, const d
   *visited = box_size(bb);
   unsigned support = 0;
   double a0 = 0.0, a1 = 0.0;  // bins lane, lane + 32
-  warp_box_iter(bb, lane, [&](bool act, int x, int y, int z) {
-    bool in = false;
-    int bin = 0;
-    double val = 0.0;
-    if (act) {
-      const double d = maha(g, c, x, y, z);
-      in = d <= 1.0;
-      if (in) {
-        bin = bin_at(P, x, y, z);
-        val = __dmul_rn(g.det_fac, kernel_value(kernel, d));
+  warp_box_iter_g(bb, lane, [&](const bool* act, const int* x, const int* y, const int* z) {
+    bool in[kG];
+    int bin[kG];
+    double val[kG];
+#pragma unroll
+    for (int j = 0; j < kG; ++j) {
+      in[j] = false;
+      bin[j] = 0;
+      val[j] = 0.0;
+      if (act[j]) {
+        const double d = maha(g, c, x[j], y[j], z[j]);
+        in[j] = d <= 1.0;
+        if (in[j]) {
+          bin[j] = bin_at(P, x[j], y[j], z[j]);
+          val[j] = __dmul_rn(g.det_fac, kernel_value(kernel, d));
+        }
       }
     }
-    const unsigned m = __ballot_sync(kFull, in);
-    const int cnt = __popc(m);
-    support += (unsigned)cnt;
-    if (in) {
-      const int r = __popc(m & ((1u << lane) - 1u));
-      s.bin[r] = bin;
-      s.v[r] = val;
+    int off = 0;
+#pragma unroll
+    for (int j = 0; j < kG; ++j) {
+      const unsigned m = __ballot_sync(kFull, in[j]);
+      if (in[j]) {
+        const int r = off + __popc(m & ((1u << lane) - 1u));
+        s.bin[r] = bin[j];
+        s.v[r] = val[j];
+      }
+      off += __popc(m);
     }
+    support += (unsigned)off;
     __syncwarp();
 #pragma unroll 4
-    for (int k = 0; k < cnt; ++k) {
+    for (int k = 0; k < off; ++k) {
       const int bk = s.bin[k];
       const double vk = s.v[k];
-      if (bk == lane) a0 = __dadd_rn(a0, vk);
-      if (bk == lane + 32) a1 = __dadd_rn(a1, vk);
+      dadd_if(bk == lane, a0, vk);
+      dadd_if(bk == lane + 32, a1, vk);
     }
     __syncwarp();
   });
@@ -278,11 +323,13 @@ __device__ bool warp_final_scores(const SeekParams& P, WarpScratch& s, const dou
 }
 
 // ------------------------------------------------------------------- shift
-__global__ void __launch_bounds__(256) shift_kernel(const SeekParams P) {
-  __shared__ WarpScratch scratch[8];
+constexpr int kSeekWarps = 4;  // warps (seeds) per block; scratch is ~6.3 KB per warp
+
+__global__ void __launch_bounds__(32 * kSeekWarps) shift_kernel(const SeekParams P) {
+  __shared__ WarpScratch scratch[kSeekWarps];
   const int lane = threadIdx.x & 31;
   const int wid = threadIdx.x >> 5;
-  const int seed = blockIdx.x * 8 + wid;
+  const int seed = blockIdx.x * kSeekWarps + wid;
   if (seed >= P.n_seeds) return;
   WarpScratch& s = scratch[wid];
   const SeedIn si = P.seeds[seed];
@@ -326,28 +373,38 @@ __global__ void __launch_bounds__(256) shift_kernel(const SeekParams P) {
       double acc = 0.0;  // lane 0: num.x, 1: num.y, 2: num.z, 3: den
       const Box bb = window_box(c, sg.main, P.nx, P.ny, P.nz);
       visits += (unsigned long long)box_size(bb);
-      warp_box_iter(bb, lane, [&](bool act, int x, int y, int z) {
-        bool in = false;
-        double g = 0.0;
-        if (act) {
-          const double dd = maha(sg.main, c, x, y, z);
-          in = dd <= 1.0;
-          if (in) g = __dmul_rn(kernel_step_weight(P.step_kernel, dd), s.w[bin_at(P, x, y, z)]);
+      warp_box_iter_g(bb, lane, [&](const bool* act, const int* x, const int* y, const int* z) {
+        bool in[kG];
+        double g[kG];
+#pragma unroll
+        for (int j = 0; j < kG; ++j) {
+          in[j] = false;
+          g[j] = 0.0;
+          if (act[j]) {
+            const double dd = maha(sg.main, c, x[j], y[j], z[j]);
+            in[j] = dd <= 1.0;
+            if (in[j])
+              g[j] = __dmul_rn(kernel_step_weight(P.step_kernel, dd), s.w[bin_at(P, x[j], y[j], z[j])]);
+          }
         }
-        const unsigned m0 = __ballot_sync(kFull, in);
-        const int cnt = __popc(m0);
-        if (in) {  // Eigen: num += g * Vector3d(sx, sy, sz) -> per-component products
-          const int r = __popc(m0 & ((1u << lane) - 1u));
-          s.v[r] = g;
-          s.t[0][r] = __dmul_rn(g, (double)x);
-          s.t[1][r] = __dmul_rn(g, (double)y);
-          s.t[2][r] = __dmul_rn(g, (double)z);
+        int off = 0;
+#pragma unroll
+        for (int j = 0; j < kG; ++j) {
+          const unsigned m0 = __ballot_sync(kFull, in[j]);
+          if (in[j]) {  // Eigen: num += g * Vector3d(sx, sy, sz) -> per-component products
+            const int r = off + __popc(m0 & ((1u << lane) - 1u));
+            s.v[r] = g[j];
+            s.t[0][r] = __dmul_rn(g[j], (double)x[j]);
+            s.t[1][r] = __dmul_rn(g[j], (double)y[j]);
+            s.t[2][r] = __dmul_rn(g[j], (double)z[j]);
+          }
+          off += __popc(m0);
         }
         __syncwarp();
         if (lane < 4) {
           const double* src = lane == 3 ? s.v : s.t[lane];
 #pragma unroll 4
-          for (int k = 0; k < cnt; ++k) acc = __dadd_rn(acc, src[k]);
+          for (int k = 0; k < off; ++k) acc = __dadd_rn(acc, src[k]);
         }
         __syncwarp();
       });
@@ -434,167 +491,193 @@ __device__ void warp_count_shell(const SeekParams& P, unsigned* cnt, const Box& 
   if (B.z1 > A.z1) count_box(Box{A.x0, A.x1, A.y0, A.y1, A.z1 + 1, B.z1});
 }
 
-__global__ void __launch_bounds__(256) ascent_kernel(const SeekParams P) {
-  __shared__ WarpScratch scratch[8];
+// One CTA per trajectory, one warp per quadrant/octant: warp q counts its
+// corner-anchored boxes for every scale (nested in k, so only the shell
+// B_k \ B_{k-1} is counted) and evaluates their entropies; thread 0 combines the
+// nq (entropy, scale) pairs into the move exactly as quadrant.cpp:55-81 does.
+// Post-scoring runs its three window histograms on three warps in parallel.
+struct AscentWarp {
+  unsigned cnt[kMaxBins];
+  double p[kMaxBins];
+  double w[kMaxBins];
+};
+
+template <int NQ>
+__global__ void __launch_bounds__(32 * NQ) ascent_kernel(const SeekParams P) {
+  __shared__ AscentWarp aw[NQ];
+  __shared__ WarpScratch ps[3];
+  __shared__ double ent[NQ];
+  __shared__ int bk[NQ];
+  __shared__ double pos[3];
+  __shared__ int ctl[3];  // stop, converged, degenerate
+  __shared__ unsigned long long vis[NQ];
+  __shared__ double score[3];  // entropy, bhattacharyya, pdf
+  __shared__ int okf[3];
   const int lane = threadIdx.x & 31;
-  const int wid = threadIdx.x >> 5;
-  const int seed = blockIdx.x * 8 + wid;
-  if (seed >= P.n_seeds) return;
-  WarpScratch& s = scratch[wid];
+  const int q = threadIdx.x >> 5;
+  const int seed = blockIdx.x;
+  if (seed >= P.n_seeds) return;  // uniform per CTA
   const SeedIn si = P.seeds[seed];
   const int M = P.bins;
-  const bool two_d = P.method == SALVOX_METHOD_QUADRANT;
-  const int nq = two_d ? 4 : 8;
+  const bool two_d = NQ == 4;
   const int min_vox = two_d ? 4 : 8;
   const double lim[3] = {(double)(P.nx - 1), (double)(P.ny - 1), (double)(P.nz - 1)};
   double p[3] = {si.pos[0], si.pos[1], si.pos[2]};
   unsigned long long visits = 0;
-  salvox_detection d;
-  memset(&d, 0, sizeof d);
-  d.seed_index = si.seed_index;
-  d.H[0] = d.H[4] = d.H[8] = 1.0;
-  double last_e[8];
-  int last_k[8];
-  bool degenerate = false, converged = false;
+  AscentWarp& s = aw[q];
   int iters = 0;
   for (int it = 0; it < P.max_iters; ++it) {
-    double ent[8];
-    int bk[8];
-    for (int q = 0; q < nq; ++q) {
-      double best_e = 0.0;
-      int best_k = P.ascent_scales[0];
-      for (int b = lane; b < M; b += 32) s.cnt[0][b] = 0u;
-      __syncwarp();
-      Box prev{0, -1, 0, -1, 0, -1};
-      bool prev_empty = true;
-      for (int i = 0; i < P.n_ascent; ++i) {
-        const int k = P.ascent_scales[i];
-        Box B;
-        axis_range(p[0], (double)c_dirs[q][0] * (double)k, P.nx, &B.x0, &B.x1);
-        axis_range(p[1], (double)c_dirs[q][1] * (double)k, P.ny, &B.y0, &B.y1);
-        if (two_d) {
-          axis_range(p[2], 0.0, P.nz, &B.z0, &B.z1);
-        } else {
-          axis_range(p[2], (double)c_dirs[q][2] * (double)k, P.nz, &B.z0, &B.z1);
-        }
-        const long long count = box_size(B);
-        if (count > 0) {
-          warp_count_shell(P, s.cnt[0], prev, B, prev_empty, lane);
-          prev = B;
-          prev_empty = false;
-        }
-        __syncwarp();
-        double e = 0.0;
-        if (count > 0 && count >= min_vox) {  // quadrant.cpp:24-26
-          visits += (unsigned long long)count;
-          const double mass = (double)count;  // exact integer mass
-          for (int b = lane; b < M; b += 32) s.p[b] = __ddiv_rn((double)s.cnt[0][b], mass);
-          __syncwarp();
-          e = warp_entropy_bits(s.p, M, lane, s.w);
-        }
-        if (e > best_e) {  // strict: smallest scale wins ties (quadrant.cpp:52)
-          best_e = e;
-          best_k = k;
-        }
+    double best_e = 0.0;
+    int best_k = P.ascent_scales[0];
+    for (int b = lane; b < M; b += 32) s.cnt[b] = 0u;
+    __syncwarp();
+    Box prev{0, -1, 0, -1, 0, -1};
+    bool prev_empty = true;
+    for (int i = 0; i < P.n_ascent; ++i) {
+      const int k = P.ascent_scales[i];
+      Box B;
+      axis_range(p[0], (double)c_dirs[q][0] * (double)k, P.nx, &B.x0, &B.x1);
+      axis_range(p[1], (double)c_dirs[q][1] * (double)k, P.ny, &B.y0, &B.y1);
+      if (two_d) {
+        axis_range(p[2], 0.0, P.nz, &B.z0, &B.z1);
+      } else {
+        axis_range(p[2], (double)c_dirs[q][2] * (double)k, P.nz, &B.z0, &B.z1);
       }
+      const long long count = box_size(B);
+      if (count > 0) {
+        warp_count_shell(P, s.cnt, prev, B, prev_empty, lane);
+        prev = B;
+        prev_empty = false;
+      }
+      __syncwarp();
+      double e = 0.0;
+      if (count > 0 && count >= min_vox) {  // quadrant.cpp:24-26
+        visits += (unsigned long long)count;
+        const double mass = (double)count;  // exact integer mass
+        for (int b = lane; b < M; b += 32) s.p[b] = __ddiv_rn((double)s.cnt[b], mass);
+        __syncwarp();
+        e = warp_entropy_bits(s.p, M, lane, s.w);
+      }
+      if (e > best_e) {  // strict: smallest scale wins ties (quadrant.cpp:52)
+        best_e = e;
+        best_k = k;
+      }
+    }
+    if (lane == 0) {
       ent[q] = best_e;
       bk[q] = best_k;
     }
+    __syncthreads();
     iters = it + 1;
-    for (int q = 0; q < nq; ++q) {
-      last_e[q] = ent[q];
-      last_k[q] = bk[q];
-    }
-    double total = 0.0;
-    for (int q = 0; q < nq; ++q) total = __dadd_rn(total, ent[q]);
-    if (total <= 0.0) {
-      degenerate = true;
-      break;
-    }
-    double ed[3] = {0.0, 0.0, 0.0};
-    for (int q = 0; q < nq; ++q) {
-      const double ne = __ddiv_rn(ent[q], total);
-      for (int a = 0; a < (two_d ? 2 : 3); ++a)
-        ed[a] = __dadd_rn(ed[a], __dmul_rn(__dmul_rn(ne, (double)c_dirs[q][a]), (double)bk[q]));
-    }
-    for (int a = 0; a < (two_d ? 2 : 3); ++a) p[a] = dclamp(__dadd_rn(p[a], ed[a]), lim[a]);
-    const double nrm =
-        two_d ? __dsqrt_rn(__dadd_rn(__dmul_rn(ed[0], ed[0]), __dmul_rn(ed[1], ed[1])))
-              : __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(ed[0], ed[0]), __dmul_rn(ed[1], ed[1])),
-                                     __dmul_rn(ed[2], ed[2])));
-    if (nrm < P.eta) {
-      converged = true;
-      break;
-    }
-  }
-  d.iterations = iters;
-  if (converged) d.flags |= SALVOX_FLAG_CONVERGED;
-  d.center[0] = p[0];
-  d.center[1] = p[1];
-  d.center[2] = two_d ? 0.0 : p[2];
-  if (P.ascent_out && lane == 0) {  // quadrant_seek_one's result (quadrant.cpp:276-282)
-    salvox_ascent_result r;
-    r.position[0] = p[0];
-    r.position[1] = p[1];
-    r.position[2] = p[2];
-    r.iterations = iters;
-    r.converged = converged;
-    r.degenerate = degenerate;
-    r.best_scale = 0;
-    r.entropy_bits = 0.0;
-    if (!degenerate) {
-      int bq = 0;
-      for (int q = 1; q < nq; ++q)
-        if (last_e[q] > last_e[bq]) bq = q;
-      r.best_scale = last_k[bq];
-      r.entropy_bits = last_e[bq];
-    }
-    P.ascent_out[seed] = r;
-  }
-  if (degenerate) {
-    d.flags |= SALVOX_FLAG_DEGENERATE;
-  } else if (P.post_score) {
-    int bq = 0;
-    for (int q = 1; q < nq; ++q)
-      if (last_e[q] > last_e[bq]) bq = q;
-    const int k = max(2, last_k[bq]);  // pipeline.cpp:343
-    const ScaleGeom& sg = P.geoms[P.geom_of_k[k]];
-    for (int i = 0; i < 9; ++i) d.H[i] = sg.H[i];
-    const double c[3] = {d.center[0], d.center[1], d.center[2]};
-    unsigned sup;
-    long long vis;
-    // Epanechnikov histogram: entropy + Bhattacharyya vs uniform (pipeline.cpp:346-350)
-    const bool okp = warp_candidate_hist(P, s, c, sg.main, 1, lane, &sup, &vis);
-    visits += (unsigned long long)vis;
-    if (okp) {
-      double rho = 0.0;
-      if (lane == 0) {
-        for (int b = 0; b < M; ++b) rho = __dadd_rn(rho, __dsqrt_rn(__dmul_rn(s.p[b], P.q[b])));
-        rho = rho < 1.0 ? rho : 1.0;
+    if (threadIdx.x == 0) {
+      double total = 0.0;
+      for (int r = 0; r < NQ; ++r) total = __dadd_rn(total, ent[r]);
+      ctl[0] = ctl[1] = ctl[2] = 0;
+      if (total <= 0.0) {
+        ctl[0] = ctl[2] = 1;
+        pos[0] = p[0], pos[1] = p[1], pos[2] = p[2];
+      } else {
+        double ed[3] = {0.0, 0.0, 0.0};
+        for (int r = 0; r < NQ; ++r) {
+          const double ne = __ddiv_rn(ent[r], total);
+          for (int a = 0; a < (two_d ? 2 : 3); ++a)
+            ed[a] = __dadd_rn(ed[a], __dmul_rn(__dmul_rn(ne, (double)c_dirs[r][a]), (double)bk[r]));
+        }
+        pos[0] = p[0], pos[1] = p[1], pos[2] = p[2];
+        for (int a = 0; a < (two_d ? 2 : 3); ++a) pos[a] = dclamp(__dadd_rn(p[a], ed[a]), lim[a]);
+        const double nrm =
+            two_d ? __dsqrt_rn(__dadd_rn(__dmul_rn(ed[0], ed[0]), __dmul_rn(ed[1], ed[1])))
+                  : __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(ed[0], ed[0]), __dmul_rn(ed[1], ed[1])),
+                                         __dmul_rn(ed[2], ed[2])));
+        if (nrm < P.eta) ctl[0] = ctl[1] = 1;
       }
-      d.bhattacharyya = __shfl_sync(kFull, rho, 0);
-      d.entropy_bits = warp_entropy_bits(s.p, M, lane, s.w);
     }
-    double pdf = 0.0;
-    if (sg.pdf_ok) {
-      const bool ok_lo = warp_candidate_hist(P, s, c, sg.lo, 0, lane, &sup, &vis);
-      visits += (unsigned long long)vis;
-      for (int b = lane; b < M; b += 32) s.w[b] = s.p[b];
-      __syncwarp();
-      const bool ok_hi = warp_candidate_hist(P, s, c, sg.hi, 0, lane, &sup, &vis);
-      visits += (unsigned long long)vis;
-      if (ok_lo && ok_hi && lane == 0) {
+    __syncthreads();
+    p[0] = pos[0], p[1] = pos[1], p[2] = pos[2];
+    if (ctl[0]) break;
+  }
+  const bool degenerate = ctl[2] != 0, converged = ctl[1] != 0;
+  int bq = 0;
+  for (int r = 1; r < NQ; ++r)
+    if (ent[r] > ent[bq]) bq = r;
+  const int best_scale = bk[bq];
+  const double best_entropy = ent[bq];
+  // post-scoring: isotropic window k = max(2, best_scale) (pipeline.cpp:343-355)
+  const int kwin = max(2, best_scale);
+  const ScaleGeom& sg = P.geoms[P.geom_of_k[kwin]];
+  const double c[3] = {p[0], p[1], two_d ? 0.0 : p[2]};
+  if (!degenerate && P.post_score && q < 3) {
+    unsigned sup;
+    long long v;
+    WarpScratch& w = ps[q];
+    if (q == 0) {  // Epanechnikov histogram: entropy + Bhattacharyya vs uniform
+      const bool okp = warp_candidate_hist(P, w, c, sg.main, 1, lane, &sup, &v);
+      visits += (unsigned long long)v;
+      double rho = 0.0, e = 0.0;
+      if (okp) {
+        if (lane == 0) {
+          for (int b = 0; b < M; ++b) rho = __dadd_rn(rho, __dsqrt_rn(__dmul_rn(w.p[b], P.q[b])));
+          rho = rho < 1.0 ? rho : 1.0;
+        }
+        e = warp_entropy_bits(w.p, M, lane, w.w);
+      }
+      if (lane == 0) {
+        okf[0] = okp;
+        score[0] = e;
+        score[1] = rho;
+      }
+    } else if (sg.pdf_ok) {  // pdf_difference flanks (window.cpp:37-39), both evaluated
+      const bool ok = warp_candidate_hist(P, w, c, q == 1 ? sg.lo : sg.hi, 0, lane, &sup, &v);
+      visits += (unsigned long long)v;
+      if (lane == 0) okf[q] = ok;
+    } else if (lane == 0) {
+      okf[q] = 0;
+    }
+  }
+  if (lane == 0) vis[q] = visits;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    salvox_detection d;
+    memset(&d, 0, sizeof d);
+    d.seed_index = si.seed_index;
+    d.H[0] = d.H[4] = d.H[8] = 1.0;
+    d.iterations = iters;
+    if (converged) d.flags |= SALVOX_FLAG_CONVERGED;
+    d.center[0] = c[0];
+    d.center[1] = c[1];
+    d.center[2] = c[2];
+    if (degenerate) {
+      d.flags |= SALVOX_FLAG_DEGENERATE;
+    } else if (P.post_score) {
+      for (int i = 0; i < 9; ++i) d.H[i] = sg.H[i];
+      if (okf[0]) {
+        d.entropy_bits = score[0];
+        d.bhattacharyya = score[1];
+      }
+      double pdf = 0.0;
+      if (sg.pdf_ok && okf[1] && okf[2]) {
         double l1 = 0.0;
-        for (int b = 0; b < M; ++b) l1 = __dadd_rn(l1, fabs(__dsub_rn(s.p[b], s.w[b])));
+        for (int b = 0; b < M; ++b) l1 = __dadd_rn(l1, fabs(__dsub_rn(ps[2].p[b], ps[1].p[b])));
         pdf = __dmul_rn(sg.pdf_fac, l1);
       }
-      pdf = __shfl_sync(kFull, pdf, 0);
+      d.pdf_diff = pdf;
     }
-    d.pdf_diff = pdf;
-  }
-  if (lane == 0) {
+    unsigned long long tv = 0;
+    for (int r = 0; r < NQ; ++r) tv += vis[r];
     P.out[seed] = d;
-    P.visits[seed] = visits;
+    P.visits[seed] = tv;
+    if (P.ascent_out) {  // quadrant_seek_one's result (quadrant.cpp:276-282)
+      salvox_ascent_result r;
+      r.position[0] = p[0];
+      r.position[1] = p[1];
+      r.position[2] = p[2];
+      r.iterations = iters;
+      r.converged = converged;
+      r.degenerate = degenerate;
+      r.best_scale = degenerate ? 0 : best_scale;
+      r.entropy_bits = degenerate ? 0.0 : best_entropy;
+      P.ascent_out[seed] = r;
+    }
   }
 }
 
@@ -788,11 +871,12 @@ void run_seek(salvox_ctx* ctx, SeekJob& job, const uint8_t* d_bins, int bins, co
   SX_CUDA(cudaMemcpyAsync(d_sd, job.seeds.data(), sbytes, cudaMemcpyHostToDevice, ctx->stream));
   P.geoms = reinterpret_cast<const ScaleGeom*>(d_geo);
   P.seeds = reinterpret_cast<const SeedIn*>(d_sd);
-  const int grid = (P.n_seeds + 7) / 8;
   if (P.method == SALVOX_METHOD_SHIFT)
-    shift_kernel<<<grid, 256, 0, ctx->stream>>>(P);
+    shift_kernel<<<(P.n_seeds + kSeekWarps - 1) / kSeekWarps, 32 * kSeekWarps, 0, ctx->stream>>>(P);
+  else if (P.method == SALVOX_METHOD_QUADRANT)
+    ascent_kernel<4><<<P.n_seeds, 128, 0, ctx->stream>>>(P);
   else
-    ascent_kernel<<<grid, 256, 0, ctx->stream>>>(P);
+    ascent_kernel<8><<<P.n_seeds, 256, 0, ctx->stream>>>(P);
   SX_LAUNCH_CHECK(ctx);
 }
 

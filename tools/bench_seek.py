@@ -1,0 +1,113 @@
+"""Seed-grid detector timings on the BASELINE configs (device-resident volumes).
+
+  C1: 128^3 PET-like phantom, 16 bins, scales 3..15, lattice 8, octant ascent
+      (4,096 trajectories) and shift (53,248 seeds)
+  C3: 256x256x160 MR phantom, 64 bins, shift, lattice 16 x scales {8, 12}
+  C5: batch of 64 x 128^3 C1-style volumes (rng_seed 1310+i, centre jittered by
+      Rng(i)), octant, volumes data-parallel (one rank here)
+Prints one JSON object per config; --cpu adds the oracle's time on all host cores.
+"""
+import argparse
+import ctypes as C
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+from paper_1310_6736_b200 import _lib, api  # noqa: E402
+from paper_1310_6736_b200._lib import Context  # noqa: E402
+from tests import phantoms  # noqa: E402
+
+C1_SCALES = [float(s) for s in range(3, 16)]
+
+
+def c5_specs(n):
+    specs = []
+    for i in range(n):
+        z = i  # splitmix64 jitter in [-8, 8] per axis from Rng(i)
+        jit = []
+        for _ in range(3):
+            z = (z + 0x9E3779B97F4A7C15) & 0xFFFFFFFFFFFFFFFF
+            t = z
+            t = ((t ^ (t >> 30)) * 0xBF58476D1CE4E5B9) & 0xFFFFFFFFFFFFFFFF
+            t = ((t ^ (t >> 27)) * 0x94D049BB133111EB) & 0xFFFFFFFFFFFFFFFF
+            t ^= t >> 31
+            jit.append(float((t >> 11) * 2.0**-53 * 16.0 - 8.0))
+        specs.append(phantoms.config_c1(seed=1310 + i, jitter=jit))
+    return specs
+
+
+def time_batch(ctx, stream, d_vols, batch, shape, window, method, scales, spacing, steps=3):
+    nz, ny, nx = shape
+    iw = _lib.Window(window[0], window[1], window[2], 0)
+    P, keep = api._detect_params(method, seed_spacing=spacing, scales=scales, k=20,
+                                 dedupe_radius=5.0)
+    out = np.empty(batch * 20, _lib.DET_DTYPE)
+    n_out = np.zeros(batch, np.int64)
+    visits = C.c_uint64(0)
+
+    def run():
+        _lib.check(_lib.load().salvox_detect_batch_device(
+            ctx.handle, C.c_void_p(d_vols.data_ptr()), batch, nx, ny, nz, C.byref(iw), C.byref(P),
+            out.ctypes.data_as(C.c_void_p), 20, n_out.ctypes.data_as(C.c_void_p), C.byref(visits)))
+
+    run()
+    ts = []
+    for _ in range(steps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        run()
+        e1.record(stream)
+        e1.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    del keep
+    return float(np.mean(ts)), int(n_out.sum())
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--cpu", action="store_true")
+    ap.add_argument("--c5", type=int, default=64)
+    args = ap.parse_args()
+    ctx = Context(0)
+    dev = torch.device("cuda", 0)
+    st = torch.cuda.current_stream(dev)
+    ctx.set_stream(st.cuda_stream)
+    res = []
+    v1, _ = api.make_phantom(phantoms.config_c1())
+    d1 = torch.from_numpy(v1).to(dev)
+    for method in ("octant", "shift"):
+        ms, sel = time_batch(ctx, st, d1, 1, v1.shape, (0.0, 16.0, 16), method, C1_SCALES, 8.0)
+        r = {"config": f"C1 {method}", "ms_per_volume": ms, "volumes_per_s": 1e3 / ms,
+             "selected": sel}
+        if args.cpu:
+            from oracle import oracle as O
+            t0 = time.perf_counter()
+            O.detect(v1, 0.0, 16.0, 16, method=method, seed_spacing=8.0, scales=C1_SCALES,
+                     top_k=20, dedupe_radius=5.0, workers=os.cpu_count() or 1)
+            r["cpu_ms"] = (time.perf_counter() - t0) * 1e3
+            r["cpu_cores"] = os.cpu_count()
+        res.append(r)
+    v3, _ = api.make_phantom(phantoms.config_c3())
+    d3 = torch.from_numpy(v3).to(dev)
+    ms, sel = time_batch(ctx, st, d3, 1, v3.shape, (0.0, 64.0, 64), "shift", [8.0, 12.0], 16.0)
+    res.append({"config": "C3 shift", "ms_per_volume": ms, "volumes_per_s": 1e3 / ms,
+                "selected": sel})
+    if args.c5 > 0:
+        vols = np.stack([api.make_phantom(s)[0] for s in c5_specs(args.c5)])
+        dv = torch.from_numpy(vols).to(dev)
+        ms, sel = time_batch(ctx, st, dv, args.c5, vols.shape[1:], (0.0, 16.0, 16), "octant",
+                             C1_SCALES, 8.0, steps=1)
+        res.append({"config": f"C5 octant batch x{args.c5}", "ms_per_batch": ms,
+                    "volumes_per_s": args.c5 * 1e3 / ms, "selected": sel})
+    for r in res:
+        print(json.dumps(r))
+
+
+if __name__ == "__main__":
+    main()
