@@ -54,6 +54,8 @@ struct SeedIn {
   double pos[3];
   int geom;        // shift: ScaleGeom index of the seed's scale
   int seed_index;
+  int slot;        // output row (launch order is longest-window-first)
+  int pad_;
 };
 
 struct SeekParams {
@@ -141,13 +143,6 @@ __device__ __forceinline__ void warp_box_iter_g(const Box& b, int lane, F&& f) {
   }
 }
 
-__device__ __forceinline__ void dadd_if(bool p, double& acc, double v) {
-  // predicated add: the chain waits on the add latency only (no select)
-  asm("{ .reg .pred q; setp.ne.b32 q, %2, 0; @q add.rn.f64 %0, %0, %1; }"
-      : "+d"(acc)
-      : "d"(v), "r"((int)p));
-}
-
 __device__ __forceinline__ Box window_box(const double c[3], const WinGeom& g, int nx, int ny,
                                           int nz) {  // window.hpp:84-89
   Box b;
@@ -231,12 +226,22 @@ __device__ bool warp_candidate_hist(const SeekParams& P, WarpScratch& s, const d
     }
     support += (unsigned)off;
     __syncwarp();
+    // acc + (+0.0) == acc exactly (masses are >= +0), so the select moves off
+    // the dependent chain: one DADD of latency per support voxel and bin lane.
+    if (M <= 32) {
 #pragma unroll 4
-    for (int k = 0; k < off; ++k) {
-      const int bk = s.bin[k];
-      const double vk = s.v[k];
-      dadd_if(bk == lane, a0, vk);
-      dadd_if(bk == lane + 32, a1, vk);
+      for (int k = 0; k < off; ++k) {
+        const double vk = s.v[k];
+        a0 = __dadd_rn(a0, s.bin[k] == lane ? vk : 0.0);
+      }
+    } else {
+#pragma unroll 4
+      for (int k = 0; k < off; ++k) {
+        const int bk = s.bin[k];
+        const double vk = s.v[k];
+        a0 = __dadd_rn(a0, bk == lane ? vk : 0.0);
+        a1 = __dadd_rn(a1, bk == lane + 32 ? vk : 0.0);
+      }
     }
     __syncwarp();
   });
@@ -323,13 +328,14 @@ __device__ bool warp_final_scores(const SeekParams& P, WarpScratch& s, const dou
 }
 
 // ------------------------------------------------------------------- shift
-constexpr int kSeekWarps = 4;  // warps (seeds) per block; scratch is ~6.3 KB per warp
-
-__global__ void __launch_bounds__(32 * kSeekWarps) shift_kernel(const SeekParams P) {
-  __shared__ WarpScratch scratch[kSeekWarps];
+// warps (seeds) per block; scratch is ~6.3 KB per warp. Small blocks free their
+// slot as soon as their own trajectories end (lengths vary widely per seed).
+template <int NW>
+__global__ void __launch_bounds__(32 * NW) shift_kernel(const SeekParams P) {
+  __shared__ WarpScratch scratch[NW];
   const int lane = threadIdx.x & 31;
   const int wid = threadIdx.x >> 5;
-  const int seed = blockIdx.x * kSeekWarps + wid;
+  const int seed = blockIdx.x * NW + wid;
   if (seed >= P.n_seeds) return;
   WarpScratch& s = scratch[wid];
   const SeedIn si = P.seeds[seed];
@@ -451,8 +457,8 @@ __global__ void __launch_bounds__(32 * kSeekWarps) shift_kernel(const SeekParams
       d.flags |= SALVOX_FLAG_DEGENERATE;
   }
   if (lane == 0) {
-    P.out[seed] = d;
-    P.visits[seed] = visits;
+    P.out[si.slot] = d;
+    P.visits[si.slot] = visits;
   }
 }
 
@@ -664,8 +670,8 @@ __global__ void __launch_bounds__(32 * NQ) ascent_kernel(const SeekParams P) {
     }
     unsigned long long tv = 0;
     for (int r = 0; r < NQ; ++r) tv += vis[r];
-    P.out[seed] = d;
-    P.visits[seed] = tv;
+    P.out[si.slot] = d;
+    P.visits[si.slot] = tv;
     if (P.ascent_out) {  // quadrant_seek_one's result (quadrant.cpp:276-282)
       salvox_ascent_result r;
       r.position[0] = p[0];
@@ -676,7 +682,7 @@ __global__ void __launch_bounds__(32 * NQ) ascent_kernel(const SeekParams P) {
       r.degenerate = degenerate;
       r.best_scale = degenerate ? 0 : best_scale;
       r.entropy_bits = degenerate ? 0.0 : best_entropy;
-      P.ascent_out[seed] = r;
+      P.ascent_out[si.slot] = r;
     }
   }
 }
@@ -811,8 +817,13 @@ void build_job(int nx, int ny, int nz, const salvox_detect_params* prm,
       std::memcpy(si.pos, recs[i].pos, sizeof si.pos);
       si.geom = it->second;
       si.seed_index = index[i];
+      si.slot = (int)i;
       job.seeds.push_back(si);
     }
+    // longest-processing-time first: seeds with the largest windows launch first
+    std::stable_sort(job.seeds.begin(), job.seeds.end(), [&](const SeedIn& a, const SeedIn& b) {
+      return job.geoms[a.geom].main.support_volume > job.geoms[b.geom].main.support_volume;
+    });
   } else {
     std::vector<int> ks;
     if (prm->n_quadrant_scales > 0) {
@@ -847,6 +858,7 @@ void build_job(int nx, int ny, int nz, const salvox_detect_params* prm,
       std::memcpy(si.pos, recs[i].pos, sizeof si.pos);
       si.geom = 0;
       si.seed_index = index[i];
+      si.slot = (int)i;
       job.seeds.push_back(si);
     }
   }
@@ -871,8 +883,16 @@ void run_seek(salvox_ctx* ctx, SeekJob& job, const uint8_t* d_bins, int bins, co
   SX_CUDA(cudaMemcpyAsync(d_sd, job.seeds.data(), sbytes, cudaMemcpyHostToDevice, ctx->stream));
   P.geoms = reinterpret_cast<const ScaleGeom*>(d_geo);
   P.seeds = reinterpret_cast<const SeedIn*>(d_sd);
-  if (P.method == SALVOX_METHOD_SHIFT)
-    shift_kernel<<<(P.n_seeds + kSeekWarps - 1) / kSeekWarps, 32 * kSeekWarps, 0, ctx->stream>>>(P);
+  static const int shift_warps = [] {
+    const char* e = std::getenv("SALVOX_SHIFT_WARPS");
+    return e ? std::atoi(e) : 2;
+  }();
+  if (P.method == SALVOX_METHOD_SHIFT && shift_warps == 4)
+    shift_kernel<4><<<(P.n_seeds + 3) / 4, 128, 0, ctx->stream>>>(P);
+  else if (P.method == SALVOX_METHOD_SHIFT && shift_warps == 2)
+    shift_kernel<2><<<(P.n_seeds + 1) / 2, 64, 0, ctx->stream>>>(P);
+  else if (P.method == SALVOX_METHOD_SHIFT)
+    shift_kernel<1><<<P.n_seeds, 32, 0, ctx->stream>>>(P);
   else if (P.method == SALVOX_METHOD_QUADRANT)
     ascent_kernel<4><<<P.n_seeds, 128, 0, ctx->stream>>>(P);
   else
