@@ -203,6 +203,18 @@ SALVOX_API int salvox_detect_batch_device(salvox_ctx* ctx, const float* d_volume
                                const salvox_detect_params* params, salvox_detection* out,
                                int64_t cap, int64_t* n_out, uint64_t* visits);
 
+/* One rank's share of detect() on a replicated volume: the
+ * seeds/trajectories of detect's plan (pipeline.cpp:311-381) with plan position
+ * j % world == rank, per-seed detections in increasing j. The caller gathers
+ * the shards (position j = rank + world * i), restores plan order and runs
+ * salvox_select once on the whole population, because the thresholds are
+ * global quantiles (pipeline.cpp:389-399). n_total = size of the whole plan. */
+SALVOX_API int salvox_detect_shard(salvox_ctx* ctx, const float* volume, int32_t nx, int32_t ny,
+                                   int32_t nz, const salvox_window* iw,
+                                   const salvox_detect_params* params, int32_t rank,
+                                   int32_t world, salvox_detection* per_seed, int64_t cap,
+                                   int64_t* n_local, int64_t* n_total, uint64_t* visits);
+
 /* Per-seed seek only (saliency_shift shift.hpp:57-59 / quadrant_seek
  * quadrant.hpp:73-76 / octant), seeds given explicitly: positions (3 per seed),
  * seed_scales (shift: isotropic half extent s, window (s,s,s) or (s,s,1) in 2D;

@@ -6,7 +6,8 @@ hand-written sm_100a kernels behind the C-ABI in include/salvox_capi.h.
 """
 from ._lib import (DET_DTYPE, MAX_DTYPE, Context, SalvoxCudaError, SalvoxError,
                    default_context)
-from .api import (DEFAULT_BUDGET, dedupe_top_k, detect, detect_records, detection_to_dict,
+from .api import (DEFAULT_BUDGET, dedupe_top_k, detect, detect_batch_device, detect_records,
+                  detect_shard, detection_to_dict,
                   exhaustive_debug_hist, kadir_brady_exhaustive, kadir_brady_exhaustive_records,
                   kadir_brady_exhaustive_slab, make_phantom, plan_seeds, quadrant_seek,
                   saliency_shift, seek_records, select)

@@ -92,7 +92,8 @@ EXPORTS = [
     "salvox_ctx_set_stream", "salvox_ctx_launch_count", "salvox_exhaustive",
     "salvox_exhaustive_slab", "salvox_exhaustive_device", "salvox_exhaustive_slab_device",
     "salvox_last_maxima",
-    "salvox_exhaustive_debug_hist", "salvox_detect", "salvox_detect_batch_device", "salvox_seek",
+    "salvox_exhaustive_debug_hist", "salvox_detect", "salvox_detect_batch_device",
+    "salvox_detect_shard", "salvox_seek",
     "salvox_select", "salvox_dedupe_top_k", "salvox_plan_seeds", "salvox_make_phantom",
     "salvox_ascent_seek",
 ]

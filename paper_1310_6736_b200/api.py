@@ -224,6 +224,53 @@ def detect_records(volume, method="shift", seed_spacing=16.0, scales=(8.0,), k=2
             int(visits.value))
 
 
+def detect_batch_device(d_volumes, batch, shape_zyx, method="shift", seed_spacing=16.0,
+                        scales=(8.0,), k=20, dedupe_radius=5.0, window_low=None,
+                        window_high=None, bins=64, entropy_quantile=0.9, pdf_quantile=0.0,
+                        workers=1, ctx=None, **extra):
+    """detect() over `batch` device-resident volumes stored back to back at the
+    device address d_volumes (an int, e.g. torch_tensor.data_ptr()): one seek
+    launch covers every volume -> ([selected DET_DTYPE per volume], visits)."""
+    nz, ny, nx = shape_zyx if len(shape_zyx) == 3 else (1,) + tuple(shape_zyx)
+    iw = _window(window_low, window_high, bins)
+    P, keep = _detect_params(method, seed_spacing, scales, k, dedupe_radius, entropy_quantile,
+                             pdf_quantile, workers, **extra)
+    kk = max(int(k), 1)
+    out = np.empty(max(batch, 1) * kk, DET_DTYPE)
+    n_out = np.zeros(max(batch, 1), np.int64)
+    visits = C.c_uint64(0)
+    check(_lib.load().salvox_detect_batch_device(
+        _ctx(ctx).handle, C.c_void_p(int(d_volumes)), int(batch), nx, ny, nz, C.byref(iw),
+        C.byref(P), ptr(out), kk, ptr(n_out), C.byref(visits)))
+    del keep
+    return [out[v * kk: v * kk + n_out[v]].copy() for v in range(batch)], int(visits.value)
+
+
+def detect_shard(volume, rank, world, method="shift", seed_spacing=16.0, scales=(8.0,), k=20,
+                 dedupe_radius=5.0, window_low=None, window_high=None, bins=64,
+                 entropy_quantile=0.9, pdf_quantile=0.0, workers=1, ctx=None, **extra):
+    """This rank's share of detect's plan (salvox_detect_shard): per-seed
+    detections for plan positions j % world == rank, in increasing j ->
+    (DET_DTYPE[n_local], n_total, visits)."""
+    v, nx, ny, nz = _volume(volume)
+    iw = _window(window_low, window_high, bins)
+    P, keep = _detect_params(method, seed_spacing, scales, k, dedupe_radius, entropy_quantile,
+                             pdf_quantile, workers, **extra)
+    c = _ctx(ctx)
+    ns = C.c_int64(0)
+    check(_lib.load().salvox_plan_seeds(nx, ny, nz, P.seed_mode, P.seed_spacing, P.seed_count,
+                                        C.cast(P.scales, C.c_void_p), P.n_scales, P.rng_seed,
+                                        None, None, 0, C.byref(ns)))
+    cap = ns.value // max(int(world), 1) + 1
+    out = np.empty(max(cap, 1), DET_DTYPE)
+    n_local, n_total, visits = C.c_int64(0), C.c_int64(0), C.c_uint64(0)
+    check(_lib.load().salvox_detect_shard(
+        c.handle, ptr(v), nx, ny, nz, C.byref(iw), C.byref(P), int(rank), int(world), ptr(out),
+        cap, C.byref(n_local), C.byref(n_total), C.byref(visits)))
+    del keep
+    return out[: n_local.value].copy(), int(n_total.value), int(visits.value)
+
+
 def detect(volume, method="shift", seed_spacing=16.0, scales=(8.0,), k=20, dedupe_radius=5.0,
            window_low=None, window_high=None, bins=64, entropy_quantile=0.9, pdf_quantile=0.0,
            workers=1, ctx=None, **extra):

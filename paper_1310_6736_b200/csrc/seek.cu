@@ -55,7 +55,7 @@ struct SeedIn {
   int geom;        // shift: ScaleGeom index of the seed's scale
   int seed_index;
   int slot;        // output row (launch order is longest-window-first)
-  int pad_;
+  int vol;         // volume of a batch (bins at binvol + vol * vol_stride)
 };
 
 struct SeekParams {
@@ -66,7 +66,8 @@ struct SeekParams {
   int n_ascent;
   int ascent_scales[64];
   int geom_of_k[129];   // ascent post-scoring: ScaleGeom index for window half-size k
-  const uint8_t* binvol;  // bin + 1, x fastest, pitch nx
+  const uint8_t* binvol;  // bin + 1, x fastest, pitch nx; batches back to back
+  size_t vol_stride;
   const double* q;        // target pmf (bins)
   const ScaleGeom* geoms;
   const SeedIn* seeds;
@@ -75,6 +76,7 @@ struct SeekParams {
   unsigned long long* visits;
   salvox_ascent_result* ascent_out;  // raw ascent results (salvox_ascent_seek), nullable
   int post_score;                    // ascent: score the converged window (detect)
+  int asc_warp_bytes;                // ascent level tables: dynamic smem per warp
 };
 
 struct WarpScratch {
@@ -177,8 +179,8 @@ __device__ __forceinline__ double kernel_step_weight(int k, double d) {  // kern
   return 1.0;
 }
 
-__device__ __forceinline__ int bin_at(const SeekParams& P, int x, int y, int z) {
-  return (int)__ldg(P.binvol + ((size_t)z * P.ny + y) * P.nx + x) - 1;
+__device__ __forceinline__ int bin_at(const SeekParams& P, const uint8_t* vb, int x, int y, int z) {
+  return (int)__ldg(vb + ((size_t)z * P.ny + y) * P.nx + x) - 1;
 }
 
 // try_candidate_histogram (window.cpp:5-19): sequential per-bin fp64 masses in
@@ -187,7 +189,7 @@ __device__ __forceinline__ int bin_at(const SeekParams& P, int x, int y, int z) 
 // shared memory in z->y->x order; lane l owns bins l and l+32 and walks the
 // compacted list with broadcast loads, adding the matching masses in order into
 // register accumulators. The only serial dependency is the fp64 add chain.
-__device__ bool warp_candidate_hist(const SeekParams& P, WarpScratch& s, const double c[3],
+__device__ bool warp_candidate_hist(const SeekParams& P, const uint8_t* vb, WarpScratch& s, const double c[3],
                                     const WinGeom& g, int kernel, int lane, unsigned* support_out,
                                     long long* visited) {
   const int M = P.bins;
@@ -208,7 +210,7 @@ __device__ bool warp_candidate_hist(const SeekParams& P, WarpScratch& s, const d
         const double d = maha(g, c, x[j], y[j], z[j]);
         in[j] = d <= 1.0;
         if (in[j]) {
-          bin[j] = bin_at(P, x[j], y[j], z[j]);
+          bin[j] = bin_at(P, vb, x[j], y[j], z[j]);
           val[j] = __dmul_rn(g.det_fac, kernel_value(kernel, d));
         }
       }
@@ -280,7 +282,7 @@ __device__ __forceinline__ double dclamp(double v, double hi) {
 // Final scores shared by shift and the ascent methods: entropy of p_score
 // (Epanechnikov), Bhattacharyya of p_step vs q, pdf_difference (identity).
 // p_step must already be in s.p. Returns false if a histogram is degenerate.
-__device__ bool warp_final_scores(const SeekParams& P, WarpScratch& s, const double c[3],
+__device__ bool warp_final_scores(const SeekParams& P, const uint8_t* vb, WarpScratch& s, const double c[3],
                                   const ScaleGeom& sg, int lane, bool have_pstep,
                                   salvox_detection& d, unsigned long long& visits,
                                   bool pstep_from_shift) {
@@ -295,7 +297,7 @@ __device__ bool warp_final_scores(const SeekParams& P, WarpScratch& s, const dou
     rho = rho < 1.0 ? rho : 1.0;
   }
   rho = __shfl_sync(kFull, rho, 0);
-  const bool ok_score = warp_candidate_hist(P, s, c, sg.main, 1, lane, &sup, &vis);
+  const bool ok_score = warp_candidate_hist(P, vb, s, c, sg.main, 1, lane, &sup, &vis);
   visits += (unsigned long long)vis;
   if (pstep_from_shift) visits += (unsigned long long)vis;  // reference recomputes p_step
   bool ok = true;
@@ -308,11 +310,11 @@ __device__ bool warp_final_scores(const SeekParams& P, WarpScratch& s, const dou
   // pdf_difference: both flanks are evaluated before the check (window.cpp:37-39)
   double pdf = 0.0;
   if (sg.pdf_ok) {
-    const bool ok_lo = warp_candidate_hist(P, s, c, sg.lo, 0, lane, &sup, &vis);
+    const bool ok_lo = warp_candidate_hist(P, vb, s, c, sg.lo, 0, lane, &sup, &vis);
     visits += (unsigned long long)vis;
     for (int b = lane; b < M; b += 32) s.w[b] = s.p[b];
     __syncwarp();
-    const bool ok_hi = warp_candidate_hist(P, s, c, sg.hi, 0, lane, &sup, &vis);
+    const bool ok_hi = warp_candidate_hist(P, vb, s, c, sg.hi, 0, lane, &sup, &vis);
     visits += (unsigned long long)vis;
     if (ok_lo && ok_hi) {
       double l1 = 0.0;
@@ -339,6 +341,7 @@ __global__ void __launch_bounds__(32 * NW) shift_kernel(const SeekParams P) {
   if (seed >= P.n_seeds) return;
   WarpScratch& s = scratch[wid];
   const SeedIn si = P.seeds[seed];
+  const uint8_t* vb = P.binvol + (size_t)si.vol * P.vol_stride;
   const ScaleGeom& sg = P.geoms[si.geom];
   const int M = P.bins;
   const double lim[3] = {(double)(P.nx - 1), (double)(P.ny - 1), (double)(P.nz - 1)};
@@ -351,7 +354,7 @@ __global__ void __launch_bounds__(32 * NW) shift_kernel(const SeekParams P) {
 
   unsigned support;
   long long vis;
-  bool ok = warp_candidate_hist(P, s, c, sg.main, P.hist_kernel, lane, &support, &vis);
+  bool ok = warp_candidate_hist(P, vb, s, c, sg.main, P.hist_kernel, lane, &support, &vis);
   // inbounds_support_fraction at the clamped seed (shift.cpp:53-57)
   auto frac_bad = [&](unsigned sup) {
     if (sg.main.support_volume <= 0.0) return 0.0 < P.min_frac;
@@ -390,7 +393,7 @@ __global__ void __launch_bounds__(32 * NW) shift_kernel(const SeekParams P) {
             const double dd = maha(sg.main, c, x[j], y[j], z[j]);
             in[j] = dd <= 1.0;
             if (in[j])
-              g[j] = __dmul_rn(kernel_step_weight(P.step_kernel, dd), s.w[bin_at(P, x[j], y[j], z[j])]);
+              g[j] = __dmul_rn(kernel_step_weight(P.step_kernel, dd), s.w[bin_at(P, vb, x[j], y[j], z[j])]);
           }
         }
         int off = 0;
@@ -437,7 +440,7 @@ __global__ void __launch_bounds__(32 * NW) shift_kernel(const SeekParams P) {
       c[2] = cl[2];
       // histogram at the new centre: its support count is the in-bounds
       // fraction check (shift.cpp:75) and its pmf the next step's p.
-      ok = warp_candidate_hist(P, s, c, sg.main, P.hist_kernel, lane, &support, &vis);
+      ok = warp_candidate_hist(P, vb, s, c, sg.main, P.hist_kernel, lane, &support, &vis);
       if (frac_bad(support)) {
         degenerate = true;
         break;
@@ -453,7 +456,7 @@ __global__ void __launch_bounds__(32 * NW) shift_kernel(const SeekParams P) {
   d.center[1] = c[1];
   d.center[2] = c[2];
   if (!degenerate) {
-    if (!warp_final_scores(P, s, c, sg, lane, ok, d, visits, true))
+    if (!warp_final_scores(P, vb, s, c, sg, lane, ok, d, visits, true))
       d.flags |= SALVOX_FLAG_DEGENERATE;
   }
   if (lane == 0) {
@@ -475,11 +478,11 @@ __device__ __forceinline__ void axis_range(double p, double dk, int n, int* lo, 
 
 // Adds the voxels of box B that are not in box A (A subset of B, or A empty)
 // to the per-octant counts.
-__device__ void warp_count_shell(const SeekParams& P, unsigned* cnt, const Box& A, const Box& B,
+__device__ void warp_count_shell(const SeekParams& P, const uint8_t* vb, unsigned* cnt, const Box& A, const Box& B,
                                  bool a_empty, int lane) {
   auto count_box = [&](const Box& bx) {
     warp_box_iter(bx, lane, [&](bool act, int x, int y, int z) {
-      if (act) atomicAdd(&cnt[bin_at(P, x, y, z)], 1u);
+      if (act) atomicAdd(&cnt[bin_at(P, vb, x, y, z)], 1u);
     });
   };
   if (a_empty) {
@@ -497,6 +500,141 @@ __device__ void warp_count_shell(const SeekParams& P, unsigned* cnt, const Box& 
   if (B.z1 > A.z1) count_box(Box{A.x0, A.x1, A.y0, A.y1, A.z1 + 1, B.z1});
 }
 
+// q = floor(n / d) for 0 <= n < 2^22, 1 <= d <= 129 through one fp32 multiply:
+// |error| of (n + 0.5) * (1/d) is below 0.5/d there, so truncation is exact.
+__device__ __forceinline__ int fdiv_small(int n, float inv_d) {
+  return (int)(((float)n + 0.5f) * inv_d);
+}
+
+// Per-warp dynamic shared memory of the level-table ascent (AscentLevels).
+struct AscentLayout {
+  __host__ __device__ static size_t a16(size_t v) { return (v + 15) & ~size_t(15); }
+  __host__ __device__ static size_t lvl() { return 0; }                      // 3 x 132 u8
+  __host__ __device__ static size_t rng() { return 400; }                    // nS x 6 int
+  __host__ __device__ static size_t boxn(int nS) { return a16(rng() + 24 * (size_t)nS); }
+  __host__ __device__ static size_t es(int nS) { return a16(boxn(nS) + 4 * (size_t)nS); }
+  __host__ __device__ static size_t cnt(int nS) { return a16(es(nS) + 8 * (size_t)nS); }
+  __host__ __device__ static size_t term(int nS, int M) { return a16(cnt(nS) + 4 * (size_t)nS * M); }
+  __host__ __device__ static size_t bytes(int nS, int M) { return a16(term(nS, M) + 8 * (size_t)nS * M); }
+};
+
+// Best (entropy, scale) of one corner-anchored direction, all scales at once.
+// The boxes [p, p + k dir] are nested in k, so every voxel of the largest box
+// has a level = the first scale whose box holds it (max over the three axes of
+// per-axis levels, tabulated per iteration). ONE pass over the largest box
+// counts (level, bin); a prefix over levels gives every scale's exact counts;
+// the nS x M terms p log p are evaluated in parallel and lanes 0..nS-1 sum
+// their scale's terms in bin order -- the same fp64 operations, in the same
+// order, as box_entropy_bits (quadrant.cpp:18-35) per scale.
+__device__ void ascent_levels(const SeekParams& P, const uint8_t* vb, unsigned char* wb,
+                              const int dir[3], const double p[3], bool two_d, int min_vox,
+                              int lane, double* best_e_out, int* best_k_out,
+                              unsigned long long* visits) {
+  const int nS = P.n_ascent, M = P.bins;
+  uint8_t* lv = wb + AscentLayout::lvl();
+  int* rng = reinterpret_cast<int*>(wb + AscentLayout::rng());
+  int* boxn = reinterpret_cast<int*>(wb + AscentLayout::boxn(nS));
+  double* es = reinterpret_cast<double*>(wb + AscentLayout::es(nS));
+  unsigned* cnt = reinterpret_cast<unsigned*>(wb + AscentLayout::cnt(nS));
+  double* term = reinterpret_cast<double*>(wb + AscentLayout::term(nS, M));
+  const int dims[3] = {P.nx, P.ny, P.nz};
+  for (int i = lane; i < nS; i += 32) {  // per-scale boxes (quadrant.cpp:20-23, 49-51)
+    const double k = (double)P.ascent_scales[i];
+    Box B;
+    axis_range(p[0], (double)dir[0] * k, P.nx, &B.x0, &B.x1);
+    axis_range(p[1], (double)dir[1] * k, P.ny, &B.y0, &B.y1);
+    axis_range(p[2], two_d ? 0.0 : (double)dir[2] * k, P.nz, &B.z0, &B.z1);
+    rng[6 * i + 0] = B.x0, rng[6 * i + 1] = B.x1, rng[6 * i + 2] = B.y0;
+    rng[6 * i + 3] = B.y1, rng[6 * i + 4] = B.z0, rng[6 * i + 5] = B.z1;
+    boxn[i] = (int)box_size(B);
+  }
+  for (int i = lane; i < nS * M; i += 32) cnt[i] = 0u;
+  __syncwarp();
+  const int* big = rng + 6 * (nS - 1);
+  const int L[3] = {big[1] - big[0] + 1, big[3] - big[2] + 1, big[5] - big[4] + 1};
+  const bool any = boxn[nS - 1] > 0;
+  if (any) {
+    for (int a = 0; a < 3; ++a)  // per-axis level of each coordinate of the largest box
+      for (int t = lane; t < L[a]; t += 32) {
+        const int x = big[2 * a] + t;
+        int i = 0;
+        while (i < nS - 1 && !(rng[6 * i + 2 * a] <= x && x <= rng[6 * i + 2 * a + 1])) ++i;
+        lv[132 * a + t] = (uint8_t)i;
+      }
+  }
+  (void)dims;
+  __syncwarp();
+  if (any) {
+    const int total = L[0] * L[1] * L[2];
+    const float ix = 1.0f / (float)L[0], iy = 1.0f / (float)L[1];
+    for (int base = 0; base < total; base += kStep) {
+      int bin[kG], lvl[kG];
+#pragma unroll
+      for (int j = 0; j < kG; ++j) {
+        const int n = base + 32 * j + lane;
+        const int nc = n < total ? n : 0;
+        const int t = fdiv_small(nc, ix);
+        const int x = nc - t * L[0];
+        const int zz = fdiv_small(t, iy);
+        const int y = t - zz * L[1];
+        bin[j] = n < total ? bin_at(P, vb, big[0] + x, big[2] + y, big[4] + zz) : -1;
+        lvl[j] = max(max((int)lv[x], (int)lv[132 + y]), (int)lv[264 + zz]);
+      }
+#pragma unroll
+      for (int j = 0; j < kG; ++j)
+        if (bin[j] >= 0) atomicAdd(&cnt[lvl[j] * M + bin[j]], 1u);
+    }
+  }
+  __syncwarp();
+  for (int b = lane; b < M; b += 32) {  // counts of box i = voxels with level <= i
+    unsigned run = 0;
+    for (int i = 0; i < nS; ++i) {
+      run += cnt[i * M + b];
+      cnt[i * M + b] = run;
+    }
+  }
+  __syncwarp();
+  const float im = 1.0f / (float)M;
+  for (int idx = lane; idx < nS * M; idx += 32) {
+    const int i = fdiv_small(idx, im);
+    const int n = boxn[i];
+    const unsigned c = cnt[idx];
+    double t = 0.0;
+    if (n > 0 && n >= min_vox && c > 0u) {  // quadrant.cpp:24-26; p = count / mass (exact mass)
+      const double pb = __ddiv_rn((double)c, (double)n);
+      t = __dmul_rn(pb, sx_log(pb));
+    }
+    term[idx] = t;
+  }
+  __syncwarp();
+  unsigned long long v = 0;
+  for (int i = lane; i < nS; i += 32) {  // entropy_bits (histogram.hpp:56-67), bin order
+    const int n = boxn[i];
+    double e = 0.0;
+    if (n > 0 && n >= min_vox) {
+      v += (unsigned long long)n;
+      for (int b = 0; b < M; ++b)
+        if (cnt[i * M + b] > 0u) e = __dsub_rn(e, term[i * M + b]);
+      e = __ddiv_rn(e < 0.0 ? 0.0 : e, kLn2);
+    }
+    es[i] = e;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  *visits += v;
+  __syncwarp();
+  double best_e = 0.0;
+  int best_k = P.ascent_scales[0];
+  for (int i = 0; i < nS; ++i)  // strict: smallest scale wins ties (quadrant.cpp:52)
+    if (es[i] > best_e) {
+      best_e = es[i];
+      best_k = P.ascent_scales[i];
+    }
+  *best_e_out = best_e;
+  *best_k_out = best_k;
+  __syncwarp();
+}
+
 // One CTA per trajectory, one warp per quadrant/octant: warp q counts its
 // corner-anchored boxes for every scale (nested in k, so only the shell
 // B_k \ B_{k-1} is counted) and evaluates their entropies; thread 0 combines the
@@ -508,9 +646,10 @@ struct AscentWarp {
   double w[kMaxBins];
 };
 
-template <int NQ>
-__global__ void __launch_bounds__(32 * NQ) ascent_kernel(const SeekParams P) {
-  __shared__ AscentWarp aw[NQ];
+template <int NQ, bool LV>
+__global__ void __launch_bounds__(32 * NQ, 24 / NQ) ascent_kernel(const SeekParams P) {
+  extern __shared__ __align__(16) unsigned char asc_dyn[];
+  __shared__ AscentWarp aw[LV ? 1 : NQ];
   __shared__ WarpScratch ps[3];
   __shared__ double ent[NQ];
   __shared__ int bk[NQ];
@@ -524,17 +663,23 @@ __global__ void __launch_bounds__(32 * NQ) ascent_kernel(const SeekParams P) {
   const int seed = blockIdx.x;
   if (seed >= P.n_seeds) return;  // uniform per CTA
   const SeedIn si = P.seeds[seed];
+  const uint8_t* vb = P.binvol + (size_t)si.vol * P.vol_stride;
   const int M = P.bins;
   const bool two_d = NQ == 4;
   const int min_vox = two_d ? 4 : 8;
   const double lim[3] = {(double)(P.nx - 1), (double)(P.ny - 1), (double)(P.nz - 1)};
   double p[3] = {si.pos[0], si.pos[1], si.pos[2]};
   unsigned long long visits = 0;
-  AscentWarp& s = aw[q];
+  AscentWarp& s = aw[LV ? 0 : q];
   int iters = 0;
   for (int it = 0; it < P.max_iters; ++it) {
     double best_e = 0.0;
     int best_k = P.ascent_scales[0];
+    if (LV) {
+      const int dir[3] = {c_dirs[q][0], c_dirs[q][1], c_dirs[q][2]};
+      ascent_levels(P, vb, asc_dyn + (size_t)q * P.asc_warp_bytes, dir, p, two_d, min_vox, lane,
+                    &best_e, &best_k, &visits);
+    } else {
     for (int b = lane; b < M; b += 32) s.cnt[b] = 0u;
     __syncwarp();
     Box prev{0, -1, 0, -1, 0, -1};
@@ -551,7 +696,7 @@ __global__ void __launch_bounds__(32 * NQ) ascent_kernel(const SeekParams P) {
       }
       const long long count = box_size(B);
       if (count > 0) {
-        warp_count_shell(P, s.cnt, prev, B, prev_empty, lane);
+        warp_count_shell(P, vb, s.cnt, prev, B, prev_empty, lane);
         prev = B;
         prev_empty = false;
       }
@@ -568,6 +713,7 @@ __global__ void __launch_bounds__(32 * NQ) ascent_kernel(const SeekParams P) {
         best_e = e;
         best_k = k;
       }
+    }
     }
     if (lane == 0) {
       ent[q] = best_e;
@@ -617,7 +763,7 @@ __global__ void __launch_bounds__(32 * NQ) ascent_kernel(const SeekParams P) {
     long long v;
     WarpScratch& w = ps[q];
     if (q == 0) {  // Epanechnikov histogram: entropy + Bhattacharyya vs uniform
-      const bool okp = warp_candidate_hist(P, w, c, sg.main, 1, lane, &sup, &v);
+      const bool okp = warp_candidate_hist(P, vb, w, c, sg.main, 1, lane, &sup, &v);
       visits += (unsigned long long)v;
       double rho = 0.0, e = 0.0;
       if (okp) {
@@ -633,7 +779,7 @@ __global__ void __launch_bounds__(32 * NQ) ascent_kernel(const SeekParams P) {
         score[1] = rho;
       }
     } else if (sg.pdf_ok) {  // pdf_difference flanks (window.cpp:37-39), both evaluated
-      const bool ok = warp_candidate_hist(P, w, c, q == 1 ? sg.lo : sg.hi, 0, lane, &sup, &v);
+      const bool ok = warp_candidate_hist(P, vb, w, c, q == 1 ? sg.lo : sg.hi, 0, lane, &sup, &v);
       visits += (unsigned long long)v;
       if (lane == 0) okf[q] = ok;
     } else if (lane == 0) {
@@ -864,12 +1010,38 @@ void build_job(int nx, int ny, int nz, const salvox_detect_params* prm,
   }
 }
 
+// Level-table ascent when its per-warp tables fit (<= 160 KB per CTA), else the
+// shell-by-shell kernel (many scales x many bins).
+template <int NQ>
+void launch_ascent_nq(salvox_ctx* ctx, SeekParams& P) {
+  const size_t per_warp = AscentLayout::bytes(P.n_ascent, P.bins);
+  static const bool force_shell = std::getenv("SALVOX_ASCENT_SHELL") != nullptr;
+  if (!force_shell && per_warp * NQ <= 160 * 1024) {
+    P.asc_warp_bytes = (int)per_warp;
+    const int dyn = (int)(per_warp * NQ);
+    SX_CUDA(cudaFuncSetAttribute(ascent_kernel<NQ, true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
+    ascent_kernel<NQ, true><<<P.n_seeds, 32 * NQ, dyn, ctx->stream>>>(P);
+  } else {
+    P.asc_warp_bytes = 0;
+    ascent_kernel<NQ, false><<<P.n_seeds, 32 * NQ, 0, ctx->stream>>>(P);
+  }
+}
+
+void launch_ascent(salvox_ctx* ctx, SeekParams& P) {
+  if (P.method == SALVOX_METHOD_QUADRANT)
+    launch_ascent_nq<4>(ctx, P);
+  else
+    launch_ascent_nq<8>(ctx, P);
+}
+
 // Runs the seek kernel for one volume whose bins are already on the device.
 void run_seek(salvox_ctx* ctx, SeekJob& job, const uint8_t* d_bins, int bins, const double* d_q,
               salvox_detection* d_out, unsigned long long* d_visits) {
   SeekParams& P = job.P;
   P.bins = bins;
   P.binvol = d_bins;
+  P.vol_stride = (size_t)P.nx * P.ny * P.nz;
   P.q = d_q;
   P.n_seeds = (int)job.seeds.size();
   P.out = d_out;
@@ -893,23 +1065,22 @@ void run_seek(salvox_ctx* ctx, SeekJob& job, const uint8_t* d_bins, int bins, co
     shift_kernel<2><<<(P.n_seeds + 1) / 2, 64, 0, ctx->stream>>>(P);
   else if (P.method == SALVOX_METHOD_SHIFT)
     shift_kernel<1><<<P.n_seeds, 32, 0, ctx->stream>>>(P);
-  else if (P.method == SALVOX_METHOD_QUADRANT)
-    ascent_kernel<4><<<P.n_seeds, 128, 0, ctx->stream>>>(P);
   else
-    ascent_kernel<8><<<P.n_seeds, 256, 0, ctx->stream>>>(P);
+    launch_ascent(ctx, P);
   SX_LAUNCH_CHECK(ctx);
 }
 
-// Uploads the volume, bins it (K1, pitch nx) and the target pmf.
-const uint8_t* prepare_volume(salvox_ctx* ctx, const float* d_vol, int nx, int ny, int nz,
-                              const salvox_window* iw, double* d_q_out_host_unused,
-                              const double* target, double** d_q) {
-  (void)d_q_out_host_unused;
+// Bins one device volume (K1, pitch nx) into d_bins (n bytes).
+void bin_into(salvox_ctx* ctx, const float* d_vol, int nx, int ny, int nz, const salvox_window* iw,
+              uint8_t* d_bins) {
   double low = iw->low, high = iw->high;
   const size_t n = (size_t)nx * ny * nz;
   if (iw->full_range) device_full_range(ctx, d_vol, n, &low, &high);
-  uint8_t* d_bins = static_cast<uint8_t*>(ctx->d_seek_bins.ensure(n));
   launch_bin_volume(ctx, d_vol, d_bins, nx, ny, nz, nx, low, high, iw->bins);
+}
+
+// Uploads the target pmf (uniform unless given).
+double* upload_target(salvox_ctx* ctx, const salvox_window* iw, const double* target) {
   std::vector<double> q(iw->bins);
   if (target) {  // histogram_from_array normalizes (bindings/py_module.cpp:48-55)
     double s = 0.0;
@@ -919,10 +1090,36 @@ const uint8_t* prepare_volume(salvox_ctx* ctx, const float* d_vol, int nx, int n
   } else {
     for (int b = 0; b < iw->bins; ++b) q[b] = 1.0 / iw->bins;  // Histogram::uniform
   }
-  *d_q = static_cast<double*>(ctx->d_target.ensure(q.size() * 8));
-  SX_CUDA(cudaMemcpyAsync(*d_q, q.data(), q.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+  double* d_q = static_cast<double*>(ctx->d_target.ensure(q.size() * 8));
+  SX_CUDA(cudaMemcpyAsync(d_q, q.data(), q.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
   SX_CUDA(cudaStreamSynchronize(ctx->stream));  // q lives on this stack frame
+  return d_q;
+}
+
+// Bins a device volume into the context's bin buffer and uploads the target pmf.
+const uint8_t* prepare_volume(salvox_ctx* ctx, const float* d_vol, int nx, int ny, int nz,
+                              const salvox_window* iw, const double* target, double** d_q) {
+  uint8_t* d_bins = static_cast<uint8_t*>(ctx->d_seek_bins.ensure((size_t)nx * ny * nz));
+  bin_into(ctx, d_vol, nx, ny, nz, iw, d_bins);
+  *d_q = upload_target(ctx, iw, target);
   return d_bins;
+}
+
+// Replicates a job's seeds over `batch` volumes: one launch covers every volume,
+// output rows vol * ns + slot. The longest-window-first order is kept.
+void expand_batch(SeekJob& job, int batch) {
+  if (batch <= 1) return;
+  const int ns = (int)job.seeds.size();
+  std::vector<SeedIn> all;
+  all.reserve((size_t)ns * batch);
+  for (const SeedIn& si : job.seeds)
+    for (int v = 0; v < batch; ++v) {
+      SeedIn t = si;
+      t.vol = v;
+      t.slot = v * ns + si.slot;
+      all.push_back(t);
+    }
+  job.seeds.swap(all);
 }
 
 // Device selection: thresholds + dedupe over n detections at d_dets. Returns
@@ -1068,7 +1265,7 @@ extern "C" int salvox_detect(salvox_ctx* ctx, const float* volume, int32_t nx, i
     float* d_vol = static_cast<float*>(ctx->d_seek_vol.ensure(n * 4));
     SX_CUDA(cudaMemcpyAsync(d_vol, volume, n * 4, cudaMemcpyHostToDevice, ctx->stream));
     double* d_q = nullptr;
-    const uint8_t* d_bins = prepare_volume(ctx, d_vol, nx, ny, nz, iw, nullptr, prm->shift_target, &d_q);
+    const uint8_t* d_bins = prepare_volume(ctx, d_vol, nx, ny, nz, iw, prm->shift_target, &d_q);
     const int ns = (int)job.seeds.size();
     char* d_dets = static_cast<char*>(ctx->d_dets.ensure((size_t)(ns + 1) * (sizeof(salvox_detection) + 8) * 2 + 512));
     salvox_detection* d_all = reinterpret_cast<salvox_detection*>(d_dets);
@@ -1109,26 +1306,80 @@ extern "C" int salvox_detect_batch_device(salvox_ctx* ctx, const float* d_volume
     SX_CUDA(cudaSetDevice(ctx->device));
     const size_t n = (size_t)nx * ny * nz;
     const int ns = (int)job.seeds.size();
-    char* d_dets = static_cast<char*>(ctx->d_dets.ensure((size_t)(ns + 1) * (sizeof(salvox_detection) + 8) * 2 + 512));
+    const size_t nall = (size_t)ns * std::max(batch, 1) + 1;
+    char* d_dets = static_cast<char*>(ctx->d_dets.ensure(nall * (sizeof(salvox_detection) + 8) + (ns + 1) * sizeof(salvox_detection) + 512));
     salvox_detection* d_all = reinterpret_cast<salvox_detection*>(d_dets);
-    salvox_detection* d_kept = d_all + (ns + 1);
+    salvox_detection* d_kept = d_all + nall;
     unsigned long long* d_vis = reinterpret_cast<unsigned long long*>(d_kept + (ns + 1));
+    if (batch == 0 || ns == 0) {
+      for (int v = 0; v < batch; ++v)
+        if (n_out) n_out[v] = 0;
+      return;
+    }
+    // all volumes binned into one buffer, then ONE seek launch over batch x ns seeds
+    uint8_t* d_bins = static_cast<uint8_t*>(ctx->d_seek_bins.ensure(n * batch));
+    for (int v = 0; v < batch; ++v)
+      bin_into(ctx, d_volumes + (size_t)v * n, nx, ny, nz, iw, d_bins + (size_t)v * n);
+    const double* d_q = upload_target(ctx, iw, prm->shift_target);
+    expand_batch(job, batch);
+    run_seek(ctx, job, d_bins, iw->bins, d_q, d_all, d_vis);
     for (int v = 0; v < batch; ++v) {
-      double* d_q = nullptr;
-      const uint8_t* d_bins =
-          prepare_volume(ctx, d_volumes + (size_t)v * n, nx, ny, nz, iw, nullptr, prm->shift_target, &d_q);
-      run_seek(ctx, job, d_bins, iw->bins, d_q, d_all, d_vis);
-      const int kept = device_select(ctx, d_all, ns, prm->entropy_quantile, prm->pdf_quantile,
-                                     prm->top_k, prm->dedupe_radius, true, d_kept);
+      const int kept = device_select(ctx, d_all + (size_t)v * ns, ns, prm->entropy_quantile,
+                                     prm->pdf_quantile, prm->top_k, prm->dedupe_radius, true, d_kept);
       if (out && cap > 0 && kept > 0)
         SX_CUDA(cudaMemcpyAsync(out + (size_t)v * cap, d_kept,
                                 (size_t)std::min<int64_t>(kept, cap) * sizeof(salvox_detection),
                                 cudaMemcpyDeviceToHost, ctx->stream));
       if (n_out) n_out[v] = kept;
-      const unsigned long long vs = sum_visits(ctx, d_vis, ns);
-      if (visits) *visits += vs;
     }
+    const unsigned long long vs = sum_visits(ctx, d_vis, ns * batch);
+    if (visits) *visits += vs;
     SX_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+extern "C" int salvox_detect_shard(salvox_ctx* ctx, const float* volume, int32_t nx, int32_t ny,
+                                   int32_t nz, const salvox_window* iw,
+                                   const salvox_detect_params* prm, int32_t rank, int32_t world,
+                                   salvox_detection* per_seed, int64_t cap, int64_t* n_local,
+                                   int64_t* n_total, uint64_t* visits) {
+  return guarded([&] {
+    if (!ctx) fail(SALVOX_EINVAL, "null context");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (nx < 1 || ny < 1 || nz < 1) fail(SALVOX_EINVAL, "Volume: dims must be >= 1");
+    if (!volume) fail(SALVOX_EINVAL, "null volume");
+    if (world < 1 || rank < 0 || rank >= world) fail(SALVOX_EINVAL, "shard: need 0 <= rank < world");
+    check_method(prm, nz);
+    check_window(iw);
+    std::vector<SeedRec> all_recs, recs;
+    std::vector<int> all_index, index;
+    plan_and_dedupe(nx, ny, nz, prm, all_recs, all_index);
+    // seed-order interleave: trajectory j belongs to rank j % world
+    for (size_t j = (size_t)rank; j < all_recs.size(); j += (size_t)world) {
+      recs.push_back(all_recs[j]);
+      index.push_back(all_index[j]);
+    }
+    const int64_t ns = (int64_t)recs.size();
+    if (n_total) *n_total = (int64_t)all_recs.size();
+    if (n_local) *n_local = ns;
+    if (ns > cap || (ns > 0 && !per_seed)) fail(SALVOX_EINVAL, "shard: per_seed capacity too small");
+    SeekJob job;
+    build_job(nx, ny, nz, prm, recs, index, job);
+    if (ns == 0) return;
+    SX_CUDA(cudaSetDevice(ctx->device));
+    const size_t n = (size_t)nx * ny * nz;
+    float* d_vol = static_cast<float*>(ctx->d_seek_vol.ensure(n * 4));
+    SX_CUDA(cudaMemcpyAsync(d_vol, volume, n * 4, cudaMemcpyHostToDevice, ctx->stream));
+    double* d_q = nullptr;
+    const uint8_t* d_bins = prepare_volume(ctx, d_vol, nx, ny, nz, iw, prm->shift_target, &d_q);
+    char* d_dets = static_cast<char*>(ctx->d_dets.ensure((size_t)(ns + 1) * (sizeof(salvox_detection) + 8) + 512));
+    salvox_detection* d_all = reinterpret_cast<salvox_detection*>(d_dets);
+    unsigned long long* d_vis = reinterpret_cast<unsigned long long*>(d_all + (ns + 1));
+    run_seek(ctx, job, d_bins, iw->bins, d_q, d_all, d_vis);
+    SX_CUDA(cudaMemcpyAsync(per_seed, d_all, (size_t)ns * sizeof(salvox_detection),
+                            cudaMemcpyDeviceToHost, ctx->stream));
+    const unsigned long long v = sum_visits(ctx, d_vis, (int)ns);
+    if (visits) *visits += v;
   });
 }
 
@@ -1160,7 +1411,7 @@ extern "C" int salvox_seek(salvox_ctx* ctx, const float* volume, int32_t nx, int
     float* d_vol = static_cast<float*>(ctx->d_seek_vol.ensure(nv * 4));
     SX_CUDA(cudaMemcpyAsync(d_vol, volume, nv * 4, cudaMemcpyHostToDevice, ctx->stream));
     double* d_q = nullptr;
-    const uint8_t* d_bins = prepare_volume(ctx, d_vol, nx, ny, nz, iw, nullptr, prm->shift_target, &d_q);
+    const uint8_t* d_bins = prepare_volume(ctx, d_vol, nx, ny, nz, iw, prm->shift_target, &d_q);
     char* d_dets = static_cast<char*>(ctx->d_dets.ensure((size_t)(n + 1) * (sizeof(salvox_detection) + 8) * 2 + 512));
     salvox_detection* d_all = reinterpret_cast<salvox_detection*>(d_dets);
     unsigned long long* d_vis = reinterpret_cast<unsigned long long*>(d_all + 2 * (n + 1));
@@ -1208,7 +1459,7 @@ extern "C" int salvox_ascent_seek(salvox_ctx* ctx, const float* volume, int32_t 
     float* d_vol = static_cast<float*>(ctx->d_seek_vol.ensure(nv * 4));
     SX_CUDA(cudaMemcpyAsync(d_vol, volume, nv * 4, cudaMemcpyHostToDevice, ctx->stream));
     double* d_q = nullptr;
-    const uint8_t* d_bins = prepare_volume(ctx, d_vol, nx, ny, nz, iw, nullptr, nullptr, &d_q);
+    const uint8_t* d_bins = prepare_volume(ctx, d_vol, nx, ny, nz, iw, nullptr, &d_q);
     char* d_dets = static_cast<char*>(ctx->d_dets.ensure(
         (size_t)(n + 1) * (sizeof(salvox_detection) + 8 + sizeof(salvox_ascent_result)) + 1024));
     salvox_detection* d_all = reinterpret_cast<salvox_detection*>(d_dets);

@@ -1,4 +1,5 @@
-"""Multi-GPU z-slab sharding of the exhaustive pass.
+"""Multi-GPU sharding: z-slabs for the exhaustive pass,
+seed interleave for the seed-grid detector.
 
 One process per GPU (torch.distributed, NCCL over NVLink on the box; gloo in the
 CPU tests). Rank g owns planes [z_g, z_{g+1}); it bins the planes
@@ -9,6 +10,13 @@ all-gather of the per-slab maxima records (fixed-capacity tensors: counts first,
 then the padded records), followed by a merge in the reference's stable order
 (score descending, linear index ascending -- pipeline.cpp:163-164), so every
 N-GPU result is byte-identical to the 1-GPU one.
+
+detect_sharded replicates the volume and gives rank g the plan positions
+j % N == g (interleaved for balance: neighbouring seeds have similar
+trajectory lengths). ONE all-gather of the fixed-size detection records
+restores plan order; the population-quantile thresholds and the dedupe then
+run once on the whole population (pipeline.cpp:383-401), so the selection is
+byte-identical to the 1-GPU detect.
 """
 from __future__ import annotations
 
@@ -16,7 +24,7 @@ import math
 
 import numpy as np
 
-from ._lib import MAX_DTYPE
+from ._lib import DET_DTYPE, MAX_DTYPE
 
 
 def halo_radius(scales) -> int:
@@ -116,3 +124,69 @@ def exhaustive_sharded(volume: np.ndarray, scales, window_low, window_high, bins
     # one rank: the slab call already returns the reference's stable order
     merged = allgather_maxima(local, group, device) if world > 1 else local
     return score, best, (z0, z1), merged, visits
+
+
+def interleave_detections(parts, n_total: int) -> np.ndarray:
+    """Plan order from per-rank shards: position j = rank + world * i."""
+    world = len(parts)
+    out = np.zeros(n_total, DET_DTYPE)
+    for r, p in enumerate(parts):
+        out[r::world] = p[: len(range(r, n_total, world))]
+    return out
+
+
+def allgather_detections(local: np.ndarray, n_total: int, group=None, device=None) -> np.ndarray:
+    """The one collective of the sharded detector: all-gather of the raw
+    136-byte detection records (padded to the largest shard)."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    dev = device if device is not None else torch.device("cpu")
+    cap = (n_total + world - 1) // world
+    raw = np.zeros((max(cap, 1), DET_DTYPE.itemsize), np.uint8)
+    if len(local):
+        raw[: len(local)] = np.ascontiguousarray(local).view(np.uint8).reshape(len(local), -1)
+    buf = torch.from_numpy(raw).to(dev)
+    bufs = [torch.zeros_like(buf) for _ in range(world)]
+    dist.all_gather(bufs, buf, group=group)
+    parts = [np.ascontiguousarray(b.cpu().numpy()).view(DET_DTYPE).reshape(-1) for b in bufs]
+    return interleave_detections(parts, n_total)
+
+
+def detect_sharded(volume: np.ndarray, method="shift", seed_spacing=16.0, scales=(8.0,), k=20,
+                   dedupe_radius=5.0, window_low=None, window_high=None, bins=64,
+                   entropy_quantile=0.9, pdf_quantile=0.0, group=None, device=None,
+                   compute=None, select=None, ctx=None, **extra):
+    """detect() with the seeds interleaved over the ranks (volume replicated).
+
+    Returns (selected detections, per-seed detections in plan order, total
+    visits). `compute(rank, world) -> (local, n_total, visits)` and
+    `select(all_dets) -> selected` may replace the device calls (the CPU
+    multi-process tests inject the oracle there).
+    """
+    import torch
+    import torch.distributed as dist
+
+    from . import api
+
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    if compute is None:
+        def compute(r, w):
+            return api.detect_shard(volume, r, w, method, seed_spacing, scales, k, dedupe_radius,
+                                    window_low, window_high, bins, entropy_quantile,
+                                    pdf_quantile, ctx=ctx, **extra)
+    local, n_total, visits = compute(rank, world)
+    if world > 1:
+        all_dets = allgather_detections(local, n_total, group, device)
+        dev = device if device is not None else torch.device("cpu")
+        v = torch.tensor([visits], dtype=torch.int64, device=dev)
+        dist.all_reduce(v, group=group)
+        visits = int(v.item())
+    else:
+        all_dets = local
+    if select is None:
+        def select(d):
+            return api.select(d, entropy_quantile, pdf_quantile, k, dedupe_radius, ctx=ctx)
+    return select(all_dets), all_dets, visits

@@ -155,3 +155,30 @@ def test_octant_on_2d_and_single_scale_quadrant(sx, oracle):
         assert np.array_equal(res2[0]["position"], ref2["position"])
     finally:
         oracle.set_log_mode(0)
+
+
+@pytest.mark.parametrize("dims,scales", [
+    (3, list(range(1, 41))),   # 40 scales x 64 bins: the shell-by-shell kernel (tables > 160 KB)
+    (3, [2, 3, 5, 8, 13]),     # level-table kernel, sparse scale set
+    (2, list(range(1, 61))),   # quadrant, shell kernel
+    (2, [0, 1, 4, 9]),         # quadrant, level tables, k = 0 (empty boxes)
+])
+def test_ascent_both_kernels_match_oracle(sx, oracle, dims, scales):
+    if dims == 3:
+        vol, _ = oracle.make_phantom(phantoms.ball_3d(36, (20.0, 15.0, 17.0), 7.0, 91))
+        seeds = [[10.0, 12.0, 14.0], [25.5, 20.25, 9.0], [0.0, 35.0, 35.0]]
+    else:
+        vol, _ = oracle.make_phantom(phantoms.square_2d(80, 41.0, 37.0, 9, 64, 92))
+        seeds = [[30.0, 30.0, 0.0], [60.5, 12.25, 0.0], [0.0, 79.0, 0.0]]
+    res, _ = sx.quadrant_seek(vol, seeds, scales, 0, 64, 64, octant=dims == 3)
+    oracle.set_log_mode(1)
+    try:
+        for r, s in zip(res, seeds):
+            ref = oracle.ascent_seek_one(vol, 0, 64, 64, s if dims == 3 else s[:2], scales,
+                                         dims=dims)
+            assert np.array_equal(r["position"][:dims], np.asarray(ref["position"])[:dims])
+            assert r["iterations"] == ref["iterations"]
+            assert r["best_scale"] == ref["best_scale"]
+            assert r["entropy_bits"] == ref["entropy_bits"]
+    finally:
+        oracle.set_log_mode(0)

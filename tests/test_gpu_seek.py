@@ -159,3 +159,51 @@ def test_raw_quadrant_and_octant_seek_match_oracle(sx, oracle):
         oracle.set_log_mode(0)
     with pytest.raises(ValueError, match="must be 2D"):
         sx.quadrant_seek(np.zeros((4, 8, 8), np.float32), [[2.0, 2.0]], [2], 0, 64, 64)
+
+
+@pytest.mark.parametrize("method,kw", [
+    ("shift", dict(seed_spacing=8.0, scales=[3.0, 5.0], k=6, dedupe_radius=4.0)),
+    ("octant", dict(seed_spacing=8.0, scales=[3.0, 4.0, 5.0], k=6, dedupe_radius=4.0)),
+])
+def test_detect_shard_interleave_equals_detect(sx, oracle, method, kw):
+    """each rank's seed share, regathered in plan order and selected
+    once, equals the 1-GPU detect byte for byte (ranks run one after another
+    here: no rank waits on another)."""
+    from paper_1310_6736_b200 import sharding
+
+    vol, _ = oracle.make_phantom(phantoms.ball_3d(24, (12.0, 10.0, 13.0), 5.0, 33))
+    sel, seeds, visits = sx.detect_records(vol, method, window_low=0, window_high=64, bins=64,
+                                           per_seed=True, **kw)
+    for world in (1, 2, 3):
+        parts, vis = [], 0
+        for r in range(world):
+            loc, n_total, v = sx.detect_shard(vol, r, world, method, window_low=0,
+                                              window_high=64, bins=64, **kw)
+            assert n_total == len(seeds)
+            parts.append(loc)
+            vis += v
+        all_dets = sharding.interleave_detections(parts, n_total)
+        assert all_dets.tobytes() == seeds.tobytes()
+        got = sx.select(all_dets, 0.9, 0.0, kw["k"], kw["dedupe_radius"])
+        assert got.tobytes() == sel.tobytes()
+        assert vis == visits
+
+
+@pytest.mark.parametrize("method", ["shift", "octant"])
+def test_batch_device_equals_per_volume_detect(sx, oracle, method):
+    """salvox_detect_batch_device: one seek launch over every volume's seeds
+    equals detect() volume by volume."""
+    import torch
+
+    vols = [oracle.make_phantom(phantoms.ball_3d(20, (8.0 + i, 10.0, 9.0 + 2 * i), 4.0 + i,
+                                                 50 + i))[0] for i in range(3)]
+    kw = dict(seed_spacing=6.0, scales=[3.0, 4.0], k=5, dedupe_radius=3.0, window_low=0,
+              window_high=64, bins=64)
+    dv = torch.from_numpy(np.stack(vols)).cuda()
+    got, visits = sx.detect_batch_device(dv.data_ptr(), 3, vols[0].shape, method, **kw)
+    tot = 0
+    for v, g in zip(vols, got):
+        ref, _, vis = sx.detect_records(v, method, **kw)
+        assert g.tobytes() == ref.tobytes()
+        tot += vis
+    assert visits == tot
