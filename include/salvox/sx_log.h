@@ -16,6 +16,7 @@
 #ifndef SALVOX_SX_LOG_H
 #define SALVOX_SX_LOG_H
 
+#include <math.h>
 #include <stdint.h>
 #include <string.h>
 
@@ -97,6 +98,56 @@ SX_HD double sx_log(double x) {
   const double ln2_lo = 1.90821492927058770002e-10; /* 0x3dea39ef35793c76 */
   const double de = (double)e;
   return SX_DADD(SX_DMUL(de, ln2_hi), SX_DADD(SX_DMUL(de, ln2_lo), logm));
+}
+
+/* Natural exp, same contract as sx_log (IEEE +,-,*,/, floor and exact bit
+ * manipulation only, so host and device agree bit for bit). Used by the
+ * Gaussian kernel profile exp(-d/2) (kernel.hpp:17-36). x = k ln2 + r with
+ * k = floor(x/ln2 + 1/2) and a Cody-Waite split (k ln2_hi exact), |r| <= 0.35;
+ * exp(r) by Horner over 1/n!, n <= 14 (truncation < 2^-60); then * 2^k. Agrees
+ * with glibc exp to a few ulp (tests/test_oracle_kats.py). */
+SX_HD double sx_ldexp_exact(double v, int k) {
+  /* v * 2^k for k in [-1074, 1023]: one or two exact power-of-two scalings */
+  if (k < -1022) {
+    v = SX_DMUL(v, 2.2250738585072014e-308); /* 2^-1022 */
+    k += 1022;
+    if (k < -1022) k = -1022;
+  }
+  return SX_DMUL(v, sx_dfrombits((uint64_t)(k + 1023) << 52));
+}
+
+SX_HD double sx_exp(double x) {
+  if (x != x) return x;
+  if (x > 709.782712893384) return 1.0 / 0.0;
+  if (x < -745.1332191019412) return 0.0;
+  const double ln2_hi = 6.93147180369123816490e-01;
+  const double ln2_lo = 1.90821492927058770002e-10;
+  const double kd = floor(SX_DADD(SX_DMUL(x, 1.4426950408889634074), 0.5));
+  const double r = SX_DSUB(SX_DSUB(x, SX_DMUL(kd, ln2_hi)), SX_DMUL(kd, ln2_lo));
+  double p = 1.0 / 87178291200.0; /* 1/14! */
+  p = SX_DADD(SX_DMUL(p, r), 1.0 / 6227020800.0);
+  p = SX_DADD(SX_DMUL(p, r), 1.0 / 479001600.0);
+  p = SX_DADD(SX_DMUL(p, r), 1.0 / 39916800.0);
+  p = SX_DADD(SX_DMUL(p, r), 1.0 / 3628800.0);
+  p = SX_DADD(SX_DMUL(p, r), 1.0 / 362880.0);
+  p = SX_DADD(SX_DMUL(p, r), 1.0 / 40320.0);
+  p = SX_DADD(SX_DMUL(p, r), 1.0 / 5040.0);
+  p = SX_DADD(SX_DMUL(p, r), 1.0 / 720.0);
+  p = SX_DADD(SX_DMUL(p, r), 1.0 / 120.0);
+  p = SX_DADD(SX_DMUL(p, r), 1.0 / 24.0);
+  p = SX_DADD(SX_DMUL(p, r), 1.0 / 6.0);
+  p = SX_DADD(SX_DMUL(p, r), 0.5);
+  p = SX_DMUL(SX_DMUL(p, r), r);        /* r^2/2 + r^3/6 + ... */
+  const double er = SX_DADD(1.0, SX_DADD(r, p));
+  return sx_ldexp_exact(er, (int)kd);
+}
+
+/* x^y for x >= 0 (the only use: EllipsoidWindow::scale, window.hpp:50-56,
+ * det^(1/6) / det2^(1/4) of a bandwidth matrix the device updates). */
+SX_HD double sx_pow(double x, double y) {
+  if (x == 0.0) return y > 0.0 ? 0.0 : (y == 0.0 ? 1.0 : 1.0 / 0.0);
+  if (x == 1.0 || y == 0.0) return 1.0;
+  return sx_exp(SX_DMUL(y, sx_log(x)));
 }
 
 #endif

@@ -87,7 +87,30 @@ class _DetectParams(C.Structure):
         ("shift_step_kernel", C.c_int),
         ("shift_hist_kernel", C.c_int),
         ("shift_min_inbounds_fraction", C.c_double),
+        ("abmsod_threshold", C.c_double),
+        ("abmsod_max_iters", C.c_int),
+        ("abmsod_kernel", C.c_int),
+        ("abmsod_lambda_min", C.c_double),
+        ("abmsod_lambda_max", C.c_double),
+        ("abmsod_min_inbounds_fraction", C.c_double),
     ]
+
+
+class _AbmsodParams(C.Structure):
+    _fields_ = [
+        ("threshold", C.c_double),
+        ("max_iterations", C.c_int),
+        ("kernel", C.c_int),
+        ("lambda_min", C.c_double),
+        ("lambda_max", C.c_double),
+        ("min_inbounds_fraction", C.c_double),
+        ("target", C.c_void_p),
+    ]
+
+
+ABMSOD_ITER_DTYPE = np.dtype([("position", "<f8", (3,)), ("H", "<f8", (9,)),
+                              ("bhattacharyya", "<f8"), ("max_bhattacharyya", "<f8"),
+                              ("eig_min", "<f8"), ("eig_max", "<f8")])
 
 
 class _AscentState(C.Structure):
@@ -174,6 +197,19 @@ def _declare(L):
     L.sxo_eigen_det3.argtypes = [_f64p]
     L.sxo_log_portable.restype = C.c_double
     L.sxo_log_portable.argtypes = [C.c_double]
+    L.sxo_exp_portable.restype = C.c_double
+    L.sxo_exp_portable.argtypes = [C.c_double]
+    L.sxo_pow_portable.restype = C.c_double
+    L.sxo_pow_portable.argtypes = [C.c_double, C.c_double]
+    L.sxo_bandwidth_from_moment.restype = C.c_int
+    L.sxo_bandwidth_from_moment.argtypes = [_f64p, C.c_double, C.c_int, C.c_double, C.c_double,
+                                            _f64p]
+    L.sxo_sym_eigen3.restype = C.c_int
+    L.sxo_sym_eigen3.argtypes = [_f64p, _f64p, _f64p]
+    L.sxo_abmsod_run.restype = C.c_int
+    L.sxo_abmsod_run.argtypes = [_f32p, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_int,
+                                 _f64p, _f64p, C.POINTER(_AbmsodParams), _detp, _vp, C.c_int,
+                                 C.POINTER(C.c_int), _u64p]
 
 
 def _vol(v):
@@ -405,7 +441,8 @@ def detect(vol, low, high, bins, method="shift", seed_mode="lattice", seed_spaci
            entropy_quantile=0.9, pdf_quantile=0.0, workers=1, quadrant_eta=0.5,
            quadrant_max_iters=50, quadrant_scales=None, shift_min_step=0.1, shift_max_iters=50,
            shift_step_kernel="identity", shift_hist_kernel="identity",
-           min_inbounds_fraction=0.1):
+           min_inbounds_fraction=0.1, abmsod_threshold=1e-4, abmsod_max_iters=15,
+           abmsod_kernel="gaussian", lambda_min=4.0, lambda_max=0.0):
     """pipeline.cpp:311-402 -> (selected detections, per-seed detections, visits)."""
     v, nx, ny, nz = _vol(vol)
     sc = (C.c_double * len(scales))(*scales)
@@ -434,6 +471,12 @@ def detect(vol, low, high, bins, method="shift", seed_mode="lattice", seed_spaci
     P.shift_step_kernel = KERNELS[shift_step_kernel]
     P.shift_hist_kernel = KERNELS[shift_hist_kernel]
     P.shift_min_inbounds_fraction = min_inbounds_fraction
+    P.abmsod_threshold = abmsod_threshold
+    P.abmsod_max_iters = abmsod_max_iters
+    P.abmsod_kernel = KERNELS[abmsod_kernel]
+    P.abmsod_lambda_min = lambda_min
+    P.abmsod_lambda_max = lambda_max
+    P.abmsod_min_inbounds_fraction = min_inbounds_fraction
     ns = plan_seeds((nz, ny, nx), seed_mode, seed_spacing, seed_count, scales, rng_seed)[0].shape[0]
     per_seed = np.zeros(max(ns, 1), DET_DTYPE)
     out = np.zeros(max(ns, 1), DET_DTYPE)
@@ -445,6 +488,68 @@ def detect(vol, low, high, bins, method="shift", seed_mode="lattice", seed_spaci
     if k < 0:
         raise OracleError(err.value.decode())
     return out[:k].copy(), per_seed[: n_seed.value].copy(), int(visits[0])
+
+
+def abmsod_run(vol, low, high, bins, seed, H=None, radius=None, threshold=1e-4, max_iterations=15,
+               kernel="gaussian", lambda_min=4.0, lambda_max=0.0, min_inbounds_fraction=0.1,
+               target=None, trace=False):
+    """abmsod.cpp:43-169 -> (detection record, trace records or None, visits). The seed
+    window is H (3x3) or EllipsoidWindow::isotropic(seed, radius) (window.hpp:46-48)."""
+    v, nx, ny, nz = _vol(vol)
+    if H is None:
+        r2 = float(radius) ** 2
+        H = np.diag([r2, r2, 1.0 if nz == 1 else r2])
+    P = _AbmsodParams(threshold, max_iterations, KERNELS[kernel], lambda_min, lambda_max,
+                      min_inbounds_fraction, None)
+    t = None
+    if target is not None:
+        t = np.ascontiguousarray(target, np.float64)
+        P.target = t.ctypes.data
+    det = np.zeros(1, DET_DTYPE)
+    cap = max_iterations if trace else 0
+    tr = np.zeros(max(cap, 1), ABMSOD_ITER_DTYPE)
+    nt = C.c_int(0)
+    visits = np.zeros(1, np.uint64)
+    s = np.zeros(3)
+    s[: len(seed)] = seed
+    rc = lib().sxo_abmsod_run(v, nx, ny, nz, low, high, bins, s,
+                              np.ascontiguousarray(np.asarray(H, np.float64).reshape(9)),
+                              C.byref(P), det, tr.ctypes.data if trace else None, cap,
+                              C.byref(nt), visits)
+    if rc == -1:
+        raise OracleError("abmsod: invalid params")
+    if rc == -2:
+        raise OracleError("abmsod: eigen decomposition failed")
+    return det[0], (tr[: nt.value].copy() if trace else None), int(visits[0])
+
+
+def bandwidth_from_moment(outer, wsum, dim, lambda_min, lambda_max):
+    H = np.zeros(9)
+    rc = lib().sxo_bandwidth_from_moment(np.ascontiguousarray(outer, np.float64).reshape(9),
+                                         float(wsum), int(dim), float(lambda_min),
+                                         float(lambda_max), H)
+    if rc in (1, 2):
+        raise OracleError("bandwidth update: " + ("zero weight mass" if rc == 1 else
+                                                   "non-finite moment"))
+    if rc == 3:
+        raise OracleError("abmsod: eigen decomposition failed")
+    return H.reshape(3, 3)
+
+
+def sym_eigen3(a):
+    """SelfAdjointEigenSolver<Matrix3d> restatement -> (ascending values, vectors as columns)."""
+    vals, vecs = np.zeros(3), np.zeros(9)
+    if lib().sxo_sym_eigen3(np.ascontiguousarray(a, np.float64).reshape(9), vals, vecs) != 0:
+        raise OracleError("abmsod: eigen decomposition failed")
+    return vals, vecs.reshape(3, 3)
+
+
+def exp_portable(x):
+    return lib().sxo_exp_portable(float(x))
+
+
+def pow_portable(x, y):
+    return lib().sxo_pow_portable(float(x), float(y))
 
 
 def select(dets, q_entropy=0.9, q_pdf=0.0, k=20, radius=5.0):

@@ -13,15 +13,20 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include "../include/salvox/sx_eig3.h"
 #include "../include/salvox/sx_log.h"
 
 #define LN2_STD 0.693147180559945309417232121458176568 /* std::numbers::ln2 */
 #define PI_STD 3.141592653589793238462643383279502884  /* std::numbers::pi */
 
-static int g_log_mode = 0; /* 0 glibc log (reference), 1 sx_log (shared host/device) */
+static int g_log_mode = 0; /* bit set: 1 sx_log, 2 sx_exp, 4 sx_pow (else glibc) */
 void sxo_set_log_mode(int mode) { g_log_mode = mode; }
-static double olog(double x) { return g_log_mode ? sx_log(x) : log(x); }
+static double olog(double x) { return (g_log_mode & 1) ? sx_log(x) : log(x); }
+static double oexp(double x) { return (g_log_mode & 2) ? sx_exp(x) : exp(x); }
+static double opow(double x, double y) { return (g_log_mode & 4) ? sx_pow(x, y) : pow(x, y); }
 double sxo_log_portable(double x) { return sx_log(x); }
+double sxo_exp_portable(double x) { return sx_exp(x); }
+double sxo_pow_portable(double x, double y) { return sx_pow(x, y); }
 
 static void set_err(char* err, int len, const char* msg) {
   if (err && len > 0) {
@@ -226,10 +231,10 @@ static double bhattacharyya(const double* p, const double* q, int bins) { /* :95
 static double kernel_value(int k, double d) { /* kernel.hpp:17-24 */
   if (k == 0) return d;
   if (k == 1) return 1.0 - d;
-  return exp(-0.5 * d);
+  return oexp(-0.5 * d);
 }
 static double kernel_step_weight(int k, double d) { /* kernel.hpp:29-36 */
-  if (k == 2) return 0.5 * exp(-0.5 * d);
+  if (k == 2) return 0.5 * oexp(-0.5 * d);
   return 1.0;
 }
 
@@ -612,10 +617,10 @@ typedef struct {
 static double win_scale(const ewin* w, int two_d) { /* window.hpp:50-56 */
   if (two_d) {
     const double det2 = w->H[0] * w->H[4] - w->H[1] * w->H[3];
-    return pow(det2 > 0.0 ? det2 : 0.0, 0.25);
+    return opow(det2 > 0.0 ? det2 : 0.0, 0.25);
   }
   const double det = sxo_eigen_det3(w->H);
-  return pow(det > 0.0 ? det : 0.0, 1.0 / 6.0);
+  return opow(det > 0.0 ? det : 0.0, 1.0 / 6.0);
 }
 static ewin win_scaled_to(const ewin* w, double s_new, int two_d) { /* window.hpp:59-66 */
   const double s = win_scale(w, two_d);
@@ -1108,6 +1113,189 @@ int64_t sxo_select(const sxo_detection* dets, int64_t n, double q_entropy, doubl
   return r;
 }
 
+/* ------------------------------------------------------------ abmsod.cpp:23-169 */
+int sxo_bandwidth_from_moment(const double outer[9], double wsum, int dim, double lambda_min,
+                              double lambda_max, double H[9]) {
+  return sx_bandwidth_from_moment(outer, wsum, dim, lambda_min, lambda_max, H);
+}
+int sxo_sym_eigen3(const double a[9], double values[3], double vectors[9]) {
+  return sx_sym_eigen3(a, values, vectors);
+}
+
+typedef struct {
+  const vview* v;
+  double low, high;
+  int bins;
+  const double* p;
+  const double* q;
+  double xn[3];
+  double outer[9], wsum;
+} bw_ctx;
+static void bw_fn(void* c, int x, int y, int z, double d) { /* abmsod.cpp:50-55 */
+  (void)d;
+  bw_ctx* b = (bw_ctx*)c;
+  const float val = b->v->vol[(size_t)x + (size_t)b->v->nx * ((size_t)y + (size_t)b->v->ny * z)];
+  const int bin = sxo_bin_of(b->low, b->high, b->bins, val);
+  const double pb = b->p[bin] > 1e-6 ? b->p[bin] : 1e-6; /* weight_for_bin */
+  const double w = sqrt(b->q[bin] / pb);
+  const double dv[3] = {b->xn[0] - (double)x, b->xn[1] - (double)y, b->xn[2] - (double)z};
+  for (int i = 0; i < 3; ++i) /* outer += w * d * d^T: (w d_i) d_j per element */
+    for (int j = 0; j < 3; ++j) b->outer[3 * i + j] += (w * dv[i]) * dv[j];
+  b->wsum += w;
+}
+
+typedef struct {
+  const vview* v;
+  double low, high;
+  int bins, kernel;
+  const double* p;
+  const double* q;
+  double num[3], den;
+} cen_ctx;
+static void cen_fn(void* c, int x, int y, int z, double d) { /* abmsod.cpp:85-90 */
+  cen_ctx* s = (cen_ctx*)c;
+  const float val = s->v->vol[(size_t)x + (size_t)s->v->nx * ((size_t)y + (size_t)s->v->ny * z)];
+  const int b = sxo_bin_of(s->low, s->high, s->bins, val);
+  const double pb = s->p[b] > 1e-6 ? s->p[b] : 1e-6;
+  const double w = sqrt(s->q[b] / pb);
+  const double g = kernel_step_weight(s->kernel, d) * w;
+  s->num[0] += g * (double)x;
+  s->num[1] += g * (double)y;
+  s->num[2] += g * (double)z;
+  s->den += g;
+}
+
+int sxo_abmsod_run(const float* vol, int nx, int ny, int nz, double low, double high, int bins,
+                   const double seed_center[3], const double seed_H[9],
+                   const sxo_abmsod_params* P, sxo_detection* det, sxo_abmsod_iter* trace,
+                   int trace_cap, int* n_trace, uint64_t* visits) {
+  if (P->threshold <= 0.0 || P->max_iterations < 1 || P->lambda_min <= 0.0) return -1;
+  const vview v = {vol, nx, ny, nz};
+  const int two_d = nz == 1;
+  const int dim = two_d ? 2 : 3;
+  double lmax = P->lambda_max; /* lambda_max_for (abmsod.hpp:34-38) */
+  if (!(lmax > 0.0)) {
+    const int m = imax(nx, imax(ny, nz));
+    const double half = m / 2.0;
+    lmax = half * half;
+  }
+  double* q = make_target(P->target, bins);
+  double* hp = (double*)malloc(sizeof(double) * 2 * (size_t)bins);
+  double* hn = hp + bins;
+  memset(det, 0, sizeof *det);
+  det->seed_index = -1;
+  const double lim[3] = {(double)(nx - 1), (double)(ny - 1), (double)(nz - 1)};
+  double x[3], H[9], x_opt[3], H_opt[9];
+  for (int i = 0; i < 3; ++i) x[i] = dclamp(seed_center[i], 0.0, lim[i]);
+  memcpy(det->center, x, sizeof x);
+  memcpy(H, seed_H, sizeof H);
+  memcpy(det->H, H, sizeof H);
+  memcpy(x_opt, x, sizeof x);
+  memcpy(H_opt, H, sizeof H);
+  double max_bhat = 0.0;
+  int stalled = 0, any = 0, nt = 0, rc = 0;
+  for (int it = 0; it < P->max_iterations; ++it) {
+    ewin win;
+    memcpy(win.center, x, sizeof x);
+    memcpy(win.H, H, sizeof H);
+    if (inbounds_support_fraction(&v, &win) < P->min_inbounds_fraction) {
+      det->flags |= 2u;
+      break;
+    }
+    if (!try_candidate_histogram(&v, &win, low, high, bins, P->kernel, hp, visits)) {
+      det->flags |= 2u;
+      break;
+    }
+    cen_ctx cc = {&v, low, high, bins, P->kernel, hp, q, {0.0, 0.0, 0.0}, 0.0};
+    const uint64_t vis = for_each_support_voxel(&v, &win, cen_fn, &cc);
+    if (visits) *visits += vis;
+    if (cc.den <= 0.0) {
+      det->flags |= 2u;
+      break;
+    }
+    double xn[3], cl[3], df[3];
+    for (int i = 0; i < 3; ++i) xn[i] = cc.num[i] / cc.den;
+    for (int i = 0; i < 3; ++i) cl[i] = dclamp(xn[i], 0.0, lim[i]);
+    for (int i = 0; i < 3; ++i) df[i] = cl[i] - xn[i];
+    if (norm3(df) > 0.0) det->flags |= 4u;
+    memcpy(xn, cl, sizeof cl);
+    ewin moved;
+    memcpy(moved.center, xn, sizeof xn);
+    memcpy(moved.H, H, sizeof H);
+    if (!try_candidate_histogram(&v, &moved, low, high, bins, P->kernel, hn, visits)) {
+      det->flags |= 2u;
+      break;
+    }
+    bw_ctx bc;
+    memset(&bc, 0, sizeof bc);
+    bc.v = &v, bc.low = low, bc.high = high, bc.bins = bins, bc.p = hn, bc.q = q;
+    memcpy(bc.xn, xn, sizeof xn);
+    const uint64_t vb = for_each_support_voxel(&v, &moved, bw_fn, &bc);
+    if (visits) *visits += vb;
+    double Hn[9];
+    const int br = sx_bandwidth_from_moment(bc.outer, bc.wsum, dim, P->lambda_min, lmax, Hn);
+    if (br == 3) {
+      rc = -2; /* std::runtime_error escapes abmsod_run */
+      break;
+    }
+    if (br != 0) {
+      det->flags |= 2u;
+      break;
+    }
+    const double bhat = bhattacharyya(hn, q, bins);
+    any = 1;
+    det->iterations = it + 1;
+    const int improved = bhat > max_bhat + P->threshold;
+    if (bhat > max_bhat) {
+      max_bhat = bhat;
+      memcpy(x_opt, xn, sizeof xn);
+      memcpy(H_opt, Hn, sizeof Hn);
+    }
+    if (trace && nt < trace_cap) {
+      sxo_abmsod_iter* r = &trace[nt];
+      double ev[3], V[9];
+      if (sx_sym_eigen3(Hn, ev, V) != 0) {
+        rc = -2;
+        break;
+      }
+      memcpy(r->position, xn, sizeof xn);
+      memcpy(r->H, Hn, sizeof Hn);
+      r->bhattacharyya = bhat;
+      r->max_bhattacharyya = max_bhat;
+      r->eig_min = ev[0] < ev[1] ? (ev[0] < ev[2] ? ev[0] : ev[2]) : (ev[1] < ev[2] ? ev[1] : ev[2]);
+      r->eig_max = ev[0] > ev[1] ? (ev[0] > ev[2] ? ev[0] : ev[2]) : (ev[1] > ev[2] ? ev[1] : ev[2]);
+      ++nt;
+    }
+    memcpy(x, xn, sizeof xn);
+    memcpy(H, Hn, sizeof Hn);
+    stalled = improved ? 0 : stalled + 1;
+    if (stalled >= 2) {
+      det->flags |= 1u;
+      break;
+    }
+  }
+  if (rc == 0) {
+    if (any) {
+      memcpy(det->center, x_opt, sizeof x_opt);
+      memcpy(det->H, H_opt, sizeof H_opt);
+      det->bhattacharyya = max_bhat;
+      ewin ow;
+      memcpy(ow.center, x_opt, sizeof x_opt);
+      memcpy(ow.H, H_opt, sizeof H_opt);
+      if (try_candidate_histogram(&v, &ow, low, high, bins, 1, hp, visits))
+        det->entropy_bits = sxo_entropy_bits(hp, bins);
+      double pd;
+      det->pdf_diff = pdf_difference(&v, &ow, low, high, bins, 0, &pd, visits) ? pd : 0.0;
+    } else {
+      det->flags |= 2u;
+    }
+  }
+  if (n_trace) *n_trace = nt;
+  free(hp);
+  free(q);
+  return rc;
+}
+
 /* ---------------------------------------------------------- pipeline.cpp:311-402 */
 typedef struct {
   const vview* v;
@@ -1131,6 +1319,18 @@ static void run_seed(det_job* J, int64_t i, uint64_t* visits, double* hbuf) {
   const vview* v = J->v;
   const int two_d = v->nz == 1;
   sxo_detection* d = &J->out[i];
+  if (P->method == 2) { /* pipeline.cpp:371-379: isotropic seed window, abmsod_run */
+    const double s = J->sscale[i];
+    double H[9] = {s * s, 0.0, 0.0, 0.0, s * s, 0.0, 0.0, 0.0, two_d ? 1.0 : s * s};
+    sxo_abmsod_params ap = {P->abmsod_threshold, P->abmsod_max_iters, P->abmsod_kernel,
+                            P->abmsod_lambda_min, P->abmsod_lambda_max,
+                            P->abmsod_min_inbounds_fraction, NULL};
+    if (sxo_abmsod_run(v->vol, v->nx, v->ny, v->nz, J->low, J->high, J->bins, J->pos + 3 * i, H,
+                       &ap, d, NULL, 0, NULL, visits) != 0)
+      d->reserved = 1;
+    d->seed_index = (int32_t)J->index[i];
+    return;
+  }
   if (P->method == 1) { /* pipeline.cpp:360-370 */
     const double s = J->sscale[i];
     const double half[3] = {s, s, two_d ? 1.0 : s};
@@ -1203,8 +1403,13 @@ int64_t sxo_detect(const float* vol, int nx, int ny, int nz, double low, double 
     set_err(err, err_len, "detect: quadrant method requires a 2D volume (nz == 1)");
     return -1;
   }
-  if (P->method != 0 && P->method != 1 && P->method != 3) {
-    set_err(err, err_len, "oracle: method not on the hot path");
+  if (P->method < 0 || P->method > 3) {
+    set_err(err, err_len, "oracle: unknown method");
+    return -1;
+  }
+  if (P->method == 2 && (P->abmsod_threshold <= 0.0 || P->abmsod_max_iters < 1 ||
+                         P->abmsod_lambda_min <= 0.0)) {
+    set_err(err, err_len, "abmsod: invalid params");
     return -1;
   }
   const int64_t ns = sxo_plan_seeds(nx, ny, nz, P->seed_mode, P->seed_spacing, P->seed_count,
@@ -1221,7 +1426,7 @@ int64_t sxo_detect(const float* vol, int nx, int ny, int nz, double low, double 
   int64_t n = 0;
   int* qs = NULL;
   int nqs = 0;
-  if (P->method == 1) {
+  if (P->method == 1 || P->method == 2) {
     for (int64_t i = 0; i < ns; ++i) index[i] = i;
     n = ns;
   } else { /* one trajectory per distinct consecutive position (pipeline.cpp:325-331) */
@@ -1279,6 +1484,12 @@ int64_t sxo_detect(const float* vol, int nx, int ny, int nz, double low, double 
     free(t);
   }
   pthread_mutex_destroy(&J.mu);
+  for (int64_t i = 0; i < n; ++i)
+    if (dets[i].reserved) { /* abmsod.cpp:16-17 runtime_error escapes detect */
+      set_err(err, err_len, "abmsod: eigen decomposition failed");
+      free(dets), free(pos), free(sscale), free(index), free(qs);
+      return -1;
+    }
   if (visits) *visits += J.visits;
   if (n_seed_out) *n_seed_out = n;
   if (per_seed)

@@ -85,7 +85,7 @@ typedef struct {
   int32_t iterations;
   uint32_t flags;
   int32_t seed_index;
-  int32_t pad_;
+  int32_t reserved; /* oracle: 1 = abmsod eigen failure (runtime_error) */
 } sxo_detection;
 
 /* ---- seeds.cpp:7-45 ---- mode 0 lattice, 1 random. Writes positions (3 per
@@ -95,8 +95,10 @@ int64_t sxo_plan_seeds(int nx, int ny, int nz, int mode, double spacing, int cou
                        const double* scales, int n_scales, uint64_t rng_seed, double* pos,
                        double* seed_scale, int64_t cap);
 
-/* entropy variant for quadrant/octant box entropies and final scores:
- * 0 = glibc log (reference), 1 = the shared portable log (sx_log). */
+/* math variant, a bit set: 0 = glibc log/exp/pow (reference); bit 1 = the
+ * shared portable log sx_log (entropies), bit 2 = sx_exp (Gaussian kernel),
+ * bit 4 = sx_pow (EllipsoidWindow::scale) -- the device's functions
+ * (include/salvox/sx_log.h). */
 void sxo_set_log_mode(int mode);
 
 /* ---- shift.cpp:15-34 shift_step. kernels: 0 id, 1 epan, 2 gauss.
@@ -174,6 +176,13 @@ typedef struct {
   int shift_step_kernel;
   int shift_hist_kernel;
   double shift_min_inbounds_fraction;
+  /* AbmsodParams (abmsod.hpp:19-40), method 2 */
+  double abmsod_threshold;
+  int abmsod_max_iters;
+  int abmsod_kernel;
+  double abmsod_lambda_min;
+  double abmsod_lambda_max;
+  double abmsod_min_inbounds_fraction;
 } sxo_detect_params;
 int64_t sxo_detect(const float* vol, int nx, int ny, int nz, double low, double high, int bins,
                    const sxo_detect_params* params, sxo_detection* per_seed, int64_t cap_seed,
@@ -185,6 +194,38 @@ int64_t sxo_select(const sxo_detection* dets, int64_t n, double q_entropy, doubl
                    double radius, sxo_detection* out);
 int64_t sxo_dedupe_top_k(const sxo_detection* dets, int64_t n, int k, double radius,
                          sxo_detection* out);
+
+/* ---- abmsod.cpp:43-169 abmsod_run. Returns 0, -1 (AbmsodParams::validate
+ * throws), -2 (eigen decomposition failed: std::runtime_error). trace (nullable)
+ * receives up to trace_cap AbmsodIterRecords (abmsod.hpp:42-48). */
+typedef struct {
+  double threshold;
+  int max_iterations;
+  int kernel;
+  double lambda_min;
+  double lambda_max;
+  double min_inbounds_fraction;
+  const double* target; /* NULL -> uniform */
+} sxo_abmsod_params;
+typedef struct {
+  double position[3];
+  double H[9];
+  double bhattacharyya;
+  double max_bhattacharyya;
+  double eig_min;
+  double eig_max;
+} sxo_abmsod_iter;
+int sxo_abmsod_run(const float* vol, int nx, int ny, int nz, double low, double high, int bins,
+                   const double seed_center[3], const double seed_H[9],
+                   const sxo_abmsod_params* params, sxo_detection* det, sxo_abmsod_iter* trace,
+                   int trace_cap, int* n_trace, uint64_t* visits);
+/* abmsod.cpp:23-41 (0 ok, 1/2 invalid_argument, 3 runtime_error) */
+int sxo_bandwidth_from_moment(const double outer[9], double wsum, int dim, double lambda_min,
+                              double lambda_max, double H[9]);
+/* SelfAdjointEigenSolver<Matrix3d> restatement: ascending values, vectors as columns */
+int sxo_sym_eigen3(const double a[9], double values[3], double vectors[9]);
+double sxo_exp_portable(double x);
+double sxo_pow_portable(double x, double y);
 
 /* Eigen 3x3 inverse / determinant restatement (exported for tests). */
 void sxo_eigen_inverse3(const double m[9], double out[9]);

@@ -117,3 +117,23 @@ def config_c3():
                 {"shape": "ball", "center": [60.0, 60.0, 40.0], "radius": 8.0,
                  "fill": {"type": "constant", "value": 60.0}}],
             "rng_seed": 176}
+
+
+def rot_z(degrees):  # test_seek.cpp:483-488
+    a = math.radians(degrees)
+    return np.array([[math.cos(a), -math.sin(a), 0.0], [math.sin(a), math.cos(a), 0.0],
+                     [0.0, 0.0, 1.0]])
+
+
+def ellipsoid_3d(axes, seed, dim=64):  # test_seek.cpp:468-481 (ellipsoid_phantom)
+    c = (dim - 1) / 2.0
+    return {"dims": [dim, dim, dim],
+            "regions": [{"shape": "ellipsoid", "center": [c, c, c],
+                         "axes": np.asarray(axes, np.float64).tolist(),
+                         "fill": {"type": "uniform", "levels": 64}}],
+            "rng_seed": seed}
+
+
+def ellipsoid_H(axes):  # RegionSpec ellipsoid H = A A^T (phantom.cpp:198-222)
+    a = np.asarray(axes, np.float64)
+    return a @ a.T
