@@ -116,12 +116,12 @@ std::vector<Detection> detect(const Volume& v, const IntensityWindow& iw, Detect
   if (params.method == Method::Quadrant && !v.is_2d())
     throw std::invalid_argument("detect: quadrant method requires a 2D volume (nz == 1)");
   params.seeds.validate();
-  if (params.method == Method::Abmsod)
-    throw unsupported_error("detect (device): abmsod is outside the accelerated path");
   if (params.method == Method::Shift) params.shift.validate();
+  if (params.method == Method::Abmsod) params.abmsod.validate();
   salvox_detect_params p{};
   p.method = params.method == Method::Quadrant ? SALVOX_METHOD_QUADRANT
              : params.method == Method::Shift  ? SALVOX_METHOD_SHIFT
+             : params.method == Method::Abmsod ? SALVOX_METHOD_ABMSOD
                                                : SALVOX_METHOD_OCTANT;
   p.seed_mode = params.seeds.mode == SeedPlan::Mode::Lattice ? 0 : 1;
   p.seed_spacing = params.seeds.spacing;
@@ -143,10 +143,20 @@ std::vector<Detection> detect(const Volume& v, const IntensityWindow& iw, Detect
   p.shift_step_kernel = int(params.shift.step_kernel);
   p.shift_hist_kernel = int(params.shift.hist_kernel);
   p.shift_min_inbounds_fraction = params.shift.min_inbounds_fraction;
-  std::vector<double> target;
+  std::vector<double> target, atarget;
   if (params.shift.target) {
     target = params.shift.target->p;
     p.shift_target = target.data();
+  }
+  p.abmsod_threshold = params.abmsod.threshold;
+  p.abmsod_max_iters = params.abmsod.max_iterations;
+  p.abmsod_kernel = int(params.abmsod.kernel);
+  p.abmsod_lambda_min = params.abmsod.lambda_min;
+  p.abmsod_lambda_max = params.abmsod.lambda_max;
+  p.abmsod_min_inbounds_fraction = params.abmsod.min_inbounds_fraction;
+  if (params.abmsod.target) {
+    atarget = params.abmsod.target->p;
+    p.abmsod_target = atarget.data();
   }
   const salvox_window w{iw.low, iw.high, iw.bins, 0};
   std::vector<salvox_detection> out(size_t(std::max(params.top_k, 1)));

@@ -18,7 +18,7 @@
 
 namespace salvox {
 
-/// Octant is new (3D quadrant ascent); Abmsod is outside the accelerated path.
+/// Octant is new (3D quadrant ascent).
 enum class Method { Quadrant, Shift, Abmsod, Octant };
 
 Method method_from_name(const std::string& name);

@@ -45,7 +45,7 @@ extern "C" {
 
 #define SALVOX_METHOD_QUADRANT 0 /* pipeline.hpp:19 Method */
 #define SALVOX_METHOD_SHIFT 1
-#define SALVOX_METHOD_ABMSOD 2 /* out of scope: SALVOX_EUNSUPPORTED */
+#define SALVOX_METHOD_ABMSOD 2 /* abmsod.cpp */
 #define SALVOX_METHOD_OCTANT 3 /* NEW: 3D generalisation of quadrant.cpp */
 
 #define SALVOX_FLAG_CONVERGED 1u /* detection.hpp:11-15 */
@@ -111,7 +111,36 @@ typedef struct {
   int32_t reserved;
   double shift_min_inbounds_fraction;
   const double* shift_target; /* NULL -> uniform over bins */
+  /* AbmsodParams (abmsod.hpp:19-40); method SALVOX_METHOD_ABMSOD */
+  double abmsod_threshold;   /* 1e-4 */
+  int32_t abmsod_max_iters;  /* 15 */
+  int32_t abmsod_kernel;     /* 2 = gaussian */
+  double abmsod_lambda_min;  /* 4.0 */
+  double abmsod_lambda_max;  /* 0 -> (max dim / 2)^2 */
+  double abmsod_min_inbounds_fraction; /* 0.1 */
+  const double* abmsod_target; /* NULL -> uniform over bins */
 } salvox_detect_params;
+
+/* AbmsodParams for salvox_abmsod_run (abmsod.hpp:19-40). */
+typedef struct {
+  double threshold;
+  int32_t max_iterations;
+  int32_t kernel; /* 0 identity, 1 epanechnikov, 2 gaussian */
+  double lambda_min;
+  double lambda_max;
+  double min_inbounds_fraction;
+  const double* target; /* NULL -> uniform over bins */
+} salvox_abmsod_params;
+
+/* AbmsodIterRecord (abmsod.hpp:42-48); H row-major. */
+typedef struct {
+  double position[3];
+  double H[9];
+  double bhattacharyya;
+  double max_bhattacharyya;
+  double eig_min;
+  double eig_max;
+} salvox_abmsod_iter;
 
 /* ------------------------------------------------------------------ context */
 SALVOX_API const char* salvox_last_error(void);
@@ -227,6 +256,24 @@ SALVOX_API int salvox_seek(salvox_ctx* ctx, const float* volume, int32_t nx, int
                 const double* seed_positions, const double* seed_scales,
                 const double* seed_half_extents, const int32_t* seed_index, int64_t n,
                 salvox_detection* out, uint64_t* visits);
+
+/* abmsod_run (abmsod.hpp:77-79, src/abmsod.cpp:43-169) for n seeds: seed window
+ * = seed_H (9 doubles per seed, row-major) or, when seed_H is NULL,
+ * EllipsoidWindow::isotropic(seed, radii[i]) (window.hpp:46-48). One detection
+ * per seed in seed order. trace (nullable) receives max_iterations
+ * AbmsodIterRecords per seed, n_trace[i] of them valid. Eigen-solver failure
+ * -> SALVOX_ERUNTIME "abmsod: eigen decomposition failed" (it throws). */
+SALVOX_API int salvox_abmsod_run(salvox_ctx* ctx, const float* volume, int32_t nx, int32_t ny,
+                                 int32_t nz, const salvox_window* iw,
+                                 const salvox_abmsod_params* params, const double* seeds,
+                                 const double* seed_H, const double* radii, int64_t n,
+                                 salvox_detection* out, salvox_abmsod_iter* trace,
+                                 int32_t* n_trace, uint64_t* visits);
+
+/* bandwidth_from_moment (abmsod.hpp:66-70, src/abmsod.cpp:23-41): host-side 3x3
+ * math shared with the kernel (include/salvox/sx_eig3.h). */
+SALVOX_API int salvox_bandwidth_from_moment(const double* outer, double weight_sum, int32_t dim,
+                                            double lambda_min, double lambda_max, double* H);
 
 /* Raw ascent trajectories: quadrant_seek / quadrant_seek_one (quadrant.hpp:64-76,
  * src/quadrant.cpp:83-125; dims = 2, nz must be 1) or the NEW octant ascent

@@ -6,7 +6,7 @@ hand-written sm_100a kernels behind the C-ABI in include/salvox_capi.h.
 """
 from ._lib import (DET_DTYPE, MAX_DTYPE, Context, SalvoxCudaError, SalvoxError,
                    default_context)
-from .api import (DEFAULT_BUDGET, dedupe_top_k, detect, detect_batch_device, detect_records,
+from .api import (DEFAULT_BUDGET, abmsod, abmsod_records, bandwidth_from_moment, dedupe_top_k, detect, detect_batch_device, detect_records,
                   detect_shard, detection_to_dict,
                   exhaustive_debug_hist, kadir_brady_exhaustive, kadir_brady_exhaustive_records,
                   kadir_brady_exhaustive_slab, make_phantom, plan_seeds, quadrant_seek,

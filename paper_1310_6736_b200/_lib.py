@@ -83,7 +83,31 @@ class DetectParams(C.Structure):
         ("reserved", C.c_int32),
         ("shift_min_inbounds_fraction", C.c_double),
         ("shift_target", C.POINTER(C.c_double)),
+        ("abmsod_threshold", C.c_double),
+        ("abmsod_max_iters", C.c_int32),
+        ("abmsod_kernel", C.c_int32),
+        ("abmsod_lambda_min", C.c_double),
+        ("abmsod_lambda_max", C.c_double),
+        ("abmsod_min_inbounds_fraction", C.c_double),
+        ("abmsod_target", C.POINTER(C.c_double)),
     ]
+
+
+class AbmsodParams(C.Structure):
+    _fields_ = [
+        ("threshold", C.c_double),
+        ("max_iterations", C.c_int32),
+        ("kernel", C.c_int32),
+        ("lambda_min", C.c_double),
+        ("lambda_max", C.c_double),
+        ("min_inbounds_fraction", C.c_double),
+        ("target", C.POINTER(C.c_double)),
+    ]
+
+
+ABMSOD_ITER_DTYPE = np.dtype([("position", "<f8", (3,)), ("H", "<f8", (9,)),
+                              ("bhattacharyya", "<f8"), ("max_bhattacharyya", "<f8"),
+                              ("eig_min", "<f8"), ("eig_max", "<f8")])
 
 
 # Every symbol include/salvox_capi.h declares (checked by tests/test_capi_symbols.py).
@@ -95,7 +119,7 @@ EXPORTS = [
     "salvox_exhaustive_debug_hist", "salvox_detect", "salvox_detect_batch_device",
     "salvox_detect_shard", "salvox_seek",
     "salvox_select", "salvox_dedupe_top_k", "salvox_plan_seeds", "salvox_make_phantom",
-    "salvox_ascent_seek",
+    "salvox_ascent_seek", "salvox_abmsod_run", "salvox_bandwidth_from_moment",
 ]
 # include/salvox_bench.h
 BENCH_EXPORTS = ["salvox_probe_smem_peak", "salvox_ctx_set_profiling", "salvox_ctx_kernel_time"]

@@ -155,12 +155,28 @@ def exhaustive_debug_hist(voxels, bins, n_scales, ctx=None):
 
 
 # --------------------------------------------------------------------- detect (E2/E3)
+def histogram_from_array(arr):
+    """histogram_from_array (py_module.cpp:46-54): 1D, normalised by the sequential
+    bin-order mass (Histogram::normalize, histogram.hpp:21-33)."""
+    a = np.asarray(arr, np.float64)
+    if a.ndim != 1:
+        raise ValueError("expected a 1D histogram")
+    mass = 0.0
+    for v in a.tolist():
+        mass += v
+    if not mass > 0.0:
+        raise ValueError("Histogram::normalize: zero total mass")
+    return np.array([v / mass for v in a.tolist()], np.float64)
+
+
 def _detect_params(method="shift", seed_spacing=16.0, scales=(8.0,), k=20, dedupe_radius=5.0,
                    entropy_quantile=0.9, pdf_quantile=0.0, workers=1, seed_mode="lattice",
                    seed_count=400, rng_seed=0, quadrant_eta=0.5, quadrant_max_iters=50,
                    quadrant_scales=None, shift_min_step=0.1, shift_max_iters=50,
                    shift_step_kernel="identity", shift_hist_kernel="identity",
-                   min_inbounds_fraction=0.1, target=None):
+                   min_inbounds_fraction=0.1, target=None, abmsod_threshold=1e-4,
+                   abmsod_max_iters=15, abmsod_kernel="gaussian", lambda_min=4.0,
+                   lambda_max=0.0):
     keep = []
     P = _lib.DetectParams()
     P.method = METHODS[method]
@@ -189,10 +205,17 @@ def _detect_params(method="shift", seed_spacing=16.0, scales=(8.0,), k=20, dedup
     P.shift_step_kernel = KERNELS[shift_step_kernel]
     P.shift_hist_kernel = KERNELS[shift_hist_kernel]
     P.shift_min_inbounds_fraction = float(min_inbounds_fraction)
+    P.abmsod_threshold = float(abmsod_threshold)
+    P.abmsod_max_iters = int(abmsod_max_iters)
+    P.abmsod_kernel = KERNELS[abmsod_kernel]
+    P.abmsod_lambda_min = float(lambda_min)
+    P.abmsod_lambda_max = float(lambda_max)
+    P.abmsod_min_inbounds_fraction = float(min_inbounds_fraction)
     if target is not None:
-        t = np.ascontiguousarray(target, np.float64)
+        t = np.ascontiguousarray(histogram_from_array(target))
         keep.append(t)
         P.shift_target = t.ctypes.data_as(C.POINTER(C.c_double))
+        P.abmsod_target = P.shift_target
     return P, keep
 
 
@@ -339,6 +362,70 @@ def quadrant_seek(volume, seeds, scale_range, window_low=None, window_high=None,
                                          int(max_iters), ptr(s), len(s), ptr(out),
                                          C.byref(visits)))
     return out, int(visits.value)
+
+
+def abmsod_records(volume, seeds, radius=None, H=None, window_low=None, window_high=None,
+                   bins=64, max_iterations=15, threshold=1e-4, kernel="gaussian",
+                   lambda_min=4.0, lambda_max=0.0, min_inbounds_fraction=0.1, target=None,
+                   trace=False, ctx=None):
+    """abmsod_run (abmsod.hpp:77-79) for many seeds on the device. Seed windows are
+    H (3x3, or one per seed) or EllipsoidWindow::isotropic(seed, radius).
+    Returns (DET_DTYPE[n], [ABMSOD_ITER_DTYPE arrays] or None, visits)."""
+    from ._lib import ABMSOD_ITER_DTYPE, AbmsodParams
+
+    v, nx, ny, nz = _volume(volume)
+    s = np.asarray(seeds, np.float64)
+    if s.ndim == 1:
+        s = s[None]
+    if s.shape[-1] == 2:
+        s = np.concatenate([s, np.zeros(s.shape[:-1] + (1,))], axis=-1)
+    s = np.ascontiguousarray(s)
+    n = len(s)
+    hs = None if H is None else np.ascontiguousarray(
+        np.broadcast_to(np.asarray(H, np.float64).reshape(-1, 9), (n, 9)))
+    rs = None if radius is None else np.ascontiguousarray(
+        np.broadcast_to(np.asarray(radius, np.float64), (n,)))
+    if hs is None and rs is None:
+        raise ValueError("abmsod: give radius or H")
+    iw = _window(window_low, window_high, bins)
+    P = AbmsodParams(float(threshold), int(max_iterations), KERNELS[kernel], float(lambda_min),
+                     float(lambda_max), float(min_inbounds_fraction), None)
+    t = None
+    if target is not None:
+        t = np.ascontiguousarray(histogram_from_array(target))
+        P.target = t.ctypes.data_as(C.POINTER(C.c_double))
+    out = np.empty(max(n, 1), DET_DTYPE)
+    tr = np.zeros(max(n, 1) * max(int(max_iterations), 1), ABMSOD_ITER_DTYPE) if trace else None
+    tn = np.zeros(max(n, 1), np.int32) if trace else None
+    visits = C.c_uint64(0)
+    check(_lib.load().salvox_abmsod_run(_ctx(ctx).handle, ptr(v), nx, ny, nz, C.byref(iw),
+                                        C.byref(P), ptr(s), ptr(hs), ptr(rs), C.c_int64(n), ptr(out),
+                                        ptr(tr), ptr(tn), C.byref(visits)))
+    del t
+    traces = None
+    if trace:
+        m = int(max_iterations)
+        traces = [tr[i * m: i * m + tn[i]].copy() for i in range(n)]
+    return out[:n].copy(), traces, int(visits.value)
+
+
+def abmsod(volume, seed, radius, window_low=None, window_high=None, bins=64, max_iterations=15,
+           threshold=1e-4, ctx=None):
+    """abmsod (py_module.cpp:172-184): one seed, isotropic seed window -> detection dict."""
+    d, _, _ = abmsod_records(volume, [seed], radius=radius, window_low=window_low,
+                             window_high=window_high, bins=bins, max_iterations=max_iterations,
+                             threshold=threshold, ctx=ctx)
+    return detection_to_dict(d[0])
+
+
+def bandwidth_from_moment(outer, weight_sum, dim, lambda_min, lambda_max):
+    """bandwidth_from_moment (abmsod.hpp:66-70) -> H (3x3)."""
+    H = np.zeros(9)
+    o = np.ascontiguousarray(outer, np.float64).reshape(9)
+    check(_lib.load().salvox_bandwidth_from_moment(
+        ptr(o), C.c_double(weight_sum), C.c_int32(int(dim)), C.c_double(lambda_min),
+        C.c_double(lambda_max), ptr(H)))
+    return H.reshape(3, 3)
 
 
 def select(dets, entropy_quantile=0.9, pdf_quantile=0.0, k=20, dedupe_radius=5.0, ctx=None):

@@ -23,6 +23,7 @@
 #include <cmath>
 #include <map>
 
+#include "../../include/salvox/sx_eig3.h"
 #include "../../include/salvox/sx_log.h"
 #include "common.cuh"
 #include "host_math.h"
@@ -34,6 +35,7 @@ constexpr int kG = 4;            // bounding-box chunks of 32 voxels per warp st
 constexpr int kStep = 32 * kG;
 constexpr unsigned kFull = 0xffffffffu;
 constexpr double kLn2 = 0.693147180559945309417232121458176568;  // std::numbers::ln2
+constexpr double kPiD = 3.141592653589793238462643383279502884;  // std::numbers::pi
 
 struct WinGeom {
   double Hinv[9];
@@ -76,6 +78,13 @@ struct SeekParams {
   unsigned long long* visits;
   salvox_ascent_result* ascent_out;  // raw ascent results (salvox_ascent_seek), nullable
   int post_score;                    // ascent: score the converged window (detect)
+  // ABMSOD (abmsod.hpp:19-40)
+  const double* seed_H;              // 9 per output slot (row-major)
+  double abm_threshold, abm_lmin, abm_lmax, abm_min_frac;
+  int abm_max_iters, abm_kernel;
+  salvox_abmsod_iter* abm_trace;     // max_iters records per slot, nullable
+  int* abm_trace_n;
+  int* err_flag;                     // device: set when a seed's call would throw
   int asc_warp_bytes;                // ascent level tables: dynamic smem per warp
 };
 
@@ -172,10 +181,10 @@ __device__ __forceinline__ double maha(const WinGeom& g, const double c[3], int 
 __device__ __forceinline__ double kernel_value(int k, double d) {  // kernel.hpp:17-24
   if (k == 0) return d;
   if (k == 1) return __dsub_rn(1.0, d);
-  return exp(__dmul_rn(-0.5, d));
+  return sx_exp(__dmul_rn(-0.5, d));  // shared exp (sx_log.h): bit-exact vs the oracle
 }
 __device__ __forceinline__ double kernel_step_weight(int k, double d) {  // kernel.hpp:29-36
-  if (k == 2) return __dmul_rn(0.5, exp(__dmul_rn(-0.5, d)));
+  if (k == 2) return __dmul_rn(0.5, sx_exp(__dmul_rn(-0.5, d)));
   return 1.0;
 }
 
@@ -462,6 +471,336 @@ __global__ void __launch_bounds__(32 * NW) shift_kernel(const SeekParams P) {
   if (lane == 0) {
     P.out[si.slot] = d;
     P.visits[si.slot] = visits;
+  }
+}
+
+// ------------------------------------------------------------------ ABMSOD
+// abmsod_run (src/abmsod.cpp:43-169), one warp per seed: every support pass is
+// the shift kernel's compacted ordered scan; the bandwidth moment runs its 9
+// outer-product chains + the weight chain on lanes 0..9 in z->y->x order; the
+// 3x3 symmetric eigensolver and the window geometry (Eigen inverse/determinant,
+// shared exp/pow) come from include/salvox/sx_eig3.h, as in the oracle.
+__device__ void dev_make_geom(const double* H, bool two_d, WinGeom& g) {  // window.hpp:69-106
+  sx_inverse3(H, g.Hinv);
+  for (int i = 0; i < 3; ++i) g.ext[i] = __dsqrt_rn(H[4 * i] < 0.0 ? 0.0 : H[4 * i]);
+  const double det = sx_det3(H);
+  g.det_fac = __ddiv_rn(1.0, __dsqrt_rn(det < 1e-300 ? 1e-300 : det));
+  if (two_d) {
+    const double det2 = __dsub_rn(__dmul_rn(H[0], H[4]), __dmul_rn(H[1], H[3]));
+    g.support_volume = __dmul_rn(kPiD, __dsqrt_rn(det2 < 0.0 ? 0.0 : det2));
+  } else {
+    g.support_volume = __dmul_rn(4.0 / 3.0 * kPiD, __dsqrt_rn(det < 0.0 ? 0.0 : det));
+  }
+}
+
+__device__ double dev_window_scale(const double* H, bool two_d) {  // window.hpp:50-56
+  if (two_d) {
+    const double det2 = __dsub_rn(__dmul_rn(H[0], H[4]), __dmul_rn(H[1], H[3]));
+    return sx_pow(det2 < 0.0 ? 0.0 : det2, 0.25);
+  }
+  const double det = sx_det3(H);
+  return sx_pow(det < 0.0 ? 0.0 : det, 1.0 / 6.0);
+}
+
+struct AbmWarp {
+  WinGeom g;              // the current window's geometry
+  double Hc[9], Hn[9];    // current / updated bandwidth
+  double acc[10];         // moment chains (lane l writes acc[l])
+};
+
+// Centroid pass (abmsod.cpp:85-90): g = step_w(d) * w[bin]; lanes 0..3 run
+// num.x / num.y / num.z / den in support order. Returns the box visits.
+__device__ long long warp_centroid(const SeekParams& P, const uint8_t* vb, WarpScratch& s,
+                                   const double c[3], const WinGeom& wg, int step_kernel,
+                                   int lane, double num[3], double* den_out) {
+  double acc = 0.0;
+  const Box bb = window_box(c, wg, P.nx, P.ny, P.nz);
+  warp_box_iter_g(bb, lane, [&](const bool* act, const int* x, const int* y, const int* z) {
+    bool in[kG];
+    double g[kG];
+#pragma unroll
+    for (int j = 0; j < kG; ++j) {
+      in[j] = false;
+      g[j] = 0.0;
+      if (act[j]) {
+        const double dd = maha(wg, c, x[j], y[j], z[j]);
+        in[j] = dd <= 1.0;
+        if (in[j]) g[j] = __dmul_rn(kernel_step_weight(step_kernel, dd), s.w[bin_at(P, vb, x[j], y[j], z[j])]);
+      }
+    }
+    int off = 0;
+#pragma unroll
+    for (int j = 0; j < kG; ++j) {
+      const unsigned m0 = __ballot_sync(kFull, in[j]);
+      if (in[j]) {
+        const int r = off + __popc(m0 & ((1u << lane) - 1u));
+        s.v[r] = g[j];
+        s.t[0][r] = __dmul_rn(g[j], (double)x[j]);
+        s.t[1][r] = __dmul_rn(g[j], (double)y[j]);
+        s.t[2][r] = __dmul_rn(g[j], (double)z[j]);
+      }
+      off += __popc(m0);
+    }
+    __syncwarp();
+    if (lane < 4) {
+      const double* src = lane == 3 ? s.v : s.t[lane];
+#pragma unroll 4
+      for (int k = 0; k < off; ++k) acc = __dadd_rn(acc, src[k]);
+    }
+    __syncwarp();
+  });
+  num[0] = __shfl_sync(kFull, acc, 0);
+  num[1] = __shfl_sync(kFull, acc, 1);
+  num[2] = __shfl_sync(kFull, acc, 2);
+  *den_out = __shfl_sync(kFull, acc, 3);
+  return box_size(bb);
+}
+
+// bandwidth_update's moment pass (abmsod.cpp:45-56): over the support of
+// (xn, H), w = weight_for_bin(hp_new), d = xn - s, outer += (w d_i) d_j, wsum += w.
+// Lane l < 9 owns outer element l (i = l / 3, j = l % 3), lane 9 owns wsum.
+__device__ long long warp_moment(const SeekParams& P, const uint8_t* vb, WarpScratch& s,
+                                 const double xn[3], const WinGeom& wg, int lane, double* acc_out) {
+  double acc = 0.0;
+  const int li = lane < 9 ? lane / 3 : 0, lj = lane < 9 ? lane % 3 : 0;
+  const Box bb = window_box(xn, wg, P.nx, P.ny, P.nz);
+  warp_box_iter_g(bb, lane, [&](const bool* act, const int* x, const int* y, const int* z) {
+    bool in[kG];
+    double w[kG];
+#pragma unroll
+    for (int j = 0; j < kG; ++j) {
+      in[j] = false;
+      w[j] = 0.0;
+      if (act[j]) {
+        const double dd = maha(wg, xn, x[j], y[j], z[j]);
+        in[j] = dd <= 1.0;
+        if (in[j]) w[j] = s.w[bin_at(P, vb, x[j], y[j], z[j])];
+      }
+    }
+    int off = 0;
+#pragma unroll
+    for (int j = 0; j < kG; ++j) {
+      const unsigned m0 = __ballot_sync(kFull, in[j]);
+      if (in[j]) {
+        const int r = off + __popc(m0 & ((1u << lane) - 1u));
+        s.v[r] = w[j];
+        s.t[0][r] = __dsub_rn(xn[0], (double)x[j]);
+        s.t[1][r] = __dsub_rn(xn[1], (double)y[j]);
+        s.t[2][r] = __dsub_rn(xn[2], (double)z[j]);
+      }
+      off += __popc(m0);
+    }
+    __syncwarp();
+    if (lane < 9) {
+      const double* di = s.t[li];
+      const double* dj = s.t[lj];
+#pragma unroll 4
+      for (int k = 0; k < off; ++k) acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(s.v[k], di[k]), dj[k]));
+    } else if (lane == 9) {
+#pragma unroll 4
+      for (int k = 0; k < off; ++k) acc = __dadd_rn(acc, s.v[k]);
+    }
+    __syncwarp();
+  });
+  *acc_out = acc;
+  return box_size(bb);
+}
+
+__device__ __forceinline__ void warp_weights(const SeekParams& P, WarpScratch& s, int lane) {
+  for (int b = lane; b < P.bins; b += 32) {  // weight_for_bin (histogram.hpp:107-113)
+    const double pb = s.p[b] > 1e-6 ? s.p[b] : 1e-6;
+    s.w[b] = __dsqrt_rn(__ddiv_rn(P.q[b], pb));
+  }
+  __syncwarp();
+}
+
+template <int NW>
+__global__ void __launch_bounds__(32 * NW) abmsod_kernel(const SeekParams P) {
+  __shared__ WarpScratch scratch[NW];
+  __shared__ AbmWarp aws[NW];
+  const int lane = threadIdx.x & 31;
+  const int wid = threadIdx.x >> 5;
+  const int seed = blockIdx.x * NW + wid;
+  if (seed >= P.n_seeds) return;
+  WarpScratch& s = scratch[wid];
+  AbmWarp& A = aws[wid];
+  const SeedIn si = P.seeds[seed];
+  const uint8_t* vb = P.binvol + (size_t)si.vol * P.vol_stride;
+  const bool two_d = P.two_d != 0;
+  const int M = P.bins;
+  const double lim[3] = {(double)(P.nx - 1), (double)(P.ny - 1), (double)(P.nz - 1)};
+  salvox_detection d;
+  memset(&d, 0, sizeof d);
+  d.seed_index = si.seed_index;
+  double x[3] = {dclamp(si.pos[0], lim[0]), dclamp(si.pos[1], lim[1]), dclamp(si.pos[2], lim[2])};
+  d.center[0] = x[0], d.center[1] = x[1], d.center[2] = x[2];  // clamp_point(seed) (abmsod.cpp:58)
+  const double* H0 = P.seed_H + 9 * (size_t)si.slot;
+  if (lane < 9) A.Hc[lane] = H0[lane];
+  __syncwarp();
+  for (int i = 0; i < 9; ++i) d.H[i] = A.Hc[i];
+  double x_opt[3] = {x[0], x[1], x[2]};
+  double H_opt[9];
+  for (int i = 0; i < 9; ++i) H_opt[i] = A.Hc[i];
+  double max_bhat = 0.0;
+  int stalled = 0, n_trace = 0;
+  bool any = false, failed = false;
+  unsigned long long visits = 0;
+  for (int it = 0; it < P.abm_max_iters; ++it) {
+    if (lane == 0) dev_make_geom(A.Hc, two_d, A.g);
+    __syncwarp();
+    unsigned support;
+    long long vis;
+    // inbounds_support_fraction (window.cpp:54-60) = the histogram pass's support count
+    const bool ok = warp_candidate_hist(P, vb, s, x, A.g, P.abm_kernel, lane, &support, &vis);
+    double frac = 0.0;
+    if (A.g.support_volume > 0.0) {
+      frac = __ddiv_rn((double)support, A.g.support_volume);
+      frac = frac < 1.0 ? frac : 1.0;
+    }
+    if (frac < P.abm_min_frac) {
+      d.flags |= SALVOX_FLAG_DEGENERATE;
+      break;
+    }
+    visits += (unsigned long long)vis;
+    if (!ok) {
+      d.flags |= SALVOX_FLAG_DEGENERATE;
+      break;
+    }
+    warp_weights(P, s, lane);
+    double num[3], den;
+    visits += (unsigned long long)warp_centroid(P, vb, s, x, A.g, P.abm_kernel, lane, num, &den);
+    if (den <= 0.0) {
+      d.flags |= SALVOX_FLAG_DEGENERATE;
+      break;
+    }
+    const double moved[3] = {__ddiv_rn(num[0], den), __ddiv_rn(num[1], den), __ddiv_rn(num[2], den)};
+    double xn[3], df[3];
+    for (int i = 0; i < 3; ++i) xn[i] = dclamp(moved[i], lim[i]);
+    for (int i = 0; i < 3; ++i) df[i] = __dsub_rn(xn[i], moved[i]);
+    if (__dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(df[0], df[0]), __dmul_rn(df[1], df[1])),
+                             __dmul_rn(df[2], df[2]))) > 0.0)
+      d.flags |= SALVOX_FLAG_BOUNDARY_CLAMPED;
+    // histogram at the moved centre with the old H (abmsod.cpp:100-106)
+    const bool ok2 = warp_candidate_hist(P, vb, s, xn, A.g, P.abm_kernel, lane, &support, &vis);
+    visits += (unsigned long long)vis;
+    if (!ok2) {
+      d.flags |= SALVOX_FLAG_DEGENERATE;
+      break;
+    }
+    warp_weights(P, s, lane);
+    double acc;
+    visits += (unsigned long long)warp_moment(P, vb, s, xn, A.g, lane, &acc);
+    if (lane < 10) A.acc[lane] = acc;
+    __syncwarp();
+    int br = 0;
+    if (lane == 0)
+      br = sx_bandwidth_from_moment(A.acc, A.acc[9], two_d ? 2 : 3, P.abm_lmin, P.abm_lmax, A.Hn);
+    br = __shfl_sync(kFull, br, 0);
+    __syncwarp();
+    if (br == 3) {  // std::runtime_error escapes abmsod_run
+      failed = true;
+      break;
+    }
+    if (br != 0) {  // std::invalid_argument -> degenerate (abmsod.cpp:107-112)
+      d.flags |= SALVOX_FLAG_DEGENERATE;
+      break;
+    }
+    double bhat = 0.0;  // bhattacharyya(hp_new, target) (histogram.hpp:95-103)
+    if (lane == 0) {
+      for (int b = 0; b < M; ++b) bhat = __dadd_rn(bhat, __dsqrt_rn(__dmul_rn(s.p[b], P.q[b])));
+      bhat = bhat < 1.0 ? bhat : 1.0;
+    }
+    bhat = __shfl_sync(kFull, bhat, 0);
+    any = true;
+    d.iterations = it + 1;
+    const bool improved = bhat > __dadd_rn(max_bhat, P.abm_threshold);
+    if (bhat > max_bhat) {
+      max_bhat = bhat;
+      for (int i = 0; i < 3; ++i) x_opt[i] = xn[i];
+      for (int i = 0; i < 9; ++i) H_opt[i] = A.Hn[i];
+    }
+    if (P.abm_trace && lane == 0 && n_trace < P.abm_max_iters) {
+      double ev[3], V[9];
+      if (sx_sym_eigen3(A.Hn, ev, V) != 0) failed = true;
+      salvox_abmsod_iter& r = P.abm_trace[(size_t)si.slot * P.abm_max_iters + n_trace];
+      for (int i = 0; i < 3; ++i) r.position[i] = xn[i];
+      for (int i = 0; i < 9; ++i) r.H[i] = A.Hn[i];
+      r.bhattacharyya = bhat;
+      r.max_bhattacharyya = max_bhat;
+      r.eig_min = fmin(fmin(ev[0], ev[1]), ev[2]);
+      r.eig_max = fmax(fmax(ev[0], ev[1]), ev[2]);
+    }
+    if (P.abm_trace) ++n_trace;
+    failed = __shfl_sync(kFull, (int)failed, 0) != 0;
+    if (failed) break;
+    for (int i = 0; i < 3; ++i) x[i] = xn[i];
+    if (lane < 9) A.Hc[lane] = A.Hn[lane];
+    __syncwarp();
+    stalled = improved ? 0 : stalled + 1;
+    if (stalled >= 2) {
+      d.flags |= SALVOX_FLAG_CONVERGED;
+      break;
+    }
+  }
+  if (!failed) {
+    if (any) {  // score the best iterate (abmsod.cpp:154-165)
+      d.center[0] = x_opt[0], d.center[1] = x_opt[1], d.center[2] = x_opt[2];
+      for (int i = 0; i < 9; ++i) d.H[i] = H_opt[i];
+      d.bhattacharyya = max_bhat;
+      if (lane < 9) A.Hc[lane] = H_opt[lane];
+      __syncwarp();
+      if (lane == 0) dev_make_geom(A.Hc, two_d, A.g);
+      __syncwarp();
+      unsigned sup;
+      long long vis;
+      if (warp_candidate_hist(P, vb, s, x_opt, A.g, 1, lane, &sup, &vis))
+        d.entropy_bits = warp_entropy_bits(s.p, M, lane, s.w);
+      visits += (unsigned long long)vis;
+      // pdf_difference (window.cpp:30-46), Identity kernel; throws -> 0.0
+      const double sc = dev_window_scale(H_opt, two_d);
+      double pdf = 0.0;
+      if (!(__dsub_rn(sc, 1.0) < 1.0)) {
+        double l1 = 0.0;
+        bool ok_lo = false, ok_hi = false;
+        for (int f = 0; f < 2; ++f) {
+          const double s_new = f == 0 ? __dsub_rn(sc, 1.0) : __dadd_rn(sc, 1.0);
+          const double r = __ddiv_rn(s_new, sc);
+          const double fac = __dmul_rn(r, r);
+          if (lane < 9) A.Hn[lane] = __dmul_rn(H_opt[lane], fac);
+          __syncwarp();
+          if (lane == 0) {
+            if (two_d) A.Hn[8] = 1.0;
+            dev_make_geom(A.Hn, two_d, A.g);
+          }
+          __syncwarp();
+          const bool okf = warp_candidate_hist(P, vb, s, x_opt, A.g, 0, lane, &sup, &vis);
+          visits += (unsigned long long)vis;
+          if (f == 0) {
+            ok_lo = okf;
+            for (int b = lane; b < M; b += 32) s.w[b] = s.p[b];  // keep p_lo
+            __syncwarp();
+          } else {
+            ok_hi = okf;
+          }
+        }
+        if (ok_lo && ok_hi) {
+          if (lane == 0)
+            for (int b = 0; b < M; ++b) l1 = __dadd_rn(l1, fabs(__dsub_rn(s.p[b], s.w[b])));
+          l1 = __shfl_sync(kFull, l1, 0);
+          pdf = __dmul_rn(__ddiv_rn(__dmul_rn(sc, sc), 2.0), l1);
+        }
+      }
+      d.pdf_diff = pdf;
+    } else {
+      d.flags |= SALVOX_FLAG_DEGENERATE;
+    }
+  } else if (lane == 0) {
+    atomicOr(P.err_flag, 1);  // eigen decomposition failed: runtime_error for the call
+  }
+  if (lane == 0) {
+    P.out[si.slot] = d;
+    P.visits[si.slot] = visits;
+    if (P.abm_trace_n) P.abm_trace_n[si.slot] = n_trace;
   }
 }
 
@@ -913,6 +1252,7 @@ ScaleGeom make_scale_geom(const Mat3& H, bool two_d) {
 struct SeekJob {
   std::vector<SeedIn> seeds;
   std::vector<ScaleGeom> geoms;
+  std::vector<double> seed_H;  // ABMSOD: 9 per output slot
   SeekParams P{};
 };
 
@@ -969,6 +1309,40 @@ void build_job(int nx, int ny, int nz, const salvox_detect_params* prm,
     // longest-processing-time first: seeds with the largest windows launch first
     std::stable_sort(job.seeds.begin(), job.seeds.end(), [&](const SeedIn& a, const SeedIn& b) {
       return job.geoms[a.geom].main.support_volume > job.geoms[b.geom].main.support_volume;
+    });
+  } else if (method == SALVOX_METHOD_ABMSOD) {
+    // AbmsodParams::validate (abmsod.hpp:27-31)
+    if (prm->abmsod_threshold <= 0.0) fail(SALVOX_EINVAL, "abmsod: threshold must be > 0");
+    if (prm->abmsod_max_iters < 1) fail(SALVOX_EINVAL, "abmsod: max_iterations must be >= 1");
+    if (prm->abmsod_lambda_min <= 0.0) fail(SALVOX_EINVAL, "abmsod: lambda_min must be > 0");
+    if (prm->abmsod_kernel < 0 || prm->abmsod_kernel > 2) fail(SALVOX_EINVAL, "unknown kernel");
+    P.abm_threshold = prm->abmsod_threshold;
+    P.abm_max_iters = prm->abmsod_max_iters;
+    P.abm_kernel = prm->abmsod_kernel;
+    P.abm_lmin = prm->abmsod_lambda_min;
+    double lmax = prm->abmsod_lambda_max;  // lambda_max_for (abmsod.hpp:34-38)
+    if (!(lmax > 0.0)) {
+      const double half = std::max({nx, ny, nz}) / 2.0;
+      lmax = half * half;
+    }
+    P.abm_lmax = lmax;
+    P.abm_min_frac = prm->abmsod_min_inbounds_fraction;
+    job.seed_H.assign(recs.size() * 9, 0.0);
+    for (size_t i = 0; i < recs.size(); ++i) {
+      // EllipsoidWindow::isotropic(position, scale, 2D) (pipeline.cpp:373-374)
+      const double r = recs[i].scale;
+      double* H = &job.seed_H[9 * i];
+      H[0] = r * r;
+      H[4] = r * r;
+      H[8] = two_d ? 1.0 : r * r;
+      SeedIn si{};
+      std::memcpy(si.pos, recs[i].pos, sizeof si.pos);
+      si.seed_index = index[i];
+      si.slot = (int)i;
+      job.seeds.push_back(si);
+    }
+    std::stable_sort(job.seeds.begin(), job.seeds.end(), [&](const SeedIn& a, const SeedIn& b) {
+      return job.seed_H[9 * a.slot] > job.seed_H[9 * b.slot];  // larger windows first
     });
   } else {
     std::vector<int> ks;
@@ -1047,19 +1421,31 @@ void run_seek(salvox_ctx* ctx, SeekJob& job, const uint8_t* d_bins, int bins, co
   P.out = d_out;
   P.visits = d_visits;
   if (P.n_seeds == 0) return;
+  auto up = [](size_t b) { return ((b + 255) / 256) * 256; };
   const size_t gbytes = job.geoms.size() * sizeof(ScaleGeom);
   const size_t sbytes = job.seeds.size() * sizeof(SeedIn);
-  char* d_geo = static_cast<char*>(ctx->d_geom.ensure(gbytes + sbytes + 256));
-  SX_CUDA(cudaMemcpyAsync(d_geo, job.geoms.data(), gbytes, cudaMemcpyHostToDevice, ctx->stream));
-  char* d_sd = d_geo + ((gbytes + 255) / 256) * 256;
+  const size_t hbytes = job.seed_H.size() * sizeof(double);
+  char* d_geo = static_cast<char*>(ctx->d_geom.ensure(up(gbytes) + up(sbytes) + up(hbytes) + 256));
+  char* d_sd = d_geo + up(gbytes);
+  char* d_h = d_sd + up(sbytes);
+  int* d_err = reinterpret_cast<int*>(d_h + up(hbytes));
+  if (gbytes)
+    SX_CUDA(cudaMemcpyAsync(d_geo, job.geoms.data(), gbytes, cudaMemcpyHostToDevice, ctx->stream));
   SX_CUDA(cudaMemcpyAsync(d_sd, job.seeds.data(), sbytes, cudaMemcpyHostToDevice, ctx->stream));
+  if (hbytes)
+    SX_CUDA(cudaMemcpyAsync(d_h, job.seed_H.data(), hbytes, cudaMemcpyHostToDevice, ctx->stream));
+  SX_CUDA(cudaMemsetAsync(d_err, 0, sizeof(int), ctx->stream));
   P.geoms = reinterpret_cast<const ScaleGeom*>(d_geo);
   P.seeds = reinterpret_cast<const SeedIn*>(d_sd);
+  P.seed_H = reinterpret_cast<const double*>(d_h);
+  P.err_flag = d_err;
   static const int shift_warps = [] {
     const char* e = std::getenv("SALVOX_SHIFT_WARPS");
     return e ? std::atoi(e) : 2;
   }();
-  if (P.method == SALVOX_METHOD_SHIFT && shift_warps == 4)
+  if (P.method == SALVOX_METHOD_ABMSOD)
+    abmsod_kernel<2><<<(P.n_seeds + 1) / 2, 64, 0, ctx->stream>>>(P);
+  else if (P.method == SALVOX_METHOD_SHIFT && shift_warps == 4)
     shift_kernel<4><<<(P.n_seeds + 3) / 4, 128, 0, ctx->stream>>>(P);
   else if (P.method == SALVOX_METHOD_SHIFT && shift_warps == 2)
     shift_kernel<2><<<(P.n_seeds + 1) / 2, 64, 0, ctx->stream>>>(P);
@@ -1068,6 +1454,12 @@ void run_seek(salvox_ctx* ctx, SeekJob& job, const uint8_t* d_bins, int bins, co
   else
     launch_ascent(ctx, P);
   SX_LAUNCH_CHECK(ctx);
+  if (P.method == SALVOX_METHOD_ABMSOD) {
+    int err = 0;
+    SX_CUDA(cudaMemcpyAsync(&err, d_err, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    SX_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (err) fail(SALVOX_ERUNTIME, "abmsod: eigen decomposition failed");  // abmsod.cpp:16-17
+  }
 }
 
 // Bins one device volume (K1, pitch nx) into d_bins (n bytes).
@@ -1079,14 +1471,13 @@ void bin_into(salvox_ctx* ctx, const float* d_vol, int nx, int ny, int nz, const
   launch_bin_volume(ctx, d_vol, d_bins, nx, ny, nz, nx, low, high, iw->bins);
 }
 
-// Uploads the target pmf (uniform unless given).
+// Uploads the target pmf (uniform unless given). A given target is used as is,
+// like ShiftParams/AbmsodParams::target (a Histogram) in the C++ reference; the
+// Python layer normalises arrays first (histogram_from_array, py_module.cpp:46-54).
 double* upload_target(salvox_ctx* ctx, const salvox_window* iw, const double* target) {
   std::vector<double> q(iw->bins);
-  if (target) {  // histogram_from_array normalizes (bindings/py_module.cpp:48-55)
-    double s = 0.0;
-    for (int b = 0; b < iw->bins; ++b) s += target[b];
-    if (s <= 0.0) fail(SALVOX_EINVAL, "Histogram::normalize: zero total mass");
-    for (int b = 0; b < iw->bins; ++b) q[b] = target[b] / s;
+  if (target) {
+    for (int b = 0; b < iw->bins; ++b) q[b] = target[b];
   } else {
     for (int b = 0; b < iw->bins; ++b) q[b] = 1.0 / iw->bins;  // Histogram::uniform
   }
@@ -1120,6 +1511,11 @@ void expand_batch(SeekJob& job, int batch) {
       all.push_back(t);
     }
   job.seeds.swap(all);
+  if (!job.seed_H.empty()) {
+    std::vector<double> h((size_t)ns * batch * 9);
+    for (int v = 0; v < batch; ++v) std::copy(job.seed_H.begin(), job.seed_H.end(), h.begin() + (size_t)v * ns * 9);
+    job.seed_H.swap(h);
+  }
 }
 
 // Device selection: thresholds + dedupe over n detections at d_dets. Returns
@@ -1200,8 +1596,8 @@ void plan_and_dedupe(int nx, int ny, int nz, const salvox_detect_params* prm,
              prm->n_scales, prm->rng_seed, all);
   recs.clear();
   index.clear();
-  if (prm->method == SALVOX_METHOD_SHIFT) {
-    recs = all;
+  if (prm->method == SALVOX_METHOD_SHIFT || prm->method == SALVOX_METHOD_ABMSOD) {
+    recs = all;  // one trajectory per seed (pipeline.cpp:360-379)
     for (size_t i = 0; i < all.size(); ++i) index.push_back((int)i);
     return;
   }
@@ -1215,14 +1611,16 @@ void plan_and_dedupe(int nx, int ny, int nz, const salvox_detect_params* prm,
   }
 }
 
+const double* target_of(const salvox_detect_params* prm) {
+  return prm->method == SALVOX_METHOD_ABMSOD ? prm->abmsod_target : prm->shift_target;
+}
+
 void check_method(const salvox_detect_params* prm, int nz) {
   if (!prm) fail(SALVOX_EINVAL, "null params");
   if (prm->method == SALVOX_METHOD_QUADRANT && nz != 1)
     fail(SALVOX_EINVAL, "detect: quadrant method requires a 2D volume (nz == 1)");
-  if (prm->method == SALVOX_METHOD_ABMSOD)
-    fail(SALVOX_EUNSUPPORTED, "detect (device): abmsod is outside the accelerated path");
   if (prm->method != SALVOX_METHOD_QUADRANT && prm->method != SALVOX_METHOD_SHIFT &&
-      prm->method != SALVOX_METHOD_OCTANT)
+      prm->method != SALVOX_METHOD_OCTANT && prm->method != SALVOX_METHOD_ABMSOD)
     fail(SALVOX_EINVAL, "unknown method");
   for (int k : {prm->shift_step_kernel, prm->shift_hist_kernel})
     if (prm->method == SALVOX_METHOD_SHIFT && (k < 0 || k > 2)) fail(SALVOX_EINVAL, "unknown kernel");
@@ -1265,7 +1663,7 @@ extern "C" int salvox_detect(salvox_ctx* ctx, const float* volume, int32_t nx, i
     float* d_vol = static_cast<float*>(ctx->d_seek_vol.ensure(n * 4));
     SX_CUDA(cudaMemcpyAsync(d_vol, volume, n * 4, cudaMemcpyHostToDevice, ctx->stream));
     double* d_q = nullptr;
-    const uint8_t* d_bins = prepare_volume(ctx, d_vol, nx, ny, nz, iw, prm->shift_target, &d_q);
+    const uint8_t* d_bins = prepare_volume(ctx, d_vol, nx, ny, nz, iw, target_of(prm), &d_q);
     const int ns = (int)job.seeds.size();
     char* d_dets = static_cast<char*>(ctx->d_dets.ensure((size_t)(ns + 1) * (sizeof(salvox_detection) + 8) * 2 + 512));
     salvox_detection* d_all = reinterpret_cast<salvox_detection*>(d_dets);
@@ -1320,7 +1718,7 @@ extern "C" int salvox_detect_batch_device(salvox_ctx* ctx, const float* d_volume
     uint8_t* d_bins = static_cast<uint8_t*>(ctx->d_seek_bins.ensure(n * batch));
     for (int v = 0; v < batch; ++v)
       bin_into(ctx, d_volumes + (size_t)v * n, nx, ny, nz, iw, d_bins + (size_t)v * n);
-    const double* d_q = upload_target(ctx, iw, prm->shift_target);
+    const double* d_q = upload_target(ctx, iw, target_of(prm));
     expand_batch(job, batch);
     run_seek(ctx, job, d_bins, iw->bins, d_q, d_all, d_vis);
     for (int v = 0; v < batch; ++v) {
@@ -1371,7 +1769,7 @@ extern "C" int salvox_detect_shard(salvox_ctx* ctx, const float* volume, int32_t
     float* d_vol = static_cast<float*>(ctx->d_seek_vol.ensure(n * 4));
     SX_CUDA(cudaMemcpyAsync(d_vol, volume, n * 4, cudaMemcpyHostToDevice, ctx->stream));
     double* d_q = nullptr;
-    const uint8_t* d_bins = prepare_volume(ctx, d_vol, nx, ny, nz, iw, prm->shift_target, &d_q);
+    const uint8_t* d_bins = prepare_volume(ctx, d_vol, nx, ny, nz, iw, target_of(prm), &d_q);
     char* d_dets = static_cast<char*>(ctx->d_dets.ensure((size_t)(ns + 1) * (sizeof(salvox_detection) + 8) + 512));
     salvox_detection* d_all = reinterpret_cast<salvox_detection*>(d_dets);
     unsigned long long* d_vis = reinterpret_cast<unsigned long long*>(d_all + (ns + 1));
@@ -1411,7 +1809,7 @@ extern "C" int salvox_seek(salvox_ctx* ctx, const float* volume, int32_t nx, int
     float* d_vol = static_cast<float*>(ctx->d_seek_vol.ensure(nv * 4));
     SX_CUDA(cudaMemcpyAsync(d_vol, volume, nv * 4, cudaMemcpyHostToDevice, ctx->stream));
     double* d_q = nullptr;
-    const uint8_t* d_bins = prepare_volume(ctx, d_vol, nx, ny, nz, iw, prm->shift_target, &d_q);
+    const uint8_t* d_bins = prepare_volume(ctx, d_vol, nx, ny, nz, iw, target_of(prm), &d_q);
     char* d_dets = static_cast<char*>(ctx->d_dets.ensure((size_t)(n + 1) * (sizeof(salvox_detection) + 8) * 2 + 512));
     salvox_detection* d_all = reinterpret_cast<salvox_detection*>(d_dets);
     unsigned long long* d_vis = reinterpret_cast<unsigned long long*>(d_all + 2 * (n + 1));
@@ -1508,4 +1906,82 @@ extern "C" int salvox_dedupe_top_k(salvox_ctx* ctx, const salvox_detection* dets
                                    int32_t k, double radius, salvox_detection* out,
                                    int64_t* n_out) {
   return select_host(ctx, dets, n, 0.0, 0.0, k, radius, false, out, n_out);
+}
+
+extern "C" int salvox_abmsod_run(salvox_ctx* ctx, const float* volume, int32_t nx, int32_t ny,
+                                 int32_t nz, const salvox_window* iw,
+                                 const salvox_abmsod_params* ap, const double* seeds,
+                                 const double* seed_H, const double* radii, int64_t n,
+                                 salvox_detection* out, salvox_abmsod_iter* trace,
+                                 int32_t* n_trace, uint64_t* visits) {
+  return guarded([&] {
+    if (!ctx) fail(SALVOX_EINVAL, "null context");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (nx < 1 || ny < 1 || nz < 1) fail(SALVOX_EINVAL, "Volume: dims must be >= 1");
+    if (!volume || !ap) fail(SALVOX_EINVAL, "null argument");
+    check_window(iw);
+    if (n < 0 || (n > 0 && (!seeds || !out || (!seed_H && !radii))))
+      fail(SALVOX_EINVAL, "bad seed arrays");
+    salvox_detect_params prm{};
+    prm.method = SALVOX_METHOD_ABMSOD;
+    prm.abmsod_threshold = ap->threshold;
+    prm.abmsod_max_iters = ap->max_iterations;
+    prm.abmsod_kernel = ap->kernel;
+    prm.abmsod_lambda_min = ap->lambda_min;
+    prm.abmsod_lambda_max = ap->lambda_max;
+    prm.abmsod_min_inbounds_fraction = ap->min_inbounds_fraction;
+    prm.abmsod_target = ap->target;
+    std::vector<SeedRec> recs((size_t)n);
+    std::vector<int> index((size_t)n);
+    for (int64_t i = 0; i < n; ++i) {
+      std::memcpy(recs[i].pos, seeds + 3 * i, 3 * sizeof(double));
+      recs[i].scale = radii ? radii[i] : 1.0;
+      index[i] = -1;  // abmsod_run leaves Detection::seed_index at its default
+    }
+    SeekJob job;
+    build_job(nx, ny, nz, &prm, recs, index, job);
+    if (seed_H) std::memcpy(job.seed_H.data(), seed_H, (size_t)n * 9 * sizeof(double));
+    if (n == 0) return;
+    SX_CUDA(cudaSetDevice(ctx->device));
+    const size_t nv = (size_t)nx * ny * nz;
+    float* d_vol = static_cast<float*>(ctx->d_seek_vol.ensure(nv * 4));
+    SX_CUDA(cudaMemcpyAsync(d_vol, volume, nv * 4, cudaMemcpyHostToDevice, ctx->stream));
+    double* d_q = nullptr;
+    const uint8_t* d_bins = prepare_volume(ctx, d_vol, nx, ny, nz, iw, ap->target, &d_q);
+    const size_t tr_n = trace ? (size_t)n * ap->max_iterations : 0;
+    char* d_dets = static_cast<char*>(ctx->d_dets.ensure(
+        (size_t)(n + 1) * (sizeof(salvox_detection) + 8 + 4) + tr_n * sizeof(salvox_abmsod_iter) + 1024));
+    salvox_detection* d_all = reinterpret_cast<salvox_detection*>(d_dets);
+    unsigned long long* d_vis = reinterpret_cast<unsigned long long*>(d_all + (n + 1));
+    int* d_tn = reinterpret_cast<int*>(d_vis + (n + 1));
+    salvox_abmsod_iter* d_tr = reinterpret_cast<salvox_abmsod_iter*>(
+        d_dets + (((size_t)(n + 1) * (sizeof(salvox_detection) + 8 + 4) + 255) / 256) * 256);
+    job.P.abm_trace = trace ? d_tr : nullptr;
+    job.P.abm_trace_n = trace ? d_tn : nullptr;
+    run_seek(ctx, job, d_bins, iw->bins, d_q, d_all, d_vis);
+    SX_CUDA(cudaMemcpyAsync(out, d_all, (size_t)n * sizeof(salvox_detection), cudaMemcpyDeviceToHost,
+                            ctx->stream));
+    if (trace) {
+      SX_CUDA(cudaMemcpyAsync(trace, d_tr, tr_n * sizeof(salvox_abmsod_iter), cudaMemcpyDeviceToHost,
+                              ctx->stream));
+      if (n_trace)
+        SX_CUDA(cudaMemcpyAsync(n_trace, d_tn, (size_t)n * sizeof(int), cudaMemcpyDeviceToHost,
+                                ctx->stream));
+    }
+    const unsigned long long v = sum_visits(ctx, d_vis, (int)n);
+    if (visits) *visits += v;
+  });
+}
+
+extern "C" int salvox_bandwidth_from_moment(const double* outer, double weight_sum, int32_t dim,
+                                            double lambda_min, double lambda_max, double* H) {
+  return guarded([&] {
+    if (!outer || !H) fail(SALVOX_EINVAL, "null argument");
+    switch (sx_bandwidth_from_moment(outer, weight_sum, dim, lambda_min, lambda_max, H)) {
+      case 1: fail(SALVOX_EINVAL, "bandwidth update: zero weight mass");
+      case 2: fail(SALVOX_EINVAL, "bandwidth update: non-finite moment");
+      case 3: fail(SALVOX_ERUNTIME, "abmsod: eigen decomposition failed");
+      default: break;
+    }
+  });
 }

@@ -11,6 +11,7 @@
 #include <string>
 #include <vector>
 
+#include "salvox/abmsod.hpp"
 #include "salvox/config.hpp"
 #include "salvox/device.hpp"
 #include "salvox/histogram.hpp"
@@ -77,6 +78,14 @@ PhantomSpec cube_3d(int dim, int half, uint64_t seed) {
 
 // ------------------------------------------------------------------ host only
 void cpu_tests() {
+  {  // test_seek.cpp:427-450: bandwidth_from_moment (host 3x3 math)
+    Eigen::Matrix3d outer = Eigen::Matrix3d::Zero();
+    outer(0, 0) = 2.0 * 9.0;
+    const Eigen::Matrix3d H = bandwidth_from_moment(outer, 2.0, 3, 4.0, 1024.0);
+    CHECK(std::abs(H(0, 0) - 45.0) < 1e-9 && std::abs(H(1, 1) - 4.0) < 1e-9 &&
+          std::abs(H(2, 2) - 4.0) < 1e-9);
+    CHECK_THROWS_AS(bandwidth_from_moment(outer, 0.0, 3, 4.0, 4096.0), std::invalid_argument);
+  }
   // test_volume.cpp:35-49
   CHECK(IntensityWindow(0, 256, 256).bin_of(0.0) == 0);
   CHECK(IntensityWindow(0, 100, 10).bin_of(55.0) == 5);
@@ -223,8 +232,12 @@ void gpu_tests() {
     p.seeds.scales = {4.0, 8.0, 12.0};
     const auto od = detect(v, IntensityWindow(0, 64, 64), p);
     CHECK(!od.empty());
-    p.method = Method::Abmsod;
-    CHECK_THROWS_AS(detect(v, IntensityWindow(0, 64, 64), p), unsupported_error);
+    p.method = Method::Abmsod;  // test_pipeline.cpp:321-354 (ABMSOD through detect)
+    p.seeds.scales = {6.0, 9.0};
+    const auto ad = detect(v, IntensityWindow(0, 64, 64), p);
+    CHECK(!ad.empty() && (ad.front().center - gt.regions[0].center).norm() <= 3.0);
+    p.abmsod.threshold = 0.0;
+    CHECK_THROWS_AS(detect(v, IntensityWindow(0, 64, 64), p), std::invalid_argument);
   }
   {  // test_pipeline.cpp:381-400
     Volume v(48, 48, 48);
@@ -270,6 +283,35 @@ void gpu_tests() {
     qp.scale_range = {3, 6, 9};
     const auto oc = octant_seek(v, {Eigen::Vector3d(40.0, 36.0, 26.0)}, qp, IntensityWindow(0, 64, 64));
     CHECK(!oc[0].degenerate && (oc[0].position - c).norm() <= 4.0);
+  }
+  {  // test_seek.cpp:495-514 + 561-571: abmsod_run on the device
+    PhantomSpec s;
+    s.dims = Eigen::Vector3i(64, 64, 64);
+    RegionSpec r;
+    r.shape = RegionSpec::Shape::Ellipsoid;
+    r.center = Eigen::Vector3d(31.5, 31.5, 31.5);
+    r.axes = Eigen::Matrix3d::Zero();
+    r.axes(0, 0) = 9.0, r.axes(1, 1) = 6.0, r.axes(2, 2) = 4.0;
+    r.fill.levels = 64;
+    s.regions.push_back(r);
+    s.rng_seed = 111;
+    auto [v, gt] = make_phantom(s);
+    EllipsoidWindow seed;
+    seed.center = gt.regions[0].center;
+    seed.H = gt.regions[0].H;
+    AbmsodParams ap;
+    ap.record_trace = true;
+    const auto res = abmsod_run(v, seed, ap, IntensityWindow(0, 64, 64));
+    CHECK(!res.det.has(kFlagDegenerate));
+    CHECK((res.det.center - gt.regions[0].center).norm() <= 1.0);
+    CHECK(!res.trace.empty() && int(res.trace.size()) == res.det.iterations);
+    for (const auto& t : res.trace) CHECK(t.eig_min >= ap.lambda_min - 1e-9);
+    Volume c(32, 32, 32);
+    for (float& f : c.data()) f = 20.0f;
+    const auto rc = abmsod_run(c, EllipsoidWindow::isotropic(Eigen::Vector3d(16, 16, 16), 6.0, false),
+                               ap, IntensityWindow(0, 64, 64));
+    CHECK(!rc.trace.empty() && std::abs(rc.trace.front().bhattacharyya - std::sqrt(1.0 / 64)) < 1e-12);
+    CHECK(rc.det.entropy_bits == 0.0);
   }
 }
 

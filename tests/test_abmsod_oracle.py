@@ -172,3 +172,17 @@ def test_abmsod_detect_and_invalid_params(oracle):  # test_pipeline.cpp:321-354 
     assert np.linalg.norm(sel[0]["center"] - c) < 6.0
     with pytest.raises(oracle.OracleError):
         oracle.abmsod_run(vol, 0, 64, 64, c, radius=6.0, threshold=0.0)
+
+
+def test_capi_bandwidth_from_moment_matches_oracle(sx, oracle):
+    """salvox_bandwidth_from_moment (host C-ABI, same sx_eig3.h) == the oracle, bit for bit."""
+    rng = np.random.default_rng(7)
+    for _ in range(20):
+        pts = rng.normal(scale=rng.uniform(1, 6, 3), size=(50, 3))
+        w = rng.uniform(0.1, 2.0, 50)
+        outer = sum(wi * np.outer(p, p) for wi, p in zip(w, pts))
+        a = sx.bandwidth_from_moment(outer, w.sum(), 3, 4.0, 1024.0)
+        b = oracle.bandwidth_from_moment(outer, w.sum(), 3, 4.0, 1024.0)
+        assert a.tobytes() == b.tobytes()
+    with pytest.raises(ValueError, match="zero weight mass"):
+        sx.bandwidth_from_moment(np.eye(3), 0.0, 3, 4.0, 1024.0)

@@ -37,10 +37,12 @@ def test_struct_layouts_match_header(sx, tmp_path):
 #include <stddef.h>
 #include "salvox_capi.h"
 int main(void) {
-  printf("%zu %zu %zu %zu %zu %zu %zu\\n", sizeof(salvox_window), sizeof(salvox_detection),
-         sizeof(salvox_maximum), sizeof(salvox_detect_params),
+  printf("%zu %zu %zu %zu %zu %zu %zu %zu %zu %zu %zu\\n", sizeof(salvox_window),
+         sizeof(salvox_detection), sizeof(salvox_maximum), sizeof(salvox_detect_params),
          offsetof(salvox_detect_params, shift_target), offsetof(salvox_detection, flags),
-         offsetof(salvox_detect_params, quadrant_scales));
+         offsetof(salvox_detect_params, quadrant_scales),
+         offsetof(salvox_detect_params, abmsod_target), sizeof(salvox_abmsod_params),
+         offsetof(salvox_abmsod_params, target), sizeof(salvox_abmsod_iter));
   return 0;
 }
 """)
@@ -50,9 +52,11 @@ int main(void) {
     got = [int(v) for v in subprocess.run([str(exe)], capture_output=True, text=True,
                                           check=True).stdout.split()]
     P = sx._lib.DetectParams
+    A = sx._lib.AbmsodParams
     assert got == [ctypes.sizeof(sx._lib.Window), sx.DET_DTYPE.itemsize, sx.MAX_DTYPE.itemsize,
                    ctypes.sizeof(P), P.shift_target.offset, sx.DET_DTYPE.fields["flags"][1],
-                   P.quadrant_scales.offset]
+                   P.quadrant_scales.offset, P.abmsod_target.offset, ctypes.sizeof(A),
+                   A.target.offset, sx._lib.ABMSOD_ITER_DTYPE.itemsize]
 
 
 def test_no_cpu_fallback_without_gpu(sx):
