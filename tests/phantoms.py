@@ -137,3 +137,22 @@ def ellipsoid_3d(axes, seed, dim=64):  # test_seek.cpp:468-481 (ellipsoid_phanto
 def ellipsoid_H(axes):  # RegionSpec ellipsoid H = A A^T (phantom.cpp:198-222)
     a = np.asarray(axes, np.float64)
     return a @ a.T
+
+
+def paper_pet():
+    """The paper's PET case shape (128x128x34, 400 seeds): C1-style
+    background with a high-entropy ball (the LV analogue)."""
+    return {"dims": [128, 128, 34],
+            "background": {"type": "gaussian", "mean": 4.0, "sigma": 1.5},
+            "regions": [{"shape": "ball", "center": [70.0, 58.0, 17.0], "radius": 10.0,
+                         "fill": {"type": "uniform", "levels": 16}}],
+            "rng_seed": 264}
+
+
+def paper_mr():
+    """The paper's MR case shape (256x256x176, 700 seeds): the C3
+    tumour phantom on 176 planes."""
+    spec = config_c3()
+    spec["dims"] = [256, 256, 176]
+    spec["rng_seed"] = 290
+    return spec

@@ -5,6 +5,10 @@
   C3: 256x256x160 MR phantom, 64 bins, shift, lattice 16 x scales {8, 12}
   C5: batch of 64 x 128^3 C1-style volumes (rng_seed 1310+i, centre jittered by
       Rng(i)), octant, volumes data-parallel (one rank here)
+  PAPER PET / MR: ABMSOD (the paper's GPU workload) on the
+      paper's shapes: 128x128x34 with 400 random seeds (16 bins) and 256x256x176
+      with 700 random seeds (64 bins), seed windows isotropic r = 8 -- the paper
+      reports 4.1 s and 7.8 s per volume on a Tesla C2050
 Prints one JSON object per config; --cpu adds the oracle's time on all host cores.
 """
 import argparse
@@ -42,11 +46,12 @@ def c5_specs(n):
     return specs
 
 
-def time_batch(ctx, stream, d_vols, batch, shape, window, method, scales, spacing, steps=3):
+def time_batch(ctx, stream, d_vols, batch, shape, window, method, scales, spacing, steps=3,
+               **extra):
     nz, ny, nx = shape
     iw = _lib.Window(window[0], window[1], window[2], 0)
     P, keep = api._detect_params(method, seed_spacing=spacing, scales=scales, k=20,
-                                 dedupe_radius=5.0)
+                                 dedupe_radius=5.0, **extra)
     out = np.empty(batch * 20, _lib.DET_DTYPE)
     n_out = np.zeros(batch, np.int64)
     visits = C.c_uint64(0)
@@ -73,6 +78,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--cpu", action="store_true")
     ap.add_argument("--c5", type=int, default=64)
+    ap.add_argument("--only", default="", help="substring filter on config names")
     args = ap.parse_args()
     ctx = Context(0)
     dev = torch.device("cuda", 0)
@@ -81,7 +87,8 @@ def main():
     res = []
     v1, _ = api.make_phantom(phantoms.config_c1())
     d1 = torch.from_numpy(v1).to(dev)
-    for method in ("octant", "shift"):
+    want = lambda name: args.only.lower() in name.lower()  # noqa: E731
+    for method in ("octant", "shift") if want("C1") else ():
         ms, sel = time_batch(ctx, st, d1, 1, v1.shape, (0.0, 16.0, 16), method, C1_SCALES, 8.0)
         r = {"config": f"C1 {method}", "ms_per_volume": ms, "volumes_per_s": 1e3 / ms,
              "selected": sel}
@@ -93,12 +100,33 @@ def main():
             r["cpu_ms"] = (time.perf_counter() - t0) * 1e3
             r["cpu_cores"] = os.cpu_count()
         res.append(r)
-    v3, _ = api.make_phantom(phantoms.config_c3())
-    d3 = torch.from_numpy(v3).to(dev)
-    ms, sel = time_batch(ctx, st, d3, 1, v3.shape, (0.0, 64.0, 64), "shift", [8.0, 12.0], 16.0)
-    res.append({"config": "C3 shift", "ms_per_volume": ms, "volumes_per_s": 1e3 / ms,
-                "selected": sel})
-    if args.c5 > 0:
+    if want("C3 shift"):
+        v3, _ = api.make_phantom(phantoms.config_c3())
+        d3 = torch.from_numpy(v3).to(dev)
+        ms, sel = time_batch(ctx, st, d3, 1, v3.shape, (0.0, 64.0, 64), "shift", [8.0, 12.0], 16.0)
+        res.append({"config": "C3 shift", "ms_per_volume": ms, "volumes_per_s": 1e3 / ms,
+                    "selected": sel})
+    for name, spec, bins, n_seeds, paper_s in (("PAPER PET abmsod", phantoms.paper_pet(), 16, 400, 4.1),
+                                               ("PAPER MR abmsod", phantoms.paper_mr(), 64, 700, 7.8)):
+        if not want(name):
+            continue
+        vp, _ = api.make_phantom(spec)
+        dp = torch.from_numpy(vp).to(dev)
+        kw = dict(seed_mode="random", seed_count=n_seeds, rng_seed=1310)
+        ms, sel = time_batch(ctx, st, dp, 1, vp.shape, (0.0, float(bins), bins), "abmsod", [8.0],
+                             16.0, **kw)
+        r = {"config": name, "shape": list(vp.shape), "seeds": n_seeds, "ms_per_volume": ms,
+             "volumes_per_s": 1e3 / ms, "selected": sel, "paper_c2050_s_per_volume": paper_s}
+        if args.cpu:
+            from oracle import oracle as O
+            t0 = time.perf_counter()
+            O.detect(vp, 0.0, float(bins), bins, method="abmsod", seed_mode="random",
+                     seed_count=n_seeds, rng_seed=1310, scales=[8.0], top_k=20, dedupe_radius=5.0,
+                     workers=os.cpu_count() or 1)
+            r["cpu_ms"] = (time.perf_counter() - t0) * 1e3
+            r["cpu_cores"] = os.cpu_count()
+        res.append(r)
+    if args.c5 > 0 and want("C5"):
         vols = np.stack([api.make_phantom(s)[0] for s in c5_specs(args.c5)])
         dv = torch.from_numpy(vols).to(dev)
         ms, sel = time_batch(ctx, st, dv, args.c5, vols.shape[1:], (0.0, 16.0, 16), "octant",
