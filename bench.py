@@ -279,9 +279,10 @@ def main():
         e2e_ms = float(t.item())
 
     # ---- secondary: 256x256x160 seed-grid (shift, 64 bins) volumes/s, device-resident
-    seed_grid = None
+    seed_grid = abmsod = None
     if not args.no_seed_grid and rank == 0:
         seed_grid = bench_seed_grid(ctx, dev, stream, flush)
+        abmsod = bench_abmsod_paper(ctx, dev, stream, flush)
 
     # ---- cpu baseline (rank 0, N = 1 only)
     cpu = None
@@ -332,6 +333,8 @@ def main():
             line["cpu_baseline"] = cpu
         if seed_grid is not None:
             line["seed_grid"] = seed_grid
+        if abmsod is not None:
+            line["abmsod_paper"] = abmsod
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -380,6 +383,63 @@ def bench_seed_grid(ctx, dev, stream, flush, steps=3):
             "config": {"workload": "C3 256x256x160 MR phantom, shift mean-shift, 64 bins, "
                                    "lattice 16 x scales {8, 12} = 5120 seeds",
                        "selected": int(n_out[0])}}
+
+
+def bench_abmsod_paper(ctx, dev, stream, flush, steps=3):
+    """ABMSOD detect (the paper's own GPU workload) on the paper's
+    volume shapes: PET 128x128x34 / 400 random seeds / 16 bins and MR 256x256x176 /
+    700 random seeds / 64 bins, isotropic seed windows r = 8, device-resident volume,
+    selection included. The paper: 4.1 s and 7.8 s per volume on a Tesla C2050
+    (PAPER.md:264, :290)."""
+    import ctypes as C
+
+    import torch
+
+    from paper_1310_6736_b200 import _lib, api
+
+    sys.path.insert(0, ROOT)
+    from tests import phantoms
+
+    out_cases = {}
+    for name, spec, bins, n_seeds, paper_s in (("pet_128x128x34_400", phantoms.paper_pet(), 16,
+                                                400, 4.1),
+                                               ("mr_256x256x176_700", phantoms.paper_mr(), 64,
+                                                700, 7.8)):
+        vol, _ = api.make_phantom(spec)
+        d_vol = torch.from_numpy(vol).to(dev)
+        iw = _lib.Window(0.0, float(bins), bins, 0)
+        P, keep = api._detect_params("abmsod", scales=(8.0,), k=20, dedupe_radius=5.0,
+                                     seed_mode="random", seed_count=n_seeds, rng_seed=1310)
+        out = np.empty(20, _lib.DET_DTYPE)
+        n_out = np.zeros(1, np.int64)
+        visits = C.c_uint64(0)
+        nz, ny, nx = vol.shape
+
+        def run():
+            _lib.check(_lib.load().salvox_detect_batch_device(
+                ctx.handle, C.c_void_p(d_vol.data_ptr()), 1, nx, ny, nz, C.byref(iw), C.byref(P),
+                out.ctypes.data_as(C.c_void_p), 20, n_out.ctypes.data_as(C.c_void_p),
+                C.byref(visits)))
+
+        run()
+        times = []
+        for _ in range(steps):
+            flush.fill_(1)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            run()
+            e1.record(stream)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1))
+        ms = float(np.mean(times))
+        del keep
+        out_cases[name] = {"ms_per_volume": ms, "volumes_per_s": 1e3 / ms, "seeds": n_seeds,
+                           "bins": bins, "selected": int(n_out[0]),
+                           "paper_c2050_s_per_volume": paper_s,
+                           "speedup_vs_paper_c2050": paper_s * 1e3 / ms}
+    return {"metric": "ABMSOD detect volumes/sec (paper shapes)", "unit": "volumes/s",
+            "cases": out_cases}
 
 
 if __name__ == "__main__":

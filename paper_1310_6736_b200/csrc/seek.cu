@@ -95,7 +95,8 @@ struct WarpScratch {
   double v[kStep];        // compacted per-step values (support voxels, in order)
   double t[3][kStep];     // compacted centroid terms g*x, g*y, g*z
   int bin[kStep];         // compacted bins
-  unsigned cnt[1][kMaxBins];  // ascent box counts (one octant at a time)
+  int cntb[kMaxBins];     // per-chunk support count per bin
+  int startb[kMaxBins];   // per-chunk start of each bin's run in v
 };
 
 struct Box {
@@ -194,18 +195,33 @@ __device__ __forceinline__ int bin_at(const SeekParams& P, const uint8_t* vb, in
 
 // try_candidate_histogram (window.cpp:5-19): sequential per-bin fp64 masses in
 // support order, normalized into s.p. Returns ok; *support, *visited.
-// Per 32-voxel chunk the support voxels are compacted (ballot + popc rank) into
-// shared memory in z->y->x order; lane l owns bins l and l+32 and walks the
-// compacted list with broadcast loads, adding the matching masses in order into
-// register accumulators. The only serial dependency is the fp64 add chain.
-__device__ bool warp_candidate_hist(const SeekParams& P, const uint8_t* vb, WarpScratch& s, const double c[3],
-                                    const WinGeom& g, int kernel, int lane, unsigned* support_out,
-                                    long long* visited) {
-  const int M = P.bins;
-  const Box bb = window_box(c, g, P.nx, P.ny, P.nz);
-  *visited = box_size(bb);
+// Per 128-voxel chunk the support voxels are counting-sorted by bin, stably
+// (__match_any_sync groups equal bins of a 32-voxel group; rank = lanes below
+// in the group + the bin's count from earlier groups), so bin b's masses sit
+// contiguously in z->y->x order. Lane l owns bins l and l+32 and adds only its
+// own run: the dependent fp64 chain is max_b count_b long per chunk instead of
+// the chunk's whole support.
+// Not inlined: ONE copy of these loops serves every call site (inlined copies
+// overflowed the instruction cache: "no instruction" was the top stall).
+struct HistRes {
+  long long visited;
+  unsigned support;
+  int ok;
+};
+
+__device__ __noinline__ HistRes warp_candidate_hist_impl(const uint8_t* vb, int nx, int ny, int nz,
+                                                         int M, WarpScratch* sp, double c0,
+                                                         double c1, double c2, const WinGeom* gp,
+                                                         int kernel) {
+  WarpScratch& s = *sp;
+  const WinGeom& g = *gp;
+  const int lane = threadIdx.x & 31;
+  const double c[3] = {c0, c1, c2};
+  const Box bb = window_box(c, g, nx, ny, nz);
+  HistRes res{box_size(bb), 0u, 0};
   unsigned support = 0;
   double a0 = 0.0, a1 = 0.0;  // bins lane, lane + 32
+  const unsigned lt = (1u << lane) - 1u;
   warp_box_iter_g(bb, lane, [&](const bool* act, const int* x, const int* y, const int* z) {
     bool in[kG];
     int bin[kG];
@@ -219,41 +235,45 @@ __device__ bool warp_candidate_hist(const SeekParams& P, const uint8_t* vb, Warp
         const double d = maha(g, c, x[j], y[j], z[j]);
         in[j] = d <= 1.0;
         if (in[j]) {
-          bin[j] = bin_at(P, vb, x[j], y[j], z[j]);
+          bin[j] = (int)__ldg(vb + ((size_t)z[j] * ny + y[j]) * nx + x[j]) - 1;
           val[j] = __dmul_rn(g.det_fac, kernel_value(kernel, d));
         }
       }
     }
-    int off = 0;
-#pragma unroll
-    for (int j = 0; j < kG; ++j) {
-      const unsigned m = __ballot_sync(kFull, in[j]);
-      if (in[j]) {
-        const int r = off + __popc(m & ((1u << lane) - 1u));
-        s.bin[r] = bin[j];
-        s.v[r] = val[j];
-      }
-      off += __popc(m);
-    }
-    support += (unsigned)off;
+    s.cntb[lane] = 0;
+    s.cntb[lane + 32] = 0;
     __syncwarp();
-    // acc + (+0.0) == acc exactly (masses are >= +0), so the select moves off
-    // the dependent chain: one DADD of latency per support voxel and bin lane.
-    if (M <= 32) {
-#pragma unroll 4
-      for (int k = 0; k < off; ++k) {
-        const double vk = s.v[k];
-        a0 = __dadd_rn(a0, s.bin[k] == lane ? vk : 0.0);
-      }
-    } else {
-#pragma unroll 4
-      for (int k = 0; k < off; ++k) {
-        const int bk = s.bin[k];
-        const double vk = s.v[k];
-        a0 = __dadd_rn(a0, bk == lane ? vk : 0.0);
-        a1 = __dadd_rn(a1, bk == lane + 32 ? vk : 0.0);
-      }
+    int rank[kG];
+#pragma unroll
+    for (int j = 0; j < kG; ++j) {  // stable per-bin ranks, group by group
+      const unsigned peers = __match_any_sync(kFull, in[j] ? bin[j] : -1);
+      int base = 0;
+      if (in[j]) base = s.cntb[bin[j]];
+      rank[j] = base + __popc(peers & lt);
+      __syncwarp();
+      if (in[j] && (peers & lt) == 0u) s.cntb[bin[j]] = base + __popc(peers);
+      __syncwarp();
     }
+    const int c0 = s.cntb[lane], c1 = s.cntb[lane + 32];
+    int i0 = c0, i1 = c1;  // inclusive scans over bins 0..31 and 32..63
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t0 = __shfl_up_sync(kFull, i0, o), t1 = __shfl_up_sync(kFull, i1, o);
+      if (lane >= o) i0 += t0, i1 += t1;
+    }
+    const int tot0 = __shfl_sync(kFull, i0, 31);
+    const int st0 = i0 - c0, st1 = tot0 + i1 - c1;
+    s.startb[lane] = st0;
+    s.startb[lane + 32] = st1;
+    support += (unsigned)(tot0 + __shfl_sync(kFull, i1, 31));
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < kG; ++j)
+      if (in[j]) s.v[s.startb[bin[j]] + rank[j]] = val[j];
+    __syncwarp();
+    for (int k = 0; k < c0; ++k) a0 = __dadd_rn(a0, s.v[st0 + k]);
+    if (M > 32)
+      for (int k = 0; k < c1; ++k) a1 = __dadd_rn(a1, s.v[st1 + k]);
     __syncwarp();
   });
   if (lane < M) s.h[lane] = a0;
@@ -263,15 +283,28 @@ __device__ bool warp_candidate_hist(const SeekParams& P, const uint8_t* vb, Warp
   if (lane == 0)
     for (int b = 0; b < M; ++b) mass = __dadd_rn(mass, s.h[b]);  // Histogram::mass
   mass = __shfl_sync(kFull, mass, 0);
-  *support_out = support;
-  if (support == 0 || mass <= 0.0) return false;
+  res.support = support;
+  if (support == 0 || mass <= 0.0) return res;
   for (int b = lane; b < M; b += 32) s.p[b] = __ddiv_rn(s.h[b], mass);
   __syncwarp();
-  return true;
+  res.ok = 1;
+  return res;
+}
+
+__device__ __forceinline__ bool warp_candidate_hist(const SeekParams& P, const uint8_t* vb,
+                                                    WarpScratch& s, const double c[3],
+                                                    const WinGeom& g, int kernel, int lane,
+                                                    unsigned* support_out, long long* visited) {
+  (void)lane;
+  const HistRes r =
+      warp_candidate_hist_impl(vb, P.nx, P.ny, P.nz, P.bins, &s, c[0], c[1], c[2], &g, kernel);
+  *support_out = r.support;
+  *visited = r.visited;
+  return r.ok != 0;
 }
 
 // entropy_bits (histogram.hpp:56-67) of pmf p, sequential in bin order.
-__device__ double warp_entropy_bits(const double* p, int M, int lane, double* tmp) {
+__device__ __noinline__ double warp_entropy_bits(const double* p, int M, int lane, double* tmp) {
   for (int b = lane; b < M; b += 32) tmp[b] = p[b] > 0.0 ? __dmul_rn(p[b], sx_log(p[b])) : 0.0;
   __syncwarp();
   double e = 0.0;
