@@ -108,6 +108,13 @@ __device__ __forceinline__ long long box_size(const Box& b) {
   return (long long)(b.x1 - b.x0 + 1) * (b.y1 - b.y0 + 1) * (b.z1 - b.z0 + 1);
 }
 
+// q = floor(n / d) for 0 <= n < 2^22 - 1 and any d >= 1 through one fp32
+// multiply: (n + 0.5) / d sits >= 0.5/d from an integer and the two roundings
+// move it by < (n + 0.5)/d * 2^-23 < 0.5/d, so truncation is exact.
+__device__ __forceinline__ int fdiv_small(int n, float inv_d) {
+  return (int)(((float)n + 0.5f) * inv_d);
+}
+
 // Visits a box in z->y->x order, 32 voxels per step (uniform control flow).
 template <class F>
 __device__ __forceinline__ void warp_box_iter(const Box& b, int lane, F&& f) {
@@ -371,6 +378,80 @@ __device__ bool warp_final_scores(const SeekParams& P, const uint8_t* vb, WarpSc
   return ok;
 }
 
+// Centroid pass (shift.cpp:25-30, abmsod.cpp:85-90): g = step_w(d) * w[bin];
+// lanes 0..3 run num.x / num.y / num.z / den in support order. Not inlined (one
+// copy for every caller). Returns the box visits.
+struct CentRes {
+  double num[3], den;
+  long long visited;
+};
+
+__device__ __noinline__ CentRes warp_centroid_impl(const uint8_t* vb, int nx, int ny, int nz,
+                                                   WarpScratch* sp, double c0, double c1,
+                                                   double c2, const WinGeom* gp, int step_kernel) {
+  WarpScratch& s = *sp;
+  const WinGeom& wg = *gp;
+  const int lane = threadIdx.x & 31;
+  const double c[3] = {c0, c1, c2};
+  double acc = 0.0;
+  const Box bb = window_box(c, wg, nx, ny, nz);
+  warp_box_iter_g(bb, lane, [&](const bool* act, const int* x, const int* y, const int* z) {
+    bool in[kG];
+    double g[kG];
+#pragma unroll
+    for (int j = 0; j < kG; ++j) {
+      in[j] = false;
+      g[j] = 0.0;
+      if (act[j]) {
+        const double dd = maha(wg, c, x[j], y[j], z[j]);
+        in[j] = dd <= 1.0;
+        if (in[j]) {
+          const int b = (int)__ldg(vb + ((size_t)z[j] * ny + y[j]) * nx + x[j]) - 1;
+          g[j] = __dmul_rn(kernel_step_weight(step_kernel, dd), s.w[b]);
+        }
+      }
+    }
+    int off = 0;
+#pragma unroll
+    for (int j = 0; j < kG; ++j) {
+      const unsigned m0 = __ballot_sync(kFull, in[j]);
+      if (in[j]) {  // Eigen: num += g * Vector3d(sx, sy, sz) -> per-component products
+        const int r = off + __popc(m0 & ((1u << lane) - 1u));
+        s.v[r] = g[j];
+        s.t[0][r] = __dmul_rn(g[j], (double)x[j]);
+        s.t[1][r] = __dmul_rn(g[j], (double)y[j]);
+        s.t[2][r] = __dmul_rn(g[j], (double)z[j]);
+      }
+      off += __popc(m0);
+    }
+    __syncwarp();
+    if (lane < 4) {
+      const double* src = lane == 3 ? s.v : s.t[lane];
+#pragma unroll 4
+      for (int k = 0; k < off; ++k) acc = __dadd_rn(acc, src[k]);
+    }
+    __syncwarp();
+  });
+  CentRes r;
+  r.num[0] = __shfl_sync(kFull, acc, 0);
+  r.num[1] = __shfl_sync(kFull, acc, 1);
+  r.num[2] = __shfl_sync(kFull, acc, 2);
+  r.den = __shfl_sync(kFull, acc, 3);
+  r.visited = box_size(bb);
+  return r;
+}
+
+__device__ __forceinline__ long long warp_centroid(const SeekParams& P, const uint8_t* vb,
+                                                   WarpScratch& s, const double c[3],
+                                                   const WinGeom& wg, int step_kernel, int lane,
+                                                   double num[3], double* den_out) {
+  (void)lane;
+  const CentRes r = warp_centroid_impl(vb, P.nx, P.ny, P.nz, &s, c[0], c[1], c[2], &wg, step_kernel);
+  num[0] = r.num[0], num[1] = r.num[1], num[2] = r.num[2];
+  *den_out = r.den;
+  return r.visited;
+}
+
 // ------------------------------------------------------------------- shift
 // warps (seeds) per block; scratch is ~6.3 KB per warp. Small blocks free their
 // slot as soon as their own trajectories end (lengths vary widely per seed).
@@ -421,48 +502,10 @@ __global__ void __launch_bounds__(32 * NW) shift_kernel(const SeekParams P) {
       __syncwarp();
       // centroid pass (shift.cpp:25-30): support voxels compacted per chunk; lanes
       // 0..3 run the num.x / num.y / num.z / den chains in z->y->x order
-      double acc = 0.0;  // lane 0: num.x, 1: num.y, 2: num.z, 3: den
-      const Box bb = window_box(c, sg.main, P.nx, P.ny, P.nz);
-      visits += (unsigned long long)box_size(bb);
-      warp_box_iter_g(bb, lane, [&](const bool* act, const int* x, const int* y, const int* z) {
-        bool in[kG];
-        double g[kG];
-#pragma unroll
-        for (int j = 0; j < kG; ++j) {
-          in[j] = false;
-          g[j] = 0.0;
-          if (act[j]) {
-            const double dd = maha(sg.main, c, x[j], y[j], z[j]);
-            in[j] = dd <= 1.0;
-            if (in[j])
-              g[j] = __dmul_rn(kernel_step_weight(P.step_kernel, dd), s.w[bin_at(P, vb, x[j], y[j], z[j])]);
-          }
-        }
-        int off = 0;
-#pragma unroll
-        for (int j = 0; j < kG; ++j) {
-          const unsigned m0 = __ballot_sync(kFull, in[j]);
-          if (in[j]) {  // Eigen: num += g * Vector3d(sx, sy, sz) -> per-component products
-            const int r = off + __popc(m0 & ((1u << lane) - 1u));
-            s.v[r] = g[j];
-            s.t[0][r] = __dmul_rn(g[j], (double)x[j]);
-            s.t[1][r] = __dmul_rn(g[j], (double)y[j]);
-            s.t[2][r] = __dmul_rn(g[j], (double)z[j]);
-          }
-          off += __popc(m0);
-        }
-        __syncwarp();
-        if (lane < 4) {
-          const double* src = lane == 3 ? s.v : s.t[lane];
-#pragma unroll 4
-          for (int k = 0; k < off; ++k) acc = __dadd_rn(acc, src[k]);
-        }
-        __syncwarp();
-      });
-      const double den = __shfl_sync(kFull, acc, 3);
-      const double nx_ = __shfl_sync(kFull, acc, 0);
-      const double ny_ = __shfl_sync(kFull, acc, 1);
-      const double nz_ = __shfl_sync(kFull, acc, 2);
+      double num[3], den;
+      visits += (unsigned long long)warp_centroid(P, vb, s, c, sg.main, P.step_kernel, lane, num,
+                                                  &den);
+      const double nx_ = num[0], ny_ = num[1], nz_ = num[2];
       if (den <= 0.0) {
         degenerate = true;
         break;
@@ -541,58 +584,10 @@ struct AbmWarp {
   double acc[10];         // moment chains (lane l writes acc[l])
 };
 
-// Centroid pass (abmsod.cpp:85-90): g = step_w(d) * w[bin]; lanes 0..3 run
-// num.x / num.y / num.z / den in support order. Returns the box visits.
-__device__ long long warp_centroid(const SeekParams& P, const uint8_t* vb, WarpScratch& s,
-                                   const double c[3], const WinGeom& wg, int step_kernel,
-                                   int lane, double num[3], double* den_out) {
-  double acc = 0.0;
-  const Box bb = window_box(c, wg, P.nx, P.ny, P.nz);
-  warp_box_iter_g(bb, lane, [&](const bool* act, const int* x, const int* y, const int* z) {
-    bool in[kG];
-    double g[kG];
-#pragma unroll
-    for (int j = 0; j < kG; ++j) {
-      in[j] = false;
-      g[j] = 0.0;
-      if (act[j]) {
-        const double dd = maha(wg, c, x[j], y[j], z[j]);
-        in[j] = dd <= 1.0;
-        if (in[j]) g[j] = __dmul_rn(kernel_step_weight(step_kernel, dd), s.w[bin_at(P, vb, x[j], y[j], z[j])]);
-      }
-    }
-    int off = 0;
-#pragma unroll
-    for (int j = 0; j < kG; ++j) {
-      const unsigned m0 = __ballot_sync(kFull, in[j]);
-      if (in[j]) {
-        const int r = off + __popc(m0 & ((1u << lane) - 1u));
-        s.v[r] = g[j];
-        s.t[0][r] = __dmul_rn(g[j], (double)x[j]);
-        s.t[1][r] = __dmul_rn(g[j], (double)y[j]);
-        s.t[2][r] = __dmul_rn(g[j], (double)z[j]);
-      }
-      off += __popc(m0);
-    }
-    __syncwarp();
-    if (lane < 4) {
-      const double* src = lane == 3 ? s.v : s.t[lane];
-#pragma unroll 4
-      for (int k = 0; k < off; ++k) acc = __dadd_rn(acc, src[k]);
-    }
-    __syncwarp();
-  });
-  num[0] = __shfl_sync(kFull, acc, 0);
-  num[1] = __shfl_sync(kFull, acc, 1);
-  num[2] = __shfl_sync(kFull, acc, 2);
-  *den_out = __shfl_sync(kFull, acc, 3);
-  return box_size(bb);
-}
-
 // bandwidth_update's moment pass (abmsod.cpp:45-56): over the support of
 // (xn, H), w = weight_for_bin(hp_new), d = xn - s, outer += (w d_i) d_j, wsum += w.
 // Lane l < 9 owns outer element l (i = l / 3, j = l % 3), lane 9 owns wsum.
-__device__ long long warp_moment(const SeekParams& P, const uint8_t* vb, WarpScratch& s,
+__device__ __noinline__ long long warp_moment(const SeekParams& P, const uint8_t* vb, WarpScratch& s,
                                  const double xn[3], const WinGeom& wg, int lane, double* acc_out) {
   double acc = 0.0;
   const int li = lane < 9 ? lane / 3 : 0, lj = lane < 9 ? lane % 3 : 0;
@@ -872,11 +867,6 @@ __device__ void warp_count_shell(const SeekParams& P, const uint8_t* vb, unsigne
   if (B.z1 > A.z1) count_box(Box{A.x0, A.x1, A.y0, A.y1, A.z1 + 1, B.z1});
 }
 
-// q = floor(n / d) for 0 <= n < 2^22, 1 <= d <= 129 through one fp32 multiply:
-// |error| of (n + 0.5) * (1/d) is below 0.5/d there, so truncation is exact.
-__device__ __forceinline__ int fdiv_small(int n, float inv_d) {
-  return (int)(((float)n + 0.5f) * inv_d);
-}
 
 // Per-warp dynamic shared memory of the level-table ascent (AscentLevels).
 struct AscentLayout {
