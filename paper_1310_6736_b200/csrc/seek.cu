@@ -455,8 +455,10 @@ __device__ __forceinline__ long long warp_centroid(const SeekParams& P, const ui
 // ------------------------------------------------------------------- shift
 // warps (seeds) per block; scratch is ~6.3 KB per warp. Small blocks free their
 // slot as soon as their own trajectories end (lengths vary widely per seed).
-template <int NW>
-__global__ void __launch_bounds__(32 * NW) shift_kernel(const SeekParams P) {
+// MINB > 1 caps registers for occupancy (many seeds: throughput-bound); MINB = 1
+// keeps every register for the per-warp chain speed (few, long trajectories).
+template <int NW, int MINB>
+__global__ void __launch_bounds__(32 * NW, MINB) shift_kernel(const SeekParams P) {
   __shared__ WarpScratch scratch[NW];
   const int lane = threadIdx.x & 31;
   const int wid = threadIdx.x >> 5;
@@ -1462,18 +1464,14 @@ void run_seek(salvox_ctx* ctx, SeekJob& job, const uint8_t* d_bins, int bins, co
   P.seeds = reinterpret_cast<const SeedIn*>(d_sd);
   P.seed_H = reinterpret_cast<const double*>(d_h);
   P.err_flag = d_err;
-  static const int shift_warps = [] {
-    const char* e = std::getenv("SALVOX_SHIFT_WARPS");
-    return e ? std::atoi(e) : 2;
-  }();
+  // throughput mode when the seeds fill the GPU several times over
+  const bool many = (long long)P.n_seeds > 64LL * ctx->sm_count;
   if (P.method == SALVOX_METHOD_ABMSOD)
     abmsod_kernel<2><<<(P.n_seeds + 1) / 2, 64, 0, ctx->stream>>>(P);
-  else if (P.method == SALVOX_METHOD_SHIFT && shift_warps == 4)
-    shift_kernel<4><<<(P.n_seeds + 3) / 4, 128, 0, ctx->stream>>>(P);
-  else if (P.method == SALVOX_METHOD_SHIFT && shift_warps == 2)
-    shift_kernel<2><<<(P.n_seeds + 1) / 2, 64, 0, ctx->stream>>>(P);
+  else if (P.method == SALVOX_METHOD_SHIFT && many)
+    shift_kernel<2, 12><<<(P.n_seeds + 1) / 2, 64, 0, ctx->stream>>>(P);
   else if (P.method == SALVOX_METHOD_SHIFT)
-    shift_kernel<1><<<P.n_seeds, 32, 0, ctx->stream>>>(P);
+    shift_kernel<2, 1><<<(P.n_seeds + 1) / 2, 64, 0, ctx->stream>>>(P);
   else
     launch_ascent(ctx, P);
   SX_LAUNCH_CHECK(ctx);
