@@ -552,6 +552,369 @@ __global__ void __launch_bounds__(32 * NW, MINB) shift_kernel(const SeekParams P
   }
 }
 
+// --------------------------------------------- CTA engine (latency mode)
+// When few seeds run (a long trajectory per SM), one seed per CTA: kProd
+// producer warps compute whole 128-voxel chunks (window test, bins, weights,
+// the stable per-bin sort or the ordered compaction) into a double-buffered
+// ring in shared memory while the consumer warp 0 runs the ordered fp64 chains
+// of the previous chunks. Chunk order and every operation are those of the
+// warp engine, so results are bit-identical; only the latency overlaps.
+constexpr int kProd = 3;
+constexpr int kCtaThreads = 32 * (kProd + 1);
+enum { PASS_HIST = 0, PASS_CENT = 1, PASS_MOM = 2 };
+
+struct CtaSlot {
+  double v[kStep];
+  double t[3][kStep];
+  int cnt[kMaxBins];
+  int start[kMaxBins];
+  int n;
+};
+
+struct CtaShared {
+  CtaSlot slot[2][kProd];
+  double h[kMaxBins], p[kMaxBins], w[kMaxBins], tmp[kMaxBins];
+  double res[16];
+  int ires[4];
+};
+
+struct PassIn {
+  const uint8_t* vb;
+  int nx, ny, nz, M;
+  double c[3];
+  const WinGeom* g;
+  int kernel;
+};
+
+template <int MODE>
+__device__ __forceinline__ void cta_produce(const PassIn& in, const Box& bb, int Lx, int Ly,
+                                            int total, int base, CtaSlot& sl, const double* w,
+                                            int lane) {
+  const WinGeom& g = *in.g;
+  bool inb[kG];
+  int bin[kG], xs[kG], ys[kG], zs[kG];
+  double val[kG];
+#pragma unroll
+  for (int j = 0; j < kG; ++j) {
+    const int L = base + 32 * j + lane;
+    const bool act = L < total;
+    const int Lc = act ? L : 0;
+    const int t = Lc / Lx;
+    xs[j] = bb.x0 + (Lc - t * Lx);
+    const int zz = t / Ly;
+    ys[j] = bb.y0 + (t - zz * Ly);
+    zs[j] = bb.z0 + zz;
+    inb[j] = false;
+    bin[j] = 0;
+    val[j] = 0.0;
+    if (act) {
+      const double d = maha(g, in.c, xs[j], ys[j], zs[j]);
+      inb[j] = d <= 1.0;
+      if (inb[j]) {
+        bin[j] = (int)__ldg(in.vb + ((size_t)zs[j] * in.ny + ys[j]) * in.nx + xs[j]) - 1;
+        if (MODE == PASS_HIST) val[j] = __dmul_rn(g.det_fac, kernel_value(in.kernel, d));
+        if (MODE == PASS_CENT) val[j] = __dmul_rn(kernel_step_weight(in.kernel, d), w[bin[j]]);
+        if (MODE == PASS_MOM) val[j] = w[bin[j]];
+      }
+    }
+  }
+  const unsigned lt = (1u << lane) - 1u;
+  if (MODE == PASS_HIST) {  // stable counting sort by bin (as warp_candidate_hist_impl)
+    sl.cnt[lane] = 0;
+    sl.cnt[lane + 32] = 0;
+    __syncwarp();
+    int rank[kG];
+#pragma unroll
+    for (int j = 0; j < kG; ++j) {
+      const unsigned peers = __match_any_sync(kFull, inb[j] ? bin[j] : -1);
+      int b0 = 0;
+      if (inb[j]) b0 = sl.cnt[bin[j]];
+      rank[j] = b0 + __popc(peers & lt);
+      __syncwarp();
+      if (inb[j] && (peers & lt) == 0u) sl.cnt[bin[j]] = b0 + __popc(peers);
+      __syncwarp();
+    }
+    const int c0 = sl.cnt[lane], c1 = sl.cnt[lane + 32];
+    int i0 = c0, i1 = c1;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t0 = __shfl_up_sync(kFull, i0, o), t1 = __shfl_up_sync(kFull, i1, o);
+      if (lane >= o) i0 += t0, i1 += t1;
+    }
+    const int tot0 = __shfl_sync(kFull, i0, 31);
+    sl.start[lane] = i0 - c0;
+    sl.start[lane + 32] = tot0 + i1 - c1;
+    const int tot1 = __shfl_sync(kFull, i1, 31);
+    if (lane == 0) sl.n = tot0 + tot1;
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < kG; ++j)
+      if (inb[j]) sl.v[sl.start[bin[j]] + rank[j]] = val[j];
+  } else {  // ordered compaction
+    int off = 0;
+#pragma unroll
+    for (int j = 0; j < kG; ++j) {
+      const unsigned m0 = __ballot_sync(kFull, inb[j]);
+      if (inb[j]) {
+        const int r = off + __popc(m0 & lt);
+        sl.v[r] = val[j];
+        if (MODE == PASS_CENT) {  // num += g * Vector3d(sx, sy, sz)
+          sl.t[0][r] = __dmul_rn(val[j], (double)xs[j]);
+          sl.t[1][r] = __dmul_rn(val[j], (double)ys[j]);
+          sl.t[2][r] = __dmul_rn(val[j], (double)zs[j]);
+        } else {  // d = x_new - s
+          sl.t[0][r] = __dsub_rn(in.c[0], (double)xs[j]);
+          sl.t[1][r] = __dsub_rn(in.c[1], (double)ys[j]);
+          sl.t[2][r] = __dsub_rn(in.c[2], (double)zs[j]);
+        }
+      }
+      off += __popc(m0);
+    }
+    if (lane == 0) sl.n = off;
+  }
+}
+
+template <int MODE>
+__device__ __forceinline__ void cta_consume(const CtaSlot& sl, int M, int lane, double& a0,
+                                            double& a1, unsigned& support) {
+  if (MODE == PASS_HIST) {
+    const int c0 = sl.cnt[lane], s0 = sl.start[lane];
+    for (int k = 0; k < c0; ++k) a0 = __dadd_rn(a0, sl.v[s0 + k]);
+    if (M > 32) {
+      const int c1 = sl.cnt[lane + 32], s1 = sl.start[lane + 32];
+      for (int k = 0; k < c1; ++k) a1 = __dadd_rn(a1, sl.v[s1 + k]);
+    }
+    support += (unsigned)sl.n;
+  } else if (MODE == PASS_CENT) {
+    if (lane < 4) {
+      const double* src = lane == 3 ? sl.v : sl.t[lane];
+      const int n = sl.n;
+#pragma unroll 4
+      for (int k = 0; k < n; ++k) a0 = __dadd_rn(a0, src[k]);
+    }
+  } else {
+    const int n = sl.n;
+    if (lane < 9) {
+      const double* di = sl.t[lane / 3];
+      const double* dj = sl.t[lane % 3];
+#pragma unroll 4
+      for (int k = 0; k < n; ++k) a0 = __dadd_rn(a0, __dmul_rn(__dmul_rn(sl.v[k], di[k]), dj[k]));
+    } else if (lane == 9) {
+#pragma unroll 4
+      for (int k = 0; k < n; ++k) a0 = __dadd_rn(a0, sl.v[k]);
+    }
+  }
+}
+
+// One support pass of the whole CTA. HIST: leaves the normalized pmf in S.p and
+// returns ok; CENT: S.res[0..3] = num.x, num.y, num.z, den; MOM: S.res[0..9] =
+// outer (row-major) and wsum. *visited = bounding-box voxels, *support.
+template <int MODE>
+__device__ __noinline__ int cta_pass(const PassIn in, CtaShared& S, long long* visited,
+                                     unsigned* support_out) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const Box bb = window_box(in.c, *in.g, in.nx, in.ny, in.nz);
+  const long long bs = box_size(bb);
+  const int Lx = bb.x1 - bb.x0 + 1, Ly = bb.y1 - bb.y0 + 1;
+  const int total = (int)bs;
+  const int nchunks = (total + kStep - 1) / kStep;
+  const int nsteps = (nchunks + kProd - 1) / kProd;
+  double a0 = 0.0, a1 = 0.0;
+  unsigned support = 0;
+  for (int step = 0; step <= nsteps; ++step) {
+    if (warp > 0 && step < nsteps) {
+      const int ch = step * kProd + (warp - 1);
+      CtaSlot& sl = S.slot[step & 1][warp - 1];
+      if (ch < nchunks) {
+        cta_produce<MODE>(in, bb, Lx, Ly, total, ch * kStep, sl, S.w, lane);
+      } else {
+        sl.cnt[lane] = 0;
+        sl.cnt[lane + 32] = 0;
+        if (lane == 0) sl.n = 0;
+      }
+    }
+    if (warp == 0 && step > 0)
+      for (int q = 0; q < kProd; ++q)
+        cta_consume<MODE>(S.slot[(step - 1) & 1][q], in.M, lane, a0, a1, support);
+    __syncthreads();
+  }
+  int ok = 1;
+  if (MODE == PASS_HIST) {
+    if (warp == 0) {
+      if (lane < in.M) S.h[lane] = a0;
+      if (lane + 32 < in.M) S.h[lane + 32] = a1;
+      __syncwarp();
+      if (lane == 0) {
+        double mass = 0.0;
+        for (int b = 0; b < in.M; ++b) mass = __dadd_rn(mass, S.h[b]);  // Histogram::mass
+        S.res[15] = mass;
+        S.ires[0] = (int)support;
+      }
+    }
+    __syncthreads();
+    const double mass = S.res[15];
+    const unsigned sup = (unsigned)S.ires[0];
+    ok = !(sup == 0 || mass <= 0.0);
+    if (ok && threadIdx.x < in.M) S.p[threadIdx.x] = __ddiv_rn(S.h[threadIdx.x], mass);
+    *support_out = sup;
+  } else {
+    if (warp == 0 && lane < (MODE == PASS_CENT ? 4 : 10)) S.res[lane] = a0;
+  }
+  __syncthreads();
+  *visited = bs;
+  return ok;
+}
+
+__device__ __forceinline__ PassIn pass_in(const SeekParams& P, const uint8_t* vb, const double c[3],
+                                          const WinGeom& g, int kernel) {
+  PassIn in;
+  in.vb = vb;
+  in.nx = P.nx, in.ny = P.ny, in.nz = P.nz, in.M = P.bins;
+  in.c[0] = c[0], in.c[1] = c[1], in.c[2] = c[2];
+  in.g = &g;
+  in.kernel = kernel;
+  return in;
+}
+
+__device__ __forceinline__ void cta_weights(const SeekParams& P, CtaShared& S) {
+  if (threadIdx.x < P.bins) {  // weight_for_bin (histogram.hpp:107-113)
+    const double pb = S.p[threadIdx.x] > 1e-6 ? S.p[threadIdx.x] : 1e-6;
+    S.w[threadIdx.x] = __dsqrt_rn(__ddiv_rn(P.q[threadIdx.x], pb));
+  }
+  __syncthreads();
+}
+
+// bhattacharyya(S.p, q) (histogram.hpp:95-103), sequential, broadcast
+__device__ double cta_bhattacharyya(const SeekParams& P, CtaShared& S) {
+  if (threadIdx.x == 0) {
+    double rho = 0.0;
+    for (int b = 0; b < P.bins; ++b) rho = __dadd_rn(rho, __dsqrt_rn(__dmul_rn(S.p[b], P.q[b])));
+    S.res[14] = rho < 1.0 ? rho : 1.0;
+  }
+  __syncthreads();
+  const double r = S.res[14];
+  __syncthreads();
+  return r;
+}
+
+__device__ double cta_entropy(const SeekParams& P, CtaShared& S) {
+  if ((threadIdx.x >> 5) == 0) {
+    const double e = warp_entropy_bits(S.p, P.bins, threadIdx.x & 31, S.tmp);
+    if (threadIdx.x == 0) S.res[13] = e;
+  }
+  __syncthreads();
+  const double e = S.res[13];
+  __syncthreads();
+  return e;
+}
+
+__global__ void __launch_bounds__(kCtaThreads) shift_cta_kernel(const SeekParams P) {
+  __shared__ CtaShared S;
+  const int seed = blockIdx.x;
+  if (seed >= P.n_seeds) return;
+  const SeedIn si = P.seeds[seed];
+  const uint8_t* vb = P.binvol + (size_t)si.vol * P.vol_stride;
+  const ScaleGeom& sg = P.geoms[si.geom];
+  const int M = P.bins;
+  const double lim[3] = {(double)(P.nx - 1), (double)(P.ny - 1), (double)(P.nz - 1)};
+  salvox_detection d;
+  memset(&d, 0, sizeof d);
+  d.seed_index = si.seed_index;
+  for (int i = 0; i < 9; ++i) d.H[i] = sg.H[i];
+  unsigned long long visits = 0;
+  double c[3] = {dclamp(si.pos[0], lim[0]), dclamp(si.pos[1], lim[1]), dclamp(si.pos[2], lim[2])};
+  unsigned support;
+  long long vis;
+  int ok = cta_pass<PASS_HIST>(pass_in(P, vb, c, sg.main, P.hist_kernel), S, &vis, &support);
+  auto frac_bad = [&](unsigned sup) {  // inbounds_support_fraction (shift.cpp:53-57, :75)
+    if (sg.main.support_volume <= 0.0) return 0.0 < P.min_frac;
+    double f = __ddiv_rn((double)sup, sg.main.support_volume);
+    f = f < 1.0 ? f : 1.0;
+    return f < P.min_frac;
+  };
+  bool degenerate = frac_bad(support);
+  if (!degenerate) {
+    for (int it = 0; it < P.max_iters; ++it) {
+      d.iterations = it + 1;
+      visits += (unsigned long long)vis;
+      if (!ok) {
+        degenerate = true;
+        break;
+      }
+      cta_weights(P, S);
+      long long cv;
+      unsigned cs;
+      cta_pass<PASS_CENT>(pass_in(P, vb, c, sg.main, P.step_kernel), S, &cv, &cs);
+      visits += (unsigned long long)cv;
+      const double den = S.res[3];
+      const double moved[3] = {__ddiv_rn(S.res[0], den), __ddiv_rn(S.res[1], den),
+                               __ddiv_rn(S.res[2], den)};
+      if (den <= 0.0) {
+        degenerate = true;
+        break;
+      }
+      double cl[3], df[3];
+      for (int i = 0; i < 3; ++i) cl[i] = dclamp(moved[i], lim[i]);
+      for (int i = 0; i < 3; ++i) df[i] = __dsub_rn(cl[i], moved[i]);
+      if (__dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(df[0], df[0]), __dmul_rn(df[1], df[1])),
+                               __dmul_rn(df[2], df[2]))) > 0.0)
+        d.flags |= SALVOX_FLAG_BOUNDARY_CLAMPED;
+      for (int i = 0; i < 3; ++i) df[i] = __dsub_rn(cl[i], c[i]);
+      const double step = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(df[0], df[0]), __dmul_rn(df[1], df[1])),
+                                               __dmul_rn(df[2], df[2])));
+      c[0] = cl[0], c[1] = cl[1], c[2] = cl[2];
+      ok = cta_pass<PASS_HIST>(pass_in(P, vb, c, sg.main, P.hist_kernel), S, &vis, &support);
+      if (frac_bad(support)) {
+        degenerate = true;
+        break;
+      }
+      if (step < P.min_step) {
+        d.flags |= SALVOX_FLAG_CONVERGED;
+        break;
+      }
+    }
+  }
+  if (degenerate) d.flags |= SALVOX_FLAG_DEGENERATE;
+  d.center[0] = c[0], d.center[1] = c[1], d.center[2] = c[2];
+  if (!degenerate) {  // final scores (shift.cpp:89-105), as warp_final_scores
+    unsigned sup;
+    long long v2;
+    double rho = 0.0;
+    if (ok) rho = cta_bhattacharyya(P, S);
+    const int ok_score = cta_pass<PASS_HIST>(pass_in(P, vb, c, sg.main, 1), S, &v2, &sup);
+    visits += 2ull * (unsigned long long)v2;  // the reference recomputes p_step too
+    if (ok_score && ok) {
+      d.entropy_bits = cta_entropy(P, S);
+      d.bhattacharyya = rho;
+    } else {
+      d.flags |= SALVOX_FLAG_DEGENERATE;
+    }
+    double pdf = 0.0;
+    if (sg.pdf_ok) {
+      const int ok_lo = cta_pass<PASS_HIST>(pass_in(P, vb, c, sg.lo, 0), S, &v2, &sup);
+      visits += (unsigned long long)v2;
+      if (threadIdx.x < M) S.tmp[threadIdx.x] = S.p[threadIdx.x];
+      __syncthreads();
+      const int ok_hi = cta_pass<PASS_HIST>(pass_in(P, vb, c, sg.hi, 0), S, &v2, &sup);
+      visits += (unsigned long long)v2;
+      if (ok_lo && ok_hi) {
+        if (threadIdx.x == 0) {
+          double l1 = 0.0;
+          for (int b = 0; b < M; ++b) l1 = __dadd_rn(l1, fabs(__dsub_rn(S.p[b], S.tmp[b])));
+          S.res[12] = __dmul_rn(sg.pdf_fac, l1);
+        }
+        __syncthreads();
+        pdf = S.res[12];
+      }
+    }
+    d.pdf_diff = pdf;
+  }
+  if (threadIdx.x == 0) {
+    P.out[si.slot] = d;
+    P.visits[si.slot] = visits;
+  }
+}
+
 // ------------------------------------------------------------------ ABMSOD
 // abmsod_run (src/abmsod.cpp:43-169), one warp per seed: every support pass is
 // the shift kernel's compacted ordered scan; the bandwidth moment runs its 9
@@ -1434,6 +1797,21 @@ void launch_ascent(salvox_ctx* ctx, SeekParams& P) {
     launch_ascent_nq<8>(ctx, P);
 }
 
+// Seek engine for shift: the CTA engine for few seeds (latency-bound), the
+// one-warp-per-seed kernel with an 80-register cap when the seeds fill the GPU
+// several times (throughput-bound). SALVOX_SEEK_ENGINE = cta | warp | warp12
+// forces one (tests cover all three).
+int seek_engine(int n_seeds, int sm_count) {
+  static const int forced = [] {
+    const char* e = std::getenv("SALVOX_SEEK_ENGINE");
+    if (!e) return -1;
+    const std::string v(e);
+    return v == "cta" ? 0 : v == "warp" ? 1 : v == "warp12" ? 2 : -1;
+  }();
+  if (forced >= 0) return forced;
+  return (long long)n_seeds > 64LL * sm_count ? 2 : 0;
+}
+
 // Runs the seek kernel for one volume whose bins are already on the device.
 void run_seek(salvox_ctx* ctx, SeekJob& job, const uint8_t* d_bins, int bins, const double* d_q,
               salvox_detection* d_out, unsigned long long* d_visits) {
@@ -1464,11 +1842,12 @@ void run_seek(salvox_ctx* ctx, SeekJob& job, const uint8_t* d_bins, int bins, co
   P.seeds = reinterpret_cast<const SeedIn*>(d_sd);
   P.seed_H = reinterpret_cast<const double*>(d_h);
   P.err_flag = d_err;
-  // throughput mode when the seeds fill the GPU several times over
-  const bool many = (long long)P.n_seeds > 64LL * ctx->sm_count;
+  const int engine = seek_engine(P.n_seeds, ctx->sm_count);
   if (P.method == SALVOX_METHOD_ABMSOD)
     abmsod_kernel<2><<<(P.n_seeds + 1) / 2, 64, 0, ctx->stream>>>(P);
-  else if (P.method == SALVOX_METHOD_SHIFT && many)
+  else if (P.method == SALVOX_METHOD_SHIFT && engine == 0)
+    shift_cta_kernel<<<P.n_seeds, kCtaThreads, 0, ctx->stream>>>(P);
+  else if (P.method == SALVOX_METHOD_SHIFT && engine == 2)
     shift_kernel<2, 12><<<(P.n_seeds + 1) / 2, 64, 0, ctx->stream>>>(P);
   else if (P.method == SALVOX_METHOD_SHIFT)
     shift_kernel<2, 1><<<(P.n_seeds + 1) / 2, 64, 0, ctx->stream>>>(P);

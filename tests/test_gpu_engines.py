@@ -1,0 +1,24 @@
+"""The shift seek has three engines with identical arithmetic (DESIGN.md "Seed
+kernels"): the CTA producer/consumer engine (few seeds), and the one-warp-per-
+seed kernel in its latency and 80-register occupancy variants (many seeds).
+The engine is picked by seed count, so the parity tests exercise whichever the
+test size selects; here every shift parity test reruns with each engine forced
+(SALVOX_SEEK_ENGINE, read once per process -> a subprocess per engine)."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.parametrize("engine", ["cta", "warp", "warp12"])
+def test_shift_parity_under_each_engine(engine):
+    env = dict(os.environ, SALVOX_SEEK_ENGINE=engine)
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-k", "shift or detect",
+                        "tests/test_gpu_seek.py", "tests/test_gpu_edge.py", "tests/test_golden.py"],
+                       cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout
