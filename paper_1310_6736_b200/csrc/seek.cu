@@ -26,6 +26,10 @@
 #include "../../include/salvox/sx_eig3.h"
 #include "../../include/salvox/sx_log.h"
 #include "common.cuh"
+
+#ifndef CTA_PRODUCERS
+#define CTA_PRODUCERS 3
+#endif
 #include "host_math.h"
 
 namespace sx {
@@ -553,14 +557,12 @@ __global__ void __launch_bounds__(32 * NW, MINB) shift_kernel(const SeekParams P
 }
 
 // --------------------------------------------- CTA engine (latency mode)
-// When few seeds run (a long trajectory per SM), one seed per CTA: kProd
+// When few seeds run (a long trajectory per SM), one seed per CTA: NP
 // producer warps compute whole 128-voxel chunks (window test, bins, weights,
 // the stable per-bin sort or the ordered compaction) into a double-buffered
 // ring in shared memory while the consumer warp 0 runs the ordered fp64 chains
 // of the previous chunks. Chunk order and every operation are those of the
 // warp engine, so results are bit-identical; only the latency overlaps.
-constexpr int kProd = 3;
-constexpr int kCtaThreads = 32 * (kProd + 1);
 enum { PASS_HIST = 0, PASS_CENT = 1, PASS_MOM = 2 };
 
 struct CtaSlot {
@@ -571,11 +573,14 @@ struct CtaSlot {
   int n;
 };
 
+template <int NP>
 struct CtaShared {
-  CtaSlot slot[2][kProd];
+  CtaSlot slot[2][NP];
   double h[kMaxBins], p[kMaxBins], w[kMaxBins], tmp[kMaxBins];
   double res[16];
   int ires[4];
+  WinGeom g;              // ABMSOD: the current window's geometry
+  double Hc[9], Hn[9];    // ABMSOD: current / updated bandwidth
 };
 
 struct PassIn {
@@ -709,8 +714,8 @@ __device__ __forceinline__ void cta_consume(const CtaSlot& sl, int M, int lane, 
 // One support pass of the whole CTA. HIST: leaves the normalized pmf in S.p and
 // returns ok; CENT: S.res[0..3] = num.x, num.y, num.z, den; MOM: S.res[0..9] =
 // outer (row-major) and wsum. *visited = bounding-box voxels, *support.
-template <int MODE>
-__device__ __noinline__ int cta_pass(const PassIn in, CtaShared& S, long long* visited,
+template <int MODE, int NP>
+__device__ __noinline__ int cta_pass(const PassIn in, CtaShared<NP>& S, long long* visited,
                                      unsigned* support_out) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const Box bb = window_box(in.c, *in.g, in.nx, in.ny, in.nz);
@@ -718,12 +723,12 @@ __device__ __noinline__ int cta_pass(const PassIn in, CtaShared& S, long long* v
   const int Lx = bb.x1 - bb.x0 + 1, Ly = bb.y1 - bb.y0 + 1;
   const int total = (int)bs;
   const int nchunks = (total + kStep - 1) / kStep;
-  const int nsteps = (nchunks + kProd - 1) / kProd;
+  const int nsteps = (nchunks + NP - 1) / NP;
   double a0 = 0.0, a1 = 0.0;
   unsigned support = 0;
   for (int step = 0; step <= nsteps; ++step) {
     if (warp > 0 && step < nsteps) {
-      const int ch = step * kProd + (warp - 1);
+      const int ch = step * NP + (warp - 1);
       CtaSlot& sl = S.slot[step & 1][warp - 1];
       if (ch < nchunks) {
         cta_produce<MODE>(in, bb, Lx, Ly, total, ch * kStep, sl, S.w, lane);
@@ -734,7 +739,7 @@ __device__ __noinline__ int cta_pass(const PassIn in, CtaShared& S, long long* v
       }
     }
     if (warp == 0 && step > 0)
-      for (int q = 0; q < kProd; ++q)
+      for (int q = 0; q < NP; ++q)
         cta_consume<MODE>(S.slot[(step - 1) & 1][q], in.M, lane, a0, a1, support);
     __syncthreads();
   }
@@ -776,7 +781,8 @@ __device__ __forceinline__ PassIn pass_in(const SeekParams& P, const uint8_t* vb
   return in;
 }
 
-__device__ __forceinline__ void cta_weights(const SeekParams& P, CtaShared& S) {
+template <int NP>
+__device__ __forceinline__ void cta_weights(const SeekParams& P, CtaShared<NP>& S) {
   if (threadIdx.x < P.bins) {  // weight_for_bin (histogram.hpp:107-113)
     const double pb = S.p[threadIdx.x] > 1e-6 ? S.p[threadIdx.x] : 1e-6;
     S.w[threadIdx.x] = __dsqrt_rn(__ddiv_rn(P.q[threadIdx.x], pb));
@@ -785,7 +791,8 @@ __device__ __forceinline__ void cta_weights(const SeekParams& P, CtaShared& S) {
 }
 
 // bhattacharyya(S.p, q) (histogram.hpp:95-103), sequential, broadcast
-__device__ double cta_bhattacharyya(const SeekParams& P, CtaShared& S) {
+template <int NP>
+__device__ double cta_bhattacharyya(const SeekParams& P, CtaShared<NP>& S) {
   if (threadIdx.x == 0) {
     double rho = 0.0;
     for (int b = 0; b < P.bins; ++b) rho = __dadd_rn(rho, __dsqrt_rn(__dmul_rn(S.p[b], P.q[b])));
@@ -797,7 +804,8 @@ __device__ double cta_bhattacharyya(const SeekParams& P, CtaShared& S) {
   return r;
 }
 
-__device__ double cta_entropy(const SeekParams& P, CtaShared& S) {
+template <int NP>
+__device__ double cta_entropy(const SeekParams& P, CtaShared<NP>& S) {
   if ((threadIdx.x >> 5) == 0) {
     const double e = warp_entropy_bits(S.p, P.bins, threadIdx.x & 31, S.tmp);
     if (threadIdx.x == 0) S.res[13] = e;
@@ -808,8 +816,10 @@ __device__ double cta_entropy(const SeekParams& P, CtaShared& S) {
   return e;
 }
 
-__global__ void __launch_bounds__(kCtaThreads) shift_cta_kernel(const SeekParams P) {
-  __shared__ CtaShared S;
+template <int NP>
+__global__ void __launch_bounds__(32 * (NP + 1)) shift_cta_kernel(const SeekParams P) {
+  extern __shared__ __align__(16) unsigned char cta_dyn[];
+  CtaShared<NP>& S = *reinterpret_cast<CtaShared<NP>*>(cta_dyn);
   const int seed = blockIdx.x;
   if (seed >= P.n_seeds) return;
   const SeedIn si = P.seeds[seed];
@@ -825,7 +835,7 @@ __global__ void __launch_bounds__(kCtaThreads) shift_cta_kernel(const SeekParams
   double c[3] = {dclamp(si.pos[0], lim[0]), dclamp(si.pos[1], lim[1]), dclamp(si.pos[2], lim[2])};
   unsigned support;
   long long vis;
-  int ok = cta_pass<PASS_HIST>(pass_in(P, vb, c, sg.main, P.hist_kernel), S, &vis, &support);
+  int ok = cta_pass<PASS_HIST, NP>(pass_in(P, vb, c, sg.main, P.hist_kernel), S, &vis, &support);
   auto frac_bad = [&](unsigned sup) {  // inbounds_support_fraction (shift.cpp:53-57, :75)
     if (sg.main.support_volume <= 0.0) return 0.0 < P.min_frac;
     double f = __ddiv_rn((double)sup, sg.main.support_volume);
@@ -844,7 +854,7 @@ __global__ void __launch_bounds__(kCtaThreads) shift_cta_kernel(const SeekParams
       cta_weights(P, S);
       long long cv;
       unsigned cs;
-      cta_pass<PASS_CENT>(pass_in(P, vb, c, sg.main, P.step_kernel), S, &cv, &cs);
+      cta_pass<PASS_CENT, NP>(pass_in(P, vb, c, sg.main, P.step_kernel), S, &cv, &cs);
       visits += (unsigned long long)cv;
       const double den = S.res[3];
       const double moved[3] = {__ddiv_rn(S.res[0], den), __ddiv_rn(S.res[1], den),
@@ -863,7 +873,7 @@ __global__ void __launch_bounds__(kCtaThreads) shift_cta_kernel(const SeekParams
       const double step = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(df[0], df[0]), __dmul_rn(df[1], df[1])),
                                                __dmul_rn(df[2], df[2])));
       c[0] = cl[0], c[1] = cl[1], c[2] = cl[2];
-      ok = cta_pass<PASS_HIST>(pass_in(P, vb, c, sg.main, P.hist_kernel), S, &vis, &support);
+      ok = cta_pass<PASS_HIST, NP>(pass_in(P, vb, c, sg.main, P.hist_kernel), S, &vis, &support);
       if (frac_bad(support)) {
         degenerate = true;
         break;
@@ -881,7 +891,7 @@ __global__ void __launch_bounds__(kCtaThreads) shift_cta_kernel(const SeekParams
     long long v2;
     double rho = 0.0;
     if (ok) rho = cta_bhattacharyya(P, S);
-    const int ok_score = cta_pass<PASS_HIST>(pass_in(P, vb, c, sg.main, 1), S, &v2, &sup);
+    const int ok_score = cta_pass<PASS_HIST, NP>(pass_in(P, vb, c, sg.main, 1), S, &v2, &sup);
     visits += 2ull * (unsigned long long)v2;  // the reference recomputes p_step too
     if (ok_score && ok) {
       d.entropy_bits = cta_entropy(P, S);
@@ -891,11 +901,11 @@ __global__ void __launch_bounds__(kCtaThreads) shift_cta_kernel(const SeekParams
     }
     double pdf = 0.0;
     if (sg.pdf_ok) {
-      const int ok_lo = cta_pass<PASS_HIST>(pass_in(P, vb, c, sg.lo, 0), S, &v2, &sup);
+      const int ok_lo = cta_pass<PASS_HIST, NP>(pass_in(P, vb, c, sg.lo, 0), S, &v2, &sup);
       visits += (unsigned long long)v2;
       if (threadIdx.x < M) S.tmp[threadIdx.x] = S.p[threadIdx.x];
       __syncthreads();
-      const int ok_hi = cta_pass<PASS_HIST>(pass_in(P, vb, c, sg.hi, 0), S, &v2, &sup);
+      const int ok_hi = cta_pass<PASS_HIST, NP>(pass_in(P, vb, c, sg.hi, 0), S, &v2, &sup);
       visits += (unsigned long long)v2;
       if (ok_lo && ok_hi) {
         if (threadIdx.x == 0) {
@@ -1191,6 +1201,192 @@ __global__ void __launch_bounds__(32 * NW) abmsod_kernel(const SeekParams P) {
     atomicOr(P.err_flag, 1);  // eigen decomposition failed: runtime_error for the call
   }
   if (lane == 0) {
+    P.out[si.slot] = d;
+    P.visits[si.slot] = visits;
+    if (P.abm_trace_n) P.abm_trace_n[si.slot] = n_trace;
+  }
+}
+
+// ABMSOD on the CTA engine (latency mode: a few hundred seeds, long passes):
+// the same operations as abmsod_kernel, each support pass run by cta_pass.
+template <int NP>
+__global__ void __launch_bounds__(32 * (NP + 1)) abmsod_cta_kernel(const SeekParams P) {
+  extern __shared__ __align__(16) unsigned char cta_dyn[];
+  CtaShared<NP>& S = *reinterpret_cast<CtaShared<NP>*>(cta_dyn);
+  const int seed = blockIdx.x;
+  if (seed >= P.n_seeds) return;
+  const SeedIn si = P.seeds[seed];
+  const uint8_t* vb = P.binvol + (size_t)si.vol * P.vol_stride;
+  const bool two_d = P.two_d != 0;
+  const int M = P.bins;
+  const double lim[3] = {(double)(P.nx - 1), (double)(P.ny - 1), (double)(P.nz - 1)};
+  salvox_detection d;
+  memset(&d, 0, sizeof d);
+  d.seed_index = si.seed_index;
+  double x[3] = {dclamp(si.pos[0], lim[0]), dclamp(si.pos[1], lim[1]), dclamp(si.pos[2], lim[2])};
+  d.center[0] = x[0], d.center[1] = x[1], d.center[2] = x[2];
+  const double* H0 = P.seed_H + 9 * (size_t)si.slot;
+  double H_opt[9];
+  for (int i = 0; i < 9; ++i) d.H[i] = H_opt[i] = H0[i];
+  if (threadIdx.x < 9) S.Hc[threadIdx.x] = H0[threadIdx.x];
+  __syncthreads();
+  double x_opt[3] = {x[0], x[1], x[2]};
+  double max_bhat = 0.0;
+  int stalled = 0, n_trace = 0;
+  bool any = false, failed = false;
+  unsigned long long visits = 0;
+  for (int it = 0; it < P.abm_max_iters; ++it) {
+    if (threadIdx.x == 0) dev_make_geom(S.Hc, two_d, S.g);
+    __syncthreads();
+    unsigned support;
+    long long vis;
+    const int ok = cta_pass<PASS_HIST, NP>(pass_in(P, vb, x, S.g, P.abm_kernel), S, &vis, &support);
+    double frac = 0.0;  // inbounds_support_fraction (window.cpp:54-60)
+    if (S.g.support_volume > 0.0) {
+      frac = __ddiv_rn((double)support, S.g.support_volume);
+      frac = frac < 1.0 ? frac : 1.0;
+    }
+    if (frac < P.abm_min_frac) {
+      d.flags |= SALVOX_FLAG_DEGENERATE;
+      break;
+    }
+    visits += (unsigned long long)vis;
+    if (!ok) {
+      d.flags |= SALVOX_FLAG_DEGENERATE;
+      break;
+    }
+    cta_weights(P, S);
+    unsigned cs;
+    cta_pass<PASS_CENT, NP>(pass_in(P, vb, x, S.g, P.abm_kernel), S, &vis, &cs);
+    visits += (unsigned long long)vis;
+    const double den = S.res[3];
+    if (den <= 0.0) {
+      d.flags |= SALVOX_FLAG_DEGENERATE;
+      break;
+    }
+    const double moved[3] = {__ddiv_rn(S.res[0], den), __ddiv_rn(S.res[1], den),
+                             __ddiv_rn(S.res[2], den)};
+    double xn[3], df[3];
+    for (int i = 0; i < 3; ++i) xn[i] = dclamp(moved[i], lim[i]);
+    for (int i = 0; i < 3; ++i) df[i] = __dsub_rn(xn[i], moved[i]);
+    if (__dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(df[0], df[0]), __dmul_rn(df[1], df[1])),
+                             __dmul_rn(df[2], df[2]))) > 0.0)
+      d.flags |= SALVOX_FLAG_BOUNDARY_CLAMPED;
+    const int ok2 = cta_pass<PASS_HIST, NP>(pass_in(P, vb, xn, S.g, P.abm_kernel), S, &vis, &support);
+    visits += (unsigned long long)vis;
+    if (!ok2) {
+      d.flags |= SALVOX_FLAG_DEGENERATE;
+      break;
+    }
+    cta_weights(P, S);
+    cta_pass<PASS_MOM, NP>(pass_in(P, vb, xn, S.g, 0), S, &vis, &cs);
+    visits += (unsigned long long)vis;
+    if (threadIdx.x == 0)
+      S.ires[1] = sx_bandwidth_from_moment(S.res, S.res[9], two_d ? 2 : 3, P.abm_lmin, P.abm_lmax, S.Hn);
+    __syncthreads();
+    const int br = S.ires[1];
+    if (br == 3) {
+      failed = true;
+      break;
+    }
+    if (br != 0) {
+      d.flags |= SALVOX_FLAG_DEGENERATE;
+      break;
+    }
+    const double bhat = cta_bhattacharyya(P, S);
+    any = true;
+    d.iterations = it + 1;
+    const bool improved = bhat > __dadd_rn(max_bhat, P.abm_threshold);
+    if (bhat > max_bhat) {
+      max_bhat = bhat;
+      for (int i = 0; i < 3; ++i) x_opt[i] = xn[i];
+      for (int i = 0; i < 9; ++i) H_opt[i] = S.Hn[i];
+    }
+    if (P.abm_trace) {
+      if (threadIdx.x == 0) {
+        double ev[3], V[9];
+        S.ires[2] = sx_sym_eigen3(S.Hn, ev, V) != 0;
+        salvox_abmsod_iter& r = P.abm_trace[(size_t)si.slot * P.abm_max_iters + n_trace];
+        for (int i = 0; i < 3; ++i) r.position[i] = xn[i];
+        for (int i = 0; i < 9; ++i) r.H[i] = S.Hn[i];
+        r.bhattacharyya = bhat;
+        r.max_bhattacharyya = max_bhat;
+        r.eig_min = fmin(fmin(ev[0], ev[1]), ev[2]);
+        r.eig_max = fmax(fmax(ev[0], ev[1]), ev[2]);
+      }
+      __syncthreads();
+      ++n_trace;
+      if (S.ires[2]) {
+        failed = true;
+        break;
+      }
+    }
+    for (int i = 0; i < 3; ++i) x[i] = xn[i];
+    __syncthreads();
+    if (threadIdx.x < 9) S.Hc[threadIdx.x] = S.Hn[threadIdx.x];
+    __syncthreads();
+    stalled = improved ? 0 : stalled + 1;
+    if (stalled >= 2) {
+      d.flags |= SALVOX_FLAG_CONVERGED;
+      break;
+    }
+  }
+  if (!failed) {
+    if (any) {  // score the best iterate (abmsod.cpp:154-165)
+      d.center[0] = x_opt[0], d.center[1] = x_opt[1], d.center[2] = x_opt[2];
+      for (int i = 0; i < 9; ++i) d.H[i] = H_opt[i];
+      d.bhattacharyya = max_bhat;
+      __syncthreads();
+      if (threadIdx.x < 9) S.Hc[threadIdx.x] = H_opt[threadIdx.x];
+      __syncthreads();
+      if (threadIdx.x == 0) dev_make_geom(S.Hc, two_d, S.g);
+      __syncthreads();
+      unsigned sup;
+      long long vis;
+      if (cta_pass<PASS_HIST, NP>(pass_in(P, vb, x_opt, S.g, 1), S, &vis, &sup))
+        d.entropy_bits = cta_entropy(P, S);
+      visits += (unsigned long long)vis;
+      const double sc = dev_window_scale(H_opt, two_d);
+      double pdf = 0.0;
+      if (!(__dsub_rn(sc, 1.0) < 1.0)) {  // pdf_difference (window.cpp:30-46)
+        int okf[2];
+        for (int f = 0; f < 2; ++f) {
+          const double s_new = f == 0 ? __dsub_rn(sc, 1.0) : __dadd_rn(sc, 1.0);
+          const double r = __ddiv_rn(s_new, sc);
+          const double fac = __dmul_rn(r, r);
+          __syncthreads();
+          if (threadIdx.x < 9) S.Hn[threadIdx.x] = __dmul_rn(H_opt[threadIdx.x], fac);
+          __syncthreads();
+          if (threadIdx.x == 0) {
+            if (two_d) S.Hn[8] = 1.0;
+            dev_make_geom(S.Hn, two_d, S.g);
+          }
+          __syncthreads();
+          okf[f] = cta_pass<PASS_HIST, NP>(pass_in(P, vb, x_opt, S.g, 0), S, &vis, &sup);
+          visits += (unsigned long long)vis;
+          if (f == 0) {
+            if (threadIdx.x < M) S.tmp[threadIdx.x] = S.p[threadIdx.x];
+            __syncthreads();
+          }
+        }
+        if (okf[0] && okf[1]) {
+          if (threadIdx.x == 0) {
+            double l1 = 0.0;
+            for (int b = 0; b < M; ++b) l1 = __dadd_rn(l1, fabs(__dsub_rn(S.p[b], S.tmp[b])));
+            S.res[12] = __dmul_rn(__ddiv_rn(__dmul_rn(sc, sc), 2.0), l1);
+          }
+          __syncthreads();
+          pdf = S.res[12];
+        }
+      }
+      d.pdf_diff = pdf;
+    } else {
+      d.flags |= SALVOX_FLAG_DEGENERATE;
+    }
+  } else if (threadIdx.x == 0) {
+    atomicOr(P.err_flag, 1);
+  }
+  if (threadIdx.x == 0) {
     P.out[si.slot] = d;
     P.visits[si.slot] = visits;
     if (P.abm_trace_n) P.abm_trace_n[si.slot] = n_trace;
@@ -1812,6 +2008,15 @@ int seek_engine(int n_seeds, int sm_count) {
   return (long long)n_seeds > 64LL * sm_count ? 2 : 0;
 }
 
+constexpr int kCtaProducers = CTA_PRODUCERS;
+
+template <int NP, class K>
+void launch_cta(K kern, salvox_ctx* ctx, const SeekParams& P) {
+  const int bytes = (int)sizeof(CtaShared<NP>);
+  SX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  kern<<<P.n_seeds, 32 * (NP + 1), bytes, ctx->stream>>>(P);
+}
+
 // Runs the seek kernel for one volume whose bins are already on the device.
 void run_seek(salvox_ctx* ctx, SeekJob& job, const uint8_t* d_bins, int bins, const double* d_q,
               salvox_detection* d_out, unsigned long long* d_visits) {
@@ -1843,10 +2048,12 @@ void run_seek(salvox_ctx* ctx, SeekJob& job, const uint8_t* d_bins, int bins, co
   P.seed_H = reinterpret_cast<const double*>(d_h);
   P.err_flag = d_err;
   const int engine = seek_engine(P.n_seeds, ctx->sm_count);
-  if (P.method == SALVOX_METHOD_ABMSOD)
+  if (P.method == SALVOX_METHOD_ABMSOD && engine == 0)
+    launch_cta<kCtaProducers>(abmsod_cta_kernel<kCtaProducers>, ctx, P);
+  else if (P.method == SALVOX_METHOD_ABMSOD)
     abmsod_kernel<2><<<(P.n_seeds + 1) / 2, 64, 0, ctx->stream>>>(P);
   else if (P.method == SALVOX_METHOD_SHIFT && engine == 0)
-    shift_cta_kernel<<<P.n_seeds, kCtaThreads, 0, ctx->stream>>>(P);
+    launch_cta<kCtaProducers>(shift_cta_kernel<kCtaProducers>, ctx, P);
   else if (P.method == SALVOX_METHOD_SHIFT && engine == 2)
     shift_kernel<2, 12><<<(P.n_seeds + 1) / 2, 64, 0, ctx->stream>>>(P);
   else if (P.method == SALVOX_METHOD_SHIFT)

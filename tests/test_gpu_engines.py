@@ -17,8 +17,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 @pytest.mark.parametrize("engine", ["cta", "warp", "warp12"])
 def test_shift_parity_under_each_engine(engine):
     env = dict(os.environ, SALVOX_SEEK_ENGINE=engine)
-    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-k", "shift or detect",
-                        "tests/test_gpu_seek.py", "tests/test_gpu_edge.py", "tests/test_golden.py"],
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-k", "shift or detect or abmsod",
+                        "tests/test_gpu_seek.py", "tests/test_gpu_edge.py", "tests/test_golden.py",
+                        "tests/test_gpu_abmsod.py"],
                        cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
     assert " passed" in r.stdout
