@@ -87,6 +87,7 @@ def kadir_brady_exhaustive_records(volume, scales, window_low=None, window_high=
     check(_lib.load().salvox_exhaustive(
         c.handle, ptr(v), nx, ny, nz, C.byref(iw), ptr(sc), len(sc), KERNELS[kernel], int(budget),
         ptr(score), ptr(best), ptr(maxima), cap, C.byref(n), C.byref(visits)))
+    _MAXIMA_HINT[id(c)] = n.value
     if n.value > cap:
         maxima = np.empty(n.value, MAX_DTYPE)
         check(_lib.load().salvox_last_maxima(c.handle, ptr(maxima), n.value, C.byref(n)))
@@ -105,6 +106,9 @@ def kadir_brady_exhaustive(volume, scales, window_low=None, window_high=None, bi
     out = [{"position": tuple(float(p) for p in m["position"]), "score": float(m["score"]),
             "scale": float(m["scale"])} for m in maxima]
     return score, out
+
+
+_MAXIMA_HINT = {}  # context id -> maxima count of its last slab call (output sizing)
 
 
 def kadir_brady_exhaustive_slab(slab, nz_total, zs0, z0, z1, scales, window_low, window_high,
@@ -126,7 +130,7 @@ def kadir_brady_exhaustive_slab(slab, nz_total, zs0, z0, z1, scales, window_low,
     else:
         score = np.empty((z1 - z0, ny, nx), np.float32)
         best = np.empty((z1 - z0, ny, nx), np.float32)
-    cap = 4096
+    cap = max(4096, int(_MAXIMA_HINT.get(id(c), 0) * 1.1))  # size from the last call
     maxima = np.empty(cap, MAX_DTYPE)
     n = C.c_int64(0)
     visits = C.c_uint64(0)
@@ -134,6 +138,7 @@ def kadir_brady_exhaustive_slab(slab, nz_total, zs0, z0, z1, scales, window_low,
         c.handle, ptr(s), nx, ny, int(nz_total), int(zs0), int(zs0 + nzs), int(z0), int(z1),
         C.byref(iw), ptr(sc), len(sc), KERNELS[kernel], int(budget), ptr(score), ptr(best),
         ptr(maxima), cap, C.byref(n), C.byref(visits)))
+    _MAXIMA_HINT[id(c)] = n.value
     if n.value > cap:
         maxima = np.empty(n.value, MAX_DTYPE)
         check(_lib.load().salvox_last_maxima(c.handle, ptr(maxima), n.value, C.byref(n)))

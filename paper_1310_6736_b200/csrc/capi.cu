@@ -29,6 +29,8 @@ salvox_ctx::~salvox_ctx() {
                     &d_sel_c, &d_sel_d, &d_visits, &d_target, &d_seek_vol, &d_seek_bins})
     b->release();
   h_stage.release();
+  for (cudaEvent_t e : events) cudaEventDestroy(e);
+  if (copy_stream) cudaStreamDestroy(copy_stream);
   if (own_stream) cudaStreamDestroy(own_stream);
 }
 

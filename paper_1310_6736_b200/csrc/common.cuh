@@ -111,6 +111,8 @@ struct salvox_ctx {
   int sm_count = 0;
   cudaStream_t own_stream = nullptr;
   cudaStream_t stream = nullptr;
+  cudaStream_t copy_stream = nullptr;  // host<->device copies overlapped with compute
+  std::vector<cudaEvent_t> events;     // pipeline events (grown on demand)
   std::mutex mu;
   uint64_t launches = 0;
   // kb_kernel timing (salvox_ctx_set_profiling)
@@ -121,8 +123,8 @@ struct salvox_ctx {
   // exhaustive path
   sx::DevBuf d_vol, d_bins, d_score, d_best, d_keys, d_keys_alt, d_cub, d_counter, d_maxima,
       d_minmax, d_dbg;
-  sx::HostBuf h_stage;
-  std::vector<salvox_maximum> last_maxima;
+  sx::HostBuf h_stage;       // pinned: the last call's maxima (salvox_last_maxima)
+  int64_t last_maxima_n = 0;
   sx::ExhState exh;
   // seek path
   sx::DevBuf d_seeds, d_dets, d_geom, d_sel_a, d_sel_b, d_sel_c, d_sel_d, d_visits, d_target,

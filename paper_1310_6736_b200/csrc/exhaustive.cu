@@ -1100,25 +1100,57 @@ void validate_exhaustive(int nx, int ny, int nz, const salvox_window* iw, const 
     fail(SALVOX_EUNSUPPORTED, "exhaustive (device): volume exceeds 2^32 voxels");
 }
 
-// Core: d_slab holds planes [zs0, zs1) of the volume (device, f32). Scores planes
-// [zc0, zc1) = [z0-1, z1+1) clipped, finds maxima of [z0, z1), sorts them.
-// Leaves: ctx->d_score/d_best (planes zc0..zc1), sorted keys, count.
-long long run_exhaustive(salvox_ctx* ctx, const float* d_slab, int nx, int ny, int nz, int zs0,
-                         int zs1, int z0, int z1, double low, double high, int bins,
-                         const double* scales, int n_scales, ExhRun* run_out) {
+// make_plan enumerates the (2R+1)^3 candidate offsets per radius (milliseconds
+// at R = 16): plans are cached per (scales, 2D, tile config).
+Plan cached_plan(const double* scales, int n_scales, bool two_d, const TileCfg& tc, int* SYo,
+                 int* SZo) {
+  struct Entry {
+    std::vector<double> scales;
+    bool two_d;
+    TileCfg tc;
+    Plan pl;
+    int SY, SZ;
+  };
+  static std::mutex mu;
+  static std::vector<Entry> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  for (const Entry& e : cache)
+    if (e.two_d == two_d && e.tc.nb == tc.nb && e.tc.tx == tc.tx && e.tc.ty == tc.ty &&
+        e.tc.tz == tc.tz && e.tc.pair == tc.pair && e.tc.tmem == tc.tmem &&
+        e.scales.size() == (size_t)n_scales &&
+        std::equal(e.scales.begin(), e.scales.end(), scales)) {
+      *SYo = e.SY;
+      *SZo = e.SZ;
+      return e.pl;
+    }
+  Entry e;
+  e.scales.assign(scales, scales + n_scales);
+  e.two_d = two_d;
+  e.tc = tc;
+  e.pl = make_plan(scales, n_scales, two_d, tc, &e.SY, &e.SZ);
+  *SYo = e.SY;
+  *SZo = e.SZ;
+  if (cache.size() >= 16) cache.erase(cache.begin());
+  cache.push_back(e);
+  return cache.back().pl;
+}
+
+// Setup of one exhaustive run over the slab planes [zs0, zs1) (device bins at
+// ctx->d_bins, pitch 16-aligned): plan, tensor map, kernel parameters for the
+// scored planes [zc0, zc1) = [z0-1, z1+1) clipped, score/best buffers.
+ExhRun setup_exhaustive(salvox_ctx* ctx, int nx, int ny, int nz, int zs0, int zs1, int z0, int z1,
+                        int bins, const double* scales, int n_scales) {
   const bool two_d = nz == 1;
   ExhRun run;
   run.tc = pick_tile(bins, two_d);
   int SY = 0, SZ = 0;
-  run.pl = make_plan(scales, n_scales, two_d, run.tc, &SY, &SZ);
+  run.pl = cached_plan(scales, n_scales, two_d, run.tc, &SY, &SZ);
   const int R = run.pl.R;
   if (zs0 > std::max(0, z0 - R - 1) || zs1 < std::min(nz, z1 + R + 1))
     fail(SALVOX_EINVAL, "exhaustive slab: the slab must cover the owned planes plus the halo");
   const int nzs = zs1 - zs0;
   const int pitch = (nx + 15) / 16 * 16;
   uint8_t* d_bins = static_cast<uint8_t*>(ctx->d_bins.ensure((size_t)pitch * ny * nzs));
-  launch_bin_volume(ctx, d_slab, d_bins, nx, ny, nzs, pitch, low, high, bins);
-
   const int zc0 = std::max(0, z0 - 1), zc1 = std::min(nz, z1 + 1);
   const size_t nscore = (size_t)nx * ny * (zc1 - zc0);
   float* d_score = static_cast<float*>(ctx->d_score.ensure(nscore * 4));
@@ -1155,32 +1187,44 @@ long long run_exhaustive(salvox_ctx* ctx, const float* d_slab, int nx, int ny, i
   run.smem = kb_smem(run.tc, kp.tile_bytes);
   run.grid = dim3((nx + run.tc.tx - 1) / run.tc.tx, (ny + run.tc.ty - 1) / run.tc.ty,
                   (zc1 - zc0 + run.tc.tz - 1) / run.tc.tz);
-  {
-    std::lock_guard<std::mutex> lk(g_const_mu);
-    upload_tables(ctx, run.pl);
-    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-    if (ctx->profiling) {
-      SX_CUDA(cudaEventCreate(&ev0));
-      SX_CUDA(cudaEventCreate(&ev1));
-      SX_CUDA(cudaEventRecord(ev0, ctx->stream));
-    }
-    dispatch_kb<false>(ctx, run.tc, run.map, kp, run.grid, run.smem);
-    if (ctx->profiling) {
-      SX_CUDA(cudaEventRecord(ev1, ctx->stream));
-      SX_CUDA(cudaEventSynchronize(ev1));
-      float ms = 0.f;
-      SX_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
-      cudaEventDestroy(ev0);
-      cudaEventDestroy(ev1);
-      ctx->kb_ms_total += ms;
-      ctx->kb_launches += 1;
-      ctx->kb_updates_total +=
-          (double)nx * ny * (zc1 - zc0) * (double)(run.pl.ball_size.back() - 1);
-    }
-    SX_CUDA(cudaEventRecord(g_const_done, ctx->stream));
-  }
+  return run;
+}
 
-  // K3: maxima of the owned planes + sort
+// KB kernel over the scored planes [a, b) (a subrange of [zc0, zc1)); the
+// constant-memory tables must already hold run.pl (caller holds g_const_mu).
+void launch_kb_chunk(salvox_ctx* ctx, const ExhRun& run, int a, int b) {
+  KbParams kp = run.kp;
+  const size_t plane = (size_t)kp.nx * kp.ny;
+  kp.score = run.kp.score + (size_t)(a - run.kp.zc0) * plane;
+  kp.best = run.kp.best + (size_t)(a - run.kp.zc0) * plane;
+  kp.zc0 = a;
+  kp.zc1 = b;
+  const dim3 grid(run.grid.x, run.grid.y, (b - a + run.tc.tz - 1) / run.tc.tz);
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  if (ctx->profiling) {
+    SX_CUDA(cudaEventCreate(&ev0));
+    SX_CUDA(cudaEventCreate(&ev1));
+    SX_CUDA(cudaEventRecord(ev0, ctx->stream));
+  }
+  dispatch_kb<false>(ctx, run.tc, run.map, kp, grid, run.smem);
+  if (ctx->profiling) {
+    SX_CUDA(cudaEventRecord(ev1, ctx->stream));
+    SX_CUDA(cudaEventSynchronize(ev1));
+    float ms = 0.f;
+    SX_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
+    cudaEventDestroy(ev0);
+    cudaEventDestroy(ev1);
+    ctx->kb_ms_total += ms;
+    ctx->kb_launches += 1;
+    ctx->kb_updates_total += (double)plane * (b - a) * (double)(run.pl.ball_size.back() - 1);
+  }
+}
+
+// K3: strict maxima of the owned planes + sort + decode. Returns the count.
+long long maxima_and_sort(salvox_ctx* ctx, const ExhRun& run, int z0, int z1) {
+  const int nx = run.kp.nx, ny = run.kp.ny, nz = run.kp.nz, zc0 = run.kp.zc0;
+  const float* d_score = run.kp.score;
+  const float* d_best = run.kp.best;
   const size_t nown = (size_t)nx * ny * (z1 - z0);
   const size_t kcap = nown / 2 + 1;
   unsigned long long* d_keys = static_cast<unsigned long long*>(ctx->d_keys.ensure(kcap * 8));
@@ -1213,9 +1257,12 @@ long long run_exhaustive(salvox_ctx* ctx, const float* d_slab, int nx, int ny, i
                            ctx->stream>>>(d_keys2, cnt, d_best, nx, ny, zc0, d_max);
     SX_LAUNCH_CHECK(ctx);
   }
-  if (run_out) *run_out = run;
-  // remember for the debug entry point
-  ctx->exh.valid = true;
+  return cnt;
+}
+
+void remember_run(salvox_ctx* ctx, const ExhRun& run, int nx, int ny, int nz, int zs0, int zs1,
+                  int z0, int z1, int bins, const double* scales, int n_scales) {
+  ctx->exh.valid = true;  // for the debug entry point
   ctx->exh.nx = nx;
   ctx->exh.ny = ny;
   ctx->exh.nz = nz;
@@ -1226,7 +1273,118 @@ long long run_exhaustive(salvox_ctx* ctx, const float* d_slab, int nx, int ny, i
   ctx->exh.bins = bins;
   ctx->exh.radii = run.pl.radii;
   ctx->exh.scales.assign(scales, scales + n_scales);
+}
+
+// Core: d_slab holds planes [zs0, zs1) of the volume (device, f32). Scores planes
+// [zc0, zc1) = [z0-1, z1+1) clipped, finds maxima of [z0, z1), sorts them.
+// Leaves: ctx->d_score/d_best (planes zc0..zc1), sorted keys, count.
+long long run_exhaustive(salvox_ctx* ctx, const float* d_slab, int nx, int ny, int nz, int zs0,
+                         int zs1, int z0, int z1, double low, double high, int bins,
+                         const double* scales, int n_scales, ExhRun* run_out) {
+  ExhRun run = setup_exhaustive(ctx, nx, ny, nz, zs0, zs1, z0, z1, bins, scales, n_scales);
+  const int pitch = (nx + 15) / 16 * 16;
+  launch_bin_volume(ctx, d_slab, ctx->d_bins.as<uint8_t>(), nx, ny, zs1 - zs0, pitch, low, high,
+                    bins);
+  {
+    std::lock_guard<std::mutex> lk(g_const_mu);
+    upload_tables(ctx, run.pl);
+    launch_kb_chunk(ctx, run, run.kp.zc0, run.kp.zc1);
+    SX_CUDA(cudaEventRecord(g_const_done, ctx->stream));
+  }
+  const long long cnt = maxima_and_sort(ctx, run, z0, z1);
+  if (run_out) *run_out = run;
+  remember_run(ctx, run, nx, ny, nz, zs0, zs1, z0, z1, bins, scales, n_scales);
   return cnt;
+}
+
+cudaEvent_t ctx_event(salvox_ctx* ctx, size_t i) {
+  while (ctx->events.size() <= i) {
+    cudaEvent_t e;
+    SX_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ctx->events.push_back(e);
+  }
+  return ctx->events[i];
+}
+
+// Host-buffer form, pipelined: the slab goes up in pieces
+// on the copy stream; the compute stream bins each piece as it lands and runs
+// the KB kernel over K z-chunks of the scored planes; each chunk's owned
+// score/best planes stream back on the copy stream while the next chunk
+// computes. Same kernels and arithmetic as run_exhaustive.
+long long run_exhaustive_pipelined(salvox_ctx* ctx, const float* h_slab, int nx, int ny, int nz,
+                                   int zs0, int zs1, int z0, int z1, double low, double high,
+                                   int bins, const double* scales, int n_scales,
+                                   float* score_out, float* best_out, ExhRun* run_out) {
+  if (!ctx->copy_stream) SX_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+  cudaStream_t cs = ctx->stream, ps = ctx->copy_stream;
+  ExhRun run = setup_exhaustive(ctx, nx, ny, nz, zs0, zs1, z0, z1, bins, scales, n_scales);
+  const int R = run.pl.R, tz = run.tc.tz;
+  const int nzs = zs1 - zs0;
+  const size_t plane = (size_t)nx * ny;
+  const int pitch = (nx + 15) / 16 * 16;
+  float* d_vol = static_cast<float*>(ctx->d_vol.ensure(plane * nzs * 4));
+  uint8_t* d_bins = ctx->d_bins.as<uint8_t>();
+  // K output chunks of whole tiles; the input in pieces of the same planes
+  const int zc0 = run.kp.zc0, zc1 = run.kp.zc1;
+  const int ntiles = (zc1 - zc0 + tz - 1) / tz;
+  const int K = std::max(1, std::min(4, ntiles / 4));
+  std::vector<int> cut(K + 1);
+  for (int k = 0; k <= K; ++k) cut[k] = std::min(zc1, zc0 + tz * (int)((long long)ntiles * k / K));
+  cut[K] = zc1;
+  const int npieces = std::max(1, std::min(8, nzs / 8));
+  std::vector<int> pc(npieces + 1);
+  for (int i = 0; i <= npieces; ++i) pc[i] = (int)((long long)nzs * i / npieces);
+  SX_CUDA(cudaEventRecord(ctx_event(ctx, 0), cs));  // order after earlier work on cs
+  SX_CUDA(cudaStreamWaitEvent(ps, ctx_event(ctx, 0), 0));
+  for (int i = 0; i < npieces; ++i) {
+    const size_t o = (size_t)pc[i] * plane, n = (size_t)(pc[i + 1] - pc[i]) * plane;
+    SX_CUDA(cudaMemcpyAsync(d_vol + o, h_slab + o, n * 4, cudaMemcpyHostToDevice, ps));
+    SX_CUDA(cudaEventRecord(ctx_event(ctx, 1 + i), ps));
+  }
+  int binned = 0;  // pieces binned so far
+  {
+    std::lock_guard<std::mutex> lk(g_const_mu);
+    upload_tables(ctx, run.pl);
+    for (int k = 0; k < K; ++k) {
+      const int need = std::min(nzs, cut[k + 1] + R + 1 - zs0);  // local planes the chunk reads
+      while (binned < npieces && pc[binned] < need) {
+        SX_CUDA(cudaStreamWaitEvent(cs, ctx_event(ctx, 1 + binned), 0));
+        const int p0 = pc[binned], p1 = pc[binned + 1];
+        launch_bin_volume(ctx, d_vol + (size_t)p0 * plane, d_bins + (size_t)p0 * pitch * ny, nx, ny,
+                          p1 - p0, pitch, low, high, bins);
+        ++binned;
+      }
+      launch_kb_chunk(ctx, run, cut[k], cut[k + 1]);
+      SX_CUDA(cudaEventRecord(ctx_event(ctx, 1 + npieces + k), cs));
+    }
+    SX_CUDA(cudaEventRecord(g_const_done, cs));
+  }
+  // owned planes of each chunk back to the host while later chunks compute
+  for (int k = 0; k < K; ++k) {
+    const int a = std::max(cut[k], z0), b = std::min(cut[k + 1], z1);
+    if (a >= b) continue;
+    SX_CUDA(cudaStreamWaitEvent(ps, ctx_event(ctx, 1 + npieces + k), 0));
+    const size_t src = (size_t)(a - zc0) * plane, dst = (size_t)(a - z0) * plane;
+    const size_t n = (size_t)(b - a) * plane;
+    if (score_out)
+      SX_CUDA(cudaMemcpyAsync(score_out + dst, run.kp.score + src, n * 4, cudaMemcpyDeviceToHost, ps));
+    if (best_out)
+      SX_CUDA(cudaMemcpyAsync(best_out + dst, run.kp.best + src, n * 4, cudaMemcpyDeviceToHost, ps));
+  }
+  const long long cnt = maxima_and_sort(ctx, run, z0, z1);
+  SX_CUDA(cudaStreamSynchronize(ps));
+  if (run_out) *run_out = run;
+  remember_run(ctx, run, nx, ny, nz, zs0, zs1, z0, z1, bins, scales, n_scales);
+  return cnt;
+}
+
+// SALVOX_EXH_PIPELINE=0 turns the host-buffer pipeline off (A/B timing).
+bool pipeline_disabled() {
+  static const bool off = [] {
+    const char* e = std::getenv("SALVOX_EXH_PIPELINE");
+    return e && std::string(e) == "0";
+  }();
+  return off;
 }
 
 uint64_t closed_form_visits(const Plan& pl, uint64_t voxels) {
@@ -1236,14 +1394,16 @@ uint64_t closed_form_visits(const Plan& pl, uint64_t voxels) {
 }
 
 void fetch_maxima(salvox_ctx* ctx, long long cnt, salvox_maximum* out, int64_t cap) {
-  ctx->last_maxima.resize((size_t)cnt);
+  // through pinned staging: one fast DMA, then at most one host copy per reader
+  ctx->last_maxima_n = cnt;
+  salvox_maximum* stage = static_cast<salvox_maximum*>(
+      ctx->h_stage.ensure(std::max<size_t>((size_t)cnt, 1) * sizeof(salvox_maximum)));
   if (cnt > 0)
-    SX_CUDA(cudaMemcpyAsync(ctx->last_maxima.data(), ctx->d_maxima.p, cnt * sizeof(salvox_maximum),
+    SX_CUDA(cudaMemcpyAsync(stage, ctx->d_maxima.p, cnt * sizeof(salvox_maximum),
                             cudaMemcpyDeviceToHost, ctx->stream));
   SX_CUDA(cudaStreamSynchronize(ctx->stream));
   if (out && cap > 0)
-    std::memcpy(out, ctx->last_maxima.data(),
-                (size_t)std::min<long long>(cnt, cap) * sizeof(salvox_maximum));
+    std::memcpy(out, stage, (size_t)std::min<long long>(cnt, cap) * sizeof(salvox_maximum));
 }
 
 int exhaustive_host(salvox_ctx* ctx, const float* slab, int32_t nx, int32_t ny, int32_t nz,
@@ -1262,21 +1422,27 @@ int exhaustive_host(salvox_ctx* ctx, const float* slab, int32_t nx, int32_t ny, 
       fail(SALVOX_EINVAL, "exhaustive slab: pass an explicit (global) intensity window");
     SX_CUDA(cudaSetDevice(ctx->device));
     const size_t nslab = (size_t)nx * ny * (zs1 - zs0);
-    float* d_vol = static_cast<float*>(ctx->d_vol.ensure(nslab * 4));
-    SX_CUDA(cudaMemcpyAsync(d_vol, slab, nslab * 4, cudaMemcpyHostToDevice, ctx->stream));
-    double low = iw->low, high = iw->high;
-    if (iw->full_range) device_full_range(ctx, d_vol, nslab, &low, &high);
-    ExhRun run;
-    const long long cnt = run_exhaustive(ctx, d_vol, nx, ny, nz, zs0, zs1, z0, z1, low, high,
-                                         iw->bins, scales, n_scales, &run);
     const size_t nown = (size_t)nx * ny * (z1 - z0);
-    const size_t off = (size_t)nx * ny * (z0 - run.kp.zc0);
-    if (score_out)
-      SX_CUDA(cudaMemcpyAsync(score_out, ctx->d_score.as<float>() + off, nown * 4,
-                              cudaMemcpyDeviceToHost, ctx->stream));
-    if (best_scale_out)
-      SX_CUDA(cudaMemcpyAsync(best_scale_out, ctx->d_best.as<float>() + off, nown * 4,
-                              cudaMemcpyDeviceToHost, ctx->stream));
+    ExhRun run;
+    long long cnt;
+    if (!iw->full_range && !pipeline_disabled()) {
+      cnt = run_exhaustive_pipelined(ctx, slab, nx, ny, nz, zs0, zs1, z0, z1, iw->low, iw->high,
+                                     iw->bins, scales, n_scales, score_out, best_scale_out, &run);
+    } else {  // full_range needs the whole slab's min/max before any binning
+      float* d_vol = static_cast<float*>(ctx->d_vol.ensure(nslab * 4));
+      SX_CUDA(cudaMemcpyAsync(d_vol, slab, nslab * 4, cudaMemcpyHostToDevice, ctx->stream));
+      double low = iw->low, high = iw->high;
+      if (iw->full_range) device_full_range(ctx, d_vol, nslab, &low, &high);
+      cnt = run_exhaustive(ctx, d_vol, nx, ny, nz, zs0, zs1, z0, z1, low, high, iw->bins, scales,
+                           n_scales, &run);
+      const size_t off = (size_t)nx * ny * (z0 - run.kp.zc0);
+      if (score_out)
+        SX_CUDA(cudaMemcpyAsync(score_out, ctx->d_score.as<float>() + off, nown * 4,
+                                cudaMemcpyDeviceToHost, ctx->stream));
+      if (best_scale_out)
+        SX_CUDA(cudaMemcpyAsync(best_scale_out, ctx->d_best.as<float>() + off, nown * 4,
+                                cudaMemcpyDeviceToHost, ctx->stream));
+    }
     fetch_maxima(ctx, cnt, maxima, cap);
     if (n_maxima) *n_maxima = cnt;
     if (visits) *visits += closed_form_visits(run.pl, nown);
@@ -1365,9 +1531,9 @@ extern "C" int salvox_last_maxima(salvox_ctx* ctx, salvox_maximum* out, int64_t 
   return guarded([&] {
     if (!ctx) fail(SALVOX_EINVAL, "null context");
     std::lock_guard<std::mutex> lk(ctx->mu);
-    const int64_t n = (int64_t)ctx->last_maxima.size();
-    if (out && cap > 0)
-      std::memcpy(out, ctx->last_maxima.data(), (size_t)std::min(n, cap) * sizeof(salvox_maximum));
+    const int64_t n = ctx->last_maxima_n;
+    if (out && cap > 0 && n > 0)
+      std::memcpy(out, ctx->h_stage.p, (size_t)std::min(n, cap) * sizeof(salvox_maximum));
     if (n_out) *n_out = n;
   });
 }
