@@ -222,6 +222,11 @@ def main():
             ctx.handle, C.c_void_p(d_slab.data_ptr()), nx, ny, nz, zs0, zs1, z0, z1, C.byref(iw),
             sc.ctypes.data_as(C.c_void_p), len(sc), 0, budget, C.c_void_p(d_score.data_ptr()),
             C.c_void_p(d_best.data_ptr()), C.byref(nmax)))
+        if world > 1:  # the job's one collective: all-gather + merge of the slab maxima
+            local = np.empty(max(nmax.value, 1), sx.MAX_DTYPE)
+            _lib.check(_lib.load().salvox_last_maxima(ctx.handle, local.ctypes.data_as(C.c_void_p),
+                                                      nmax.value, C.byref(nmax)))
+            sharding.allgather_maxima(local[: nmax.value], device=dev)
 
     for _ in range(args.warmup):
         device_pass()
