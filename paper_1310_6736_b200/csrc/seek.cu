@@ -27,6 +27,9 @@
 #include "../../include/salvox/sx_log.h"
 #include "common.cuh"
 
+#ifndef ASCENT_G
+#define ASCENT_G 4
+#endif
 #ifndef CTA_PRODUCERS
 #define CTA_PRODUCERS 3
 #endif
@@ -1490,10 +1493,11 @@ __device__ void ascent_levels(const SeekParams& P, const uint8_t* vb, unsigned c
   if (any) {
     const int total = L[0] * L[1] * L[2];
     const float ix = 1.0f / (float)L[0], iy = 1.0f / (float)L[1];
-    for (int base = 0; base < total; base += kStep) {
-      int bin[kG], lvl[kG];
+    constexpr int G = ASCENT_G;  // voxels per lane per step: bin loads in flight
+    for (int base = 0; base < total; base += 32 * G) {
+      int bin[G], lvl[G];
 #pragma unroll
-      for (int j = 0; j < kG; ++j) {
+      for (int j = 0; j < G; ++j) {
         const int n = base + 32 * j + lane;
         const int nc = n < total ? n : 0;
         const int t = fdiv_small(nc, ix);
@@ -1504,7 +1508,7 @@ __device__ void ascent_levels(const SeekParams& P, const uint8_t* vb, unsigned c
         lvl[j] = max(max((int)lv[x], (int)lv[132 + y]), (int)lv[264 + zz]);
       }
 #pragma unroll
-      for (int j = 0; j < kG; ++j)
+      for (int j = 0; j < G; ++j)
         if (bin[j] >= 0) atomicAdd(&cnt[lvl[j] * M + bin[j]], 1u);
     }
   }
