@@ -43,6 +43,12 @@ extern "C" {
 #define SALVOX_KERNEL_EPANECHNIKOV 1
 #define SALVOX_KERNEL_GAUSSIAN 2
 
+/* MetaImage ElementType codes (meta_io.cpp:85-90) for the on-device widening */
+#define SALVOX_MET_UCHAR 0
+#define SALVOX_MET_SHORT 1
+#define SALVOX_MET_USHORT 2
+#define SALVOX_MET_FLOAT 3
+
 #define SALVOX_METHOD_QUADRANT 0 /* pipeline.hpp:19 Method */
 #define SALVOX_METHOD_SHIFT 1
 #define SALVOX_METHOD_ABMSOD 2 /* abmsod.cpp */
@@ -307,6 +313,15 @@ SALVOX_API int salvox_dedupe_top_k(salvox_ctx* ctx, const salvox_detection* dets
 SALVOX_API int salvox_plan_seeds(int32_t nx, int32_t ny, int32_t nz, int32_t mode, double spacing,
                       int32_t count, const double* scales, int32_t n_scales, uint64_t rng_seed,
                       double* positions, double* seed_scales, int64_t cap, int64_t* n_out);
+
+/* load_volume's payload widening (meta_io.cpp:30-33, :100-105) on the device
+ * (SURVEY 8(f) rank 2): salvox_upload_widen copies a host payload of n elements
+ * at its native width and widens it to f32 into d_out (device); the _device
+ * form widens a device payload. static_cast<float> of u8/i16/u16 is exact. */
+SALVOX_API int salvox_upload_widen(salvox_ctx* ctx, int32_t element_type, const void* raw,
+                                   int64_t n, float* d_out);
+SALVOX_API int salvox_widen_device(salvox_ctx* ctx, int32_t element_type, const void* d_raw,
+                                   int64_t n, float* d_out);
 
 /* make_phantom (phantom.hpp:125, src/phantom.cpp:364-421). shape 0 box, 1 ball,
  * 2 ellipsoid; fill_type 0 uniform(levels), 1 constant(value); bg_type 0
