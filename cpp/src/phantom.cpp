@@ -189,6 +189,32 @@ std::string GroundTruth::to_json_text() const {
   return json::dump(j);
 }
 
+GroundTruth GroundTruth::from_json_text(const std::string& text) {  // phantom.cpp:213-235
+  const Value j = json::parse(text);
+  GroundTruth gt;
+  const Value& dims = j.at("dims");
+  if (!dims.is_array() || dims.arr.size() < 3) throw std::invalid_argument("json: bad dims");
+  for (int i = 0; i < 3; ++i) gt.dims[i] = int(dims.arr[size_t(i)].as_number());
+  for (const Value& rj : j.at("regions").arr) {
+    GroundTruthRegion r;
+    const Value& c = rj.at("center");
+    for (int i = 0; i < 3; ++i) r.center[i] = c.arr.at(size_t(i)).as_number();
+    const Value& h = rj.at("H");
+    if (h.arr.size() != 9) throw std::runtime_error("ground truth H must have 9 entries");
+    for (int row = 0; row < 3; ++row)
+      for (int col = 0; col < 3; ++col) r.H(row, col) = h.arr[size_t(row * 3 + col)].as_number();
+    const Value& rle = rj.at("mask_rle");
+    if (rle.arr.size() % 2 != 0) throw std::runtime_error("mask_rle must have even length");
+    for (size_t i = 0; i < rle.arr.size(); i += 2) {
+      const uint64_t start = uint64_t(rle.arr[i].as_number());
+      const uint64_t len = uint64_t(rle.arr[i + 1].as_number());
+      for (uint64_t k = 0; k < len; ++k) r.mask.push_back(start + k);
+    }
+    gt.regions.push_back(std::move(r));
+  }
+  return gt;
+}
+
 std::pair<Volume, GroundTruth> make_phantom(const PhantomSpec& spec) {
   Volume v(spec.dims[0], spec.dims[1], spec.dims[2], spec.spacing);
   const size_t nr = spec.regions.size(), m = std::max<size_t>(nr, 1);

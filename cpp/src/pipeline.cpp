@@ -170,4 +170,37 @@ std::vector<Detection> detect(const Volume& v, const IntensityWindow& iw, Detect
   return dets;
 }
 
+std::vector<uint64_t> rasterize_window(const Volume& frame, const EllipsoidWindow& win) {
+  double c[3], h[9];
+  for (int i = 0; i < 3; ++i) c[i] = win.center[i];
+  for (int r = 0; r < 3; ++r)
+    for (int k = 0; k < 3; ++k) h[3 * r + k] = win.H(r, k);
+  int64_t n = 0;
+  check_status(salvox_rasterize_window(ctx(), frame.nx(), frame.ny(), frame.nz(), c, h, nullptr, 0, &n));
+  std::vector<uint64_t> out(static_cast<size_t>(n));
+  if (n > 0)
+    check_status(salvox_rasterize_window(ctx(), frame.nx(), frame.ny(), frame.nz(), c, h,
+                                         out.data(), n, &n));
+  return out;
+}
+
+double jaccard(const std::vector<uint64_t>& a, const std::vector<uint64_t>& b) {
+  if (a.empty() && b.empty()) throw std::invalid_argument("jaccard: both sets are empty");
+  size_t i = 0, j = 0, inter = 0;  // sorted-merge intersection
+  while (i < a.size() && j < b.size()) {
+    if (a[i] == b[j]) {
+      ++inter, ++i, ++j;
+    } else if (a[i] < b[j]) {
+      ++i;
+    } else {
+      ++j;
+    }
+  }
+  return double(inter) / double(a.size() + b.size() - inter);
+}
+
+double jaccard(const Volume& frame, const EllipsoidWindow& win, const std::vector<uint64_t>& mask) {
+  return jaccard(rasterize_window(frame, win), mask);
+}
+
 }  // namespace salvox

@@ -7,6 +7,7 @@
 //   salvox-b200 phantom SPEC.json OUT.mhd
 //   salvox-b200 exhaustive --volume V.mhd --scales a,b --out MAXIMA.json [--window L:H]
 //                          [--bins N] [--budget B]
+//   salvox-b200 eval DETS.json GT.json [--out METRICS.json]   (tools/main.cpp:161-229)
 // Exit codes: 0 success, 1 config/IO/device error, 2 detect found nothing.
 #include <chrono>
 #include <cstdio>
@@ -142,17 +143,93 @@ int cmd_phantom(const std::string& spec_path, const std::string& out_path) {
   return 0;
 }
 
+// eval (reference tools/main.cpp:161-229): Jaccard of each detection window
+// (rasterised on the device) against each ground-truth region mask.
+int cmd_eval(const std::string& dets_path, const std::string& gt_path, const std::string& out_path) {
+  const json::Value report = json::parse(read_file(dets_path));
+  const GroundTruth gt = GroundTruth::from_json_text(read_file(gt_path));
+  const json::Value& dims = report.at("header").at("volume_dims");
+  for (int i = 0; i < 3; ++i)
+    if (int(dims.arr.at(size_t(i)).as_number()) != gt.dims[i])
+      throw std::invalid_argument("eval: detection report and ground truth dims differ");
+  Volume frame(gt.dims[0], gt.dims[1], gt.dims[2]);
+  struct Row {
+    size_t det;
+    int region;
+    double jaccard;
+  };
+  std::vector<Row> rows;
+  std::vector<double> best(gt.regions.size(), 0.0);
+  const auto& dets = report.at("detections").arr;
+  for (size_t i = 0; i < dets.size(); ++i) {
+    EllipsoidWindow win;
+    const json::Value& c = dets[i].at("center");
+    win.center = Eigen::Vector3d(c.arr.at(0).as_number(), c.arr.at(1).as_number(), c.arr.at(2).as_number());
+    const json::Value& h = dets[i].at("H");
+    for (int r = 0; r < 3; ++r)
+      for (int k = 0; k < 3; ++k) win.H(r, k) = h.arr.at(size_t(r * 3 + k)).as_number();
+    const auto det_mask = rasterize_window(frame, win);
+    Row row{i, -1, 0.0};
+    for (size_t g = 0; g < gt.regions.size(); ++g) {
+      if (det_mask.empty() && gt.regions[g].mask.empty()) continue;
+      const double jac = jaccard(det_mask, gt.regions[g].mask);
+      if (jac > row.jaccard) {
+        row.jaccard = jac;
+        row.region = int(g);
+      }
+      best[g] = std::max(best[g], jac);
+    }
+    rows.push_back(row);
+  }
+  int matched = 0;
+  double sum = 0.0;
+  for (double j : best)
+    if (j > 0.0) ++matched, sum += j;
+  json::Value out = json::Value::object();
+  out.set("regions", json::Value::number(double(gt.regions.size())));
+  out.set("detections", json::Value::number(double(dets.size())));
+  out.set("recall", json::Value::number(gt.regions.empty() ? 0.0 : double(matched) / double(gt.regions.size())));
+  out.set("mean_jaccard_matched", json::Value::number(matched == 0 ? 0.0 : sum / matched));
+  json::Value pr = json::Value::array();
+  for (double j : best) pr.push(json::Value::number(j));
+  out.set("per_region_best_jaccard", pr);
+  json::Value table = json::Value::array();
+  for (const Row& r : rows) {
+    json::Value t = json::Value::object();
+    t.set("detection", json::Value::number(double(r.det)));
+    t.set("region", json::Value::number(r.region));
+    t.set("jaccard", json::Value::number(r.jaccard));
+    table.push(t);
+  }
+  out.set("per_detection", table);
+  const std::string text = json::dump(out, 2) + "\n";
+  if (out_path.empty())
+    std::cout << text;
+  else
+    write_file_atomic(out_path, text);
+  return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
   if (argc < 2) {
-    std::cerr << "usage: salvox-b200 {detect|exhaustive|phantom} ...\n";
+    std::cerr << "usage: salvox-b200 {detect|exhaustive|phantom|eval} ...\n";
     return 1;
   }
   const std::string cmd = argv[1];
   try {
     if (cmd == "detect") return cmd_detect(parse_flags(argc, argv, 2));
     if (cmd == "exhaustive") return cmd_exhaustive(parse_flags(argc, argv, 2));
+    if (cmd == "eval") {
+      if (argc != 4 && argc != 6) throw std::invalid_argument("usage: salvox-b200 eval DETS.json GT.json [--out M.json]");
+      std::string out;
+      if (argc == 6) {
+        if (std::string(argv[4]) != "--out") throw std::invalid_argument("eval: unexpected argument");
+        out = argv[5];
+      }
+      return cmd_eval(argv[2], argv[3], out);
+    }
     if (cmd == "phantom") {
       if (argc != 4) throw std::invalid_argument("usage: salvox-b200 phantom SPEC.json OUT.mhd");
       return cmd_phantom(argv[2], argv[3]);

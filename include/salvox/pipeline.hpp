@@ -67,4 +67,11 @@ struct DetectParams {
 std::vector<Detection> detect(const Volume& v, const IntensityWindow& iw, DetectParams params,
                               EvalCounter* counter = nullptr);
 
+/// Sorted linear indices of the window's in-bounds support voxels on `frame`'s
+/// grid (pipeline.cpp:185-192), rasterised on the device.
+std::vector<uint64_t> rasterize_window(const Volume& frame, const EllipsoidWindow& win);
+/// Jaccard index |A∩B| / |A∪B| over sorted voxel index sets (pipeline.cpp:194-211).
+double jaccard(const std::vector<uint64_t>& a, const std::vector<uint64_t>& b);
+double jaccard(const Volume& frame, const EllipsoidWindow& win, const std::vector<uint64_t>& mask);
+
 }  // namespace salvox

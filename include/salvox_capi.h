@@ -323,6 +323,14 @@ SALVOX_API int salvox_upload_widen(salvox_ctx* ctx, int32_t element_type, const 
 SALVOX_API int salvox_widen_device(salvox_ctx* ctx, int32_t element_type, const void* d_raw,
                                    int64_t n, float* d_out);
 
+/* rasterize_window (pipeline.hpp:61, src/pipeline.cpp:185-192): the linear
+ * indices (ascending) of the in-bounds voxels of the window (center, H
+ * row-major) on an nx*ny*nz frame; up to cap go to out, *n_out = count. The
+ * evaluation path of `salvox eval` (Jaccard vs ground-truth masks). */
+SALVOX_API int salvox_rasterize_window(salvox_ctx* ctx, int32_t nx, int32_t ny, int32_t nz,
+                                       const double* center, const double* H, uint64_t* out,
+                                       int64_t cap, int64_t* n_out);
+
 /* make_phantom (phantom.hpp:125, src/phantom.cpp:364-421). shape 0 box, 1 ball,
  * 2 ellipsoid; fill_type 0 uniform(levels), 1 constant(value); bg_type 0
  * constant, 1 gaussian. Writes the volume and 3 centroid doubles per region. */

@@ -197,6 +197,8 @@ def _declare(L):
     L.sxo_eigen_det3.argtypes = [_f64p]
     L.sxo_log_portable.restype = C.c_double
     L.sxo_log_portable.argtypes = [C.c_double]
+    L.sxo_rasterize_window.restype = C.c_int64
+    L.sxo_rasterize_window.argtypes = [C.c_int, C.c_int, C.c_int, _f64p, _f64p, _vp, C.c_int64]
     L.sxo_exp_portable.restype = C.c_double
     L.sxo_exp_portable.argtypes = [C.c_double]
     L.sxo_pow_portable.restype = C.c_double
@@ -542,6 +544,16 @@ def sym_eigen3(a):
     if lib().sxo_sym_eigen3(np.ascontiguousarray(a, np.float64).reshape(9), vals, vecs) != 0:
         raise OracleError("abmsod: eigen decomposition failed")
     return vals, vecs.reshape(3, 3)
+
+
+def rasterize_window(shape_zyx, center, H):
+    nz, ny, nx = shape_zyx
+    c = np.ascontiguousarray(center, np.float64)
+    h = np.ascontiguousarray(np.asarray(H, np.float64).reshape(9))
+    n = lib().sxo_rasterize_window(nx, ny, nz, c, h, None, 0)
+    out = np.zeros(max(n, 1), np.uint64)
+    lib().sxo_rasterize_window(nx, ny, nz, c, h, out.ctypes.data, n)
+    return out[:n]
 
 
 def exp_portable(x):

@@ -765,6 +765,29 @@ static double inbounds_support_fraction(const vview* v, const ewin* w) { /* wind
   return f < 1.0 ? f : 1.0;
 }
 
+typedef struct {
+  int nx, ny;
+  uint64_t* out;
+  int64_t cap, n;
+} raster_ctx;
+static void raster_fn(void* c, int x, int y, int z, double d) {
+  (void)d;
+  raster_ctx* r = (raster_ctx*)c;
+  if (r->n < r->cap) r->out[r->n] = (uint64_t)x + (uint64_t)r->nx * ((uint64_t)y + (uint64_t)r->ny * z);
+  r->n++;
+}
+/* rasterize_window (pipeline.cpp:185-192): support indices in z->y->x order */
+int64_t sxo_rasterize_window(int nx, int ny, int nz, const double center[3], const double H[9],
+                             uint64_t* out, int64_t cap) {
+  const vview v = {NULL, nx, ny, nz};
+  ewin w;
+  memcpy(w.center, center, sizeof w.center);
+  memcpy(w.H, H, sizeof w.H);
+  raster_ctx c = {nx, ny, out, cap, 0};
+  for_each_support_voxel(&v, &w, raster_fn, &c);
+  return c.n;
+}
+
 /* ------------------------------------------------------------ shift.cpp:7-107 */
 static ewin window_at(const double x[3], const double half_in[3], int two_d) { /* shift.cpp:7-11 */
   double half[3] = {half_in[0], half_in[1], two_d ? 1.0 : half_in[2]};

@@ -227,6 +227,10 @@ int sxo_sym_eigen3(const double a[9], double values[3], double vectors[9]);
 double sxo_exp_portable(double x);
 double sxo_pow_portable(double x, double y);
 
+/* pipeline.cpp:185-192 rasterize_window; returns the count (writes up to cap) */
+int64_t sxo_rasterize_window(int nx, int ny, int nz, const double center[3], const double H[9],
+                             uint64_t* out, int64_t cap);
+
 /* Eigen 3x3 inverse / determinant restatement (exported for tests). */
 void sxo_eigen_inverse3(const double m[9], double out[9]);
 double sxo_eigen_det3(const double m[9]);

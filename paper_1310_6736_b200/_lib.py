@@ -120,7 +120,7 @@ EXPORTS = [
     "salvox_detect_shard", "salvox_seek",
     "salvox_select", "salvox_dedupe_top_k", "salvox_plan_seeds", "salvox_make_phantom",
     "salvox_ascent_seek", "salvox_abmsod_run", "salvox_bandwidth_from_moment",
-    "salvox_upload_widen", "salvox_widen_device",
+    "salvox_upload_widen", "salvox_widen_device", "salvox_rasterize_window",
 ]
 # include/salvox_bench.h
 BENCH_EXPORTS = ["salvox_probe_smem_peak", "salvox_ctx_set_profiling", "salvox_ctx_kernel_time"]

@@ -433,6 +433,33 @@ def bandwidth_from_moment(outer, weight_sum, dim, lambda_min, lambda_max):
     return H.reshape(3, 3)
 
 
+def rasterize_window(shape_zyx, center, H, ctx=None):
+    """rasterize_window (pipeline.hpp:61): sorted linear indices of the window's
+    in-bounds support on a frame of the given shape, rasterised on the device."""
+    nz, ny, nx = shape_zyx if len(shape_zyx) == 3 else (1,) + tuple(shape_zyx)
+    c = np.ascontiguousarray(center, np.float64)
+    h = np.ascontiguousarray(np.asarray(H, np.float64).reshape(9))
+    n = C.c_int64(0)
+    cx = _ctx(ctx)
+    check(_lib.load().salvox_rasterize_window(cx.handle, nx, ny, nz, ptr(c), ptr(h), None,
+                                              C.c_int64(0), C.byref(n)))
+    out = np.zeros(max(n.value, 1), np.uint64)
+    if n.value:
+        check(_lib.load().salvox_rasterize_window(cx.handle, nx, ny, nz, ptr(c), ptr(h), ptr(out),
+                                                  C.c_int64(n.value), C.byref(n)))
+    return out[: n.value]
+
+
+def jaccard(a, b):
+    """jaccard (pipeline.hpp:63): |A n B| / |A u B| over sorted voxel index sets."""
+    a = np.asarray(a, np.uint64)
+    b = np.asarray(b, np.uint64)
+    if len(a) == 0 and len(b) == 0:
+        raise ValueError("jaccard: both sets are empty")
+    inter = len(np.intersect1d(a, b, assume_unique=True))
+    return inter / float(len(a) + len(b) - inter)
+
+
 def select(dets, entropy_quantile=0.9, pdf_quantile=0.0, k=20, dedupe_radius=5.0, ctx=None):
     """Alive filter + population-quantile thresholds + dedupe (pipeline.cpp:383-401)."""
     d = np.ascontiguousarray(dets, DET_DTYPE)

@@ -101,3 +101,53 @@ def test_cli_detect_and_exhaustive(cpp_build, tmp_path, oracle):
                         "--window", "0:64", "--seeds", "lattice:16", "--scales", "6"],
                        capture_output=True, text=True)
     assert r.returncode == 2, r.stderr
+
+
+@pytest.mark.gpu
+def test_cli_eval_jaccard(cpp_build, tmp_path):  # test_cli.cpp:169-192
+    cli = os.path.join(cpp_build, "salvox-b200")
+    ball = {"dims": [48, 48, 48],
+            "regions": [{"shape": "ball", "center": [24, 22, 25], "radius": 8,
+                         "fill": {"type": "uniform", "levels": 64}}], "rng_seed": 5}
+    (tmp_path / "spec.json").write_text(json.dumps(ball))
+    subprocess.run([cli, "phantom", str(tmp_path / "spec.json"), str(tmp_path / "ball.mhd")],
+                   check=True, capture_output=True)
+    r = subprocess.run([cli, "detect", "--method", "shift", "--volume", str(tmp_path / "ball.mhd"),
+                        "--window", "0:64", "--seeds", "lattice:12", "--scales", "6,8", "--k", "5",
+                        "--out", str(tmp_path / "dets.json")], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    r = subprocess.run([cli, "eval", str(tmp_path / "dets.json"), str(tmp_path / "ball.gt.json"),
+                        "--out", str(tmp_path / "metrics.json")], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    m = json.loads((tmp_path / "metrics.json").read_text())
+    assert m["recall"] == 1.0 and m["mean_jaccard_matched"] > 0.0
+    small = {"dims": [32, 32, 32], "regions": [{"shape": "ball", "center": [16, 16, 16],
+                                                "radius": 6, "fill": {"type": "uniform",
+                                                                      "levels": 64}}],
+             "rng_seed": 1}
+    (tmp_path / "spec2.json").write_text(json.dumps(small))
+    subprocess.run([cli, "phantom", str(tmp_path / "spec2.json"), str(tmp_path / "small.mhd")],
+                   check=True, capture_output=True)
+    r = subprocess.run([cli, "eval", str(tmp_path / "dets.json"), str(tmp_path / "small.gt.json")],
+                       capture_output=True, text=True)
+    assert r.returncode == 1  # dims mismatch (tools/main.cpp:166-169)
+
+
+@pytest.mark.gpu
+def test_rasterize_window_matches_oracle(sx, oracle):
+    rng = np.random.default_rng(9)
+    for _ in range(25):
+        shape = tuple(int(v) for v in rng.integers(1, 40, size=3))
+        center = rng.uniform(-5, 45, size=3)
+        A = rng.normal(size=(3, 3)) * rng.uniform(1, 6)
+        H = A @ A.T + np.eye(3)
+        got = sx.rasterize_window(shape, center, H)
+        ref = oracle.rasterize_window(shape, center, H)
+        assert np.array_equal(got, ref)
+    a = sx.rasterize_window((30, 30, 30), [15, 15, 15], np.diag([25.0] * 3))
+    b = sx.rasterize_window((30, 30, 30), [17, 15, 15], np.diag([25.0] * 3))
+    inter = len(np.intersect1d(a, b))
+    assert sx.jaccard(a, b) == inter / (len(a) + len(b) - inter)
+    assert sx.jaccard(a, a) == 1.0
+    with pytest.raises(ValueError):
+        sx.jaccard([], [])
