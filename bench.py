@@ -264,6 +264,9 @@ def main():
     out_pinned = (torch.empty((z1 - z0, ny, nx), dtype=torch.float32).pin_memory().numpy(),
                   torch.empty((z1 - z0, ny, nx), dtype=torch.float32).pin_memory().numpy())
     h2d = (zs1 - zs0) * ny * nx * 4
+    # pinned maxima buffer (a voxel is a strict maximum at most every other voxel)
+    max_pinned = torch.empty(((z1 - z0) * ny * nx // 8 + 4096) * sx.MAX_DTYPE.itemsize,
+                             dtype=torch.uint8).pin_memory().numpy().view(sx.MAX_DTYPE)
     e2e_times, d2h = [], 0
     for i in range(args.warmup + args.steps):
         torch.cuda.synchronize(dev)
@@ -272,7 +275,7 @@ def main():
         t0 = time.perf_counter()
         score, best, (oz0, oz1), merged, _ = sharding.exhaustive_sharded(
             vol_pinned, SCALES, LOW, HIGH, BINS, budget=budget, device=dev if world > 1 else None,
-            ctx=ctx, out=out_pinned)
+            ctx=ctx, out=out_pinned, maxima_out=max_pinned)
         t1 = time.perf_counter()
         if i >= args.warmup:
             e2e_times.append((t1 - t0) * 1e3)

@@ -113,7 +113,7 @@ _MAXIMA_HINT = {}  # context id -> maxima count of its last slab call (output si
 
 def kadir_brady_exhaustive_slab(slab, nz_total, zs0, z0, z1, scales, window_low, window_high,
                                 bins=64, kernel="identity", budget=DEFAULT_BUDGET, ctx=None,
-                                out=None):
+                                out=None, maxima_out=None):
     """z-slab form (salvox_exhaustive_slab): `slab` holds planes [zs0, zs0+len) of a volume
     with nz_total planes; returns owned-plane maps [z0, z1) and global maxima."""
     s = np.ascontiguousarray(slab, dtype=np.float32)
@@ -130,8 +130,13 @@ def kadir_brady_exhaustive_slab(slab, nz_total, zs0, z0, z1, scales, window_low,
     else:
         score = np.empty((z1 - z0, ny, nx), np.float32)
         best = np.empty((z1 - z0, ny, nx), np.float32)
-    cap = max(4096, int(_MAXIMA_HINT.get(id(c), 0) * 1.1))  # size from the last call
-    maxima = np.empty(cap, MAX_DTYPE)
+    if maxima_out is not None:  # caller-provided (e.g. pinned) maxima buffer
+        maxima = maxima_out
+        assert maxima.dtype == MAX_DTYPE and maxima.flags.c_contiguous
+        cap = len(maxima)
+    else:
+        cap = max(4096, int(_MAXIMA_HINT.get(id(c), 0) * 1.1))  # size from the last call
+        maxima = np.empty(cap, MAX_DTYPE)
     n = C.c_int64(0)
     visits = C.c_uint64(0)
     check(_lib.load().salvox_exhaustive_slab(

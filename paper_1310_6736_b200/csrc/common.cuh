@@ -125,6 +125,7 @@ struct salvox_ctx {
       d_minmax, d_dbg;
   sx::HostBuf h_stage;       // pinned: the last call's maxima (salvox_last_maxima)
   int64_t last_maxima_n = 0;
+  bool stage_valid = false;  // h_stage holds them (else read d_maxima again)
   sx::ExhState exh;
   // seek path
   sx::DevBuf d_seeds, d_dets, d_geom, d_sel_a, d_sel_b, d_sel_c, d_sel_d, d_visits, d_target,

@@ -1394,14 +1394,23 @@ uint64_t closed_form_visits(const Plan& pl, uint64_t voxels) {
 }
 
 void fetch_maxima(salvox_ctx* ctx, long long cnt, salvox_maximum* out, int64_t cap) {
-  // through pinned staging: one fast DMA, then at most one host copy per reader
   ctx->last_maxima_n = cnt;
+  ctx->stage_valid = false;
+  if (out && cap >= cnt) {  // straight into the caller's buffer (fast when it is pinned)
+    if (cnt > 0)
+      SX_CUDA(cudaMemcpyAsync(out, ctx->d_maxima.p, cnt * sizeof(salvox_maximum),
+                              cudaMemcpyDeviceToHost, ctx->stream));
+    SX_CUDA(cudaStreamSynchronize(ctx->stream));
+    return;
+  }
+  // through pinned staging: one DMA, then the caller's share
   salvox_maximum* stage = static_cast<salvox_maximum*>(
       ctx->h_stage.ensure(std::max<size_t>((size_t)cnt, 1) * sizeof(salvox_maximum)));
   if (cnt > 0)
     SX_CUDA(cudaMemcpyAsync(stage, ctx->d_maxima.p, cnt * sizeof(salvox_maximum),
                             cudaMemcpyDeviceToHost, ctx->stream));
   SX_CUDA(cudaStreamSynchronize(ctx->stream));
+  ctx->stage_valid = true;
   if (out && cap > 0)
     std::memcpy(out, stage, (size_t)std::min<long long>(cnt, cap) * sizeof(salvox_maximum));
 }
@@ -1532,8 +1541,16 @@ extern "C" int salvox_last_maxima(salvox_ctx* ctx, salvox_maximum* out, int64_t 
     if (!ctx) fail(SALVOX_EINVAL, "null context");
     std::lock_guard<std::mutex> lk(ctx->mu);
     const int64_t n = ctx->last_maxima_n;
-    if (out && cap > 0 && n > 0)
-      std::memcpy(out, ctx->h_stage.p, (size_t)std::min(n, cap) * sizeof(salvox_maximum));
+    if (out && cap > 0 && n > 0) {
+      const size_t bytes = (size_t)std::min(n, cap) * sizeof(salvox_maximum);
+      if (ctx->stage_valid) {
+        std::memcpy(out, ctx->h_stage.p, bytes);
+      } else {  // the device copy of the last call's maxima is still resident
+        SX_CUDA(cudaSetDevice(ctx->device));
+        SX_CUDA(cudaMemcpyAsync(out, ctx->d_maxima.p, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+        SX_CUDA(cudaStreamSynchronize(ctx->stream));
+      }
+    }
     if (n_out) *n_out = n;
   });
 }

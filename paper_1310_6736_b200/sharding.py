@@ -92,7 +92,8 @@ def allgather_maxima(local: np.ndarray, group=None, device=None) -> np.ndarray:
 
 
 def exhaustive_sharded(volume: np.ndarray, scales, window_low, window_high, bins=64,
-                       budget=None, group=None, device=None, compute=None, ctx=None, out=None):
+                       budget=None, group=None, device=None, compute=None, ctx=None, out=None,
+                       maxima_out=None):
     """kadir_brady_exhaustive over z-slabs, one per rank.
 
     Returns (owned score planes, owned best_scale planes, (z0, z1), merged maxima,
@@ -120,7 +121,8 @@ def exhaustive_sharded(volume: np.ndarray, scales, window_low, window_high, bins
     else:
         score, best, local, visits = api.kadir_brady_exhaustive_slab(
             vol[zs0:zs1], nz, zs0, z0, z1, scales, window_low, window_high, bins,
-            budget=budget if budget is not None else api.DEFAULT_BUDGET, ctx=ctx, out=out)
+            budget=budget if budget is not None else api.DEFAULT_BUDGET, ctx=ctx, out=out,
+            maxima_out=maxima_out)
     # one rank: the slab call already returns the reference's stable order
     merged = allgather_maxima(local, group, device) if world > 1 else local
     return score, best, (z0, z1), merged, visits
