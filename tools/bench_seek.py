@@ -129,10 +129,11 @@ def main():
     if args.c5 > 0 and want("C5"):
         vols = np.stack([api.make_phantom(s)[0] for s in c5_specs(args.c5)])
         dv = torch.from_numpy(vols).to(dev)
-        ms, sel = time_batch(ctx, st, dv, args.c5, vols.shape[1:], (0.0, 16.0, 16), "octant",
-                             C1_SCALES, 8.0, steps=1)
-        res.append({"config": f"C5 octant batch x{args.c5}", "ms_per_batch": ms,
-                    "volumes_per_s": args.c5 * 1e3 / ms, "selected": sel})
+        for method in ("octant", "shift"):
+            ms, sel = time_batch(ctx, st, dv, args.c5, vols.shape[1:], (0.0, 16.0, 16), method,
+                                 C1_SCALES, 8.0, steps=1)
+            res.append({"config": f"C5 {method} batch x{args.c5}", "ms_per_batch": ms,
+                        "volumes_per_s": args.c5 * 1e3 / ms, "selected": sel})
     for r in res:
         print(json.dumps(r))
 
