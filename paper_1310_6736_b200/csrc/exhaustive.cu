@@ -708,6 +708,7 @@ __global__ void __launch_bounds__(1024, 1)
     const bool doE = (bd.flags & 2) && T > 0u && TA > 0u && TB > 0u;
     const float invT = doH ? 1.0f / (float)T : 0.f;
     float hacc = 0.f;
+    uint32_t dom = 0u;  // the bin holding more than half the mass (at most one)
     unsigned long long num = 0ull;
 #pragma unroll
     for (int c = 0; c < NS; c += 8) {
@@ -719,12 +720,16 @@ __global__ void __launch_bounds__(1024, 1)
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const uint32_t cv = cur[j];
-        if (doH && cv) {
+#ifndef KB_SKIP_MATH
+        // -p log2 p with MUFU log2; a dominant bin (p > 1/2) is deferred to one
+        // log1pf after the loop, so the slow path never diverges across bins
+        if (2u * cv > T) {
+          dom = cv;
+        } else if (doH && cv) {
           const float pb = (float)cv * invT;
-          const float lg = (2u * cv > T) ? log1pf(-(float)(T - cv) * invT) * 1.4426950408889634f
-                                         : __log2f(pb);
-          hacc -= pb * lg;
+          hacc -= pb * __log2f(pb);
         }
+#endif
         if (doE) {
           const unsigned long long x = (unsigned long long)cv * TA, y = (unsigned long long)a[j] * T;
           num += x > y ? x - y : y - x;
@@ -734,6 +739,10 @@ __global__ void __launch_bounds__(1024, 1)
       tm_st8(slotA + c, cur);  // the older slot becomes the newest snapshot
     }
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    if (doH && dom) {
+      const float pb = (float)dom * invT;
+      hacc -= pb * (log1pf(-(float)(T - dom) * invT) * 1.4426950408889634f);
+    }
     if (DBG && dbg_me) p.dbg_out[(size_t)i * (p.bins + 1) + p.bins] = T;
     if (doE) {
       const double y = ((double)Hb * bd.fac) * ((double)num / ((double)T * (double)TA));
