@@ -156,3 +156,21 @@ def paper_mr():
     spec["dims"] = [256, 256, 176]
     spec["rng_seed"] = 290
     return spec
+
+
+def config_c4():
+    """C4: 512^3, the C2 generator with centres x2 plus four more regions,
+    rng_seed 512."""
+    u = {"type": "uniform", "levels": 32}
+    regs = [{"shape": r["shape"], "center": [2.0 * c for c in r["center"]], "fill": u,
+             **({"radius": 2.0 * r["radius"]} if "radius" in r else
+                {"half_extents": [2.0 * h for h in r["half_extents"]]})}
+            for r in config_c2()["regions"]]
+    regs += [{"shape": "ball", "center": [100.0, 400.0, 300.0], "radius": 14.0, "fill": u},
+             {"shape": "ball", "center": [420.0, 120.0, 420.0], "radius": 10.0, "fill": u},
+             {"shape": "box", "center": [300.0, 300.0, 100.0], "half_extents": [12.0, 8.0, 10.0],
+              "fill": u},
+             {"shape": "ball", "center": [60.0, 60.0, 460.0], "radius": 15.0, "fill": u}]
+    return {"dims": [512, 512, 512],
+            "background": {"type": "gaussian", "mean": 8.0, "sigma": 2.0},
+            "regions": regs, "rng_seed": 512}
