@@ -239,7 +239,11 @@ __global__ void __launch_bounds__(TX* TY* TZ, 1)
   // (+o and -o): per update one address add, one LDS.U8, one IMAD, one ATOMS.
   const int4* offs4 = c_offs;
   int lvl = 0;
-  for (int i = 0; i < p.n_radii; ++i) {
+  // A warp with no valid voxel (z-planes past zc1 in a slab's last tile layer,
+  // x/y past the edge) skips the walk: its TMEM slice and histogram columns are
+  // private, so the other warps run alone and finish sooner.
+  const int n_radii = __any_sync(0xffffffffu, valid) ? p.n_radii : 0;
+  for (int i = 0; i < n_radii; ++i) {
     const KbBound bd = c_bounds[i];
     for (; lvl < bd.lend; ++lvl) {
       const KbLevel L = c_levels[lvl];
@@ -671,7 +675,11 @@ __global__ void __launch_bounds__(1024, 1)
 
   const int4* offs4 = c_offs;
   int lvl = 0;
-  for (int i = 0; i < p.n_radii; ++i) {
+  // A warp with no valid voxel (z-planes past zc1 in a slab's last tile layer,
+  // x/y past the edge) skips the walk: its TMEM slice and histogram columns are
+  // private, so the other warps run alone and finish sooner.
+  const int n_radii = __any_sync(0xffffffffu, valid) ? p.n_radii : 0;
+  for (int i = 0; i < n_radii; ++i) {
     const KbBound bd = c_bounds[i];
     for (; lvl < bd.lend; ++lvl) {
       const KbLevel L = c_levels[lvl];
