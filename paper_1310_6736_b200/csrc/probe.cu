@@ -19,6 +19,7 @@ __constant__ int4 c_probe[kProbeTable / 4];
 // (bins from a register hash: the one-atomic-per-update floor of any design).
 template <int NT, int NB, int MODE>
 __global__ void __launch_bounds__(NT, 1) smem_probe_kernel(int iters, uint32_t* out) {
+  static_assert(NT == 512 || NT == 1024, "probe thread mapping");
   extern __shared__ __align__(1024) uint8_t smem[];
   uint32_t* hist = reinterpret_cast<uint32_t*>(smem);
   uint8_t* tile = smem + NB * NT * 4;
@@ -31,7 +32,10 @@ __global__ void __launch_bounds__(NT, 1) smem_probe_kernel(int iters, uint32_t* 
   }
   for (int i = tid; i < NB * NT; i += NT) hist[i] = 0;
   __syncthreads();
-  const int lx = tid & 7, ly = (tid >> 3) & 7, lz = tid >> 6;
+  // 512 threads: 8x8x8 voxels; 1024 threads: 16x8x8 (kb_tmem_kernel's tile)
+  const int lx = NT == 1024 ? (tid & 15) : (tid & 7);
+  const int ly = NT == 1024 ? ((tid >> 4) & 7) : ((tid >> 3) & 7);
+  const int lz = NT == 1024 ? (tid >> 7) : (tid >> 6);
   const uint8_t* tb = tile + (lz + 16) * 1920 + (ly + 16) * 48 + (lx + 16);
   uint32_t* hc = hist + tid;
   uint32_t acc = 0;
@@ -98,10 +102,12 @@ extern "C" int salvox_probe_smem_peak(salvox_ctx* ctx, int iters, double* atoms_
     }
     SX_CUDA(cudaMemcpyToSymbolAsync(c_probe, tab.data(), tab.size() * 4, 0, cudaMemcpyHostToDevice,
                                     ctx->stream));
-    constexpr int NT = 512, NB = 33;
-    const size_t smem = (size_t)NB * NT * 4 + 76800;
-    uint32_t* d_out = static_cast<uint32_t*>(ctx->d_dbg.ensure((size_t)ctx->sm_count * 2 * NT * 4));
-    auto run = [&](auto kern, double* rate, double per_iter) {
+    // both thread counts the kernels use (512: kb_kernel, 1024: kb_tmem_kernel);
+    // each rate is the best of the two (the peak an SM sustains)
+    constexpr int NB = 33;
+    uint32_t* d_out = static_cast<uint32_t*>(ctx->d_dbg.ensure((size_t)ctx->sm_count * 2 * 1024 * 4));
+    auto run = [&](auto kern, int NT, double* rate, double per_iter) {
+      const size_t smem = (size_t)NB * NT * 4 + 76800;
       SX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       const int grid = ctx->sm_count * 2;
       kern<<<grid, NT, smem, ctx->stream>>>(1, d_out);  // warm-up
@@ -118,11 +124,17 @@ extern "C" int salvox_probe_smem_peak(salvox_ctx* ctx, int iters, double* atoms_
       SX_CUDA(cudaEventElapsedTime(&ms, a, b));
       cudaEventDestroy(a);
       cudaEventDestroy(b);
-      if (rate) *rate = (double)grid * NT * iters * per_iter / (ms * 1e-3);
+      const double r = (double)grid * NT * iters * per_iter / (ms * 1e-3);
+      if (rate && r > *rate) *rate = r;
     };
-    run(smem_probe_kernel<NT, NB, 0>, atoms_updates_per_s, 2.0 * kProbeTable);
-    run(smem_probe_kernel<NT, NB, 1>, lds_fetches_per_s, 2.0 * kProbeTable);
-    run(smem_probe_kernel<NT, NB, 2>, atoms_only_per_s, 2.0 * kProbeTable);
+    for (double* r : {atoms_updates_per_s, lds_fetches_per_s, atoms_only_per_s})
+      if (r) *r = 0.0;
+    run(smem_probe_kernel<512, NB, 0>, 512, atoms_updates_per_s, 2.0 * kProbeTable);
+    run(smem_probe_kernel<512, NB, 1>, 512, lds_fetches_per_s, 2.0 * kProbeTable);
+    run(smem_probe_kernel<512, NB, 2>, 512, atoms_only_per_s, 2.0 * kProbeTable);
+    run(smem_probe_kernel<1024, NB, 0>, 1024, atoms_updates_per_s, 2.0 * kProbeTable);
+    run(smem_probe_kernel<1024, NB, 1>, 1024, lds_fetches_per_s, 2.0 * kProbeTable);
+    run(smem_probe_kernel<1024, NB, 2>, 1024, atoms_only_per_s, 2.0 * kProbeTable);
   });
 }
 
