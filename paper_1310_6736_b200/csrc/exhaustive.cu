@@ -780,6 +780,245 @@ __global__ void __launch_bounds__(1024, 1)
   }
 }
 
+// K2-quad (3D, NB <= 33, the default): 256 threads, FOUR x-adjacent voxels per
+// thread. The tile row pitch and the box start are multiples of 16 and each
+// thread's first voxel sits on a 4-byte boundary, so the 4 bins a thread needs
+// at offset o are one aligned 32-bit word when dx = 0 (mod 4), else two words
+// joined by a funnel shift -- warp-uniform, from the offset itself. That cuts
+// the bin fetches from one LDS per update to ~0.44 (tools/quad_probe.cu: 4.95e12
+// vs 4.33e12 updates/s for the one-voxel mix), and 8 warps with 32 independent
+// atomics each keep the atomic pipe fed. Histogram column (v, tid) of bin b is
+// word (4 b + v) * 256 + tid (bank = tid: conflict-free); its byte address is
+// base + v*1024 + (b << 12), built with a shift, a mask and one add per update.
+// Snapshots: 4 voxels x 2 slots x 32 bins = all 256 TMEM columns of the
+// thread's lane (warp w: lanes 32*(w%4), columns 256*(w/4)).
+__device__ __forceinline__ uint32_t fetch4(const uint8_t* tb, int off) {
+  // tb is 4-aligned, so (tb + off) & 3 = off & 3 = dx mod 4 (warp-uniform):
+  // two aligned words and one funnel shift by 8 * (off & 3) (SHF uses the low
+  // 5 bits of off << 3); when off = 0 (mod 4) the second word is simply unused
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(tb + (off & ~3));
+  return __funnelshift_r(w[0], w[1], (uint32_t)off << 3);
+}
+__device__ __forceinline__ void red4(uint32_t hb, uint32_t w, uint32_t n) {
+  // byte v of w is the bin of voxel v: address hb + v*1024 + (bin << 12)
+  // (PRMT extracts the byte, LEA shifts-and-adds)
+#pragma unroll
+  for (int v = 0; v < 4; ++v) {
+    const uint32_t bin = __byte_perm(w, 0u, 0x4440u | (uint32_t)v);
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(hb + 1024u * v + (bin << 12)), "r"(n));
+  }
+}
+
+template <int NB, bool DBG>
+__global__ void __launch_bounds__(256, 1)
+    kb_quad_kernel(const __grid_constant__ CUtensorMap tmap, const KbParams p) {
+  constexpr int TX = 16, TY = 8, TZ = 8, NT = 256, NV = 1024;
+  constexpr int NS = NB - 1;  // snapshot bins (1..NB-1)
+  static_assert(NS % 8 == 0 && 2 * NS <= 64, "TMEM: 64 columns per voxel");
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint32_t* hist = reinterpret_cast<uint32_t*>(smem);  // [NB][4][NT]
+  uint8_t* tile = smem + NB * NV * 4;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(tile + ((p.tile_bytes + 15u) & ~15u));
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 1);
+  const int tid = threadIdx.x, warp = tid >> 5;
+
+  int tx0, ty0, tz0;
+  long long dbg_lin = -1;
+  if (DBG) {
+    dbg_lin = p.dbg_vox[blockIdx.x];
+    const int vx = (int)(dbg_lin % p.nx);
+    const int vy = (int)((dbg_lin / p.nx) % p.ny);
+    const int vz = (int)(dbg_lin / ((long long)p.nx * p.ny));
+    tx0 = vx / TX * TX;
+    ty0 = vy / TY * TY;
+    tz0 = p.zc0 + (vz - p.zc0) / TZ * TZ;
+  } else {
+    tx0 = blockIdx.x * TX;
+    ty0 = blockIdx.y * TY;
+    tz0 = p.zc0 + blockIdx.z * TZ;
+  }
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {  // all 512 TMEM columns: one CTA per SM (shared memory bound)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     smem_u32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tbase = *tmem_slot;
+  const int xs = tx0 - p.R;
+  const int xa = xs - (((xs % 16) + 16) % 16);
+  const int delta = xs - xa;
+  if (tid == 0) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(p.tile_bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(tile)),
+        "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(xa), "r"(ty0 - p.R),
+        "r"(tz0 - p.Rz - p.zs0), "r"(smem_u32(bar))
+        : "memory");
+  }
+  {
+    uint4* h4 = reinterpret_cast<uint4*>(hist);
+    for (int i = tid; i < NB * NV / 4; i += NT) h4[i] = make_uint4(0u, 0u, 0u, 0u);
+  }
+  {
+    uint32_t done = 0;
+    while (!done) {
+      asm volatile(
+          "{ .reg .pred q; mbarrier.try_wait.parity.shared::cta.b64 q, [%1], 0; selp.u32 %0, 1, 0, q; }"
+          : "=r"(done)
+          : "r"(smem_u32(bar))
+          : "memory");
+    }
+  }
+  __syncthreads();
+  // thread -> 4 x-adjacent voxels; a warp covers 4 (x-quads) x 8 (y) of one z plane
+  const int lx = 4 * (tid & 3), ly = (tid >> 2) & 7, lz = tid >> 5;
+  const int gx = tx0 + lx, gy = ty0 + ly, gz = tz0 + lz;
+  const bool rowv = gy < p.ny && gz < p.zc1;
+  int dbg_v = -1;
+  if (DBG && rowv)
+    for (int v = 0; v < 4; ++v)
+      if (gx + v < p.nx &&
+          ((long long)(gx + v) + (long long)p.nx * ((long long)gy + (long long)p.ny * gz)) == dbg_lin)
+        dbg_v = v;
+  // (lx + R + delta) is a multiple of 4: R + delta = tx0 - xa = 0 (mod 16)
+  const uint8_t* tb = tile + (lz + p.Rz) * p.SZ + (ly + p.R) * p.SY + (lx + p.R + delta);
+  const uint32_t hb = smem_u32(hist) + 4u * (uint32_t)tid;
+  const uint32_t lane_base = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(256 * (warp >> 2));
+  {  // zero all snapshot slots ("radius 0")
+    uint32_t z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+    for (int c = 0; c < 256; c += 8) tm_st8(lane_base + c, z);
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  uint32_t TA[4] = {0u, 0u, 0u, 0u}, TB[4] = {0u, 0u, 0u, 0u};
+  float Hb[4] = {0.f, 0.f, 0.f, 0.f};
+  double best[4] = {0.0, 0.0, 0.0, 0.0};
+  float best_s[4] = {0.f, 0.f, 0.f, 0.f};
+  int best_rank[4] = {INT_MAX, INT_MAX, INT_MAX, INT_MAX};
+  int older = 0;  // which of the two slots (0/1) holds the older snapshot
+
+  const int4* offs4 = c_offs;
+  int lvl = 0;
+  const bool warp_live = __any_sync(0xffffffffu, rowv && gx < p.nx);
+  const int n_radii = warp_live ? p.n_radii : 0;
+  for (int i = 0; i < n_radii; ++i) {
+    const KbBound bd = c_bounds[i];
+    for (; lvl < bd.lend; ++lvl) {
+      const KbLevel L = c_levels[lvl];
+      const uint32_t n = (uint32_t)L.n;
+      const int g0 = L.start0 >> 2, g1 = (L.start0 + L.count0) >> 2;
+      int4 wn = offs4[g0];  // software-pipelined table reads (8 warps: LDC latency shows)
+      for (int g = g0; g < g1; ++g) {
+        const int4 w = wn;
+        wn = offs4[min(g + 1, kMaxOffs / 4 - 1)];
+        const uint32_t p0 = fetch4(tb, w.x), m0 = fetch4(tb, -w.x);
+        const uint32_t p1 = fetch4(tb, w.y), m1 = fetch4(tb, -w.y);
+        const uint32_t p2 = fetch4(tb, w.z), m2 = fetch4(tb, -w.z);
+        const uint32_t p3 = fetch4(tb, w.w), m3 = fetch4(tb, -w.w);
+        red4(hb, p0, n);
+        red4(hb, m0, n);
+        red4(hb, p1, n);
+        red4(hb, m1, n);
+        red4(hb, p2, n);
+        red4(hb, m2, n);
+        red4(hb, p3, n);
+        red4(hb, m3, n);
+      }
+      const int rem = (L.count0 & 3);
+      if (rem) {
+        const int4 w = offs4[g1];
+        const int o[3] = {w.x, w.y, w.z};
+        for (int j = 0; j < rem; ++j) {
+          const uint32_t pp = fetch4(tb, o[j]), mm = fetch4(tb, -o[j]);
+          red4(hb, pp, n);
+          red4(hb, mm, n);
+        }
+      }
+    }
+    // ---- boundary: per voxel v, the same arithmetic as kb_tmem_kernel
+    __syncwarp();
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const uint32_t* hc = hist + v * NT + tid;  // bin b at hc[b * 4 * NT]
+      const uint32_t T = bd.W - hc[0];
+      const bool doH = (bd.flags & 1) && T > 0u;
+      const bool doE = (bd.flags & 2) && T > 0u && TA[v] > 0u && TB[v] > 0u;
+      const float invT = doH ? 1.0f / (float)T : 0.f;
+      float hacc = 0.f;
+      uint32_t dom = 0u;
+      unsigned long long num = 0ull;
+      const uint32_t slot = lane_base + 64u * v + (uint32_t)(32 * older);
+#pragma unroll
+      for (int c = 0; c < NS; c += 8) {
+        uint32_t a[8], cur[8];
+        tm_ld8(slot + c, a);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) cur[j] = hc[(1 + c + j) * 4 * NT];
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint32_t cv = cur[j];
+          if (2u * cv > T) {
+            dom = cv;
+          } else if (doH && cv) {
+            const float pb = (float)cv * invT;
+            hacc -= pb * __log2f(pb);
+          }
+          if (doE) {
+            const unsigned long long x = (unsigned long long)cv * TA[v], y = (unsigned long long)a[j] * T;
+            num += x > y ? x - y : y - x;
+          }
+          if (DBG && v == dbg_v && c + j < p.bins) p.dbg_out[(size_t)i * (p.bins + 1) + c + j] = cv;
+        }
+        tm_st8(slot + c, cur);  // the older slot becomes the newest snapshot
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      if (doH && dom) {
+        const float pb = (float)dom * invT;
+        hacc -= pb * (log1pf(-(float)(T - dom) * invT) * 1.4426950408889634f);
+      }
+      if (DBG && v == dbg_v) p.dbg_out[(size_t)i * (p.bins + 1) + p.bins] = T;
+      if (doE) {
+        const double y = ((double)Hb[v] * bd.fac) * ((double)num / ((double)T * (double)TA[v]));
+        if (y > best[v] || (y == best[v] && y > 0.0 && bd.rank < best_rank[v])) {
+          best[v] = y;
+          best_s[v] = bd.scale;
+          best_rank[v] = bd.rank;
+        }
+      }
+      TA[v] = TB[v];
+      TB[v] = T;
+      Hb[v] = doH ? fmaxf(hacc, 0.f) : 0.f;
+    }
+    older ^= 1;
+  }
+  if (!DBG && rowv) {
+#pragma unroll
+    for (int v = 0; v < 4; ++v)
+      if (gx + v < p.nx) {
+        const size_t o = ((size_t)(gz - p.zc0) * p.ny + gy) * p.nx + gx + v;
+        p.score[o] = (float)best[v];
+        p.best[o] = best_s[v];
+      }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tbase) : "memory");
+  }
+}
+
 // ----------------------------------------------------------------------------- K3
 __global__ void maxima_kernel(const float* __restrict__ score, int nx, int ny, int nz, int zc0,
                               int z0, int z1, unsigned long long* keys, unsigned int* counter) {
@@ -862,6 +1101,7 @@ struct TileCfg {
   int nb, tx, ty, tz;
   bool pair;          // kb_pair_kernel (two voxels per thread, tx = 8)
   bool tmem = false;  // kb_tmem_kernel (1024 threads, snapshots in TMEM)
+  bool quad = false;  // kb_quad_kernel (256 threads x 4 voxels, snapshots in TMEM)
 };
 
 TileCfg pick_tile(int bins, bool two_d) {
@@ -872,12 +1112,17 @@ TileCfg pick_tile(int bins, bool two_d) {
   //   0: kb_kernel -- 512 threads, snapshots in registers, 80.2 ms (2D default)
   //   1: kb_pair_kernel -- 2 voxels/thread, 25% fewer smem wavefronts but 247
   //      registers -> 8 warps/SM, latency-bound, 85.9 ms
+  //   3: kb_quad_kernel -- 256 threads x 4 voxels, one 32-bit word of 4 bins
+  //      per offset (0.5 LDS wavefronts per update instead of 1), snapshots in
+  //      TMEM: 78.2 ms -- issue-bound (5.8 instructions per update: byte
+  //      extract + address per atomic, funnel-shifted fetches) on 8 warps/SM
   static const int mode = [] {
     const char* e = std::getenv("SALVOX_KB_VARIANT");
     return e ? std::atoi(e) : 2;
   }();
   if (mode == 1) return two_d ? TileCfg{nb, 8, 64, 1, true} : TileCfg{nb, 8, 8, 8, true};
   if (mode == 2 && !two_d) return TileCfg{nb, 16, 8, 8, false, true};
+  if (mode == 3 && !two_d) return TileCfg{nb, 16, 8, 8, false, false, true};
   return two_d ? TileCfg{nb, 32, 16, 1, false} : TileCfg{nb, 8, 8, 8, false};
 }
 
@@ -886,7 +1131,8 @@ size_t kb_smem(const TileCfg& tc, uint32_t tile_bytes) {
   const size_t voxels = (size_t)tc.tx * tc.ty * tc.tz;
   if (tc.pair)
     return (size_t)tc.nb * voxels * 4 + 2 * (((size_t)tile_bytes + 127) & ~(size_t)127) + 16;
-  if (tc.tmem) return (size_t)tc.nb * voxels * 4 + (((size_t)tile_bytes + 15) & ~(size_t)15) + 32;
+  if (tc.tmem || tc.quad)
+    return (size_t)tc.nb * voxels * 4 + (((size_t)tile_bytes + 15) & ~(size_t)15) + 32;
   return (size_t)tc.nb * voxels * 4 + (((size_t)tile_bytes + 15) & ~(size_t)15) + 16;
 }
 
@@ -1041,7 +1287,7 @@ template <bool DBG>
 void dispatch_kb(salvox_ctx* ctx, const TileCfg& tc, const CUtensorMap& map, const KbParams& kp,
                  dim3 grid, size_t smem) {
 #define SX_KB(NB, TX, TY, TZ)                                             \
-  if (!tc.pair && !tc.tmem && tc.nb == NB && tc.tx == TX && tc.ty == TY && tc.tz == TZ) { \
+  if (!tc.pair && !tc.tmem && !tc.quad && tc.nb == NB && tc.tx == TX && tc.ty == TY && tc.tz == TZ) { \
     launch_kb<NB, TX, TY, TZ, DBG>(ctx, map, kp, grid, smem);             \
     return;                                                               \
   }
@@ -1059,6 +1305,13 @@ void dispatch_kb(salvox_ctx* ctx, const TileCfg& tc, const CUtensorMap& map, con
     k<<<grid, 4 * TY * TZ, smem, ctx->stream>>>(map, kp);                                    \
     SX_LAUNCH_CHECK(ctx);                                                                    \
     return;                                                                                  \
+  }
+  if (tc.quad) {
+    auto k = tc.nb == 17 ? kb_quad_kernel<17, DBG> : kb_quad_kernel<33, DBG>;
+    SX_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k<<<grid, 256, smem, ctx->stream>>>(map, kp);
+    SX_LAUNCH_CHECK(ctx);
+    return;
   }
   if (tc.tmem) {
     auto k = tc.nb == 17 ? kb_tmem_kernel<17, DBG> : kb_tmem_kernel<33, DBG>;

@@ -23,3 +23,17 @@ def test_shift_parity_under_each_engine(engine):
                        cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
     assert " passed" in r.stdout
+
+
+@pytest.mark.parametrize("variant", ["0", "3"])
+def test_exhaustive_kernel_variants_parity(variant):
+    """The non-default exhaustive kernels (kb_kernel: 512 threads / register
+    snapshots; kb_quad_kernel: 4 voxels per thread) stay exact: the exhaustive
+    parity suites rerun with SALVOX_KB_VARIANT forced."""
+    env = dict(os.environ, SALVOX_KB_VARIANT=variant)
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu",
+                        "tests/test_gpu_exhaustive.py", "tests/test_golden.py", "-k",
+                        "exh or square or squares or histograms or slabs or scales or range"],
+                       cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout
