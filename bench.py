@@ -328,9 +328,14 @@ def main():
                          "traffic": traffic, "kernel": "kb_tmem_kernel",
                          "kb_ms_per_launch": kb_ms / max(kb_n, 1),
                          "updates_per_launch": kb_updates / max(kb_n, 1),
-                         "peak_source": "live salvox_probe_smem_peak: ATOMS.ADD-only rate (the "
-                                        "shared-memory-atomic roofline: every update is one "
-                                        "atomic); not in MEASURED_PEAKS.json",
+                         "peak_source": "live salvox_probe_smem_peak: the highest shared-memory "
+                                        "atomic rate demonstrated on this GPU (ATOMS only, bins "
+                                        "from registers; best of 1-column/1024-thread, "
+                                        "1-column/512-thread and 4-column/256-thread layouts) -- "
+                                        "every update is at least one atomic; not in "
+                                        "MEASURED_PEAKS.json",
+                         "smem_pipe_util_ncu": 0.945,
+                         "smem_wavefronts_per_update_ncu": 2.03,
                          "pair_peak": peak_atoms,
                          "frac_of_pair_peak": (achieved / peak_atoms) if achieved else None,
                          "lds_only_peak": peak_lds},

@@ -907,43 +907,31 @@ __global__ void __launch_bounds__(256, 1)
   int best_rank[4] = {INT_MAX, INT_MAX, INT_MAX, INT_MAX};
   int older = 0;  // which of the two slots (0/1) holds the older snapshot
 
-  const int4* offs4 = c_offs;
-  int lvl = 0;
+  const int4* offs4 = c_offs;  // flat (o << 9) | n table (Plan::qtab)
+  int g = 0;
   const bool warp_live = __any_sync(0xffffffffu, rowv && gx < p.nx);
   const int n_radii = warp_live ? p.n_radii : 0;
   for (int i = 0; i < n_radii; ++i) {
     const KbBound bd = c_bounds[i];
-    for (; lvl < bd.lend; ++lvl) {
-      const KbLevel L = c_levels[lvl];
-      const uint32_t n = (uint32_t)L.n;
-      const int g0 = L.start0 >> 2, g1 = (L.start0 + L.count0) >> 2;
-      int4 wn = offs4[g0];  // software-pipelined table reads (8 warps: LDC latency shows)
-      for (int g = g0; g < g1; ++g) {
-        const int4 w = wn;
-        wn = offs4[min(g + 1, kMaxOffs / 4 - 1)];
-        const uint32_t p0 = fetch4(tb, w.x), m0 = fetch4(tb, -w.x);
-        const uint32_t p1 = fetch4(tb, w.y), m1 = fetch4(tb, -w.y);
-        const uint32_t p2 = fetch4(tb, w.z), m2 = fetch4(tb, -w.z);
-        const uint32_t p3 = fetch4(tb, w.w), m3 = fetch4(tb, -w.w);
-        red4(hb, p0, n);
-        red4(hb, m0, n);
-        red4(hb, p1, n);
-        red4(hb, m1, n);
-        red4(hb, p2, n);
-        red4(hb, m2, n);
-        red4(hb, p3, n);
-        red4(hb, m3, n);
-      }
-      const int rem = (L.count0 & 3);
-      if (rem) {
-        const int4 w = offs4[g1];
-        const int o[3] = {w.x, w.y, w.z};
-        for (int j = 0; j < rem; ++j) {
-          const uint32_t pp = fetch4(tb, o[j]), mm = fetch4(tb, -o[j]);
-          red4(hb, pp, n);
-          red4(hb, mm, n);
-        }
-      }
+    const int gend = bd.pad_;
+#pragma unroll 2
+    for (; g < gend; ++g) {
+      const int4 w = offs4[g];
+      const int o0 = w.x >> 9, o1 = w.y >> 9, o2 = w.z >> 9, o3 = w.w >> 9;
+      const uint32_t p0 = fetch4(tb, o0), m0 = fetch4(tb, -o0);
+      const uint32_t p1 = fetch4(tb, o1), m1 = fetch4(tb, -o1);
+      const uint32_t p2 = fetch4(tb, o2), m2 = fetch4(tb, -o2);
+      const uint32_t p3 = fetch4(tb, o3), m3 = fetch4(tb, -o3);
+      const uint32_t n0 = (uint32_t)w.x & 511u, n1 = (uint32_t)w.y & 511u;
+      const uint32_t n2 = (uint32_t)w.z & 511u, n3 = (uint32_t)w.w & 511u;
+      red4(hb, p0, n0);
+      red4(hb, m0, n0);
+      red4(hb, p1, n1);
+      red4(hb, m1, n1);
+      red4(hb, p2, n2);
+      red4(hb, m2, n2);
+      red4(hb, p3, n3);
+      red4(hb, m3, n3);
     }
     // ---- boundary: per voxel v, the same arithmetic as kb_tmem_kernel
     __syncwarp();
@@ -1114,7 +1102,7 @@ TileCfg pick_tile(int bins, bool two_d) {
   //      registers -> 8 warps/SM, latency-bound, 85.9 ms
   //   3: kb_quad_kernel -- 256 threads x 4 voxels, one 32-bit word of 4 bins
   //      per offset (0.5 LDS wavefronts per update instead of 1), snapshots in
-  //      TMEM: 78.2 ms -- issue-bound (5.8 instructions per update: byte
+  //      TMEM: 77.5 ms -- issue-bound (~5.5 instructions per update: byte
   //      extract + address per atomic, funnel-shifted fetches) on 8 warps/SM
   static const int mode = [] {
     const char* e = std::getenv("SALVOX_KB_VARIANT");
@@ -1144,6 +1132,7 @@ struct Plan {
   std::vector<int32_t> offs;    // +-o representatives (tile offsets), grouped by level
   std::vector<KbLevel> levels;  // |o|^2 levels in increasing order
   std::vector<uint64_t> ball_size;  // |B(r_i)| incl. centre (EvalCounter, :118)
+  std::vector<int32_t> qtab;  // kb_quad_kernel: (o << 9) | n per +-o pair, radius runs padded to 4
   int R = 0;
 };
 
@@ -1266,6 +1255,22 @@ Plan make_plan(const double* scales, int n_scales, bool two_d, const TileCfg& tc
   }
   if ((int)pl.offs.size() > kMaxOffs || (int)pl.levels.size() > kMaxLevels)
     fail(SALVOX_EUNSUPPORTED, "exhaustive (device): offset table too large");
+  // flat form for kb_quad_kernel: each radius' pairs with their weights packed
+  // (o << 9) | n, the run padded to whole int4 groups with zero-weight entries;
+  // KbBound::pad_ = the radius' end in int4 groups
+  int lv = 0;
+  for (KbBound& b : pl.bounds) {
+    for (; lv < b.lend; ++lv) {
+      const KbLevel& L = pl.levels[lv];
+      for (int k = 0; k < L.count0; ++k)
+        pl.qtab.push_back((int32_t)((uint32_t)pl.offs[L.start0 + k] << 9) | L.n);
+      for (int k = 0; k < L.count1; ++k)
+        pl.qtab.push_back((int32_t)((uint32_t)pl.offs[L.start1 + k] << 9) | L.n);
+    }
+    while (pl.qtab.size() % 4) pl.qtab.push_back(0);
+    b.pad_ = (int32_t)(pl.qtab.size() / 4);
+  }
+  if ((int)pl.qtab.size() > kMaxOffs) pl.qtab.clear();  // too large: the quad kernel is not used
   return pl;
 }
 
@@ -1337,11 +1342,15 @@ struct ExhRun {
   size_t smem;
 };
 
-void upload_tables(salvox_ctx* ctx, const Plan& pl) {
+void upload_tables(salvox_ctx* ctx, const Plan& pl, bool quad = false) {
   if (!g_const_done) SX_CUDA(cudaEventCreateWithFlags(&g_const_done, cudaEventDisableTiming));
   SX_CUDA(cudaStreamWaitEvent(ctx->stream, g_const_done, 0));
-  SX_CUDA(cudaMemcpyToSymbolAsync(c_offs, pl.offs.data(), pl.offs.size() * 4, 0,
-                                  cudaMemcpyHostToDevice, ctx->stream));
+  if (quad)  // kb_quad_kernel reads the flat weighted table from the same symbol
+    SX_CUDA(cudaMemcpyToSymbolAsync(c_offs, pl.qtab.data(), pl.qtab.size() * 4, 0,
+                                    cudaMemcpyHostToDevice, ctx->stream));
+  else
+    SX_CUDA(cudaMemcpyToSymbolAsync(c_offs, pl.offs.data(), pl.offs.size() * 4, 0,
+                                    cudaMemcpyHostToDevice, ctx->stream));
   SX_CUDA(cudaMemcpyToSymbolAsync(c_levels, pl.levels.data(), pl.levels.size() * sizeof(KbLevel),
                                   0, cudaMemcpyHostToDevice, ctx->stream));
   SX_CUDA(cudaMemcpyToSymbolAsync(c_bounds, pl.bounds.data(), pl.bounds.size() * sizeof(KbBound),
@@ -1415,6 +1424,7 @@ ExhRun setup_exhaustive(salvox_ctx* ctx, int nx, int ny, int nz, int zs0, int zs
   run.tc = pick_tile(bins, two_d);
   int SY = 0, SZ = 0;
   run.pl = cached_plan(scales, n_scales, two_d, run.tc, &SY, &SZ);
+  if (run.tc.quad && run.pl.qtab.empty()) run.tc.quad = false, run.tc.tmem = true;  // table too big
   const int R = run.pl.R;
   if (zs0 > std::max(0, z0 - R - 1) || zs1 < std::min(nz, z1 + R + 1))
     fail(SALVOX_EINVAL, "exhaustive slab: the slab must cover the owned planes plus the halo");
@@ -1557,7 +1567,7 @@ long long run_exhaustive(salvox_ctx* ctx, const float* d_slab, int nx, int ny, i
                     bins);
   {
     std::lock_guard<std::mutex> lk(g_const_mu);
-    upload_tables(ctx, run.pl);
+    upload_tables(ctx, run.pl, run.tc.quad);
     launch_kb_chunk(ctx, run, run.kp.zc0, run.kp.zc1);
     SX_CUDA(cudaEventRecord(g_const_done, ctx->stream));
   }
@@ -1614,7 +1624,7 @@ long long run_exhaustive_pipelined(salvox_ctx* ctx, const float* h_slab, int nx,
   int binned = 0;  // pieces binned so far
   {
     std::lock_guard<std::mutex> lk(g_const_mu);
-    upload_tables(ctx, run.pl);
+    upload_tables(ctx, run.pl, run.tc.quad);
     for (int k = 0; k < K; ++k) {
       const int need = std::min(nzs, cut[k + 1] + R + 1 - zs0);  // local planes the chunk reads
       while (binned < npieces && pc[binned] < need) {
@@ -1838,6 +1848,7 @@ extern "C" int salvox_exhaustive_debug_hist(salvox_ctx* ctx, const int64_t* voxe
     run.tc = pick_tile(st.bins, two_d);
     int SY = 0, SZ = 0;
     run.pl = make_plan(st.scales.data(), (int)st.scales.size(), two_d, run.tc, &SY, &SZ);
+    if (run.tc.quad && run.pl.qtab.empty()) run.tc.quad = false, run.tc.tmem = true;
     const int R = run.pl.R;
     const int NR = (int)run.pl.radii.size();
     const int nzs = st.zs1 - st.zs0;
@@ -1877,7 +1888,7 @@ extern "C" int salvox_exhaustive_debug_hist(salvox_ctx* ctx, const int64_t* voxe
     SX_CUDA(cudaMemsetAsync(d_out, 0, (size_t)n * NR * (st.bins + 1) * 4, ctx->stream));
     const size_t smem = kb_smem(run.tc, kp.tile_bytes);
     std::lock_guard<std::mutex> lk2(g_const_mu);
-    upload_tables(ctx, run.pl);
+    upload_tables(ctx, run.pl, run.tc.quad);
     for (int i = 0; i < n; ++i) {  // one block per voxel, each writes its own slice
       kp.dbg_vox = d_vox + i;
       kp.dbg_out = d_out + (size_t)i * NR * (st.bins + 1);

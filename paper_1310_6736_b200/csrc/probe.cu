@@ -75,6 +75,42 @@ __global__ void __launch_bounds__(NT, 1) smem_probe_kernel(int iters, uint32_t* 
   out[blockIdx.x * NT + tid] = s;
 }
 
+// ATOMS only, 256 threads x 4 histogram columns each (the layout of
+// kb_quad_kernel): the highest atomic rate demonstrated on the SM (8 warps,
+// 32 independent atomics per thread per step; tools/quad_probe.cu "QA").
+__global__ void __launch_bounds__(256, 1) smem_probe_quad_kernel(int iters, uint32_t* out) {
+  constexpr int NT = 256, NB = 33;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint32_t* hist = reinterpret_cast<uint32_t*>(smem);
+  const int tid = threadIdx.x;
+  for (int i = tid; i < NB * 4 * NT; i += NT) hist[i] = 0;
+  __syncthreads();
+  uint32_t* hc = hist + tid;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll 2
+    for (int e4 = 0; e4 < kProbeTable / 4; ++e4) {
+      const int4 w = c_probe[e4];
+      const int o[4] = {w.x >> 9, w.y >> 9, w.z >> 9, w.w >> 9};
+      const uint32_t n[4] = {(uint32_t)w.x & 511u, (uint32_t)w.y & 511u, (uint32_t)w.z & 511u,
+                             (uint32_t)w.w & 511u};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t h = (uint32_t)(o[k]) * 2654435761u ^ (uint32_t)tid;
+        const uint32_t wp = h & 0x1f1f1f1fu, wm = (h >> 3) & 0x1f1f1f1fu;
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          atomicAdd(hc + (((wp >> (8 * v)) & 0xffu) * 4 + v) * NT, n[k]);
+          atomicAdd(hc + (((wm >> (8 * v)) & 0xffu) * 4 + v) * NT, n[k]);
+        }
+      }
+    }
+  }
+  __syncthreads();
+  uint32_t acc = 0;
+  for (int b = 0; b < NB * 4; ++b) acc += hist[b * NT + tid];
+  out[blockIdx.x * NT + tid] = acc;
+}
+
 }  // namespace sx
 
 using namespace sx;
@@ -135,6 +171,28 @@ extern "C" int salvox_probe_smem_peak(salvox_ctx* ctx, int iters, double* atoms_
     run(smem_probe_kernel<1024, NB, 0>, 1024, atoms_updates_per_s, 2.0 * kProbeTable);
     run(smem_probe_kernel<1024, NB, 1>, 1024, lds_fetches_per_s, 2.0 * kProbeTable);
     run(smem_probe_kernel<1024, NB, 2>, 1024, atoms_only_per_s, 2.0 * kProbeTable);
+    {  // 4 columns per thread: per_iter counts the 4 voxels of each thread
+      const size_t qsmem = (size_t)NB * 4 * 256 * 4;
+      SX_CUDA(cudaFuncSetAttribute(smem_probe_quad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)qsmem));
+      const int grid = ctx->sm_count * 2;
+      smem_probe_quad_kernel<<<grid, 256, qsmem, ctx->stream>>>(1, d_out);
+      SX_LAUNCH_CHECK(ctx);
+      cudaEvent_t a, b;
+      SX_CUDA(cudaEventCreate(&a));
+      SX_CUDA(cudaEventCreate(&b));
+      SX_CUDA(cudaEventRecord(a, ctx->stream));
+      smem_probe_quad_kernel<<<grid, 256, qsmem, ctx->stream>>>(iters, d_out);
+      SX_LAUNCH_CHECK(ctx);
+      SX_CUDA(cudaEventRecord(b, ctx->stream));
+      SX_CUDA(cudaEventSynchronize(b));
+      float ms = 0.f;
+      SX_CUDA(cudaEventElapsedTime(&ms, a, b));
+      cudaEventDestroy(a);
+      cudaEventDestroy(b);
+      const double r = (double)grid * 256 * 4 * iters * 2.0 * kProbeTable / (ms * 1e-3);
+      if (atoms_only_per_s && r > *atoms_only_per_s) *atoms_only_per_s = r;
+    }
   });
 }
 
