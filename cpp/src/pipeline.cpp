@@ -3,8 +3,11 @@
 #include "salvox/pipeline.hpp"
 
 #include <algorithm>
+#include <cmath>
+#include <limits>
 
 #include "salvox/device.hpp"
+#include "salvox/hu.hpp"
 #include "salvox_capi.h"
 
 namespace salvox {
@@ -201,6 +204,49 @@ double jaccard(const std::vector<uint64_t>& a, const std::vector<uint64_t>& b) {
 
 double jaccard(const Volume& frame, const EllipsoidWindow& win, const std::vector<uint64_t>& mask) {
   return jaccard(rasterize_window(frame, win), mask);
+}
+
+HuVector hu_moments(const Volume& slice) {  // hu.cpp:8-58 on the device
+  if (!slice.is_2d()) throw std::invalid_argument("hu_moments: expected a 2D slice");
+  HuVector h{};
+  check_status(salvox_hu_moments(ctx(), slice.data().data(), slice.nx(), slice.ny(), h.data()));
+  return h;
+}
+
+double hu_distance(const HuVector& a, const HuVector& b) {  // hu.cpp:60-64
+  double d2 = 0.0;
+  for (int i = 0; i < 7; ++i) d2 += (a[size_t(i)] - b[size_t(i)]) * (a[size_t(i)] - b[size_t(i)]);
+  return std::sqrt(d2);
+}
+
+namespace {
+std::vector<double> hu_distances(const std::vector<Detection>& dets, const Volume& v,
+                                 const Volume& t, int slices) {
+  if (!t.is_2d()) throw std::invalid_argument("hu_moments: expected a 2D slice");
+  std::vector<salvox_detection> c(dets.size());
+  std::transform(dets.begin(), dets.end(), c.begin(), to_c);
+  std::vector<double> d(dets.size());
+  check_status(salvox_hu_template_distance(ctx(), v.data().data(), v.nx(), v.ny(), v.nz(), c.data(),
+                                           int64_t(c.size()), t.data().data(), t.nx(), t.ny(),
+                                           slices, d.data()));
+  return d;
+}
+}  // namespace
+
+double hu_template_distance(const Detection& det, const Volume& v, const Volume& template_2d,
+                            int slices) {
+  return hu_distances({det}, v, template_2d, slices).front();
+}
+
+size_t hu_filter(const std::vector<Detection>& dets, const Volume& v, const Volume& template_2d,
+                 int slices) {  // pipeline.cpp:258-271
+  if (dets.empty()) throw std::invalid_argument("hu_filter: no detections");
+  const auto d = hu_distances(dets, v, template_2d, slices);
+  size_t best = 0;
+  double best_d = std::numeric_limits<double>::infinity();
+  for (size_t i = 0; i < d.size(); ++i)
+    if (d[i] < best_d) best_d = d[i], best = i;
+  return best;
 }
 
 }  // namespace salvox

@@ -1,6 +1,6 @@
 // salvox-b200: command-line driver of the B200 drop-in (mirrors the reference's
 // tools/main.cpp "detect" and "phantom" subcommands, plus "exhaustive").
-//   salvox-b200 detect --volume V.mhd --out R.json [--config C.json] [--method M]
+//   salvox-b200 detect --volume V.mhd --out R.json [--config C.json] [--method M] [--hu-template T.mhd]
 //                      [--window LOW:HIGH] [--bins N] [--seeds lattice:S|random:N]
 //                      [--scales a,b,c] [--k K] [--dedupe-radius R] [--workers W]
 //                      [--rng-seed S] [--entropy-quantile Q] [--pdf-quantile Q]
@@ -99,7 +99,25 @@ int cmd_detect(const std::map<std::string, std::string>& f) {
   const auto dets = detect(v, cfg.intensity_window(v), cfg.detect_params());
   const double ms =
       std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-  write_file_atomic(cfg.out_path, detection_report_json(cfg, v, dets, ms));
+  if (f.count("hu-template") && !dets.empty()) {  // tools/main.cpp:130-139: annotate, keep top-k
+    const Volume tmpl = load_volume(f.at("hu-template"));
+    std::vector<double> dist(dets.size());
+    size_t best = 0;
+    for (size_t i = 0; i < dets.size(); ++i) {  // hu_filter's argmin (pipeline.cpp:258-271)
+      dist[i] = hu_template_distance(dets[i], v, tmpl);
+      if (dist[i] < dist[best]) best = i;
+    }
+    json::Value report = json::parse(detection_report_json(cfg, v, dets, ms));
+    for (auto& kv : report.obj) {
+      if (kv.first == "detections")
+        for (size_t i = 0; i < kv.second.arr.size() && i < dets.size(); ++i)
+          kv.second.arr[i].set("hu_distance", json::Value::number(dist[i]));
+      if (kv.first == "header") kv.second.set("hu_best_index", json::Value::number(double(best)));
+    }
+    write_file_atomic(cfg.out_path, json::dump(report, 2) + "\n");
+  } else {
+    write_file_atomic(cfg.out_path, detection_report_json(cfg, v, dets, ms));
+  }
   size_t usable = 0;
   for (const auto& d : dets) usable += d.has(kFlagDegenerate) ? 0 : 1;
   std::cerr << "detect: " << usable << " detection(s) written to " << cfg.out_path << "\n";

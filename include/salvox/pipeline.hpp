@@ -67,6 +67,15 @@ struct DetectParams {
 std::vector<Detection> detect(const Volume& v, const IntensityWindow& iw, DetectParams params,
                               EvalCounter* counter = nullptr);
 
+/// Hu vectors of `slices` axial crops about the window's central slice compared
+/// to the template by mean Euclidean distance (pipeline.cpp:218-256). Returns the
+/// argmin index; throws on an empty list.
+size_t hu_filter(const std::vector<Detection>& dets, const Volume& v, const Volume& template_2d,
+                 int slices = 5);
+/// Per-detection mean Hu distance to the template (same slicing as hu_filter).
+double hu_template_distance(const Detection& det, const Volume& v, const Volume& template_2d,
+                            int slices = 5);
+
 /// Sorted linear indices of the window's in-bounds support voxels on `frame`'s
 /// grid (pipeline.cpp:185-192), rasterised on the device.
 std::vector<uint64_t> rasterize_window(const Volume& frame, const EllipsoidWindow& win);

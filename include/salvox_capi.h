@@ -331,6 +331,20 @@ SALVOX_API int salvox_rasterize_window(salvox_ctx* ctx, int32_t nx, int32_t ny, 
                                        const double* center, const double* H, uint64_t* out,
                                        int64_t cap, int64_t* n_out);
 
+/* hu_moments (hu.hpp:16, src/hu.cpp:8-58) of an nx*ny float image on the
+ * device (out7 = the 7 invariants); SALVOX_EINVAL "hu_moments: zero total
+ * mass" like the reference's throw. */
+SALVOX_API int salvox_hu_moments(salvox_ctx* ctx, const float* image, int32_t nx, int32_t ny,
+                                 double* out7);
+/* hu_template_distance (pipeline.hpp:73-74, src/pipeline.cpp:218-256) for n
+ * detections: mean Hu distance of `slices` axial crops about each detection's
+ * central slice to the template; +inf when no crop has mass. hu_filter is the
+ * argmin of these (first minimum). */
+SALVOX_API int salvox_hu_template_distance(salvox_ctx* ctx, const float* volume, int32_t nx,
+                                           int32_t ny, int32_t nz, const salvox_detection* dets,
+                                           int64_t n, const float* tmpl, int32_t tnx, int32_t tny,
+                                           int32_t slices, double* out_dist);
+
 /* make_phantom (phantom.hpp:125, src/phantom.cpp:364-421). shape 0 box, 1 ball,
  * 2 ellipsoid; fill_type 0 uniform(levels), 1 constant(value); bg_type 0
  * constant, 1 gaussian. Writes the volume and 3 centroid doubles per region. */

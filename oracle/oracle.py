@@ -197,6 +197,11 @@ def _declare(L):
     L.sxo_eigen_det3.argtypes = [_f64p]
     L.sxo_log_portable.restype = C.c_double
     L.sxo_log_portable.argtypes = [C.c_double]
+    L.sxo_hu_moments.restype = C.c_int
+    L.sxo_hu_moments.argtypes = [_f32p, C.c_int, C.c_int, C.c_int, _f64p]
+    L.sxo_hu_template_distance.restype = C.c_double
+    L.sxo_hu_template_distance.argtypes = [_f32p, C.c_int, C.c_int, C.c_int, _f64p, _f64p, _f32p,
+                                           C.c_int, C.c_int, C.c_int]
     L.sxo_rasterize_window.restype = C.c_int64
     L.sxo_rasterize_window.argtypes = [C.c_int, C.c_int, C.c_int, _f64p, _f64p, _vp, C.c_int64]
     L.sxo_exp_portable.restype = C.c_double
@@ -544,6 +549,26 @@ def sym_eigen3(a):
     if lib().sxo_sym_eigen3(np.ascontiguousarray(a, np.float64).reshape(9), vals, vecs) != 0:
         raise OracleError("abmsod: eigen decomposition failed")
     return vals, vecs.reshape(3, 3)
+
+
+def hu_moments(img):
+    a = np.ascontiguousarray(img, np.float32)
+    if a.ndim == 3:
+        a = a[0]
+    out = np.zeros(7)
+    if lib().sxo_hu_moments(a, a.shape[1], a.shape[0], a.shape[1], out) != 0:
+        raise OracleError("hu_moments: zero total mass")
+    return out
+
+
+def hu_template_distance(vol, center, H, tmpl, slices=5):
+    v, nx, ny, nz = _vol(vol)
+    t = np.ascontiguousarray(tmpl, np.float32)
+    if t.ndim == 3:
+        t = t[0]
+    return lib().sxo_hu_template_distance(v, nx, ny, nz, np.ascontiguousarray(center, np.float64),
+                                          np.ascontiguousarray(np.asarray(H, np.float64).reshape(9)),
+                                          t, t.shape[1], t.shape[0], int(slices))
 
 
 def rasterize_window(shape_zyx, center, H):

@@ -1529,3 +1529,72 @@ int64_t sxo_detect(const float* vol, int nx, int ny, int nz, double low, double 
   free(qs);
   return ks;
 }
+
+/* ------------------------------------------------------------------ hu.cpp:8-64 */
+int sxo_hu_moments(const float* img, int nx, int ny, int pitch, double out[7]) {
+  double m00 = 0, m10 = 0, m01 = 0;
+  for (int y = 0; y < ny; ++y)
+    for (int x = 0; x < nx; ++x) {
+      const double f = img[(size_t)y * pitch + x];
+      m00 += f;
+      m10 += f * x;
+      m01 += f * y;
+    }
+  if (m00 <= 0.0) return -1; /* invalid_argument: zero total mass */
+  const double cx = m10 / m00, cy = m01 / m00;
+  double mu20 = 0, mu02 = 0, mu11 = 0, mu30 = 0, mu03 = 0, mu21 = 0, mu12 = 0;
+  for (int y = 0; y < ny; ++y) {
+    const double dy = y - cy;
+    for (int x = 0; x < nx; ++x) {
+      const double f = img[(size_t)y * pitch + x];
+      const double dx = x - cx;
+      mu20 += f * dx * dx;
+      mu02 += f * dy * dy;
+      mu11 += f * dx * dy;
+      mu30 += f * dx * dx * dx;
+      mu03 += f * dy * dy * dy;
+      mu21 += f * dx * dx * dy;
+      mu12 += f * dx * dy * dy;
+    }
+  }
+  const double s2 = m00 * m00 /* pow(x, 2) is exactly rounded */, s3 = opow(m00, 2.5);
+  const double n20 = mu20 / s2, n02 = mu02 / s2, n11 = mu11 / s2;
+  const double n30 = mu30 / s3, n03 = mu03 / s3, n21 = mu21 / s3, n12 = mu12 / s3;
+  out[0] = n20 + n02;
+  out[1] = (n20 - n02) * (n20 - n02) + 4.0 * n11 * n11;
+  out[2] = (n30 - 3 * n12) * (n30 - 3 * n12) + (3 * n21 - n03) * (3 * n21 - n03);
+  out[3] = (n30 + n12) * (n30 + n12) + (n21 + n03) * (n21 + n03);
+  out[4] = (n30 - 3 * n12) * (n30 + n12) * ((n30 + n12) * (n30 + n12) - 3 * (n21 + n03) * (n21 + n03)) +
+           (3 * n21 - n03) * (n21 + n03) * (3 * (n30 + n12) * (n30 + n12) - (n21 + n03) * (n21 + n03));
+  out[5] = (n20 - n02) * ((n30 + n12) * (n30 + n12) - (n21 + n03) * (n21 + n03)) +
+           4.0 * n11 * (n30 + n12) * (n21 + n03);
+  out[6] = (3 * n21 - n03) * (n30 + n12) * ((n30 + n12) * (n30 + n12) - 3 * (n21 + n03) * (n21 + n03)) -
+           (n30 - 3 * n12) * (n21 + n03) * (3 * (n30 + n12) * (n30 + n12) - (n21 + n03) * (n21 + n03));
+  return 0;
+}
+
+/* pipeline.cpp:218-256 hu_template_distance (crop_slice :220-233) */
+double sxo_hu_template_distance(const float* vol, int nx, int ny, int nz, const double center[3],
+                                const double H[9], const float* tmpl, int tnx, int tny, int slices) {
+  double target[7], h[7];
+  if (sxo_hu_moments(tmpl, tnx, tny, tnx, target) != 0) return -1.0;
+  const int zc = (int)lround(center[2]);
+  const int half = slices / 2;
+  const double ex = sqrt(H[0] > 1.0 ? H[0] : 1.0), ey = sqrt(H[4] > 1.0 ? H[4] : 1.0);
+  const int x0 = imax(0, (int)floor(center[0] - ex)), x1 = imin(nx - 1, (int)ceil(center[0] + ex));
+  const int y0 = imax(0, (int)floor(center[1] - ey)), y1 = imin(ny - 1, (int)ceil(center[1] + ey));
+  double sum = 0.0;
+  int used = 0;
+  for (int dz = -half; dz <= half; ++dz) {
+    const int z = zc + dz;
+    if (z < 0 || z >= nz) continue;
+    const float* crop = vol + ((size_t)z * ny + y0) * nx + x0;
+    if (sxo_hu_moments(crop, x1 - x0 + 1, y1 - y0 + 1, nx, h) != 0) continue;
+    double d2 = 0.0;
+    for (int i = 0; i < 7; ++i) d2 += (h[i] - target[i]) * (h[i] - target[i]);
+    sum += sqrt(d2);
+    ++used;
+  }
+  if (used == 0) return 1.0 / 0.0;
+  return sum / used;
+}

@@ -231,6 +231,12 @@ double sxo_pow_portable(double x, double y);
 int64_t sxo_rasterize_window(int nx, int ny, int nz, const double center[3], const double H[9],
                              uint64_t* out, int64_t cap);
 
+/* hu.cpp:8-58 (pitch = row stride in floats); -1 on zero mass. And
+ * pipeline.cpp:218-256 hu_template_distance (-1 if the template has no mass). */
+int sxo_hu_moments(const float* img, int nx, int ny, int pitch, double out[7]);
+double sxo_hu_template_distance(const float* vol, int nx, int ny, int nz, const double center[3],
+                                const double H[9], const float* tmpl, int tnx, int tny, int slices);
+
 /* Eigen 3x3 inverse / determinant restatement (exported for tests). */
 void sxo_eigen_inverse3(const double m[9], double out[9]);
 double sxo_eigen_det3(const double m[9]);

@@ -12,7 +12,7 @@ from .api import (DEFAULT_BUDGET, abmsod, abmsod_records, bandwidth_from_moment,
                   kadir_brady_exhaustive_slab, make_phantom, plan_seeds, quadrant_seek,
                   saliency_shift, seek_records, select)
 
-from .api import jaccard, rasterize_window
+from .api import hu_filter, hu_moments, hu_template_distance, jaccard, rasterize_window
 from .meta_io import load_volume, load_volume_device, save_volume
 
 __version__ = "0.1.0"

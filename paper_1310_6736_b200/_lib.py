@@ -121,6 +121,7 @@ EXPORTS = [
     "salvox_select", "salvox_dedupe_top_k", "salvox_plan_seeds", "salvox_make_phantom",
     "salvox_ascent_seek", "salvox_abmsod_run", "salvox_bandwidth_from_moment",
     "salvox_upload_widen", "salvox_widen_device", "salvox_rasterize_window",
+    "salvox_hu_moments", "salvox_hu_template_distance",
 ]
 # include/salvox_bench.h
 BENCH_EXPORTS = ["salvox_probe_smem_peak", "salvox_ctx_set_profiling", "salvox_ctx_kernel_time"]

@@ -438,6 +438,55 @@ def bandwidth_from_moment(outer, weight_sum, dim, lambda_min, lambda_max):
     return H.reshape(3, 3)
 
 
+def hu_moments(image, ctx=None):
+    """hu_moments (py_module.cpp:149-155): the seven invariants of a 2D image (device)."""
+    a = np.ascontiguousarray(image, np.float32)
+    if a.ndim == 3 and a.shape[0] == 1:
+        a = a[0]
+    if a.ndim != 2:
+        raise ValueError("hu_moments: expected a 2D slice")
+    out = np.zeros(7)
+    check(_lib.load().salvox_hu_moments(_ctx(ctx).handle, ptr(a), a.shape[1], a.shape[0], ptr(out)))
+    return out
+
+
+def _as_records(dets):
+    if isinstance(dets, np.ndarray) and dets.dtype == DET_DTYPE:
+        return np.ascontiguousarray(dets)
+    recs = np.zeros(len(dets), DET_DTYPE)
+    for i, d in enumerate(dets):
+        recs[i]["center"] = d["center"]
+        recs[i]["H"] = np.asarray(d["H"], np.float64).reshape(9)
+    return recs
+
+
+def hu_template_distance(dets, volume, template, slices=5, ctx=None):
+    """hu_template_distance (pipeline.hpp:73-74) for each detection (records or
+    dicts) -> array of mean Hu distances (inf when no crop has mass)."""
+    v, nx, ny, nz = _volume(volume)
+    t = np.ascontiguousarray(template, np.float32)
+    if t.ndim == 3 and t.shape[0] == 1:
+        t = t[0]
+    recs = _as_records(dets)
+    out = np.zeros(max(len(recs), 1))
+    check(_lib.load().salvox_hu_template_distance(
+        _ctx(ctx).handle, ptr(v), nx, ny, nz, ptr(recs), C.c_int64(len(recs)), ptr(t), t.shape[1],
+        t.shape[0], int(slices), ptr(out)))
+    return out[: len(recs)]
+
+
+def hu_filter(dets, volume, template, slices=5, ctx=None):
+    """hu_filter (pipeline.hpp:69-70): index of the detection whose crops best match."""
+    if len(dets) == 0:
+        raise ValueError("hu_filter: no detections")
+    d = hu_template_distance(dets, volume, template, slices, ctx)
+    best, best_d = 0, np.inf
+    for i, x in enumerate(d):
+        if x < best_d:
+            best, best_d = i, x
+    return best
+
+
 def rasterize_window(shape_zyx, center, H, ctx=None):
     """rasterize_window (pipeline.hpp:61): sorted linear indices of the window's
     in-bounds support on a frame of the given shape, rasterised on the device."""

@@ -180,3 +180,187 @@ extern "C" int salvox_rasterize_window(salvox_ctx* ctx, int32_t nx, int32_t ny, 
     if (n_out) *n_out = n;
   });
 }
+
+// ------------------------------------------------------------------ Hu moments
+// hu_moments (reference src/hu.cpp:8-58) and hu_template_distance
+// (src/pipeline.cpp:218-256), one warp per image: the raw and central moment
+// sums run as ordered fp64 chains (lane k owns sum k, all pixels in y->x order,
+// like the reference's double loop), the invariants on lane 0 in the
+// reference's operation order. pow(m00, 2) = m00*m00 (exactly rounded either
+// way); pow(m00, 2.5) uses the shared sx_pow (a few ulp from glibc).
+#include "../../include/salvox/sx_log.h"
+
+namespace sx {
+
+struct HuJob {
+  const float* img;  // first pixel of the crop
+  int w, h;          // crop size
+  int pitch;         // row pitch (floats)
+};
+
+__device__ __forceinline__ double hu_px(const HuJob& j, int i) {
+  const int y = i / j.w, x = i - y * j.w;
+  return (double)__ldg(j.img + (size_t)y * j.pitch + x);
+}
+
+// out[8 * k + 0..6] = Hu vector, out[8 * k + 7] = 1 if the mass is positive
+__global__ void hu_kernel(const HuJob* jobs, int n, double* out) {
+  const int lane = threadIdx.x & 31;
+  const int k = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (k >= n) return;
+  const HuJob j = jobs[k];
+  const int np = j.w * j.h;
+  double acc = 0.0;  // lane 0: m00, 1: m10, 2: m01
+  for (int i = 0; i < np; ++i) {
+    const double f = hu_px(j, i);
+    const int y = i / j.w, x = i - y * j.w;
+    if (lane == 0) acc = __dadd_rn(acc, f);
+    else if (lane == 1) acc = __dadd_rn(acc, __dmul_rn(f, (double)x));
+    else if (lane == 2) acc = __dadd_rn(acc, __dmul_rn(f, (double)y));
+  }
+  const double m00 = __shfl_sync(0xffffffffu, acc, 0);
+  const double m10 = __shfl_sync(0xffffffffu, acc, 1);
+  const double m01 = __shfl_sync(0xffffffffu, acc, 2);
+  if (!(m00 > 0.0)) {  // hu_moments: zero total mass (hu.cpp:21)
+    if (lane == 0) out[8 * k + 7] = 0.0;
+    return;
+  }
+  const double cx = __ddiv_rn(m10, m00), cy = __ddiv_rn(m01, m00);
+  // lane: 0 mu20, 1 mu02, 2 mu11, 3 mu30, 4 mu03, 5 mu21, 6 mu12 (hu.cpp:25-38)
+  acc = 0.0;
+  for (int i = 0; i < np; ++i) {
+    const double f = hu_px(j, i);
+    const int y = i / j.w, x = i - y * j.w;
+    const double dy = __dsub_rn((double)y, cy), dx = __dsub_rn((double)x, cx);
+    double t = 0.0;
+    switch (lane) {
+      case 0: t = __dmul_rn(__dmul_rn(f, dx), dx); break;
+      case 1: t = __dmul_rn(__dmul_rn(f, dy), dy); break;
+      case 2: t = __dmul_rn(__dmul_rn(f, dx), dy); break;
+      case 3: t = __dmul_rn(__dmul_rn(__dmul_rn(f, dx), dx), dx); break;
+      case 4: t = __dmul_rn(__dmul_rn(__dmul_rn(f, dy), dy), dy); break;
+      case 5: t = __dmul_rn(__dmul_rn(__dmul_rn(f, dx), dx), dy); break;
+      case 6: t = __dmul_rn(__dmul_rn(__dmul_rn(f, dx), dy), dy); break;
+      default: break;
+    }
+    acc = __dadd_rn(acc, t);
+  }
+  double mu[7];
+#pragma unroll
+  for (int q = 0; q < 7; ++q) mu[q] = __shfl_sync(0xffffffffu, acc, q);
+  if (lane != 0) return;
+  const double s2 = __dmul_rn(m00, m00);  // std::pow(m00, 2.0)
+  const double s3 = sx_pow(m00, 2.5);     // std::pow(m00, 2.5)
+  const double n20 = __ddiv_rn(mu[0], s2), n02 = __ddiv_rn(mu[1], s2), n11 = __ddiv_rn(mu[2], s2);
+  const double n30 = __ddiv_rn(mu[3], s3), n03 = __ddiv_rn(mu[4], s3), n21 = __ddiv_rn(mu[5], s3),
+               n12 = __ddiv_rn(mu[6], s3);
+#define M(a, b) __dmul_rn((a), (b))
+#define A(a, b) __dadd_rn((a), (b))
+#define S(a, b) __dsub_rn((a), (b))
+  const double a1 = S(n30, M(3.0, n12)), a2 = S(M(3.0, n21), n03);
+  const double b1 = A(n30, n12), b2 = A(n21, n03);
+  double h[7];
+  h[0] = A(n20, n02);
+  h[1] = A(M(S(n20, n02), S(n20, n02)), M(M(4.0, n11), n11));
+  h[2] = A(M(a1, a1), M(a2, a2));
+  h[3] = A(M(b1, b1), M(b2, b2));
+  h[4] = A(M(M(a1, b1), S(M(b1, b1), M(M(3.0, b2), b2))),
+           M(M(a2, b2), S(M(M(3.0, b1), b1), M(b2, b2))));
+  h[5] = A(M(S(n20, n02), S(M(b1, b1), M(b2, b2))), M(M(M(4.0, n11), b1), b2));
+  h[6] = S(M(M(a2, b1), S(M(b1, b1), M(M(3.0, b2), b2))),
+           M(M(a1, b2), S(M(M(3.0, b1), b1), M(b2, b2))));
+#undef M
+#undef A
+#undef S
+  for (int q = 0; q < 7; ++q) out[8 * k + q] = h[q];
+  out[8 * k + 7] = 1.0;
+}
+
+void run_hu(salvox_ctx* ctx, const std::vector<HuJob>& jobs, std::vector<double>& res) {
+  res.assign(jobs.size() * 8, 0.0);
+  if (jobs.empty()) return;
+  char* base = static_cast<char*>(ctx->d_sel_c.ensure(jobs.size() * (sizeof(HuJob) + 64) + 256));
+  HuJob* d_jobs = reinterpret_cast<HuJob*>(base);
+  double* d_out = reinterpret_cast<double*>(base + ((jobs.size() * sizeof(HuJob) + 255) / 256) * 256);
+  SX_CUDA(cudaMemcpyAsync(d_jobs, jobs.data(), jobs.size() * sizeof(HuJob), cudaMemcpyHostToDevice,
+                          ctx->stream));
+  hu_kernel<<<(int)(jobs.size() + 3) / 4, 128, 0, ctx->stream>>>(d_jobs, (int)jobs.size(), d_out);
+  SX_LAUNCH_CHECK(ctx);
+  SX_CUDA(cudaMemcpyAsync(res.data(), d_out, res.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  SX_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+}  // namespace sx
+
+extern "C" int salvox_hu_moments(salvox_ctx* ctx, const float* image, int32_t nx, int32_t ny,
+                                 double* out7) {
+  return guarded([&] {
+    if (!ctx) fail(SALVOX_EINVAL, "null context");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (!image || !out7 || nx < 1 || ny < 1) fail(SALVOX_EINVAL, "hu_moments: expected a 2D slice");
+    SX_CUDA(cudaSetDevice(ctx->device));
+    const size_t n = (size_t)nx * ny;
+    float* d_img = static_cast<float*>(ctx->d_seek_vol.ensure(n * 4));
+    SX_CUDA(cudaMemcpyAsync(d_img, image, n * 4, cudaMemcpyHostToDevice, ctx->stream));
+    std::vector<double> res;
+    run_hu(ctx, {HuJob{d_img, nx, ny, nx}}, res);
+    if (res[7] == 0.0) fail(SALVOX_EINVAL, "hu_moments: zero total mass");
+    for (int q = 0; q < 7; ++q) out7[q] = res[q];
+  });
+}
+
+extern "C" int salvox_hu_template_distance(salvox_ctx* ctx, const float* volume, int32_t nx,
+                                           int32_t ny, int32_t nz, const salvox_detection* dets,
+                                           int64_t n, const float* tmpl, int32_t tnx, int32_t tny,
+                                           int32_t slices, double* out_dist) {
+  return guarded([&] {
+    if (!ctx) fail(SALVOX_EINVAL, "null context");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (!volume || !tmpl || nx < 1 || ny < 1 || nz < 1 || tnx < 1 || tny < 1)
+      fail(SALVOX_EINVAL, "hu_template_distance: bad arguments");
+    if (n < 0 || (n > 0 && (!dets || !out_dist))) fail(SALVOX_EINVAL, "bad detection arrays");
+    SX_CUDA(cudaSetDevice(ctx->device));
+    const size_t nv = (size_t)nx * ny * nz, nt = (size_t)tnx * tny;
+    float* d_vol = static_cast<float*>(ctx->d_seek_vol.ensure((nv + nt) * 4));
+    float* d_tmpl = d_vol + nv;
+    SX_CUDA(cudaMemcpyAsync(d_vol, volume, nv * 4, cudaMemcpyHostToDevice, ctx->stream));
+    SX_CUDA(cudaMemcpyAsync(d_tmpl, tmpl, nt * 4, cudaMemcpyHostToDevice, ctx->stream));
+    // job 0: the template; then every (detection, slice) crop (pipeline.cpp:218-233)
+    std::vector<HuJob> jobs{HuJob{d_tmpl, tnx, tny, tnx}};
+    std::vector<std::pair<int64_t, int>> owner;
+    const int half = slices / 2;
+    for (int64_t i = 0; i < n; ++i) {
+      const salvox_detection& d = dets[i];
+      const double ex = std::sqrt(std::max(d.H[0], 1.0)), ey = std::sqrt(std::max(d.H[4], 1.0));
+      const int x0 = std::max(0, (int)std::floor(d.center[0] - ex));
+      const int x1 = std::min(nx - 1, (int)std::ceil(d.center[0] + ex));
+      const int y0 = std::max(0, (int)std::floor(d.center[1] - ey));
+      const int y1 = std::min(ny - 1, (int)std::ceil(d.center[1] + ey));
+      const int zc = (int)std::lround(d.center[2]);
+      for (int dz = -half; dz <= half; ++dz) {
+        const int z = zc + dz;
+        if (z < 0 || z >= nz) continue;  // thinner than requested: use what exists
+        jobs.push_back(HuJob{d_vol + ((size_t)z * ny + y0) * nx + x0, x1 - x0 + 1, y1 - y0 + 1, nx});
+        owner.emplace_back(i, dz);
+      }
+    }
+    std::vector<double> res;
+    run_hu(ctx, jobs, res);
+    if (res[7] == 0.0) fail(SALVOX_EINVAL, "hu_moments: zero total mass");  // the template
+    std::vector<double> sum((size_t)n, 0.0);
+    std::vector<int> used((size_t)n, 0);
+    for (size_t j = 1; j < jobs.size(); ++j) {  // dz ascending per detection (the reference's loop)
+      if (res[8 * j + 7] == 0.0) continue;       // zero-mass crop contributes nothing
+      double d2 = 0.0;                           // hu_distance (hu.cpp:60-64)
+      for (int q = 0; q < 7; ++q) {
+        const double e = res[8 * j + q] - res[q];
+        d2 += e * e;
+      }
+      sum[(size_t)owner[j - 1].first] += std::sqrt(d2);
+      used[(size_t)owner[j - 1].first]++;
+    }
+    for (int64_t i = 0; i < n; ++i)
+      out_dist[i] = used[(size_t)i] == 0 ? std::numeric_limits<double>::infinity()
+                                         : sum[(size_t)i] / used[(size_t)i];
+  });
+}

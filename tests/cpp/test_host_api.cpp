@@ -15,6 +15,7 @@
 #include "salvox/config.hpp"
 #include "salvox/device.hpp"
 #include "salvox/histogram.hpp"
+#include "salvox/hu.hpp"
 #include "salvox/meta_io.hpp"
 #include "salvox/phantom.hpp"
 #include "salvox/pipeline.hpp"
@@ -312,6 +313,36 @@ void gpu_tests() {
                                ap, IntensityWindow(0, 64, 64));
     CHECK(!rc.trace.empty() && std::abs(rc.trace.front().bhattacharyya - std::sqrt(1.0 / 64)) < 1e-12);
     CHECK(rc.det.entropy_bits == 0.0);
+  }
+  {  // test_pipeline.cpp:149-206: Hu invariances and the disk
+    Volume img(64, 64, 1);
+    uint64_t st = 31;
+    for (int y = 16; y < 48; ++y)
+      for (int x = 16; x < 48; ++x) {
+        st = st * 6364136223846793005ull + 1442695040888963407ull;
+        img.at(x, y, 0) = float((st >> 40) % 64);
+      }
+    const HuVector base = hu_moments(img);
+    Volume sh(64, 64, 1);
+    for (int y = 0; y < 64; ++y)
+      for (int x = 0; x < 64; ++x) sh.at((x + 5) % 64, (y + 3) % 64, 0) = img.at(x, y, 0);
+    const HuVector hs = hu_moments(sh);
+    for (int i = 0; i < 7; ++i) CHECK(std::abs(hs[i] - base[i]) < 1e-9);
+    Volume rot(64, 64, 1);
+    for (int y = 0; y < 64; ++y)
+      for (int x = 0; x < 64; ++x) rot.at(63 - y, x, 0) = img.at(x, y, 0);
+    const HuVector hr = hu_moments(rot);
+    for (int i = 0; i < 7; ++i) CHECK(std::abs(hr[i] - base[i]) <= 1e-6 * std::max(1e-12, std::abs(base[i])));
+    CHECK(hu_distance(base, base) == 0.0);
+    Volume disk(64, 64, 1);
+    for (int y = 0; y < 64; ++y)
+      for (int x = 0; x < 64; ++x)
+        disk.at(x, y, 0) = (x - 31.5) * (x - 31.5) + (y - 31.5) * (y - 31.5) <= 196.0 ? 1.0f : 0.0f;
+    const HuVector hd = hu_moments(disk);
+    CHECK(hd[0] > 0.15 && hd[0] < 0.17);
+    for (int i = 2; i < 7; ++i) CHECK(std::abs(hd[i]) < 1e-9);
+    CHECK_THROWS_AS(hu_moments(Volume(8, 8, 1)), std::invalid_argument);
+    CHECK_THROWS_AS(hu_moments(Volume(8, 8, 2)), std::invalid_argument);
   }
 }
 

@@ -151,3 +151,29 @@ def test_rasterize_window_matches_oracle(sx, oracle):
     assert sx.jaccard(a, a) == 1.0
     with pytest.raises(ValueError):
         sx.jaccard([], [])
+
+
+@pytest.mark.gpu
+def test_cli_detect_hu_template(cpp_build, tmp_path, sx):  # tools/main.cpp:130-139
+    cli = os.path.join(cpp_build, "salvox-b200")
+    spec = {"dims": [64, 64, 24],
+            "regions": [{"shape": "ball", "center": [20.0, 32.0, 12.0], "radius": 8.0,
+                         "fill": {"type": "constant", "value": 40.0}},
+                        {"shape": "box", "center": [46.0, 32.0, 12.0], "half_extents": [10.0, 4.0, 8.0],
+                         "fill": {"type": "constant", "value": 40.0}}], "rng_seed": 2}
+    (tmp_path / "spec.json").write_text(json.dumps(spec))
+    subprocess.run([cli, "phantom", str(tmp_path / "spec.json"), str(tmp_path / "v.mhd")],
+                   check=True, capture_output=True)
+    y, x = np.mgrid[0:24, 0:24]
+    disk = np.where((x - 11.5) ** 2 + (y - 11.5) ** 2 <= 64.0, 40.0, 0.0).astype(np.float32)
+    sx.save_volume(disk[None], str(tmp_path / "t.mhd"))
+    r = subprocess.run([cli, "detect", "--method", "shift", "--volume", str(tmp_path / "v.mhd"),
+                        "--window", "0:64", "--seeds", "lattice:8", "--scales", "6,8", "--k", "4",
+                        "--hu-template", str(tmp_path / "t.mhd"), "--out", str(tmp_path / "d.json")],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    rep = json.loads((tmp_path / "d.json").read_text())
+    dets = rep["detections"]
+    assert dets and all("hu_distance" in d for d in dets)
+    best = int(rep["header"]["hu_best_index"])
+    assert dets[best]["hu_distance"] == min(d["hu_distance"] for d in dets)
