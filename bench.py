@@ -38,6 +38,9 @@ BINS = 32
 LOW, HIGH = 0.0, 32.0  # window [0, 32), SURVEY.md 8(d) C2
 METRIC = "voxel-scale entropy evals/sec (exhaustive); 256³ seed-grid volumes/sec"
 UNIT = "voxel-scale evals/s"
+# the 3D exhaustive kernel the library picks (csrc/exhaustive.cu pick_tile; A/B knob SALVOX_KB_VARIANT)
+KB_KERNEL = {"0": "kb_kernel", "1": "kb_pair_kernel", "2": "kb_tmem_kernel"}.get(
+    os.environ.get("SALVOX_KB_VARIANT", "3"), "kb_quad_kernel")
 
 
 def c2_spec():
@@ -302,12 +305,14 @@ def main():
     if rank == 0:
         achieved = kb_updates / (kb_ms * 1e-3) if kb_ms > 0 else None
         traffic = None
-        prof = os.path.join(ROOT, "profiles", "kb_kernel_ncu.json")
+        prof_d = {}
+        prof = os.path.join(ROOT, "profiles", "kb_kernel_ncu.json")  # the default kernel's ncu capture
         if os.path.exists(prof):
             try:
-                traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+                prof_d = json.load(open(prof))
+                traffic = prof_d.get("dram_bytes_per_launch")
             except Exception:
-                traffic = None
+                prof_d, traffic = {}, None
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -325,7 +330,7 @@ def main():
             "roofline": {"bound": "smem", "achieved": achieved, "peak": peak_atoms_only,
                          "unit": "histogram updates/s",
                          "frac": (achieved / peak_atoms_only) if achieved else None,
-                         "traffic": traffic, "kernel": "kb_tmem_kernel",
+                         "traffic": traffic, "kernel": KB_KERNEL,
                          "kb_ms_per_launch": kb_ms / max(kb_n, 1),
                          "updates_per_launch": kb_updates / max(kb_n, 1),
                          "peak_source": "live salvox_probe_smem_peak: the highest shared-memory "
@@ -334,8 +339,9 @@ def main():
                                         "1-column/512-thread and 4-column/256-thread layouts) -- "
                                         "every update is at least one atomic; not in "
                                         "MEASURED_PEAKS.json",
-                         "smem_pipe_util_ncu": 0.945,
-                         "smem_wavefronts_per_update_ncu": 2.03,
+                         "smem_pipe_util_ncu": (prof_d.get("smem_pipe_pct_of_peak_elapsed", 0.0) / 100.0
+                                                if prof_d else None),
+                         "smem_wavefronts_per_update_ncu": prof_d.get("wavefronts_per_warp_update"),
                          "pair_peak": peak_atoms,
                          "frac_of_pair_peak": (achieved / peak_atoms) if achieved else None,
                          "lds_only_peak": peak_lds},

@@ -134,6 +134,9 @@ constexpr int kMaxRadii = 192;
 __constant__ int4 c_offs[kMaxOffs / 4];
 __constant__ KbLevel c_levels[kMaxLevels];
 __constant__ KbBound c_bounds[kMaxRadii];
+// kb_quad_kernel: per radius, the ends (in int4 groups of c_offs) of its three
+// class runs (x, y, z); the radius' first run starts at the previous radius' z
+__constant__ int4 c_qruns[kMaxRadii];
 
 struct KbParams {
   int nx, ny, nz;   // global dims
@@ -553,7 +556,7 @@ __global__ void __launch_bounds__(4 * TY * TZ, 1)
   }
 }
 
-// K2'' (3D, NB <= 33): 1024 threads per CTA (32 warps/SM, twice kb_kernel's
+// K2'' (3D, NB <= 33; SALVOX_KB_VARIANT=2): 1024 threads per CTA (32 warps/SM, twice kb_kernel's
 // latency hiding) with the two radius snapshots held in TENSOR MEMORY. At 1024
 // threads the register file allows 64 registers per thread, too few for the
 // 2 x 32 snapshot words, so each thread parks them in its TMEM lane: warp w
@@ -780,33 +783,111 @@ __global__ void __launch_bounds__(1024, 1)
   }
 }
 
-// K2-quad (3D, NB <= 33, the default): 256 threads, FOUR x-adjacent voxels per
-// thread. The tile row pitch and the box start are multiples of 16 and each
-// thread's first voxel sits on a 4-byte boundary, so the 4 bins a thread needs
-// at offset o are one aligned 32-bit word when dx = 0 (mod 4), else two words
-// joined by a funnel shift -- warp-uniform, from the offset itself. That cuts
-// the bin fetches from one LDS per update to ~0.44 (tools/quad_probe.cu: 4.95e12
-// vs 4.33e12 updates/s for the one-voxel mix), and 8 warps with 32 independent
-// atomics each keep the atomic pipe fed. Histogram column (v, tid) of bin b is
-// word (4 b + v) * 256 + tid (bank = tid: conflict-free); its byte address is
-// base + v*1024 + (b << 12), built with a shift, a mask and one add per update.
+// K2-quad (3D, NB <= 33; the default): 256 threads, FOUR x-adjacent
+// voxels per thread, built so an update costs ~2.9 instructions and ~1.44
+// shared-pipe wavefronts instead of kb_tmem_kernel's ~4 and 2:
+//  * bins: the tile row pitch and box start are multiples of 16 and each
+//    thread's first voxel sits on a 4-byte boundary, so the 4 bins a thread
+//    needs at offset o are bytes s..s+3 of two aligned words, s = o.x mod 4.
+//    The table stores each +-o pair with the representative whose s is 0, 1 or
+//    2 ("class"), in one run per (radius, class), so s is a template constant;
+//  * address = ONE PRMT: column c of a 64-column panel is byte c*4 of the
+//    address and the bin is byte 1, so PRMT(word, c*4, sel) = bin*256 + c*4 --
+//    byte extract and address in one instruction -- and the panel (which of the
+//    16 panels of 64 columns x NB bins: voxel v, column group G) is the atomic's
+//    immediate. G = warp % 4 is the SM sub-partition, so each sub-partition runs
+//    one specialisation of the loop (one copy in its instruction cache).
 // Snapshots: 4 voxels x 2 slots x 32 bins = all 256 TMEM columns of the
 // thread's lane (warp w: lanes 32*(w%4), columns 256*(w/4)).
-__device__ __forceinline__ uint32_t fetch4(const uint8_t* tb, int off) {
-  // tb is 4-aligned, so (tb + off) & 3 = off & 3 = dx mod 4 (warp-uniform):
-  // two aligned words and one funnel shift by 8 * (off & 3) (SHF uses the low
-  // 5 bits of off << 3); when off = 0 (mod 4) the second word is simply unused
-  const uint32_t* w = reinterpret_cast<const uint32_t*>(tb + (off & ~3));
-  return __funnelshift_r(w[0], w[1], (uint32_t)off << 3);
+__device__ __forceinline__ uint32_t lds32(const uint8_t* p) {
+  return *reinterpret_cast<const uint32_t*>(p);
 }
-__device__ __forceinline__ void red4(uint32_t hb, uint32_t w, uint32_t n) {
-  // byte v of w is the bin of voxel v: address hb + v*1024 + (bin << 12)
-  // (PRMT extracts the byte, LEA shifts-and-adds)
+
+// The first byte of dynamic shared memory sits at shared::cta address
+// (CTA-rank << 24) + 0x400 (1 KB reserved; the kernel checks it). The rank bits
+// ride in bytes 2-3 of c, the 0x400 in the atomic's immediate.
+constexpr uint32_t kDsmemBase = 0x400u;
+
+template <int J>
+__device__ __forceinline__ uint32_t quad_prmt(uint32_t w0, uint32_t w1, uint32_t c) {
+  // volatile: keeps the 8 PRMTs of an entry ahead of its 8 REDs (the ALU
+  // latency is then covered without relying on other warps -- 2 per SMSP)
+  uint32_t r;
+  asm volatile("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(J < 4 ? w0 : w1), "r"(c),
+               "n"(0x7604u | ((uint32_t)(J & 3) << 4)));
+  return r;
+}
+
+template <int NB, int G, int V>
+__device__ __forceinline__ void quad_red2(uint32_t ap, uint32_t am, uint32_t n) {
+  constexpr uint32_t IMM = kDsmemBase + (uint32_t)((V * 4 + G) * NB * 256);
+  asm volatile("red.shared.add.u32 [%0+%2], %1;" ::"r"(ap), "r"(n), "n"(IMM));
+  asm volatile("red.shared.add.u32 [%0+%2], %1;" ::"r"(am), "r"(n), "n"(IMM));
+}
+
+template <int NB, int G, int SP, int SM>
+__device__ __forceinline__ void quad_entry_issue(uint32_t p0, uint32_t p1, uint32_t m0, uint32_t m1,
+                                                 uint32_t c, uint32_t n) {
+  const uint32_t a0 = quad_prmt<0 + SP>(p0, p1, c), b0 = quad_prmt<0 + SM>(m0, m1, c);
+  const uint32_t a1 = quad_prmt<1 + SP>(p0, p1, c), b1 = quad_prmt<1 + SM>(m0, m1, c);
+  const uint32_t a2 = quad_prmt<2 + SP>(p0, p1, c), b2 = quad_prmt<2 + SM>(m0, m1, c);
+  const uint32_t a3 = quad_prmt<3 + SP>(p0, p1, c), b3 = quad_prmt<3 + SM>(m0, m1, c);
+  quad_red2<NB, G, 0>(a0, b0, n);
+  quad_red2<NB, G, 1>(a1, b1, n);
+  quad_red2<NB, G, 2>(a2, b2, n);
+  quad_red2<NB, G, 3>(a3, b3, n);
+}
+
+// One int4 group = 4 table entries = 4 +-o pairs = 32 updates: all bin words
+// are loaded first, then the PRMT/RED stream is issued.
+template <int CLS>
+struct QuadGroup {
+  uint32_t p0[4], p1[4], m0[4], m1[4], n[4];
+  __device__ __forceinline__ void load(const uint8_t* tb, int4 w) {
+    const int e[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
-  for (int v = 0; v < 4; ++v) {
-    const uint32_t bin = __byte_perm(w, 0u, 0x4440u | (uint32_t)v);
-    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(hb + 1024u * v + (bin << 12)), "r"(n));
+    for (int k = 0; k < 4; ++k) {
+      const int a = e[k] >> 9;
+      n[k] = (uint32_t)e[k] & 511u;
+      const uint8_t* pp = tb + a;
+      const uint8_t* pm = tb - a - (CLS ? 4 : 0);
+      p0[k] = lds32(pp);
+      m0[k] = lds32(pm);
+      p1[k] = CLS ? lds32(pp + 4) : 0u;
+      m1[k] = CLS ? lds32(pm + 4) : 0u;
+    }
   }
+};
+
+template <int NB, int G, int CLS>
+__device__ __forceinline__ void quad_issue(const QuadGroup<CLS>& q, uint32_t c) {
+  constexpr int SP = CLS, SM = CLS == 1 ? 3 : CLS;  // byte shifts of +o and -o
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    quad_entry_issue<NB, G, SP, SM>(q.p0[k], q.p1[k], q.m0[k], q.m1[k], c, q.n[k]);
+}
+
+template <int NB, int G, int CLS>
+__device__ __forceinline__ void quad_run(const uint8_t* tb, uint32_t c, int g, int gend) {
+  // the next group's table entries are fetched one iteration ahead (the
+  // constant-cache latency was the largest single stall); c_offs holds at
+  // least one int4 past every run (make_plan), so the read never overruns
+  int4 w = c_offs[g];
+#pragma unroll 1
+  for (; g < gend; ++g) {
+    const int4 wn = c_offs[g + 1];
+    QuadGroup<CLS> q;
+    q.load(tb, w);
+    quad_issue<NB, G, CLS>(q, c);
+    w = wn;
+  }
+}
+
+template <int NB, int G>
+__device__ __noinline__ void quad_walk(const uint8_t* tb, uint32_t c, int g, int4 e) {
+  quad_run<NB, G, 0>(tb, c, g, e.x);
+  quad_run<NB, G, 1>(tb, c, e.x, e.y);
+  quad_run<NB, G, 2>(tb, c, e.y, e.z);
 }
 
 template <int NB, bool DBG>
@@ -814,13 +895,14 @@ __global__ void __launch_bounds__(256, 1)
     kb_quad_kernel(const __grid_constant__ CUtensorMap tmap, const KbParams p) {
   constexpr int TX = 16, TY = 8, TZ = 8, NT = 256, NV = 1024;
   constexpr int NS = NB - 1;  // snapshot bins (1..NB-1)
+  constexpr int PANEL = NB * 256;  // bytes: NB bins x 64 columns
   static_assert(NS % 8 == 0 && 2 * NS <= 64, "TMEM: 64 columns per voxel");
   extern __shared__ __align__(1024) uint8_t smem[];
-  uint32_t* hist = reinterpret_cast<uint32_t*>(smem);  // [NB][4][NT]
+  uint8_t* hist = smem;  // 16 panels [v * 4 + G][bin][64 columns]
   uint8_t* tile = smem + NB * NV * 4;
   uint64_t* bar = reinterpret_cast<uint64_t*>(tile + ((p.tile_bytes + 15u) & ~15u));
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 1);
-  const int tid = threadIdx.x, warp = tid >> 5;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
   int tx0, ty0, tz0;
   long long dbg_lin = -1;
@@ -892,7 +974,10 @@ __global__ void __launch_bounds__(256, 1)
         dbg_v = v;
   // (lx + R + delta) is a multiple of 4: R + delta = tx0 - xa = 0 (mod 16)
   const uint8_t* tb = tile + (lz + p.Rz) * p.SZ + (ly + p.R) * p.SY + (lx + p.R + delta);
-  const uint32_t hb = smem_u32(hist) + 4u * (uint32_t)tid;
+  const int G = warp & 3, col = lane + 32 * (warp >> 2);
+  const uint32_t hs0 = smem_u32(smem);
+  if ((hs0 & 0xffffu) != kDsmemBase) __trap();  // the immediates below assume it
+  const uint32_t cb = (hs0 & 0xffff0000u) | (4u * (uint32_t)col);  // bytes 0, 2, 3 of every address
   const uint32_t lane_base = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(256 * (warp >> 2));
   {  // zero all snapshot slots ("radius 0")
     uint32_t z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -907,37 +992,25 @@ __global__ void __launch_bounds__(256, 1)
   int best_rank[4] = {INT_MAX, INT_MAX, INT_MAX, INT_MAX};
   int older = 0;  // which of the two slots (0/1) holds the older snapshot
 
-  const int4* offs4 = c_offs;  // flat (o << 9) | n table (Plan::qtab)
   int g = 0;
   const bool warp_live = __any_sync(0xffffffffu, rowv && gx < p.nx);
   const int n_radii = warp_live ? p.n_radii : 0;
   for (int i = 0; i < n_radii; ++i) {
     const KbBound bd = c_bounds[i];
-    const int gend = bd.pad_;
-#pragma unroll 2
-    for (; g < gend; ++g) {
-      const int4 w = offs4[g];
-      const int o0 = w.x >> 9, o1 = w.y >> 9, o2 = w.z >> 9, o3 = w.w >> 9;
-      const uint32_t p0 = fetch4(tb, o0), m0 = fetch4(tb, -o0);
-      const uint32_t p1 = fetch4(tb, o1), m1 = fetch4(tb, -o1);
-      const uint32_t p2 = fetch4(tb, o2), m2 = fetch4(tb, -o2);
-      const uint32_t p3 = fetch4(tb, o3), m3 = fetch4(tb, -o3);
-      const uint32_t n0 = (uint32_t)w.x & 511u, n1 = (uint32_t)w.y & 511u;
-      const uint32_t n2 = (uint32_t)w.z & 511u, n3 = (uint32_t)w.w & 511u;
-      red4(hb, p0, n0);
-      red4(hb, m0, n0);
-      red4(hb, p1, n1);
-      red4(hb, m1, n1);
-      red4(hb, p2, n2);
-      red4(hb, m2, n2);
-      red4(hb, p3, n3);
-      red4(hb, m3, n3);
+    const int4 e = c_qruns[i];
+    switch (G) {  // warp-uniform; G = warp % 4 = the warp's SM sub-partition
+      case 0: quad_walk<NB, 0>(tb, cb, g, e); break;
+      case 1: quad_walk<NB, 1>(tb, cb, g, e); break;
+      case 2: quad_walk<NB, 2>(tb, cb, g, e); break;
+      default: quad_walk<NB, 3>(tb, cb, g, e); break;
     }
+    g = e.z;
     // ---- boundary: per voxel v, the same arithmetic as kb_tmem_kernel
     __syncwarp();
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
-      const uint32_t* hc = hist + v * NT + tid;  // bin b at hc[b * 4 * NT]
+      // bin b of this voxel's column at hc[b * 64]
+      const uint32_t* hc = reinterpret_cast<const uint32_t*>(hist + (v * 4 + G) * PANEL) + col;  // same panel as quad_red
       const uint32_t T = bd.W - hc[0];
       const bool doH = (bd.flags & 1) && T > 0u;
       const bool doE = (bd.flags & 2) && T > 0u && TA[v] > 0u && TB[v] > 0u;
@@ -951,17 +1024,19 @@ __global__ void __launch_bounds__(256, 1)
         uint32_t a[8], cur[8];
         tm_ld8(slot + c, a);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) cur[j] = hc[(1 + c + j) * 4 * NT];
+        for (int j = 0; j < 8; ++j) cur[j] = hc[(1 + c + j) * 64];
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           const uint32_t cv = cur[j];
+#ifndef KB_SKIP_MATH
           if (2u * cv > T) {
             dom = cv;
           } else if (doH && cv) {
             const float pb = (float)cv * invT;
             hacc -= pb * __log2f(pb);
           }
+#endif
           if (doE) {
             const unsigned long long x = (unsigned long long)cv * TA[v], y = (unsigned long long)a[j] * T;
             num += x > y ? x - y : y - x;
@@ -1096,17 +1171,18 @@ TileCfg pick_tile(int bins, bool two_d) {
   const int nb = bins <= 16 ? 17 : (bins <= 32 ? 33 : 65);
   if (nb == 65) return two_d ? TileCfg{65, 32, 8, 1, false} : TileCfg{65, 8, 8, 4, false};
   // Variants (A/B knob SALVOX_KB_VARIANT; measured at C2 on one B200, r01):
-  //   2 (default, 3D): kb_tmem_kernel -- 1024 threads, snapshots in TMEM, 71.2 ms
+  //   3 (default, 3D): kb_quad_kernel -- 256 threads x 4 voxels, 4 bins per
+  //      32-bit word, one PRMT per update builds the atomic's address, snapshots
+  //      in TMEM: 65.6 ms (1.44 smem wavefronts per update; latency-bound on
+  //      8 warps/SM, issue active ~49%)
+  //   2: kb_tmem_kernel -- 1024 threads, snapshots in TMEM, 70.7 ms (2.03
+  //      wavefronts per update, shared pipe 94.5%: the LDS+ATOMS pair bound)
   //   0: kb_kernel -- 512 threads, snapshots in registers, 80.2 ms (2D default)
   //   1: kb_pair_kernel -- 2 voxels/thread, 25% fewer smem wavefronts but 247
   //      registers -> 8 warps/SM, latency-bound, 85.9 ms
-  //   3: kb_quad_kernel -- 256 threads x 4 voxels, one 32-bit word of 4 bins
-  //      per offset (0.5 LDS wavefronts per update instead of 1), snapshots in
-  //      TMEM: 77.5 ms -- issue-bound (~5.5 instructions per update: byte
-  //      extract + address per atomic, funnel-shifted fetches) on 8 warps/SM
   static const int mode = [] {
     const char* e = std::getenv("SALVOX_KB_VARIANT");
-    return e ? std::atoi(e) : 2;
+    return e ? std::atoi(e) : 3;
   }();
   if (mode == 1) return two_d ? TileCfg{nb, 8, 64, 1, true} : TileCfg{nb, 8, 8, 8, true};
   if (mode == 2 && !two_d) return TileCfg{nb, 16, 8, 8, false, true};
@@ -1132,7 +1208,8 @@ struct Plan {
   std::vector<int32_t> offs;    // +-o representatives (tile offsets), grouped by level
   std::vector<KbLevel> levels;  // |o|^2 levels in increasing order
   std::vector<uint64_t> ball_size;  // |B(r_i)| incl. centre (EvalCounter, :118)
-  std::vector<int32_t> qtab;  // kb_quad_kernel: (o << 9) | n per +-o pair, radius runs padded to 4
+  std::vector<int32_t> qtab;  // kb_quad_kernel: (a << 9) | n per +-o pair, (radius, class) runs
+  std::vector<int4> qruns;    // kb_quad_kernel: per radius, the three run ends (int4 groups)
   int R = 0;
 };
 
@@ -1255,22 +1332,34 @@ Plan make_plan(const double* scales, int n_scales, bool two_d, const TileCfg& tc
   }
   if ((int)pl.offs.size() > kMaxOffs || (int)pl.levels.size() > kMaxLevels)
     fail(SALVOX_EUNSUPPORTED, "exhaustive (device): offset table too large");
-  // flat form for kb_quad_kernel: each radius' pairs with their weights packed
-  // (o << 9) | n, the run padded to whole int4 groups with zero-weight entries;
-  // KbBound::pad_ = the radius' end in int4 groups
-  int lv = 0;
-  for (KbBound& b : pl.bounds) {
-    for (; lv < b.lend; ++lv) {
-      const KbLevel& L = pl.levels[lv];
-      for (int k = 0; k < L.count0; ++k)
-        pl.qtab.push_back((int32_t)((uint32_t)pl.offs[L.start0 + k] << 9) | L.n);
-      for (int k = 0; k < L.count1; ++k)
-        pl.qtab.push_back((int32_t)((uint32_t)pl.offs[L.start1 + k] << 9) | L.n);
+  // flat form for kb_quad_kernel: per radius, three runs of (a << 9) | n, one per
+  // class s = o.x mod 4 in {0, 1, 2} of the pair's representative (-o when
+  // o.x = 3 mod 4), a = o - s the 4-aligned byte offset of +o's first word;
+  // each run padded to whole int4 groups with zero-weight entries
+  {
+    int lv = 0;
+    for (KbBound& b : pl.bounds) {
+      std::vector<int32_t> runs[3];
+      for (; lv < b.lend; ++lv) {
+        const KbLevel& L = pl.levels[lv];
+        for (int k = 0; k < L.count0 + L.count1; ++k) {
+          int o = k < L.count0 ? pl.offs[L.start0 + k] : pl.offs[L.start1 + k - L.count0];
+          if ((o & 3) == 3) o = -o;
+          const int s = o & 3;
+          runs[s].push_back((int32_t)((uint32_t)(o - s) << 9) | L.n);
+        }
+      }
+      int4 e{};
+      for (int s = 0; s < 3; ++s) {
+        for (int32_t v : runs[s]) pl.qtab.push_back(v);
+        while (pl.qtab.size() % 4) pl.qtab.push_back(0);
+        (s == 0 ? e.x : s == 1 ? e.y : e.z) = (int)(pl.qtab.size() / 4);
+      }
+      pl.qruns.push_back(e);
     }
-    while (pl.qtab.size() % 4) pl.qtab.push_back(0);
-    b.pad_ = (int32_t)(pl.qtab.size() / 4);
   }
-  if ((int)pl.qtab.size() > kMaxOffs) pl.qtab.clear();  // too large: the quad kernel is not used
+  // too large (one int4 of slack for kb_quad_kernel's look-ahead): not used
+  if ((int)pl.qtab.size() + 4 > kMaxOffs) pl.qtab.clear(), pl.qruns.clear();
   return pl;
 }
 
@@ -1345,10 +1434,12 @@ struct ExhRun {
 void upload_tables(salvox_ctx* ctx, const Plan& pl, bool quad = false) {
   if (!g_const_done) SX_CUDA(cudaEventCreateWithFlags(&g_const_done, cudaEventDisableTiming));
   SX_CUDA(cudaStreamWaitEvent(ctx->stream, g_const_done, 0));
-  if (quad)  // kb_quad_kernel reads the flat weighted table from the same symbol
+  if (quad) {  // kb_quad_kernel reads the flat weighted table from the same symbol
     SX_CUDA(cudaMemcpyToSymbolAsync(c_offs, pl.qtab.data(), pl.qtab.size() * 4, 0,
                                     cudaMemcpyHostToDevice, ctx->stream));
-  else
+    SX_CUDA(cudaMemcpyToSymbolAsync(c_qruns, pl.qruns.data(), pl.qruns.size() * sizeof(int4), 0,
+                                    cudaMemcpyHostToDevice, ctx->stream));
+  } else
     SX_CUDA(cudaMemcpyToSymbolAsync(c_offs, pl.offs.data(), pl.offs.size() * 4, 0,
                                     cudaMemcpyHostToDevice, ctx->stream));
   SX_CUDA(cudaMemcpyToSymbolAsync(c_levels, pl.levels.data(), pl.levels.size() * sizeof(KbLevel),
