@@ -355,6 +355,20 @@ SALVOX_API int salvox_make_phantom(int32_t nx, int32_t ny, int32_t nz, int32_t b
                         const int32_t* fill_levels, const double* fill_value, uint64_t rng_seed,
                         float* out_volume, double* out_centroids);
 
+/* make_phantom generated ON THE DEVICE: same arguments and
+ * errors as salvox_make_phantom, the volume written to device memory d_volume
+ * (nx*ny*nz floats). splitmix64 is counter-based, so every voxel's draw index
+ * is computed from per-row inside counts (scan) instead of a serial walk.
+ * Integer/constant fills are bit-identical to the host generator; the gaussian
+ * background may differ in the last float place (libdevice log/sin/cos). */
+SALVOX_API int salvox_make_phantom_device(salvox_ctx* ctx, int32_t nx, int32_t ny, int32_t nz,
+                        int32_t bg_type, double bg_value, double bg_mean, double bg_sigma,
+                        int32_t n_regions, const int32_t* shape, const double* center,
+                        const double* half_extents, const double* radius, const double* axes,
+                        const int32_t* fill_type, const int32_t* fill_levels,
+                        const double* fill_value, uint64_t rng_seed, float* d_volume,
+                        double* out_centroids);
+
 #ifdef __cplusplus
 }
 #endif

@@ -9,7 +9,7 @@ from ._lib import (DET_DTYPE, MAX_DTYPE, Context, SalvoxCudaError, SalvoxError,
 from .api import (DEFAULT_BUDGET, abmsod, abmsod_records, bandwidth_from_moment, dedupe_top_k, detect, detect_batch_device, detect_records,
                   detect_shard, detection_to_dict,
                   exhaustive_debug_hist, kadir_brady_exhaustive, kadir_brady_exhaustive_records,
-                  kadir_brady_exhaustive_slab, make_phantom, plan_seeds, quadrant_seek,
+                  kadir_brady_exhaustive_slab, make_phantom, make_phantom_device, plan_seeds, quadrant_seek,
                   saliency_shift, seek_records, select)
 
 from .api import hu_filter, hu_moments, hu_template_distance, jaccard, rasterize_window

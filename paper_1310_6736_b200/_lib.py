@@ -119,6 +119,7 @@ EXPORTS = [
     "salvox_exhaustive_debug_hist", "salvox_detect", "salvox_detect_batch_device",
     "salvox_detect_shard", "salvox_seek",
     "salvox_select", "salvox_dedupe_top_k", "salvox_plan_seeds", "salvox_make_phantom",
+    "salvox_make_phantom_device",
     "salvox_ascent_seek", "salvox_abmsod_run", "salvox_bandwidth_from_moment",
     "salvox_upload_widen", "salvox_widen_device", "salvox_rasterize_window",
     "salvox_hu_moments", "salvox_hu_template_distance",
@@ -184,6 +185,8 @@ def _declare(L):
                                     _i64, _pi64]
     L.salvox_make_phantom.argtypes = [_i32, _i32, _i32, _i32, _dbl, _dbl, _dbl, _i32, _vp, _vp,
                                       _vp, _vp, _vp, _vp, _vp, _vp, _u64, _vp, _vp]
+    L.salvox_make_phantom_device.argtypes = [_vp, _i32, _i32, _i32, _i32, _dbl, _dbl, _dbl, _i32,
+                                             _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _u64, _vp, _vp]
     L.salvox_probe_smem_peak.argtypes = [_vp, C.c_int, C.POINTER(_dbl), C.POINTER(_dbl),
                                          C.POINTER(_dbl)]
     L.salvox_ctx_set_profiling.argtypes = [_vp, C.c_int]

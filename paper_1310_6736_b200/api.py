@@ -554,9 +554,8 @@ def plan_seeds(shape_zyx, mode="lattice", spacing=16.0, count=0, scales=(8.0,), 
 _SHAPES = {"box": 0, "ball": 1, "ellipsoid": 2}
 
 
-def make_phantom(spec):
-    """make_phantom (py_module.cpp:96-112): spec is PhantomSpec JSON text or a dict
-    (phantom.cpp:226-277). Returns (array[z,y,x], regions[{center, H}])."""
+def _phantom_args(spec):
+    """PhantomSpec JSON text / dict (phantom.cpp:226-277) -> the C-ABI argument arrays."""
     if isinstance(spec, str):
         spec = json.loads(spec)
     nx, ny, nz = (int(d) for d in spec["dims"])
@@ -590,12 +589,41 @@ def make_phantom(spec):
         ftype[i] = 0 if f["type"] == "uniform" else 1
         flev[i] = int(f.get("levels", 64))
         fval[i] = float(f.get("value", 0.0))
+    arrays = (shape, center, half, radius, axes, ftype, flev, fval)
+    head = (nx, ny, nz, 0 if bg["type"] == "constant" else 1, float(bg.get("value", 0.0)),
+            float(bg.get("mean", 0.0)), float(bg.get("sigma", 1.0)), len(regions))
+    return head, arrays, int(spec.get("rng_seed", 0)), Hs
+
+
+def make_phantom(spec):
+    """make_phantom (py_module.cpp:96-112): spec is PhantomSpec JSON text or a dict
+    (phantom.cpp:226-277). Returns (array[z,y,x], regions[{center, H}])."""
+    head, arrays, seed, Hs = _phantom_args(spec)
+    nx, ny, nz, nreg = head[0], head[1], head[2], head[7]
     out = np.empty((nz, ny, nx), np.float32)
-    cent = np.zeros(3 * n)
-    check(_lib.load().salvox_make_phantom(
-        nx, ny, nz, 0 if bg["type"] == "constant" else 1, float(bg.get("value", 0.0)),
-        float(bg.get("mean", 0.0)), float(bg.get("sigma", 1.0)), len(regions), ptr(shape),
-        ptr(center), ptr(half), ptr(radius), ptr(axes), ptr(ftype), ptr(flev), ptr(fval),
-        int(spec.get("rng_seed", 0)), ptr(out), ptr(cent)))
-    gt = [{"center": tuple(cent[3 * i:3 * i + 3]), "H": Hs[i]} for i in range(len(regions))]
+    cent = np.zeros(3 * max(nreg, 1))
+    check(_lib.load().salvox_make_phantom(*head, *(ptr(a) for a in arrays), seed, ptr(out), ptr(cent)))
+    gt = [{"center": tuple(cent[3 * i:3 * i + 3]), "H": Hs[i]} for i in range(nreg)]
+    return out, gt
+
+
+def make_phantom_device(spec, device=0, out=None, ctx=None):
+    """make_phantom generated on the GPU -> (torch CUDA
+    tensor [z, y, x] float32, regions). Integer / constant fills are
+    bit-identical to make_phantom; a gaussian background may differ in the last
+    float place. `out` may be a preallocated contiguous CUDA float32 tensor."""
+    import torch
+
+    head, arrays, seed, Hs = _phantom_args(spec)
+    nx, ny, nz, nreg = head[0], head[1], head[2], head[7]
+    if out is None:
+        out = torch.empty((nz, ny, nx), dtype=torch.float32, device=torch.device("cuda", device))
+    elif (tuple(out.shape) != (nz, ny, nx) or out.dtype != torch.float32 or not out.is_cuda
+          or not out.is_contiguous()):
+        raise ValueError("make_phantom_device: out must be a contiguous CUDA float32 [z, y, x] tensor")
+    cent = np.zeros(3 * max(nreg, 1))
+    check(_lib.load().salvox_make_phantom_device(_ctx(ctx).handle, *head,
+                                                 *(ptr(a) for a in arrays), seed,
+                                                 C.c_void_p(out.data_ptr()), ptr(cent)))
+    gt = [{"center": tuple(cent[3 * i:3 * i + 3]), "H": Hs[i]} for i in range(nreg)]
     return out, gt

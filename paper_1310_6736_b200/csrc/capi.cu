@@ -128,33 +128,12 @@ extern "C" int salvox_make_phantom(int32_t nx, int32_t ny, int32_t nz, int32_t b
     std::vector<uint8_t> occupied(n, 0);
     const int dims[3] = {nx, ny, nz};
     for (int ri = 0; ri < n_regions; ++ri) {
-      const double* c = center + 3 * ri;
-      const double* half = half_extents + 3 * ri;
-      Mat3 H{};
-      if (shape[ri] == 0) {  // half.cwiseProduct(half).asDiagonal()
-        H.m[0] = half[0] * half[0];
-        H.m[4] = half[1] * half[1];
-        H.m[8] = half[2] * half[2];
-      } else if (shape[ri] == 1) {  // Identity() * r * r
-        H.m[0] = H.m[4] = H.m[8] = (1.0 * radius[ri]) * radius[ri];
-      } else {  // axes * axes^T
-        const double* a = axes + 9 * ri;
-        for (int i = 0; i < 3; ++i)
-          for (int j = 0; j < 3; ++j)
-            H.m[i * 3 + j] = (a[i * 3] * a[j * 3] + a[i * 3 + 1] * a[j * 3 + 1]) + a[i * 3 + 2] * a[j * 3 + 2];
-      }
-      double ext[3];
-      for (int i = 0; i < 3; ++i)
-        ext[i] = shape[ri] == 0 ? half[i] : std::sqrt(std::max(H.m[i * 4], 0.0));
-      for (int i = 0; i < 3; ++i)
-        if (c[i] - ext[i] < 0.0 || c[i] + ext[i] > dims[i] - 1)
-          fail(SALVOX_ERUNTIME, "make_phantom: region extends outside the volume");
-      const Mat3 Hi = shape[ri] == 0 ? Mat3{} : eigen_inverse(H);
-      int lo[3], hi[3];
-      for (int i = 0; i < 3; ++i) {
-        lo[i] = std::max(0, (int)std::floor(c[i] - ext[i]));
-        hi[i] = std::min(dims[i] - 1, (int)std::ceil(c[i] + ext[i]));
-      }
+      const PhRegion g = phantom_region(ri, dims, shape, center, half_extents, radius, axes);
+      const double* c = g.c;
+      const double* half = g.half;
+      const Mat3& Hi = g.Hi;
+      const int* lo = g.lo;
+      const int* hi = g.hi;
       double cs[3] = {0, 0, 0};
       uint64_t cnt = 0;
       for (int z = lo[2]; z <= hi[2]; ++z)

@@ -162,4 +162,49 @@ inline void plan_seeds(int nx, int ny, int nz, int mode, double spacing, int cou
     for (int s = 0; s < n_scales; ++s) out.push_back({{p[0], p[1], p[2]}, scales[s]});
 }
 
+
+// One phantom region's rasterisation geometry (phantom.cpp:198-222 region_H /
+// region_extents, :252-271 the checks and bounding box), shared by the host
+// generator (capi.cu) and the device one (ingest.cu).
+struct PhRegion {
+  int shape;            // 0 box, 1 ball, 2 ellipsoid
+  double c[3], half[3];
+  Mat3 Hi;              // H^-1 (Eigen 3x3 inverse); unused for boxes
+  int lo[3], hi[3];     // inclusive bounding box
+};
+
+inline PhRegion phantom_region(int ri, const int dims[3], const int32_t* shape, const double* center,
+                               const double* half_extents, const double* radius,
+                               const double* axes) {
+  PhRegion g{};
+  g.shape = shape[ri];
+  const double* c = center + 3 * ri;
+  const double* half = half_extents + 3 * ri;
+  for (int i = 0; i < 3; ++i) g.c[i] = c[i], g.half[i] = half[i];
+  Mat3 H{};
+  if (g.shape == 0) {  // half.cwiseProduct(half).asDiagonal()
+    H.m[0] = half[0] * half[0];
+    H.m[4] = half[1] * half[1];
+    H.m[8] = half[2] * half[2];
+  } else if (g.shape == 1) {  // Identity() * r * r
+    H.m[0] = H.m[4] = H.m[8] = (1.0 * radius[ri]) * radius[ri];
+  } else {  // axes * axes^T
+    const double* a = axes + 9 * ri;
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j)
+        H.m[i * 3 + j] = (a[i * 3] * a[j * 3] + a[i * 3 + 1] * a[j * 3 + 1]) + a[i * 3 + 2] * a[j * 3 + 2];
+  }
+  double ext[3];
+  for (int i = 0; i < 3; ++i) ext[i] = g.shape == 0 ? half[i] : std::sqrt(std::max(H.m[i * 4], 0.0));
+  for (int i = 0; i < 3; ++i)
+    if (c[i] - ext[i] < 0.0 || c[i] + ext[i] > dims[i] - 1)
+      fail(SALVOX_ERUNTIME, "make_phantom: region extends outside the volume");
+  g.Hi = g.shape == 0 ? Mat3{} : eigen_inverse(H);
+  for (int i = 0; i < 3; ++i) {
+    g.lo[i] = std::max(0, (int)std::floor(c[i] - ext[i]));
+    g.hi[i] = std::min(dims[i] - 1, (int)std::ceil(c[i] + ext[i]));
+  }
+  return g;
+}
+
 }  // namespace sx

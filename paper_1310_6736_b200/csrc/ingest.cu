@@ -7,6 +7,7 @@
 // of these integer types is exact, so the result is bit-identical.
 #include "../../include/salvox_capi.h"
 #include "common.cuh"
+#include "host_math.h"
 
 namespace sx {
 
@@ -362,5 +363,246 @@ extern "C" int salvox_hu_template_distance(salvox_ctx* ctx, const float* volume,
     for (int64_t i = 0; i < n; ++i)
       out_dist[i] = used[(size_t)i] == 0 ? std::numeric_limits<double>::infinity()
                                          : sum[(size_t)i] / used[(size_t)i];
+  });
+}
+
+// ------------------------------------------------------------------ phantoms
+// make_phantom on the device (reference src/phantom.cpp:
+// 237-294, include/salvox/rng.hpp). splitmix64 is counter-based -- draw j of a
+// generator seeded s is mix(s + (j + 1) * golden) -- so every voxel's draws
+// are computable in parallel once the draws before it are counted:
+//  * gaussian background: voxel i takes Box-Muller pair i / 2 (draws 2k, 2k+1),
+//    the cosine for even i and the sine for odd i (the reference's spare);
+//  * region r (bounding box in z -> y -> x order, like the reference's loops):
+//    pass 1 counts the inside voxels of every box row (one warp per row), an
+//    exclusive scan gives each row's first rank, pass 2 writes each inside
+//    voxel with draw (background draws + earlier uniform regions + its rank).
+// Every fp64 step uses the reference's operation order without contraction;
+// integer fills and constant values are bit-identical to the host generator;
+// the gaussian background uses libdevice log/sin/cos (<= 2 ulp in fp64), so a
+// float can differ from the glibc one in the last place, rarely.
+namespace sx {
+
+constexpr uint64_t kGolden = 0x9e3779b97f4a7c15ULL;
+
+__device__ __forceinline__ uint64_t sm_draw(uint64_t seed, unsigned long long j) {
+  uint64_t z = seed + (uint64_t)(j + 1ull) * kGolden;  // rng.hpp:16
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+__device__ __forceinline__ double sm_unit(uint64_t x) { return (double)(x >> 11) * 0x1.0p-53; }
+
+struct PhDev {
+  int shape;
+  double c[3], half[3], Hi[9];
+  int lo[3], hi[3];
+};
+
+__device__ __forceinline__ bool ph_inside(const PhDev& g, int x, int y, int z) {
+  const double d0 = (double)x - g.c[0], d1 = (double)y - g.c[1], d2 = (double)z - g.c[2];
+  if (g.shape == 0) return fabs(d0) <= g.half[0] && fabs(d1) <= g.half[1] && fabs(d2) <= g.half[2];
+  double hd[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+    hd[i] = __dadd_rn(__dadd_rn(__dmul_rn(g.Hi[i * 3], d0), __dmul_rn(g.Hi[i * 3 + 1], d1)),
+                      __dmul_rn(g.Hi[i * 3 + 2], d2));
+  return __dadd_rn(__dadd_rn(__dmul_rn(d0, hd[0]), __dmul_rn(d1, hd[1])), __dmul_rn(d2, hd[2])) <= 1.0;
+}
+
+__global__ void ph_bg_kernel(float* __restrict__ v, long long n, int type, float cval, double mean,
+                             double sigma, uint64_t seed, unsigned* err) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long t0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (type == 0) {
+    for (long long i = t0; i < n; i += stride) v[i] = cval;
+    return;
+  }
+  for (long long k = t0; 2 * k < n; k += stride) {
+    const double u1 = sm_unit(sm_draw(seed, 2ull * k)), u2 = sm_unit(sm_draw(seed, 2ull * k + 1ull));
+    if (!(u1 > 0.0)) {  // the reference redraws u1 (rng.hpp:39): a 2^-53 event per pair
+      atomicOr(err, 1u);
+      continue;
+    }
+    const double r = sqrt(__dmul_rn(-2.0, log(u1)));
+    const double theta = __dmul_rn(6.283185307179586476925286766559, u2);
+    v[2 * k] = (float)__dadd_rn(mean, __dmul_rn(sigma, __dmul_rn(r, cos(theta))));
+    if (2 * k + 1 < n) v[2 * k + 1] = (float)__dadd_rn(mean, __dmul_rn(sigma, __dmul_rn(r, sin(theta))));
+  }
+}
+
+// pass 1: inside voxels per bounding-box row (one warp per row)
+__global__ void ph_count_kernel(PhDev g, long long rows, unsigned long long* __restrict__ row_cnt) {
+  const int lane = threadIdx.x & 31;
+  const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (w >= rows) return;
+  const int ny_r = g.hi[1] - g.lo[1] + 1;
+  const int y = g.lo[1] + (int)(w % ny_r), z = g.lo[2] + (int)(w / ny_r);
+  unsigned long long cnt = 0;
+  for (int x0 = g.lo[0]; x0 <= g.hi[0]; x0 += 32) {
+    const int x = x0 + lane;
+    const bool in = x <= g.hi[0] && ph_inside(g, x, y, z);
+    cnt += (unsigned)__popc(__ballot_sync(0xffffffffu, in));
+  }
+  if (lane == 0) row_cnt[w] = cnt;
+}
+
+__global__ void ph_total_kernel(const unsigned long long* base, const unsigned long long* cnt,
+                                long long rows, unsigned long long* total) {
+  *total = base[rows - 1] + cnt[rows - 1];
+}
+
+// pass 2: write every inside voxel; per-region centroid sums (exact integers)
+__global__ void ph_write_kernel(PhDev g, long long rows, const unsigned long long* __restrict__ row_base,
+                                float* __restrict__ v, int nx, int ny, unsigned* __restrict__ occ,
+                                int uniform, uint64_t levels, float cval, uint64_t seed,
+                                unsigned long long draw0, unsigned long long* sums, unsigned* flag) {
+  const int lane = threadIdx.x & 31;
+  const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (w >= rows) return;
+  const int ny_r = g.hi[1] - g.lo[1] + 1;
+  const int y = g.lo[1] + (int)(w % ny_r), z = g.lo[2] + (int)(w / ny_r);
+  unsigned long long rank = row_base[w];
+  unsigned long long sx = 0, sy = 0, sz = 0;
+  bool overlap = false;
+  for (int x0 = g.lo[0]; x0 <= g.hi[0]; x0 += 32) {
+    const int x = x0 + lane;
+    const bool in = x <= g.hi[0] && ph_inside(g, x, y, z);
+    const unsigned m = __ballot_sync(0xffffffffu, in);
+    if (in) {
+      const unsigned long long idx = (unsigned long long)x + (unsigned long long)nx * ((unsigned long long)y + (unsigned long long)ny * z);
+      const unsigned bit = 1u << (idx & 31);
+      if (atomicOr(occ + (idx >> 5), bit) & bit) overlap = true;  // "regions overlap" (phantom.cpp:278)
+      const unsigned long long r = rank + (unsigned)__popc(m & ((1u << lane) - 1u));
+      v[idx] = uniform ? (float)(sm_draw(seed, draw0 + r) % levels) : cval;
+      sx += (unsigned)x;
+      sy += (unsigned)y;
+      sz += (unsigned)z;
+    }
+    rank += (unsigned)__popc(m);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    sx += __shfl_xor_sync(0xffffffffu, sx, o);
+    sy += __shfl_xor_sync(0xffffffffu, sy, o);
+    sz += __shfl_xor_sync(0xffffffffu, sz, o);
+  }
+  if (__any_sync(0xffffffffu, overlap) && lane == 0) atomicOr(flag, 1u);
+  if (lane == 0 && (sx | sy | sz)) {
+    atomicAdd(sums + 0, sx);
+    atomicAdd(sums + 1, sy);
+    atomicAdd(sums + 2, sz);
+  }
+}
+
+}  // namespace sx
+
+extern "C" int salvox_make_phantom_device(salvox_ctx* ctx, int32_t nx, int32_t ny, int32_t nz,
+                                          int32_t bg_type, double bg_value, double bg_mean,
+                                          double bg_sigma, int32_t n_regions, const int32_t* shape,
+                                          const double* center, const double* half_extents,
+                                          const double* radius, const double* axes,
+                                          const int32_t* fill_type, const int32_t* fill_levels,
+                                          const double* fill_value, uint64_t rng_seed, float* d_volume,
+                                          double* out_centroids) {
+  return guarded([&] {
+    if (!ctx) fail(SALVOX_EINVAL, "null context");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (nx < 1 || ny < 1 || nz < 1) fail(SALVOX_EINVAL, "Volume: dims must be >= 1");
+    if (!d_volume) fail(SALVOX_EINVAL, "make_phantom (device): null output");
+    if (bg_type == 1 && !(bg_sigma > 0.0)) fail(SALVOX_ERUNTIME, "background.sigma must be > 0");
+    const long long n = (long long)nx * ny * nz;
+    const int dims[3] = {nx, ny, nz};
+    // geometry on the host; an out-of-volume region is reported in region order
+    // (after the overlap / empty checks of the regions before it), like the
+    // reference's single pass
+    std::vector<PhDev> geo(n_regions);
+    std::vector<std::string> outside(n_regions);
+    std::vector<long long> rows(n_regions, 0);
+    for (int r = 0; r < n_regions; ++r) {
+      try {
+        const PhRegion g = phantom_region(r, dims, shape, center, half_extents, radius, axes);
+        PhDev& d = geo[r];
+        d.shape = g.shape;
+        for (int i = 0; i < 3; ++i) d.c[i] = g.c[i], d.half[i] = g.half[i], d.lo[i] = g.lo[i], d.hi[i] = g.hi[i];
+        for (int i = 0; i < 9; ++i) d.Hi[i] = g.Hi.m[i];
+        rows[r] = (long long)(g.hi[1] - g.lo[1] + 1) * (g.hi[2] - g.lo[2] + 1);
+      } catch (const Error& e) {
+        outside[r] = e.what();
+      }
+      if (fill_type[r] == 0 && fill_levels[r] < 1) fail(SALVOX_ERUNTIME, "fill.levels must be >= 1");
+    }
+    long long total_rows = 0;
+    for (long long x : rows) total_rows += x;
+    // scratch: occupancy bits | row counts | row bases | per-region {sums[3], total, flag}
+    const size_t occ_words = (size_t)(n + 31) / 32;
+    const size_t bytes = occ_words * 4 + 16 + (size_t)total_rows * 16 + (size_t)std::max(n_regions, 1) * 48 + 64;
+    char* base = static_cast<char*>(ctx->d_sel_c.ensure(bytes));
+    unsigned* occ = reinterpret_cast<unsigned*>(base);
+    unsigned long long* row_cnt = reinterpret_cast<unsigned long long*>(base + ((occ_words * 4 + 15) & ~(size_t)15));
+    unsigned long long* row_base = row_cnt + total_rows;
+    unsigned long long* per = row_base + total_rows;  // 6 words per region: sx sy sz total flag pad
+    unsigned* err = reinterpret_cast<unsigned*>(per + 6 * std::max(n_regions, 1));
+    SX_CUDA(cudaMemsetAsync(occ, 0, occ_words * 4, ctx->stream));
+    SX_CUDA(cudaMemsetAsync(per, 0, (size_t)std::max(n_regions, 1) * 48 + 8, ctx->stream));
+    {
+      const int block = 256;
+      const long long work = bg_type == 0 ? n : (n + 1) / 2;
+      const int grid = (int)std::max<long long>(1, std::min<long long>((work + block - 1) / block, ctx->sm_count * 8LL));
+      ph_bg_kernel<<<grid, block, 0, ctx->stream>>>(d_volume, n, bg_type, (float)bg_value, bg_mean, bg_sigma,
+                                                    rng_seed, err);
+      SX_LAUNCH_CHECK(ctx);
+    }
+    // pass 1 + scan for every region
+    long long off = 0;
+    for (int r = 0; r < n_regions; ++r) {
+      if (!outside[r].empty() || rows[r] == 0) continue;
+      unsigned long long* cnt = row_cnt + off;
+      unsigned long long* bas = row_base + off;
+      const int grid = (int)((rows[r] * 32 + 255) / 256);
+      ph_count_kernel<<<grid, 256, 0, ctx->stream>>>(geo[r], rows[r], cnt);
+      SX_LAUNCH_CHECK(ctx);
+      size_t tmp = 0;
+      SX_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, bas, (int)rows[r], ctx->stream));
+      void* d_tmp = ctx->d_cub.ensure(tmp);
+      SX_CUDA(cub::DeviceScan::ExclusiveSum(d_tmp, tmp, cnt, bas, (int)rows[r], ctx->stream));
+      ph_total_kernel<<<1, 1, 0, ctx->stream>>>(bas, cnt, rows[r], per + 6 * r + 3);
+      SX_LAUNCH_CHECK(ctx);
+      off += rows[r];
+    }
+    std::vector<unsigned long long> h_per((size_t)std::max(n_regions, 1) * 6);
+    SX_CUDA(cudaMemcpyAsync(h_per.data(), per, h_per.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    SX_CUDA(cudaStreamSynchronize(ctx->stream));
+    // pass 2: draw bases in region order
+    unsigned long long draw = bg_type == 1 ? 2ull * (unsigned long long)((n + 1) / 2) : 0ull;
+    off = 0;
+    for (int r = 0; r < n_regions; ++r) {
+      if (!outside[r].empty()) break;  // the reference stops at this region
+      if (rows[r] == 0) continue;
+      const int grid = (int)((rows[r] * 32 + 255) / 256);
+      const bool uni = fill_type[r] == 0;
+      ph_write_kernel<<<grid, 256, 0, ctx->stream>>>(
+          geo[r], rows[r], row_base + off, d_volume, nx, ny, occ, uni ? 1 : 0,
+          uni ? (uint64_t)fill_levels[r] : 1ull, (float)fill_value[r], rng_seed, draw, per + 6 * r,
+          reinterpret_cast<unsigned*>(per + 6 * r + 4));
+      SX_LAUNCH_CHECK(ctx);
+      if (uni) draw += h_per[6 * r + 3];
+      off += rows[r];
+    }
+    unsigned h_err = 0;
+    SX_CUDA(cudaMemcpyAsync(h_per.data(), per, h_per.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    SX_CUDA(cudaMemcpyAsync(&h_err, err, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    SX_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (int r = 0; r < n_regions; ++r) {  // the reference's error order
+      if (!outside[r].empty()) fail(SALVOX_ERUNTIME, outside[r]);
+      if (h_per[6 * r + 4]) fail(SALVOX_ERUNTIME, "make_phantom: regions overlap");
+      if (h_per[6 * r + 3] == 0) fail(SALVOX_ERUNTIME, "make_phantom: region rasterizes to no voxel");
+    }
+    if (h_err & 1u)
+      fail(SALVOX_EUNSUPPORTED,
+           "make_phantom (device): a Box-Muller pair drew u1 == 0 (the reference redraws; 2^-53 event)");
+    if (out_centroids)
+      for (int r = 0; r < n_regions; ++r)
+        for (int i = 0; i < 3; ++i) out_centroids[3 * r + i] = (double)h_per[6 * r + i] / (double)h_per[6 * r + 3];
   });
 }
