@@ -7,4 +7,4 @@ for l in open('gpurun_out/q3_bench.log'):
     if l.startswith('{'):
         d=json.loads(l); print('kb_ms', d['roofline']['kb_ms_per_launch'], 'ms/step', d['ms_per_step'])
 P
-if [ "${NCU:-0}" = 1 ]; then timeout 600 ncu --section WarpStateStats --section SchedulerStats --section InstructionStats --metrics l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed,smsp__inst_executed.sum --clock-control none --kernel-name regex:kb_quad_kernel --launch-skip 1 --launch-count 1 -o gpurun_out/quad6 python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-seed-grid > gpurun_out/quad6_ncu.log 2>&1; tail -1 gpurun_out/quad6_ncu.log; fi
+if [ "${NCU:-0}" = 1 ]; then timeout 600 ncu --section WarpStateStats --section SchedulerStats --section InstructionStats --metrics l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed,smsp__inst_executed.sum --clock-control none --kernel-name regex:kb_quad_kernel --launch-skip 1 --launch-count 1 --section SourceCounters --import-source on -o gpurun_out/quad6 python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-seed-grid > gpurun_out/quad6_ncu.log 2>&1; tail -1 gpurun_out/quad6_ncu.log; fi
