@@ -10,8 +10,11 @@ evaluations per second (nx*ny*nz*13 per pass).
   python bench.py [--gpus N --steps K --warmup W]            # B200 arm
   python bench.py --impl reference [--steps K --warmup W]     # CPU reference arm
 
-N > 1 runs under torchrun: the volume is z-slab sharded (strong scaling), the
-per-slab maxima meet in one NCCL all-gather (paper_1310_6736_b200/sharding.py).
+N > 1 runs under torchrun with WEAK scaling: every rank owns one C2-sized slab
+(256^3 voxels) of a volume that grows with N -- 256x256x512 at N=2, 256x512x512
+at N=4 and the 512^3 C4 phantom (BASELINE.json configs[3]) at N=8 -- z-slab
+sharded with read-only halos; the per-slab maxima meet in one NCCL all-gather
+(paper_1310_6736_b200/sharding.py), the job's only collective.
 `value` times the device-resident pass (CUDA events on the launching stream,
 L2 flushed between steps, max over ranks); `e2e` times the public API call with
 the pinned host volume in and the maps + maxima out. The roofline denominator is
@@ -40,12 +43,48 @@ METRIC = "voxel-scale entropy evals/sec (exhaustive); 256³ seed-grid volumes/se
 UNIT = "voxel-scale evals/s"
 # the 3D exhaustive kernel the library picks (csrc/exhaustive.cu pick_tile; A/B knob SALVOX_KB_VARIANT)
 KB_KERNEL = {"0": "kb_kernel", "1": "kb_pair_kernel", "2": "kb_tmem_kernel"}.get(
-    os.environ.get("SALVOX_KB_VARIANT", "3"), "kb_quad_kernel")
+    os.environ.get("SALVOX_KB_VARIANT", "4"), "kb_quad_kernel")
 
 
 def c2_spec():
     from tests import phantoms
     return phantoms.config_c2()
+
+
+def weak_spec(world):
+    """The whole-job volume at N ranks: N x 256^3 voxels, so each rank's slab holds
+    as many voxels as the N=1 workload. N=1 is C2 itself and N=8 the C4 512^3
+    phantom; other N stack C2's region layout once per 256^3 block."""
+    from tests import phantoms
+    if world == 1:
+        return phantoms.config_c2()
+    if world == 8:
+        return phantoms.config_c4()
+    dims = {2: [256, 256, 512], 4: [256, 512, 512]}.get(world, [256, 256, 256 * world])
+    base = phantoms.config_c2()
+    regs = []
+    for bz in range(dims[2] // 256):
+        for by in range(dims[1] // 256):
+            for bx in range(dims[0] // 256):
+                for r in base["regions"]:
+                    q = dict(r)
+                    q["center"] = [r["center"][0] + 256 * bx, r["center"][1] + 256 * by,
+                                   r["center"][2] + 256 * bz]
+                    regs.append(q)
+    return {"dims": dims, "background": base["background"], "regions": regs,
+            "rng_seed": base["rng_seed"]}
+
+
+def weak_workload(world, dims):
+    nx, ny, nz = dims
+    if world == 1:
+        return ("exhaustive Kadir-Brady saliency, 256^3 C2 phantom (BASELINE.json configs[1]), "
+                "32 bins, scales 3..15, per-voxel best scale + strict maxima")
+    name = "512^3 C4 phantom (BASELINE.json configs[3])" if world == 8 else \
+        f"{nx}x{ny}x{nz} phantom (C2 regions per 256^3 block)"
+    return (f"exhaustive Kadir-Brady saliency, {name}, z-slab sharded over {world} GPUs "
+            f"(one 256^3-voxel slab per GPU), 32 bins, scales 3..15, per-voxel best scale "
+            f"+ strict maxima")
 
 
 def c3_spec():
@@ -122,7 +161,7 @@ def cpu_sample_run(vol, threads, planes):
                  z_range=(z0, z0 + planes))
     dt = time.perf_counter() - t0
     evals = nx * ny * planes * len(SCALES)
-    return evals / dt, (f"C2 volume, planes z={z0}..{z0 + planes - 1} "
+    return evals / dt, (f"{nx}x{ny}x{nz} volume, planes z={z0}..{z0 + planes - 1} "
                         f"({nx * ny * planes} voxels x 13 scales, {dt:.1f} s)")
 
 
@@ -130,9 +169,10 @@ def run_reference(args, rank, world):
     if rank != 0:
         return
     from paper_1310_6736_b200 import api
-    vol, _ = api.make_phantom(c2_spec())
+    vol, _ = api.make_phantom(weak_spec(world))
     threads = os.cpu_count() or 1
-    planes = max(1, threads // 2)  # ~5-10 s per step on the box's cores
+    # ~5-10 s per step on the box's cores: threads/2 planes of 256^2 voxels
+    planes = max(1, (threads // 2) * 65536 // (vol.shape[1] * vol.shape[2]))
     for _ in range(min(args.warmup, 1)):
         cpu_sample_run(vol, threads, 1)
     vals = []
@@ -145,15 +185,15 @@ def run_reference(args, rank, world):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": total_evals / value * 1e3, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "exhaustive Kadir-Brady, 256^3 C2 phantom, 32 bins, scales 3..15",
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": weak_workload(world, vol.shape[::-1]),
                    "sample_per_step": sample},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "note": "reference C++ is unbuildable here (Eigen3/vendor absent); the literal oracle "
-                "restatement (oracle/salvox_oracle.c, fp64, reference loop order) is timed; "
-                "ms_per_step extrapolates the sample to one full 256^3 pass",
+                "restatement (oracle/salvox_oracle.c, fp64, reference loop order) is timed on "
+                "rank 0's host cores; ms_per_step extrapolates the sample to one full pass",
     }
     print(json.dumps(line), flush=True)
 
@@ -198,7 +238,7 @@ def main():
     ctx = Context(local)
     ctx.set_stream(stream.cuda_stream)
 
-    vol, _ = api.make_phantom(c2_spec())
+    vol, _ = api.make_phantom(weak_spec(world))
     nz, ny, nx = vol.shape
     R = sharding.halo_radius(SCALES)
     z0, z1, zs0, zs1 = sharding.slab_bounds(nz, world, rank, R)
@@ -316,11 +356,10 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
             "data": "synthetic",
-            "config": {"workload": "exhaustive Kadir-Brady saliency, 256^3 C2 phantom "
-                                   "(BASELINE.json configs[1]), 32 bins, scales 3..15, "
-                                   "per-voxel best scale + strict maxima",
+            "config": {"workload": weak_workload(world, (nx, ny, nz)),
+                       "dims": [nx, ny, nz],
                        "voxels": nx * ny * nz, "scales": len(SCALES),
                        "evals_per_pass": total_evals, "parallelism": f"z-slab x{world}",
                        "l2": "flushed between timed steps (256 MiB write)"},

@@ -29,6 +29,7 @@
 #include <array>
 #include <climits>
 #include <cmath>
+#include <map>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -137,6 +138,9 @@ __constant__ KbBound c_bounds[kMaxRadii];
 // kb_quad_kernel: per radius, the ends (in int4 groups of c_offs) of its three
 // class runs (x, y, z); the radius' first run starts at the previous radius' z
 __constant__ int4 c_qruns[kMaxRadii];
+// kb_quad_kernel<DBL>: per radius, two more run ends: the x-adjacent doubles of
+// class 0 and class 1 (see make_plan)
+__constant__ int2 c_qruns2[kMaxRadii];
 
 struct KbParams {
   int nx, ny, nz;   // global dims
@@ -843,6 +847,7 @@ __device__ __forceinline__ void quad_entry_issue(uint32_t p0, uint32_t p1, uint3
 template <int CLS>
 struct QuadGroup {
   uint32_t p0[4], p1[4], m0[4], m1[4], n[4];
+  __device__ __forceinline__ uint32_t ld(const uint8_t* p) { return lds32(p); }
   __device__ __forceinline__ void load(const uint8_t* tb, int4 w) {
     const int e[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
@@ -851,10 +856,10 @@ struct QuadGroup {
       n[k] = (uint32_t)e[k] & 511u;
       const uint8_t* pp = tb + a;
       const uint8_t* pm = tb - a - (CLS ? 4 : 0);
-      p0[k] = lds32(pp);
-      m0[k] = lds32(pm);
-      p1[k] = CLS ? lds32(pp + 4) : 0u;
-      m1[k] = CLS ? lds32(pm + 4) : 0u;
+      p0[k] = ld(pp);
+      m0[k] = ld(pm);
+      p1[k] = CLS ? ld(pp + 4) : 0u;
+      m1[k] = CLS ? ld(pm + 4) : 0u;
     }
   }
 };
@@ -865,6 +870,58 @@ __device__ __forceinline__ void quad_issue(const QuadGroup<CLS>& q, uint32_t c) 
 #pragma unroll
   for (int k = 0; k < 4; ++k)
     quad_entry_issue<NB, G, SP, SM>(q.p0[k], q.p1[k], q.m0[k], q.m1[k], c, q.n[k]);
+}
+
+// A double = two x-adjacent offsets o1, o2 = o1 + (1,0,0) of the same radius
+// run (and their mirrors -o1, -o2): the 4 voxels of a thread need bytes s..s+4
+// of the +side words and bytes 3-s..7-s of the -side words, i.e. TWO words per
+// side for EIGHT updates (a single needs one or two per four). Entry
+// (a << 15) | ((n2 - n1 + 32) << 9) | n1, a = o1 - s; the -side words start at
+// -a - 4. The representative is chosen so that s = o1.x mod 4 is 0 or 1 (the
+// mirror of class 3 is class 0, of class 2 class 1).
+template <int CLS>
+struct QuadDbl {
+  uint32_t p0[4], p1[4], m0[4], m1[4], n1[4], n2[4];
+  __device__ __forceinline__ void load(const uint8_t* tb, int4 w) {
+    const int e[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int a = e[k] >> 15;
+      n1[k] = (uint32_t)e[k] & 511u;
+      n2[k] = n1[k] + (((uint32_t)e[k] >> 9) & 63u) - 32u;
+      const uint8_t* pp = tb + a;
+      const uint8_t* pm = tb - a - 4;
+      p0[k] = lds32(pp);
+      p1[k] = lds32(pp + 4);
+      m0[k] = lds32(pm);
+      m1[k] = lds32(pm + 4);
+    }
+  }
+};
+
+template <int NB, int G, int CLS>
+__device__ __forceinline__ void quad_issue(const QuadDbl<CLS>& q, uint32_t c) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    quad_entry_issue<NB, G, CLS, 4 - CLS>(q.p0[k], q.p1[k], q.m0[k], q.m1[k], c, q.n1[k]);
+    quad_entry_issue<NB, G, CLS + 1, 3 - CLS>(q.p0[k], q.p1[k], q.m0[k], q.m1[k], c, q.n2[k]);
+  }
+}
+
+// One run of the doubles walk (any group type); the next group's table entries
+// are fetched one iteration ahead, like quad_run (fetching two ahead and
+// software-pipelining the bin-word loads were both measured slower, r01).
+template <int NB, int G, class Q>
+__device__ __forceinline__ void quad_run_t(const uint8_t* tb, uint32_t c, int g, int gend) {
+  int4 w = c_offs[g];
+#pragma unroll 1
+  for (; g < gend; ++g) {
+    const int4 wn = c_offs[g + 1];
+    Q q;
+    q.load(tb, w);
+    quad_issue<NB, G>(q, c);
+    w = wn;
+  }
 }
 
 template <int NB, int G, int CLS>
@@ -890,7 +947,17 @@ __device__ __noinline__ void quad_walk(const uint8_t* tb, uint32_t c, int g, int
   quad_run<NB, G, 2>(tb, c, e.y, e.z);
 }
 
-template <int NB, bool DBG>
+template <int NB, int G>
+__device__ __noinline__ void quad_walk_dbl(const uint8_t* tb, uint32_t c, int g, int4 e, int2 d) {
+  quad_run_t<NB, G, QuadGroup<0>>(tb, c, g, e.x);
+  quad_run_t<NB, G, QuadGroup<1>>(tb, c, e.x, e.y);
+  quad_run_t<NB, G, QuadGroup<2>>(tb, c, e.y, e.z);
+  quad_run_t<NB, G, QuadDbl<0>>(tb, c, e.z, d.x);
+  quad_run_t<NB, G, QuadDbl<1>>(tb, c, d.x, d.y);
+}
+
+// DBL: singles + x-adjacent doubles (variant 4, the default) or singles only (3)
+template <int NB, bool DBG, bool DBL>
 __global__ void __launch_bounds__(256, 1)
     kb_quad_kernel(const __grid_constant__ CUtensorMap tmap, const KbParams p) {
   constexpr int TX = 16, TY = 8, TZ = 8, NT = 256, NV = 1024;
@@ -998,13 +1065,24 @@ __global__ void __launch_bounds__(256, 1)
   for (int i = 0; i < n_radii; ++i) {
     const KbBound bd = c_bounds[i];
     const int4 e = c_qruns[i];
-    switch (G) {  // warp-uniform; G = warp % 4 = the warp's SM sub-partition
-      case 0: quad_walk<NB, 0>(tb, cb, g, e); break;
-      case 1: quad_walk<NB, 1>(tb, cb, g, e); break;
-      case 2: quad_walk<NB, 2>(tb, cb, g, e); break;
-      default: quad_walk<NB, 3>(tb, cb, g, e); break;
+    if (DBL) {
+      const int2 d = c_qruns2[i];
+      switch (G) {  // warp-uniform; G = warp % 4 = the warp's SM sub-partition
+        case 0: quad_walk_dbl<NB, 0>(tb, cb, g, e, d); break;
+        case 1: quad_walk_dbl<NB, 1>(tb, cb, g, e, d); break;
+        case 2: quad_walk_dbl<NB, 2>(tb, cb, g, e, d); break;
+        default: quad_walk_dbl<NB, 3>(tb, cb, g, e, d); break;
+      }
+      g = d.y;
+    } else {
+      switch (G) {
+        case 0: quad_walk<NB, 0>(tb, cb, g, e); break;
+        case 1: quad_walk<NB, 1>(tb, cb, g, e); break;
+        case 2: quad_walk<NB, 2>(tb, cb, g, e); break;
+        default: quad_walk<NB, 3>(tb, cb, g, e); break;
+      }
+      g = e.z;
     }
-    g = e.z;
     // ---- boundary: per voxel v, the same arithmetic as kb_tmem_kernel
     __syncwarp();
 #pragma unroll
@@ -1165,15 +1243,19 @@ struct TileCfg {
   bool pair;          // kb_pair_kernel (two voxels per thread, tx = 8)
   bool tmem = false;  // kb_tmem_kernel (1024 threads, snapshots in TMEM)
   bool quad = false;  // kb_quad_kernel (256 threads x 4 voxels, snapshots in TMEM)
+  bool dbl = false;  // kb_quad_kernel<DBL>: x-adjacent offset doubles share bin words
 };
 
 TileCfg pick_tile(int bins, bool two_d) {
   const int nb = bins <= 16 ? 17 : (bins <= 32 ? 33 : 65);
   if (nb == 65) return two_d ? TileCfg{65, 32, 8, 1, false} : TileCfg{65, 8, 8, 4, false};
   // Variants (A/B knob SALVOX_KB_VARIANT; measured at C2 on one B200, r01):
-  //   3 (default, 3D): kb_quad_kernel -- 256 threads x 4 voxels, 4 bins per
+  //   4 (default, 3D): kb_quad_kernel<DBL> -- as 3, plus x-adjacent offset
+  //      doubles of a radius run share their bin words (2 words per side for 8
+  //      updates): bin-word wavefronts 4.21e9 -> 3.05e9 per launch, 64.1 ms
+  //   3: kb_quad_kernel -- 256 threads x 4 voxels, 4 bins per
   //      32-bit word, one PRMT per update builds the atomic's address, snapshots
-  //      in TMEM: 65.6 ms (1.44 smem wavefronts per update; latency-bound on
+  //      in TMEM: 65.6 ms (1.53 smem wavefronts per update; latency-bound on
   //      8 warps/SM, issue active ~49%)
   //   2: kb_tmem_kernel -- 1024 threads, snapshots in TMEM, 70.7 ms (2.03
   //      wavefronts per update, shared pipe 94.5%: the LDS+ATOMS pair bound)
@@ -1182,11 +1264,12 @@ TileCfg pick_tile(int bins, bool two_d) {
   //      registers -> 8 warps/SM, latency-bound, 85.9 ms
   static const int mode = [] {
     const char* e = std::getenv("SALVOX_KB_VARIANT");
-    return e ? std::atoi(e) : 3;
+    return e ? std::atoi(e) : 4;
   }();
   if (mode == 1) return two_d ? TileCfg{nb, 8, 64, 1, true} : TileCfg{nb, 8, 8, 8, true};
   if (mode == 2 && !two_d) return TileCfg{nb, 16, 8, 8, false, true};
   if (mode == 3 && !two_d) return TileCfg{nb, 16, 8, 8, false, false, true};
+  if (mode == 4 && !two_d) return TileCfg{nb, 16, 8, 8, false, false, true, true};
   return two_d ? TileCfg{nb, 32, 16, 1, false} : TileCfg{nb, 8, 8, 8, false};
 }
 
@@ -1210,6 +1293,7 @@ struct Plan {
   std::vector<uint64_t> ball_size;  // |B(r_i)| incl. centre (EvalCounter, :118)
   std::vector<int32_t> qtab;  // kb_quad_kernel: (a << 9) | n per +-o pair, (radius, class) runs
   std::vector<int4> qruns;    // kb_quad_kernel: per radius, the three run ends (int4 groups)
+  std::vector<int2> qruns2;   // kb_quad_kernel<DBL>: per radius, the two doubles run ends
   int R = 0;
 };
 
@@ -1358,8 +1442,83 @@ Plan make_plan(const double* scales, int n_scales, bool two_d, const TileCfg& tc
       pl.qruns.push_back(e);
     }
   }
-  // too large (one int4 of slack for kb_quad_kernel's look-ahead): not used
-  if ((int)pl.qtab.size() + 4 > kMaxOffs) pl.qtab.clear(), pl.qruns.clear();
+  // kb_quad_kernel<DBL>: per radius, the representatives are grouped by row
+  // (z, y); each row's contiguous x segments are cut into x-adjacent doubles
+  // (an odd segment leaves one single, at an x = 0 mod 4 position when it can).
+  // Singles keep the three class runs above, doubles get two more (classes 0, 1).
+  if (tc.dbl) {
+    pl.qtab.clear();
+    pl.qruns.clear();
+    size_t c2 = 0;
+    for (int i = 0; i < NR; ++i) {
+      std::map<std::pair<int, int>, std::vector<int>> rows;  // (z, y) -> x
+      for (; c2 < cand.size() && cand[c2].n <= Nmax[i]; ++c2) {
+        const Off& o = cand[c2];
+        if (o.z > 0 || (o.z == 0 && (o.y > 0 || (o.y == 0 && o.x > 0))))
+          rows[{o.z, o.y}].push_back(o.x);
+      }
+      std::vector<int32_t> runs[5];
+      for (auto& kv : rows) {
+        const int z = kv.first.first, y = kv.first.second;
+        std::vector<int>& xs = kv.second;
+        std::sort(xs.begin(), xs.end());
+        auto single = [&](int x) {
+          int o = z * SZ + y * SY + x;
+          if ((o & 3) == 3) o = -o;
+          const int s = o & 3;
+          runs[s].push_back((int32_t)((uint32_t)(o - s) << 9) | (x * x + y * y + z * z));
+        };
+        auto dbl = [&](int x) {  // o1 = (x, y, z), o2 = (x + 1, y, z)
+          int o1 = z * SZ + y * SY + x;
+          int n1 = x * x + y * y + z * z, n2 = n1 + 2 * x + 1;
+          if ((o1 & 3) >= 2) {  // mirror: (-o2, -o1), class 3 - s
+            o1 = -(o1 + 1);
+            std::swap(n1, n2);
+          }
+          const int s = o1 & 3;
+          runs[3 + s].push_back((int32_t)((uint32_t)(o1 - s) << 15) |
+                                ((n2 - n1 + 32) << 9) | n1);
+        };
+        size_t a = 0;
+        while (a < xs.size()) {
+          size_t b = a + 1;
+          while (b < xs.size() && xs[b] == xs[b - 1] + 1) ++b;
+          size_t one = SIZE_MAX;
+          if ((b - a) % 2) {
+            one = a;
+            for (size_t k = a; k < b; k += 2)
+              if ((xs[k] & 3) == 0) {
+                one = k;
+                break;
+              }
+          }
+          for (size_t k = a; k < b;) {
+            if (k == one) {
+              single(xs[k]);
+              ++k;
+            } else {
+              dbl(xs[k]);
+              k += 2;
+            }
+          }
+          a = b;
+        }
+      }
+      int4 e{};
+      int2 d{};
+      for (int s = 0; s < 5; ++s) {
+        for (int32_t v : runs[s]) pl.qtab.push_back(v);
+        while (pl.qtab.size() % 4) pl.qtab.push_back(s < 3 ? 0 : (32 << 9));  // zero weight
+        const int end = (int)(pl.qtab.size() / 4);
+        if (s == 0) e.x = end; else if (s == 1) e.y = end; else if (s == 2) e.z = end;
+        else if (s == 3) d.x = end; else d.y = end;
+      }
+      pl.qruns.push_back(e);
+      pl.qruns2.push_back(d);
+    }
+  }
+  // too large (two int4 of slack for kb_quad_kernel's look-ahead): not used
+  if ((int)pl.qtab.size() + 8 > kMaxOffs) pl.qtab.clear(), pl.qruns.clear(), pl.qruns2.clear();
   return pl;
 }
 
@@ -1401,7 +1560,8 @@ void dispatch_kb(salvox_ctx* ctx, const TileCfg& tc, const CUtensorMap& map, con
     return;                                                                                  \
   }
   if (tc.quad) {
-    auto k = tc.nb == 17 ? kb_quad_kernel<17, DBG> : kb_quad_kernel<33, DBG>;
+    auto k = tc.dbl ? (tc.nb == 17 ? kb_quad_kernel<17, DBG, true> : kb_quad_kernel<33, DBG, true>)
+                    : (tc.nb == 17 ? kb_quad_kernel<17, DBG, false> : kb_quad_kernel<33, DBG, false>);
     SX_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k<<<grid, 256, smem, ctx->stream>>>(map, kp);
     SX_LAUNCH_CHECK(ctx);
@@ -1439,6 +1599,9 @@ void upload_tables(salvox_ctx* ctx, const Plan& pl, bool quad = false) {
                                     cudaMemcpyHostToDevice, ctx->stream));
     SX_CUDA(cudaMemcpyToSymbolAsync(c_qruns, pl.qruns.data(), pl.qruns.size() * sizeof(int4), 0,
                                     cudaMemcpyHostToDevice, ctx->stream));
+    if (!pl.qruns2.empty())
+      SX_CUDA(cudaMemcpyToSymbolAsync(c_qruns2, pl.qruns2.data(), pl.qruns2.size() * sizeof(int2),
+                                      0, cudaMemcpyHostToDevice, ctx->stream));
   } else
     SX_CUDA(cudaMemcpyToSymbolAsync(c_offs, pl.offs.data(), pl.offs.size() * 4, 0,
                                     cudaMemcpyHostToDevice, ctx->stream));

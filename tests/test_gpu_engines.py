@@ -25,10 +25,11 @@ def test_shift_parity_under_each_engine(engine):
     assert " passed" in r.stdout
 
 
-@pytest.mark.parametrize("variant", ["0", "3"])
+@pytest.mark.parametrize("variant", ["0", "2", "3"])
 def test_exhaustive_kernel_variants_parity(variant):
     """The non-default exhaustive kernels (kb_kernel: 512 threads / register
-    snapshots; kb_quad_kernel: 4 voxels per thread) stay exact: the exhaustive
+    snapshots; kb_tmem_kernel: 1024 threads / TMEM snapshots; kb_quad_kernel
+    without the offset doubles) stay exact: the exhaustive
     parity suites rerun with SALVOX_KB_VARIANT forced."""
     env = dict(os.environ, SALVOX_KB_VARIANT=variant)
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu",
