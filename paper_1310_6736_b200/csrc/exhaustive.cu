@@ -807,6 +807,23 @@ __device__ __forceinline__ uint32_t lds32(const uint8_t* p) {
   return *reinterpret_cast<const uint32_t*>(p);
 }
 
+__device__ __forceinline__ float lg2_ftz(float x) {
+  float r;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+// q += max(c * ta + a * nt, 0) with 32-bit signed factors and a 64-bit sum
+__device__ __forceinline__ void l1_pos_acc(long long& q, int c, int ta, int a, int nt) {
+  asm("{ .reg .s64 x; .reg .pred p;\n\t"
+      "mul.wide.s32 x, %1, %2;\n\t"
+      "mad.wide.s32 x, %3, %4, x;\n\t"
+      "setp.gt.s64 p, x, 0;\n\t"
+      "@p add.s64 %0, %0, x; }"
+      : "+l"(q)
+      : "r"(c), "r"(ta), "r"(a), "r"(nt));
+}
+
 // The first byte of dynamic shared memory sits at shared::cta address
 // (CTA-rank << 24) + 0x400 (1 KB reserved; the kernel checks it). The rank bits
 // ride in bytes 2-3 of c, the 0x400 in the atomic's immediate.
@@ -1085,6 +1102,9 @@ __global__ void __launch_bounds__(256, 1)
     }
     // ---- boundary: per voxel v, the same arithmetic as kb_tmem_kernel
     __syncwarp();
+#ifdef KB_SKIP_BOUNDARY  // profiling knob: the walk alone (results are wrong)
+    continue;
+#endif
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
       // bin b of this voxel's column at hc[b * 64]
@@ -1097,32 +1117,48 @@ __global__ void __launch_bounds__(256, 1)
       uint32_t dom = 0u;
       unsigned long long num = 0ull;
       const uint32_t slot = lane_base + 64u * v + (uint32_t)(32 * older);
+      // one tcgen05.ld wait per voxel: the whole older slot and the live column
+      // are fetched first; then the bins are reduced with independent partial
+      // sums (the boundary was ~30% of the kernel's time with the serial,
+      // branchy per-bin loop: KB_SKIP_BOUNDARY A/B, r01)
+      uint32_t a[NS], cur[NS];
 #pragma unroll
-      for (int c = 0; c < NS; c += 8) {
-        uint32_t a[8], cur[8];
-        tm_ld8(slot + c, a);
+      for (int c = 0; c < NS; c += 8) tm_ld8(slot + c, a + c);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) cur[j] = hc[(1 + c + j) * 64];
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      for (int j = 0; j < NS; ++j) cur[j] = hc[(1 + j) * 64];
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const uint32_t cv = cur[j];
+      for (int c = 0; c < NS; c += 8) tm_st8(slot + c, cur + c);  // the older slot becomes the newest
 #ifndef KB_SKIP_MATH
-          if (2u * cv > T) {
-            dom = cv;
-          } else if (doH && cv) {
-            const float pb = (float)cv * invT;
-            hacc -= pb * __log2f(pb);
-          }
-#endif
-          if (doE) {
-            const unsigned long long x = (unsigned long long)cv * TA[v], y = (unsigned long long)a[j] * T;
-            num += x > y ? x - y : y - x;
-          }
-          if (DBG && v == dbg_v && c + j < p.bins) p.dbg_out[(size_t)i * (p.bins + 1) + c + j] = cv;
+      if (bd.flags & 1) {  // entropy of this radius (warp-uniform)
+        float h4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int j = 0; j < NS; ++j) {
+          const uint32_t cv = cur[j];
+          const bool isd = 2u * cv > T;  // at most one bin; added below with log1p
+          dom = isd ? cv : dom;
+          const float pb = (float)cv * invT;  // >= 1/T >= 2^-22 when cv > 0: no denormals
+          // empty bins: 0 * lg2(1e-30) = 0 (no branch, no NaN)
+          const float t = pb * lg2_ftz(fmaxf(pb, 1e-30f));
+          h4[j & 3] -= isd ? 0.f : t;
         }
-        tm_st8(slot + c, cur);  // the older slot becomes the newest snapshot
+        hacc = (h4[0] + h4[1]) + (h4[2] + h4[3]);
       }
+#endif
+      if (doE) {
+        // L1 numerator sum_b |S_b(hi) T_lo - S_b(lo) T_hi| exactly: the signed
+        // terms sum to T_hi T_lo - T_lo T_hi = 0, so it is twice their positive part
+        long long q0 = 0, q1 = 0;  // all factors < 2^22: 32-bit signed operands, 64-bit products
+        const int ta = (int)TA[v], nt = -(int)T;
+#pragma unroll
+        for (int j = 0; j < NS; ++j) {
+          if (j & 1) l1_pos_acc(q1, (int)cur[j], ta, (int)a[j], nt);
+          else l1_pos_acc(q0, (int)cur[j], ta, (int)a[j], nt);
+        }
+        num = 2ull * (unsigned long long)(q0 + q1);
+      }
+      if (DBG && v == dbg_v)
+        for (int j = 0; j < NS && j < p.bins; ++j) p.dbg_out[(size_t)i * (p.bins + 1) + j] = cur[j];
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       if (doH && dom) {
         const float pb = (float)dom * invT;
