@@ -1129,33 +1129,45 @@ __global__ void __launch_bounds__(256, 1)
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
       for (int c = 0; c < NS; c += 8) tm_st8(slot + c, cur + c);  // the older slot becomes the newest
-#ifndef KB_SKIP_MATH
-      if (bd.flags & 1) {  // entropy of this radius (warp-uniform)
+      {
+        // per bin: the entropy term (radii that are scales) and the exact L1 term
+        // (radii s+1), branch-free inside chunks of 8 bins; a chunk empty at r in
+        // every lane of the warp is empty at r - 2 too (S_b grows with r) and
+        // contributes nothing: one warp vote skips it (the high bins of a
+        // mostly-background warp)
+        const bool wH = bd.flags & 1, wE = bd.flags & 2;  // warp-uniform
         float h4[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-        for (int j = 0; j < NS; ++j) {
-          const uint32_t cv = cur[j];
-          const bool isd = 2u * cv > T;  // at most one bin; added below with log1p
-          dom = isd ? cv : dom;
-          const float pb = (float)cv * invT;  // >= 1/T >= 2^-22 when cv > 0: no denormals
-          // empty bins: 0 * lg2(1e-30) = 0 (no branch, no NaN)
-          const float t = pb * lg2_ftz(fmaxf(pb, 1e-30f));
-          h4[j & 3] -= isd ? 0.f : t;
-        }
-        hacc = (h4[0] + h4[1]) + (h4[2] + h4[3]);
-      }
-#endif
-      if (doE) {
-        // L1 numerator sum_b |S_b(hi) T_lo - S_b(lo) T_hi| exactly: the signed
-        // terms sum to T_hi T_lo - T_lo T_hi = 0, so it is twice their positive part
         long long q0 = 0, q1 = 0;  // all factors < 2^22: 32-bit signed operands, 64-bit products
         const int ta = (int)TA[v], nt = -(int)T;
 #pragma unroll
-        for (int j = 0; j < NS; ++j) {
-          if (j & 1) l1_pos_acc(q1, (int)cur[j], ta, (int)a[j], nt);
-          else l1_pos_acc(q0, (int)cur[j], ta, (int)a[j], nt);
+        for (int c = 0; c < NS; c += 8) {
+          uint32_t orv = 0u;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) orv |= cur[c + j];
+          if (!__any_sync(0xffffffffu, orv != 0u)) continue;
+#pragma unroll
+          for (int j = c; j < c + 8; ++j) {
+            const uint32_t cv = cur[j];
+#ifndef KB_SKIP_MATH
+            if (wH) {
+              const bool isd = 2u * cv > T;  // at most one bin; added below with log1p
+              dom = isd ? cv : dom;
+              const float pb = (float)cv * invT;  // >= 1/T >= 2^-22 when cv > 0: no denormals
+              // empty bins: 0 * lg2(1e-30) = 0 (no branch, no NaN)
+              const float t = pb * lg2_ftz(fmaxf(pb, 1e-30f));
+              h4[j & 3] -= isd ? 0.f : t;
+            }
+#endif
+            // L1 numerator sum_b |S_b(hi) T_lo - S_b(lo) T_hi| exactly: the signed
+            // terms sum to T_hi T_lo - T_lo T_hi = 0, so it is twice their positive part
+            if (wE) {
+              if (j & 1) l1_pos_acc(q1, (int)cv, ta, (int)a[j], nt);
+              else l1_pos_acc(q0, (int)cv, ta, (int)a[j], nt);
+            }
+          }
         }
-        num = 2ull * (unsigned long long)(q0 + q1);
+        if (wH) hacc = (h4[0] + h4[1]) + (h4[2] + h4[3]);
+        if (doE) num = 2ull * (unsigned long long)(q0 + q1);
       }
       if (DBG && v == dbg_v)
         for (int j = 0; j < NS && j < p.bins; ++j) p.dbg_out[(size_t)i * (p.bins + 1) + j] = cur[j];
