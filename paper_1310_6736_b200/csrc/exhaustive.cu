@@ -150,6 +150,7 @@ struct KbParams {
   int n_radii;
   int bins;
   uint32_t tile_bytes;
+  int lag;          // kb_quad_kernel: warps 4-7 start the walk this many cycles late
   float* score;     // planes [zc0, zc1)
   float* best;
   const long long* dbg_vox;  // debug launch: one block per voxel
@@ -1079,6 +1080,11 @@ __global__ void __launch_bounds__(256, 1)
   int g = 0;
   const bool warp_live = __any_sync(0xffffffffu, rowv && gx < p.nx);
   const int n_radii = warp_live ? p.n_radii : 0;
+  if (warp >= 4 && p.lag > 0) {  // offset the two warps of each sub-partition so their
+    // radius boundaries (little shared-pipe work) overlap the other warp's walk
+    const long long t0 = clock64();
+    while (clock64() - t0 < p.lag) __nanosleep(256);
+  }
   for (int i = 0; i < n_radii; ++i) {
     const KbBound bd = c_bounds[i];
     const int4 e = c_qruns[i];
@@ -1171,14 +1177,15 @@ __global__ void __launch_bounds__(256, 1)
       }
       if (DBG && v == dbg_v)
         for (int j = 0; j < NS && j < p.bins; ++j) p.dbg_out[(size_t)i * (p.bins + 1) + j] = cur[j];
-      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       if (doH && dom) {
         const float pb = (float)dom * invT;
         hacc -= pb * (log1pf(-(float)(T - dom) * invT) * 1.4426950408889634f);
       }
       if (DBG && v == dbg_v) p.dbg_out[(size_t)i * (p.bins + 1) + p.bins] = T;
       if (doE) {
-        const double y = ((double)Hb[v] * bd.fac) * ((double)num / ((double)T * (double)TA[v]));
+        // (reciprocal, not a correctly rounded division: y is compared within
+        // the 1e-5 parity tolerance and stored as float)
+        const double y = ((double)Hb[v] * bd.fac) * ((double)num * __drcp_rn((double)T * (double)TA[v]));
         if (y > best[v] || (y == best[v] && y > 0.0 && bd.rank < best_rank[v])) {
           best[v] = y;
           best_s[v] = bd.scale;
@@ -1189,6 +1196,7 @@ __global__ void __launch_bounds__(256, 1)
       TB[v] = T;
       Hb[v] = doH ? fmaxf(hacc, 0.f) : 0.f;
     }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");  // before the next radius' loads
     older ^= 1;
   }
   if (!DBG && rowv) {
@@ -1319,6 +1327,19 @@ TileCfg pick_tile(int bins, bool two_d) {
   if (mode == 3 && !two_d) return TileCfg{nb, 16, 8, 8, false, false, true};
   if (mode == 4 && !two_d) return TileCfg{nb, 16, 8, 8, false, false, true, true};
   return two_d ? TileCfg{nb, 32, 16, 1, false} : TileCfg{nb, 8, 8, 8, false};
+}
+
+// kb_quad_kernel: warps 4-7 start their walk ~10 us late, so each sub-partition's
+// two warps reach their radius boundaries (entropy/L1 math, TMEM snapshots:
+// little shared-pipe work) at different times and the other warp keeps the
+// atomics flowing. C2 sweep (r01, cycles -> ms): 0 53.1, 4k 53.1, 10k 52.0,
+// 20k 51.1, 40k 51.3. A/B knob SALVOX_KB_LAG.
+int kb_lag() {
+  static const int lag = [] {
+    const char* e = std::getenv("SALVOX_KB_LAG");
+    return e ? std::atoi(e) : 20000;
+  }();
+  return lag;
 }
 
 // Dynamic shared memory of one CTA: histogram columns, tile(s), mbarrier.
@@ -1756,6 +1777,7 @@ ExhRun setup_exhaustive(salvox_ctx* ctx, int nx, int ny, int nz, int zs0, int zs
   kp.zc0 = zc0;
   kp.zc1 = zc1;
   kp.R = R;
+  kp.lag = kb_lag();
   kp.Rz = two_d ? 0 : R;
   kp.SY = SY;
   kp.SZ = SZ;
@@ -2177,6 +2199,7 @@ extern "C" int salvox_exhaustive_debug_hist(salvox_ctx* ctx, const int64_t* voxe
     kp.zc0 = std::max(0, st.z0 - 1);
     kp.zc1 = std::min(st.nz, st.z1 + 1);
     kp.R = R;
+  kp.lag = kb_lag();
     kp.Rz = two_d ? 0 : R;
     kp.SY = SY;
     kp.SZ = SZ;
