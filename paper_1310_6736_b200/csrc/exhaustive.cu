@@ -825,6 +825,15 @@ __device__ __forceinline__ void l1_pos_acc(long long& q, int c, int ta, int a, i
       : "r"(c), "r"(ta), "r"(a), "r"(nt));
 }
 
+template <class T>
+__device__ __forceinline__ void rot4(T (&x)[4]) {
+  const T t = x[0];
+  x[0] = x[1];
+  x[1] = x[2];
+  x[2] = x[3];
+  x[3] = t;
+}
+
 // The first byte of dynamic shared memory sits at shared::cta address
 // (CTA-rank << 24) + 0x400 (1 KB reserved; the kernel checks it). The rank bits
 // ride in bytes 2-3 of c, the 0x400 in the atomic's immediate.
@@ -1111,13 +1120,16 @@ __global__ void __launch_bounds__(256, 1)
 #ifdef KB_SKIP_BOUNDARY  // profiling knob: the walk alone (results are wrong)
     continue;
 #endif
-#pragma unroll
+    // one copy of the per-voxel code (instruction cache: the unrolled 4-voxel
+    // boundary was ~10k instructions, stall_no_instruction 7%): the per-voxel
+    // state rotates through slot 0 and is back in place after the 4 voxels
+#pragma unroll 1
     for (int v = 0; v < 4; ++v) {
       // bin b of this voxel's column at hc[b * 64]
       const uint32_t* hc = reinterpret_cast<const uint32_t*>(hist + (v * 4 + G) * PANEL) + col;  // same panel as quad_red
       const uint32_t T = bd.W - hc[0];
       const bool doH = (bd.flags & 1) && T > 0u;
-      const bool doE = (bd.flags & 2) && T > 0u && TA[v] > 0u && TB[v] > 0u;
+      const bool doE = (bd.flags & 2) && T > 0u && TA[0] > 0u && TB[0] > 0u;
       const float invT = doH ? 1.0f / (float)T : 0.f;
       float hacc = 0.f;
       uint32_t dom = 0u;
@@ -1144,7 +1156,7 @@ __global__ void __launch_bounds__(256, 1)
         const bool wH = bd.flags & 1, wE = bd.flags & 2;  // warp-uniform
         float h4[4] = {0.f, 0.f, 0.f, 0.f};
         long long q0 = 0, q1 = 0;  // all factors < 2^22: 32-bit signed operands, 64-bit products
-        const int ta = (int)TA[v], nt = -(int)T;
+        const int ta = (int)TA[0], nt = -(int)T;
 #pragma unroll
         for (int c = 0; c < NS; c += 8) {
           uint32_t orv = 0u;
@@ -1185,16 +1197,22 @@ __global__ void __launch_bounds__(256, 1)
       if (doE) {
         // (reciprocal, not a correctly rounded division: y is compared within
         // the 1e-5 parity tolerance and stored as float)
-        const double y = ((double)Hb[v] * bd.fac) * ((double)num * __drcp_rn((double)T * (double)TA[v]));
-        if (y > best[v] || (y == best[v] && y > 0.0 && bd.rank < best_rank[v])) {
-          best[v] = y;
-          best_s[v] = bd.scale;
-          best_rank[v] = bd.rank;
+        const double y = ((double)Hb[0] * bd.fac) * ((double)num * __drcp_rn((double)T * (double)TA[0]));
+        if (y > best[0] || (y == best[0] && y > 0.0 && bd.rank < best_rank[0])) {
+          best[0] = y;
+          best_s[0] = bd.scale;
+          best_rank[0] = bd.rank;
         }
       }
-      TA[v] = TB[v];
-      TB[v] = T;
-      Hb[v] = doH ? fmaxf(hacc, 0.f) : 0.f;
+      TA[0] = TB[0];
+      TB[0] = T;
+      Hb[0] = doH ? fmaxf(hacc, 0.f) : 0.f;
+      rot4(TA);
+      rot4(TB);
+      rot4(Hb);
+      rot4(best);
+      rot4(best_s);
+      rot4(best_rank);
     }
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");  // before the next radius' loads
     older ^= 1;
