@@ -1,4 +1,4 @@
-for L in 0 4000 10000 20000 40000; do
+for L in ${LAGS:-0 10000 20000 30000}; do
   SALVOX_KB_LAG=$L timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-seed-grid > gpurun_out/lag.log 2>&1
   python - $L <<'P'
 import json, sys
