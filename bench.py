@@ -245,8 +245,6 @@ def main():
     total_evals = float(nx * ny * nz * len(SCALES))
     budget = 10**15
 
-    # live roofline denominator (same GPU, same run)
-    peak_atoms, peak_lds, peak_atoms_only = ctx.probe_smem_peak(64)
 
     # ---- value: device-resident slab, events on the launching stream
     slab_host = torch.from_numpy(np.ascontiguousarray(vol[zs0:zs1])).pin_memory()
@@ -274,6 +272,9 @@ def main():
     for _ in range(args.warmup):
         device_pass()
     torch.cuda.synchronize(dev)
+    # live roofline denominator (same GPU, same run; after the warm-up passes so
+    # the clocks have ramped; best of 3 trials per probe layout)
+    peak_atoms, peak_lds, peak_atoms_only = ctx.probe_smem_peak(64)
     if world > 1:
         dist.barrier()
     ctx.set_profiling(True)

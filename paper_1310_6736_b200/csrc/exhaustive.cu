@@ -814,6 +814,13 @@ __device__ __forceinline__ float lg2_ftz(float x) {
   return r;
 }
 
+// p log2 p of one bin (p >= 2^-22 when the bin is not empty: no denormals; an
+// empty bin gives 0 * lg2(1e-30) = 0 -- no branch, no NaN)
+__device__ __forceinline__ float ent_term(float pb) {
+  const float l = lg2_ftz(pb + 1e-30f);
+  return __fmul_rn(pb, l);
+}
+
 // q += max(c * ta + a * nt, 0) with 32-bit signed factors and a 64-bit sum
 __device__ __forceinline__ void l1_pos_acc(long long& q, int c, int ta, int a, int nt) {
   asm("{ .reg .s64 x; .reg .pred p;\n\t"
@@ -1123,11 +1130,26 @@ __global__ void __launch_bounds__(256, 1)
     // one copy of the per-voxel code (instruction cache: the unrolled 4-voxel
     // boundary was ~10k instructions, stall_no_instruction 7%): the per-voxel
     // state rotates through slot 0 and is back in place after the 4 voxels
+    // The live columns of voxel v + 1 are loaded while voxel v's math runs
+    // (their loads queue behind the other warps' atomics).
+    uint32_t nxt[NS + 1];
+    {
+      const uint32_t* hc = reinterpret_cast<const uint32_t*>(hist + G * PANEL) + col;
+#pragma unroll
+      for (int j = 0; j <= NS; ++j) nxt[j] = hc[j * 64];
+    }
 #pragma unroll 1
     for (int v = 0; v < 4; ++v) {
-      // bin b of this voxel's column at hc[b * 64]
-      const uint32_t* hc = reinterpret_cast<const uint32_t*>(hist + (v * 4 + G) * PANEL) + col;  // same panel as quad_red
-      const uint32_t T = bd.W - hc[0];
+      // bin b of this voxel's column at hc[b * 64] (same panel as quad_red)
+      uint32_t cur[NS];
+#pragma unroll
+      for (int j = 0; j < NS; ++j) cur[j] = nxt[1 + j];
+      const uint32_t T = bd.W - nxt[0];
+      if (v < 3) {
+        const uint32_t* hn = reinterpret_cast<const uint32_t*>(hist + ((v + 1) * 4 + G) * PANEL) + col;
+#pragma unroll
+        for (int j = 0; j <= NS; ++j) nxt[j] = hn[j * 64];
+      }
       const bool doH = (bd.flags & 1) && T > 0u;
       const bool doE = (bd.flags & 2) && T > 0u && TA[0] > 0u && TB[0] > 0u;
       const float invT = doH ? 1.0f / (float)T : 0.f;
@@ -1139,11 +1161,9 @@ __global__ void __launch_bounds__(256, 1)
       // are fetched first; then the bins are reduced with independent partial
       // sums (the boundary was ~30% of the kernel's time with the serial,
       // branchy per-bin loop: KB_SKIP_BOUNDARY A/B, r01)
-      uint32_t a[NS], cur[NS];
+      uint32_t a[NS];
 #pragma unroll
       for (int c = 0; c < NS; c += 8) tm_ld8(slot + c, a + c);
-#pragma unroll
-      for (int j = 0; j < NS; ++j) cur[j] = hc[(1 + j) * 64];
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
       for (int c = 0; c < NS; c += 8) tm_st8(slot + c, cur + c);  // the older slot becomes the newest
@@ -1168,12 +1188,8 @@ __global__ void __launch_bounds__(256, 1)
             const uint32_t cv = cur[j];
 #ifndef KB_SKIP_MATH
             if (wH) {
-              const bool isd = 2u * cv > T;  // at most one bin; added below with log1p
-              dom = isd ? cv : dom;
-              const float pb = (float)cv * invT;  // >= 1/T >= 2^-22 when cv > 0: no denormals
-              // empty bins: 0 * lg2(1e-30) = 0 (no branch, no NaN)
-              const float t = pb * lg2_ftz(fmaxf(pb, 1e-30f));
-              h4[j & 3] -= isd ? 0.f : t;
+              dom = max(dom, cv);  // a bin with 2 S > T (at most one) is redone below
+              h4[j & 3] -= ent_term((float)cv * invT);
             }
 #endif
             // L1 numerator sum_b |S_b(hi) T_lo - S_b(lo) T_hi| exactly: the signed
@@ -1189,8 +1205,9 @@ __global__ void __launch_bounds__(256, 1)
       }
       if (DBG && v == dbg_v)
         for (int j = 0; j < NS && j < p.bins; ++j) p.dbg_out[(size_t)i * (p.bins + 1) + j] = cur[j];
-      if (doH && dom) {
+      if (doH && 2u * dom > T) {  // dominant bin: its term again, accurately (log1p)
         const float pb = (float)dom * invT;
+        hacc += ent_term(pb);
         hacc -= pb * (log1pf(-(float)(T - dom) * invT) * 1.4426950408889634f);
       }
       if (DBG && v == dbg_v) p.dbg_out[(size_t)i * (p.bins + 1) + p.bins] = T;
