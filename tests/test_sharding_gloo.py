@@ -179,3 +179,27 @@ def test_interleave_detections_ragged():
     d["seed_index"] = np.arange(7)
     parts = [np.concatenate([d[r::3], np.zeros(1, sharding.DET_DTYPE)]) for r in range(3)]
     assert list(sharding.interleave_detections(parts, 7)["seed_index"]) == list(range(7))
+
+
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_bench_weak_scaling_slabs(world):
+    """bench.py's N-rank volume (weak scaling): N x 256^3 voxels, every rank's
+    owned slab holds exactly 256^3 voxels; N=1 is C2, N=8 the 512^3 C4 spec."""
+    import bench
+    from paper_1310_6736_b200 import sharding
+    from tests import phantoms
+
+    spec = bench.weak_spec(world)
+    nx, ny, nz = spec["dims"]
+    assert nx * ny * nz == world * 256 ** 3
+    if world == 1:
+        assert spec == phantoms.config_c2()
+    if world == 8:
+        assert spec == phantoms.config_c4()
+    for r in spec["regions"]:  # every region lies inside the volume
+        assert all(0 <= c < d for c, d in zip(r["center"], spec["dims"]))
+    R = sharding.halo_radius(bench.SCALES)
+    for rank in range(world):
+        z0, z1, zs0, zs1 = sharding.slab_bounds(nz, world, rank, R)
+        assert (z1 - z0) * nx * ny == 256 ** 3
+        assert zs0 == max(0, z0 - R - 1) and zs1 == min(nz, z1 + R + 1)
