@@ -275,6 +275,7 @@ def main():
     # live roofline denominator (same GPU, same run; after the warm-up passes so
     # the clocks have ramped; best of 3 trials per probe layout)
     peak_atoms, peak_lds, peak_atoms_only = ctx.probe_smem_peak(64)
+    peak_prmt = ctx.probe_prmt_rate()
     if world > 1:
         dist.barrier()
     ctx.set_profiling(True)
@@ -375,16 +376,18 @@ def main():
                          "updates_per_launch": kb_updates / max(kb_n, 1),
                          "peak_source": "live salvox_probe_smem_peak: the highest shared-memory "
                                         "atomic rate demonstrated on this GPU (ATOMS only, bins "
-                                        "from registers; best of 1-column/1024-thread, "
-                                        "1-column/512-thread and 4-column/256-thread layouts) -- "
-                                        "every update is at least one atomic; not in "
-                                        "MEASURED_PEAKS.json",
+                                        "from registers; best of 3 trials of each of the "
+                                        "1-column/1024-thread, 1-column/512-thread, "
+                                        "4-column/256-thread and kb_quad_kernel-walk-without-"
+                                        "loads layouts) -- every update is at least one atomic; "
+                                        "not in MEASURED_PEAKS.json",
                          "smem_pipe_util_ncu": (prof_d.get("smem_pipe_pct_of_peak_elapsed", 0.0) / 100.0
                                                 if prof_d else None),
                          "smem_wavefronts_per_update_ncu": prof_d.get("wavefronts_per_warp_update"),
                          "pair_peak": peak_atoms,
                          "frac_of_pair_peak": (achieved / peak_atoms) if achieved else None,
-                         "lds_only_peak": peak_lds},
+                         "lds_only_peak": peak_lds,
+                         "atoms_prmt_walk_peak": peak_prmt},
             "gpu_launches": launches,
             "clocks": clk.summary(),
         }

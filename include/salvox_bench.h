@@ -18,6 +18,11 @@ extern "C" {
  * one-atomic-per-update floor of any shared-memory histogram design). */
 SALVOX_API int salvox_probe_smem_peak(salvox_ctx* ctx, int iters, double* atoms_updates_per_s,
                                       double* lds_fetches_per_s, double* atoms_only_per_s);
+/* Of the last salvox_probe_smem_peak call: the ATOMS rate of kb_quad_kernel's
+ * walk with its bin-word loads removed (PRMT-built addresses, panel in the
+ * immediate, 8 warps x 4 columns); it is one of the layouts whose best is
+ * *atoms_only_per_s. */
+SALVOX_API double salvox_probe_prmt_rate(void);
 
 /* Times every exhaustive kb_kernel launch with CUDA events on the launching
  * stream while on (resets the accumulators). */

@@ -125,7 +125,8 @@ EXPORTS = [
     "salvox_hu_moments", "salvox_hu_template_distance",
 ]
 # include/salvox_bench.h
-BENCH_EXPORTS = ["salvox_probe_smem_peak", "salvox_ctx_set_profiling", "salvox_ctx_kernel_time"]
+BENCH_EXPORTS = ["salvox_probe_smem_peak", "salvox_probe_prmt_rate", "salvox_ctx_set_profiling",
+                 "salvox_ctx_kernel_time"]
 
 _lib = None
 _lock = threading.Lock()
@@ -194,6 +195,8 @@ def _declare(L):
     for name in EXPORTS + BENCH_EXPORTS:
         if name not in ("salvox_last_error",):
             getattr(L, name).restype = C.c_int
+    L.salvox_probe_prmt_rate.argtypes = []
+    L.salvox_probe_prmt_rate.restype = _dbl
 
 
 def check(rc):
@@ -245,6 +248,10 @@ class Context:
         check(load().salvox_probe_smem_peak(self._h, int(iters), C.byref(a), C.byref(b),
                                             C.byref(c)))
         return a.value, b.value, c.value
+
+    def probe_prmt_rate(self):
+        """ATOMS rate of kb_quad_kernel's walk minus its bin loads (last probe call)."""
+        return float(load().salvox_probe_prmt_rate())
 
     def close(self):
         if self._h:

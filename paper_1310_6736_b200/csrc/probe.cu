@@ -10,6 +10,8 @@
 #include "../../include/salvox_bench.h"
 #include "common.cuh"
 
+#include <algorithm>
+
 namespace sx {
 
 constexpr int kProbeTable = 2048;
@@ -111,11 +113,77 @@ __global__ void __launch_bounds__(256, 1) smem_probe_quad_kernel(int iters, uint
   out[blockIdx.x * NT + tid] = acc;
 }
 
+// ATOMS only in kb_quad_kernel's exact walk form: 256 threads x 4 columns,
+// 16 panels of 64 columns x 33 bins, the atomic address built by ONE PRMT from
+// a word of 4 bins (here from a register sequence instead of the tile), the
+// panel in the RED's immediate -- the walk without its bin-word loads.
+template <int G, int V>
+__device__ __forceinline__ void probe_prmt_vox(uint32_t wp, uint32_t wm, uint32_t c, uint32_t n) {
+  constexpr uint32_t sel = 0x7604u | (V << 4), imm = 0x400u + (V * 4 + G) * 33 * 256;
+  uint32_t ap, am;
+  asm volatile("prmt.b32 %0, %1, %2, %3;" : "=r"(ap) : "r"(wp), "r"(c), "n"(sel));
+  asm volatile("prmt.b32 %0, %1, %2, %3;" : "=r"(am) : "r"(wm), "r"(c), "n"(sel));
+  asm volatile("red.shared.add.u32 [%0+%2], %1;" ::"r"(ap), "r"(n), "n"(imm));
+  asm volatile("red.shared.add.u32 [%0+%2], %1;" ::"r"(am), "r"(n), "n"(imm));
+}
+
+template <int G>
+__device__ __forceinline__ void probe_prmt_entry(uint32_t wp, uint32_t wm, uint32_t c, uint32_t n) {
+  probe_prmt_vox<G, 0>(wp, wm, c, n);
+  probe_prmt_vox<G, 1>(wp, wm, c, n);
+  probe_prmt_vox<G, 2>(wp, wm, c, n);
+  probe_prmt_vox<G, 3>(wp, wm, c, n);
+}
+
+template <int G>
+__device__ __noinline__ void probe_prmt_walk(int iters, uint32_t c, uint32_t seed) {
+  uint32_t h = seed;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll 1
+    for (int e4 = 0; e4 < kProbeTable / 4; ++e4) {
+      const int4 w = c_probe[e4];
+      const int e[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        h = h * 1664525u + 1013904223u;
+        probe_prmt_entry<G>(h & 0x1f1f1f1fu, (h >> 3) & 0x1f1f1f1fu, c, (uint32_t)e[k] & 511u);
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256, 1) smem_probe_prmt_kernel(int iters, uint32_t* out) {
+  constexpr int NB = 33, NV = 1024;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint32_t* hist = reinterpret_cast<uint32_t*>(smem);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int i = tid; i < NB * NV; i += 256) hist[i] = 0;
+  __syncthreads();
+  const uint32_t hs0 = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  if ((hs0 & 0xffffu) != 0x400u) __trap();  // the immediates assume it (as kb_quad_kernel)
+  const int G = warp & 3, col = lane + 32 * (warp >> 2);
+  const uint32_t c = (hs0 & 0xffff0000u) | (4u * (uint32_t)col);
+  const uint32_t seed = 2654435761u * (uint32_t)(tid + 1) + blockIdx.x;
+  switch (G) {
+    case 0: probe_prmt_walk<0>(iters, c, seed); break;
+    case 1: probe_prmt_walk<1>(iters, c, seed); break;
+    case 2: probe_prmt_walk<2>(iters, c, seed); break;
+    default: probe_prmt_walk<3>(iters, c, seed); break;
+  }
+  __syncthreads();
+  uint32_t acc = 0;
+  for (int i = tid; i < NB * NV; i += 256) acc += hist[i];
+  out[blockIdx.x * 256 + tid] = acc;
+}
+
 }  // namespace sx
 
 using namespace sx;
 
 constexpr int kProbeTrials = 3;
+double g_prmt_probe_rate = 0.0;  // last run's PRMT-walk ATOMS rate (updates/s)
+
+extern "C" double salvox_probe_prmt_rate() { return g_prmt_probe_rate; }
 
 extern "C" int salvox_probe_smem_peak(salvox_ctx* ctx, int iters, double* atoms_updates_per_s,
                                       double* lds_fetches_per_s, double* atoms_only_per_s) {
@@ -194,6 +262,31 @@ extern "C" int salvox_probe_smem_peak(salvox_ctx* ctx, int iters, double* atoms_
         float ms = 0.f;
         SX_CUDA(cudaEventElapsedTime(&ms, a, b));
         const double r = (double)grid * 256 * 4 * iters * 2.0 * kProbeTable / (ms * 1e-3);
+        if (atoms_only_per_s && r > *atoms_only_per_s) *atoms_only_per_s = r;
+      }
+      cudaEventDestroy(a);
+      cudaEventDestroy(b);
+    }
+    {  // kb_quad_kernel's walk without the bin-word loads (PRMT-built addresses)
+      const size_t psmem = (size_t)33 * 1024 * 4;
+      SX_CUDA(cudaFuncSetAttribute(smem_probe_prmt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)psmem));
+      const int grid = ctx->sm_count * 2;
+      smem_probe_prmt_kernel<<<grid, 256, psmem, ctx->stream>>>(1, d_out);
+      SX_LAUNCH_CHECK(ctx);
+      cudaEvent_t a, b;
+      SX_CUDA(cudaEventCreate(&a));
+      SX_CUDA(cudaEventCreate(&b));
+      for (int trial = 0; trial < kProbeTrials; ++trial) {
+        SX_CUDA(cudaEventRecord(a, ctx->stream));
+        smem_probe_prmt_kernel<<<grid, 256, psmem, ctx->stream>>>(iters, d_out);
+        SX_LAUNCH_CHECK(ctx);
+        SX_CUDA(cudaEventRecord(b, ctx->stream));
+        SX_CUDA(cudaEventSynchronize(b));
+        float ms = 0.f;
+        SX_CUDA(cudaEventElapsedTime(&ms, a, b));
+        const double r = (double)grid * 256 * 4 * iters * 2.0 * kProbeTable / (ms * 1e-3);
+        g_prmt_probe_rate = std::max(g_prmt_probe_rate, r);
         if (atoms_only_per_s && r > *atoms_only_per_s) *atoms_only_per_s = r;
       }
       cudaEventDestroy(a);
