@@ -206,8 +206,46 @@ SALVOX_API int salvox_exhaustive_slab_device(salvox_ctx* ctx, const float* d_sla
                                              int32_t kernel, uint64_t budget, float* d_score,
                                              float* d_best_scale, int64_t* n_maxima);
 
+/* z-slab form with a neighbour-plane exchange (multi-GPU; the split of
+ * salvox_exhaustive_slab a rank uses when its neighbours exchange boundary
+ * planes instead of each scoring one extra plane per side -- replaces the same
+ * reference call, src/pipeline.cpp:63-166, for one slab of a sharded volume).
+ * 1) salvox_exhaustive_slab_scores: bins the slab and scores ONLY the owned
+ *    planes [z0, z1); `slab`, `score_out`, `best_scale_out` are host pointers
+ *    (on_device = 0; pipelined H2D/compute/D2H) or device pointers
+ *    (on_device = 1); no maxima yet. Same validation and halo rule as
+ *    salvox_exhaustive_slab; *visits gets the owned planes' EvalCounter share.
+ * 2) salvox_exhaustive_slab_edges: the first and last owned score planes into
+ *    device buffers (nx*ny floats each, nullable) -- what the neighbours need.
+ * 3) salvox_exhaustive_slab_maxima: d_below = plane z0-1 (the lower
+ *    neighbour's last owned plane; required when z0 > 0), d_above = plane z1
+ *    (the upper neighbour's first; required when z1 < nz), device pointers;
+ *    strict maxima of the owned planes, in the reference's order, as
+ *    salvox_exhaustive_slab returns them; maxima == NULL leaves them on the
+ *    device (salvox_last_maxima / salvox_last_maxima_device). */
+SALVOX_API int salvox_exhaustive_slab_scores(salvox_ctx* ctx, const float* slab, int32_t on_device,
+                                             int32_t nx, int32_t ny, int32_t nz, int32_t zs0,
+                                             int32_t zs1, int32_t z0, int32_t z1,
+                                             const salvox_window* iw, const double* scales,
+                                             int32_t n_scales, int32_t kernel, uint64_t budget,
+                                             float* score_out, float* best_scale_out,
+                                             uint64_t* visits);
+SALVOX_API int salvox_exhaustive_slab_edges(salvox_ctx* ctx, float* d_first, float* d_last);
+SALVOX_API int salvox_exhaustive_slab_maxima(salvox_ctx* ctx, const float* d_below,
+                                             const float* d_above, salvox_maximum* maxima,
+                                             int64_t cap, int64_t* n_maxima);
+
 /* Copies the maxima of the last exhaustive call on ctx. */
 SALVOX_API int salvox_last_maxima(salvox_ctx* ctx, salvox_maximum* out, int64_t cap, int64_t* n_out);
+/* Device form: the last call's maxima into a device buffer (D2D). */
+SALVOX_API int salvox_last_maxima_device(salvox_ctx* ctx, salvox_maximum* d_out, int64_t cap,
+                                         int64_t* n_out);
+/* Sorts n maxima records (device) into the reference's order -- score
+ * descending, ties by linear index ascending (the stable_sort of
+ * src/pipeline.cpp:163-164) -- on the device: the merge of the per-slab lists a
+ * multi-GPU run all-gathers. d_in and d_out are device buffers of n records. */
+SALVOX_API int salvox_merge_maxima_device(salvox_ctx* ctx, const salvox_maximum* d_in, int64_t n,
+                                          salvox_maximum* d_out);
 
 /* Exact integer identity-kernel histograms of the last exhaustive call, for
  * `n` voxels (global linear indices in the owned planes) at every needed

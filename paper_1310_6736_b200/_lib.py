@@ -115,7 +115,9 @@ EXPORTS = [
     "salvox_last_error", "salvox_version", "salvox_ctx_create", "salvox_ctx_destroy",
     "salvox_ctx_set_stream", "salvox_ctx_launch_count", "salvox_exhaustive",
     "salvox_exhaustive_slab", "salvox_exhaustive_device", "salvox_exhaustive_slab_device",
-    "salvox_last_maxima",
+    "salvox_exhaustive_slab_scores", "salvox_exhaustive_slab_edges",
+    "salvox_exhaustive_slab_maxima", "salvox_last_maxima", "salvox_last_maxima_device",
+    "salvox_merge_maxima_device",
     "salvox_exhaustive_debug_hist", "salvox_detect", "salvox_detect_batch_device",
     "salvox_detect_shard", "salvox_seek",
     "salvox_select", "salvox_dedupe_top_k", "salvox_plan_seeds", "salvox_make_phantom",
@@ -170,7 +172,14 @@ def _declare(L):
     L.salvox_exhaustive_slab_device.argtypes = [_vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32,
                                                 _i32, C.POINTER(Window), _vp, _i32, _i32, _u64,
                                                 _vp, _vp, _pi64]
+    L.salvox_exhaustive_slab_scores.argtypes = [_vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32,
+                                                _i32, _i32, C.POINTER(Window), _vp, _i32, _i32,
+                                                _u64, _vp, _vp, C.POINTER(_u64)]
+    L.salvox_exhaustive_slab_edges.argtypes = [_vp, _vp, _vp]
+    L.salvox_exhaustive_slab_maxima.argtypes = [_vp, _vp, _vp, _vp, _i64, _pi64]
     L.salvox_last_maxima.argtypes = [_vp, _vp, _i64, _pi64]
+    L.salvox_last_maxima_device.argtypes = [_vp, _vp, _i64, _pi64]
+    L.salvox_merge_maxima_device.argtypes = [_vp, _vp, _i64, _vp]
     L.salvox_exhaustive_debug_hist.argtypes = [_vp, _vp, _i32, _vp, _vp, C.POINTER(_i32)]
     L.salvox_detect.argtypes = [_vp, _vp, _i32, _i32, _i32, C.POINTER(Window),
                                 C.POINTER(DetectParams), _vp, _i64, _pi64, _vp, _i64, _pi64, _pu64]

@@ -150,6 +150,104 @@ def kadir_brady_exhaustive_slab(slab, nz_total, zs0, z0, z1, scales, window_low,
     return score, best, maxima[: n.value], int(visits.value)
 
 
+def exhaustive_slab_scores(slab, nz_total, zs0, z0, z1, scales, window_low, window_high,
+                           bins=64, kernel="identity", budget=DEFAULT_BUDGET, ctx=None, out=None):
+    """Step 1 of the exchange form (salvox_exhaustive_slab_scores): scores ONLY the
+    owned planes [z0, z1). `slab` is a host array (pipelined H2D/compute/D2H;
+    returns host maps, `out` may supply pinned ones) or a CUDA torch tensor
+    (device-resident; returns device tensors). Returns (score, best, visits)."""
+    sc = np.ascontiguousarray(scales, dtype=np.float64)
+    iw = _window(window_low, window_high, bins)
+    if iw.full_range:
+        raise ValueError("exhaustive slab: pass an explicit (global) intensity window")
+    c = _ctx(ctx)
+    visits = C.c_uint64(0)
+    on_device = hasattr(slab, "is_cuda") and slab.is_cuda
+    if on_device:
+        import torch
+        s = slab.contiguous()
+        nzs, ny, nx = s.shape
+        if out is not None:
+            score, best = out
+        else:
+            score = torch.empty((z1 - z0, ny, nx), dtype=torch.float32, device=s.device)
+            best = torch.empty_like(score)
+        sp, op, bp = C.c_void_p(s.data_ptr()), C.c_void_p(score.data_ptr()), C.c_void_p(best.data_ptr())
+    else:
+        s = np.ascontiguousarray(slab, dtype=np.float32)
+        nzs, ny, nx = s.shape
+        if out is not None:
+            score, best = out
+            assert score.shape == best.shape == (z1 - z0, ny, nx)
+        else:
+            score = np.empty((z1 - z0, ny, nx), np.float32)
+            best = np.empty((z1 - z0, ny, nx), np.float32)
+        sp, op, bp = ptr(s), ptr(score), ptr(best)
+    check(_lib.load().salvox_exhaustive_slab_scores(
+        c.handle, sp, 1 if on_device else 0, nx, ny, int(nz_total), int(zs0), int(zs0 + nzs),
+        int(z0), int(z1), C.byref(iw), ptr(sc), len(sc), KERNELS[kernel], int(budget), op, bp,
+        C.byref(visits)))
+    return score, best, int(visits.value)
+
+
+def exhaustive_slab_edges(first, last, ctx=None):
+    """Step 2: the first / last owned score planes into device tensors (nx*ny floats)."""
+    c = _ctx(ctx)
+    check(_lib.load().salvox_exhaustive_slab_edges(
+        c.handle, C.c_void_p(first.data_ptr()) if first is not None else None,
+        C.c_void_p(last.data_ptr()) if last is not None else None))
+
+
+def exhaustive_slab_maxima(below, above, ctx=None, maxima_out=None, on_device=False):
+    """Step 3: strict maxima of the owned planes given the neighbour planes z0-1
+    (`below`) and z1 (`above`) as device tensors (None at the volume ends).
+    on_device=True leaves them on the device and returns their count."""
+    c = _ctx(ctx)
+    if on_device:
+        n = C.c_int64(0)
+        check(_lib.load().salvox_exhaustive_slab_maxima(
+            c.handle, C.c_void_p(below.data_ptr()) if below is not None else None,
+            C.c_void_p(above.data_ptr()) if above is not None else None, None, 0, C.byref(n)))
+        return int(n.value)
+    if maxima_out is not None:
+        maxima = maxima_out
+        cap = len(maxima)
+    else:
+        cap = max(4096, int(_MAXIMA_HINT.get(id(c), 0) * 1.1))
+        maxima = np.empty(cap, MAX_DTYPE)
+    n = C.c_int64(0)
+    check(_lib.load().salvox_exhaustive_slab_maxima(
+        c.handle, C.c_void_p(below.data_ptr()) if below is not None else None,
+        C.c_void_p(above.data_ptr()) if above is not None else None, ptr(maxima), cap,
+        C.byref(n)))
+    _MAXIMA_HINT[id(c)] = n.value
+    if n.value > cap:
+        maxima = np.empty(n.value, MAX_DTYPE)
+        check(_lib.load().salvox_last_maxima(c.handle, ptr(maxima), n.value, C.byref(n)))
+    return maxima[: n.value]
+
+
+def last_maxima_device(out, ctx=None):
+    """The last exhaustive call's maxima into a CUDA uint8 tensor of shape (cap, 48)
+    (salvox_last_maxima_device); returns the full count."""
+    c = _ctx(ctx)
+    n = C.c_int64(0)
+    check(_lib.load().salvox_last_maxima_device(c.handle, C.c_void_p(out.data_ptr()),
+                                                int(out.shape[0]), C.byref(n)))
+    return int(n.value)
+
+
+def merge_maxima_device(records, ctx=None):
+    """Device sort of maxima records (CUDA uint8 tensor (n, 48)) into the reference's
+    order (score desc, linear index asc); returns a new tensor."""
+    import torch
+    c = _ctx(ctx)
+    out = torch.empty_like(records)
+    check(_lib.load().salvox_merge_maxima_device(c.handle, C.c_void_p(records.data_ptr()),
+                                                 int(records.shape[0]), C.c_void_p(out.data_ptr())))
+    return out
+
+
 def exhaustive_debug_hist(voxels, bins, n_scales, ctx=None):
     """Exact S_b(r) / T(r) of the last exhaustive call for the given linear voxel indices.
     Returns (radii, hist[n, n_radii, bins+1] uint32; column `bins` holds T(r))."""

@@ -122,7 +122,7 @@ struct salvox_ctx {
   double kb_updates_total = 0.0;
   // exhaustive path
   sx::DevBuf d_vol, d_bins, d_score, d_best, d_keys, d_keys_alt, d_cub, d_counter, d_maxima,
-      d_minmax, d_dbg;
+      d_merge_idx, d_minmax, d_dbg;
   sx::HostBuf h_stage;       // pinned: the last call's maxima (salvox_last_maxima)
   int64_t last_maxima_n = 0;
   bool stage_valid = false;  // h_stage holds them (else read d_maxima again)

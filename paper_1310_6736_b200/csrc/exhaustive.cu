@@ -1691,9 +1691,17 @@ struct ExhRun {
   TileCfg tc;
   Plan pl;
   CUtensorMap map;
-  KbParams kp;
+  KbParams kp;  // kp.zc0 / zc1: the planes the KB kernel scores
   dim3 grid;
   size_t smem;
+  // the score / best-scale buffers cover planes [zb0, zb1) = the owned planes
+  // plus one neighbour plane each side; without the exchange (the default) the
+  // kernel scores all of them, with it only the owned planes and the caller
+  // supplies the neighbour planes (salvox_exhaustive_slab_maxima)
+  int zb0 = 0, zb1 = 0, z0 = 0, z1 = 0;
+  float* score_base = nullptr;
+  float* best_base = nullptr;
+  bool exch = false;
 };
 
 void upload_tables(salvox_ctx* ctx, const Plan& pl, bool quad = false) {
@@ -1777,7 +1785,7 @@ Plan cached_plan(const double* scales, int n_scales, bool two_d, const TileCfg& 
 // ctx->d_bins, pitch 16-aligned): plan, tensor map, kernel parameters for the
 // scored planes [zc0, zc1) = [z0-1, z1+1) clipped, score/best buffers.
 ExhRun setup_exhaustive(salvox_ctx* ctx, int nx, int ny, int nz, int zs0, int zs1, int z0, int z1,
-                        int bins, const double* scales, int n_scales) {
+                        int bins, const double* scales, int n_scales, bool exch = false) {
   const bool two_d = nz == 1;
   ExhRun run;
   run.tc = pick_tile(bins, two_d);
@@ -1790,10 +1798,18 @@ ExhRun setup_exhaustive(salvox_ctx* ctx, int nx, int ny, int nz, int zs0, int zs
   const int nzs = zs1 - zs0;
   const int pitch = (nx + 15) / 16 * 16;
   uint8_t* d_bins = static_cast<uint8_t*>(ctx->d_bins.ensure((size_t)pitch * ny * nzs));
-  const int zc0 = std::max(0, z0 - 1), zc1 = std::min(nz, z1 + 1);
-  const size_t nscore = (size_t)nx * ny * (zc1 - zc0);
+  const int zb0 = std::max(0, z0 - 1), zb1 = std::min(nz, z1 + 1);
+  const int zc0 = exch ? z0 : zb0, zc1 = exch ? z1 : zb1;
+  const size_t nscore = (size_t)nx * ny * (zb1 - zb0);
   float* d_score = static_cast<float*>(ctx->d_score.ensure(nscore * 4));
   float* d_best = static_cast<float*>(ctx->d_best.ensure(nscore * 4));
+  run.zb0 = zb0;
+  run.zb1 = zb1;
+  run.z0 = z0;
+  run.z1 = z1;
+  run.score_base = d_score;
+  run.best_base = d_best;
+  run.exch = exch;
 
   const int BX = SY, BY = SZ / SY, BZ = run.tc.tz + 2 * R;
   cuuint64_t gdim[3] = {(cuuint64_t)nx, (cuuint64_t)ny, (cuuint64_t)nzs};
@@ -1820,8 +1836,8 @@ ExhRun setup_exhaustive(salvox_ctx* ctx, int nx, int ny, int nz, int zs0, int zs
   kp.n_radii = (int)run.pl.radii.size();
   kp.bins = bins;
   kp.tile_bytes = (uint32_t)(BX * BY * (two_d ? 1 : BZ));
-  kp.score = d_score;
-  kp.best = d_best;
+  kp.score = d_score + (size_t)nx * ny * (zc0 - zb0);
+  kp.best = d_best + (size_t)nx * ny * (zc0 - zb0);
   kp.dbg_vox = nullptr;
   kp.dbg_out = nullptr;
   run.smem = kb_smem(run.tc, kp.tile_bytes);
@@ -1862,9 +1878,9 @@ void launch_kb_chunk(salvox_ctx* ctx, const ExhRun& run, int a, int b) {
 
 // K3: strict maxima of the owned planes + sort + decode. Returns the count.
 long long maxima_and_sort(salvox_ctx* ctx, const ExhRun& run, int z0, int z1) {
-  const int nx = run.kp.nx, ny = run.kp.ny, nz = run.kp.nz, zc0 = run.kp.zc0;
-  const float* d_score = run.kp.score;
-  const float* d_best = run.kp.best;
+  const int nx = run.kp.nx, ny = run.kp.ny, nz = run.kp.nz, zc0 = run.zb0;
+  const float* d_score = run.score_base;
+  const float* d_best = run.best_base;
   const size_t nown = (size_t)nx * ny * (z1 - z0);
   const size_t kcap = nown / 2 + 1;
   unsigned long long* d_keys = static_cast<unsigned long long*>(ctx->d_keys.ensure(kcap * 8));
@@ -1920,8 +1936,8 @@ void remember_run(salvox_ctx* ctx, const ExhRun& run, int nx, int ny, int nz, in
 // Leaves: ctx->d_score/d_best (planes zc0..zc1), sorted keys, count.
 long long run_exhaustive(salvox_ctx* ctx, const float* d_slab, int nx, int ny, int nz, int zs0,
                          int zs1, int z0, int z1, double low, double high, int bins,
-                         const double* scales, int n_scales, ExhRun* run_out) {
-  ExhRun run = setup_exhaustive(ctx, nx, ny, nz, zs0, zs1, z0, z1, bins, scales, n_scales);
+                         const double* scales, int n_scales, ExhRun* run_out, bool exch = false) {
+  ExhRun run = setup_exhaustive(ctx, nx, ny, nz, zs0, zs1, z0, z1, bins, scales, n_scales, exch);
   const int pitch = (nx + 15) / 16 * 16;
   launch_bin_volume(ctx, d_slab, ctx->d_bins.as<uint8_t>(), nx, ny, zs1 - zs0, pitch, low, high,
                     bins);
@@ -1931,7 +1947,7 @@ long long run_exhaustive(salvox_ctx* ctx, const float* d_slab, int nx, int ny, i
     launch_kb_chunk(ctx, run, run.kp.zc0, run.kp.zc1);
     SX_CUDA(cudaEventRecord(g_const_done, ctx->stream));
   }
-  const long long cnt = maxima_and_sort(ctx, run, z0, z1);
+  const long long cnt = exch ? 0 : maxima_and_sort(ctx, run, z0, z1);
   if (run_out) *run_out = run;
   remember_run(ctx, run, nx, ny, nz, zs0, zs1, z0, z1, bins, scales, n_scales);
   return cnt;
@@ -1954,10 +1970,11 @@ cudaEvent_t ctx_event(salvox_ctx* ctx, size_t i) {
 long long run_exhaustive_pipelined(salvox_ctx* ctx, const float* h_slab, int nx, int ny, int nz,
                                    int zs0, int zs1, int z0, int z1, double low, double high,
                                    int bins, const double* scales, int n_scales,
-                                   float* score_out, float* best_out, ExhRun* run_out) {
+                                   float* score_out, float* best_out, ExhRun* run_out,
+                                   bool exch = false) {
   if (!ctx->copy_stream) SX_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
   cudaStream_t cs = ctx->stream, ps = ctx->copy_stream;
-  ExhRun run = setup_exhaustive(ctx, nx, ny, nz, zs0, zs1, z0, z1, bins, scales, n_scales);
+  ExhRun run = setup_exhaustive(ctx, nx, ny, nz, zs0, zs1, z0, z1, bins, scales, n_scales, exch);
   const int R = run.pl.R, tz = run.tc.tz;
   const int nzs = zs1 - zs0;
   const size_t plane = (size_t)nx * ny;
@@ -2011,7 +2028,7 @@ long long run_exhaustive_pipelined(salvox_ctx* ctx, const float* h_slab, int nx,
     if (best_out)
       SX_CUDA(cudaMemcpyAsync(best_out + dst, run.kp.best + src, n * 4, cudaMemcpyDeviceToHost, ps));
   }
-  const long long cnt = maxima_and_sort(ctx, run, z0, z1);
+  const long long cnt = exch ? 0 : maxima_and_sort(ctx, run, z0, z1);
   SX_CUDA(cudaStreamSynchronize(ps));
   if (run_out) *run_out = run;
   remember_run(ctx, run, nx, ny, nz, zs0, zs1, z0, z1, bins, scales, n_scales);
@@ -2084,7 +2101,7 @@ int exhaustive_host(salvox_ctx* ctx, const float* slab, int32_t nx, int32_t ny, 
       if (iw->full_range) device_full_range(ctx, d_vol, nslab, &low, &high);
       cnt = run_exhaustive(ctx, d_vol, nx, ny, nz, zs0, zs1, z0, z1, low, high, iw->bins, scales,
                            n_scales, &run);
-      const size_t off = (size_t)nx * ny * (z0 - run.kp.zc0);
+      const size_t off = (size_t)nx * ny * (z0 - run.zb0);
       if (score_out)
         SX_CUDA(cudaMemcpyAsync(score_out, ctx->d_score.as<float>() + off, nown * 4,
                                 cudaMemcpyDeviceToHost, ctx->stream));
@@ -2144,7 +2161,7 @@ static int exhaustive_device_impl(salvox_ctx* ctx, const float* d_slab, int32_t 
     const long long cnt = run_exhaustive(ctx, d_slab, nx, ny, nz, zs0, zs1, z0, z1, low, high,
                                          iw->bins, scales, n_scales, &run);
     const size_t nown = (size_t)nx * ny * (z1 - z0);
-    const size_t off = (size_t)nx * ny * (z0 - run.kp.zc0);
+    const size_t off = (size_t)nx * ny * (z0 - run.zb0);
     if (d_score)
       SX_CUDA(cudaMemcpyAsync(d_score, ctx->d_score.as<float>() + off, nown * 4,
                               cudaMemcpyDeviceToDevice, ctx->stream));
@@ -2173,6 +2190,183 @@ extern "C" int salvox_exhaustive_slab_device(salvox_ctx* ctx, const float* d_sla
                                              float* d_best_scale, int64_t* n_maxima) {
   return exhaustive_device_impl(ctx, d_slab, nx, ny, nz, zs0, zs1, z0, z1, iw, scales, n_scales,
                                 kernel, budget, d_score, d_best_scale, n_maxima, true);
+}
+
+// ---- z-slab exhaustive with a neighbour-plane exchange (multi-GPU) ----------
+// The default slab call scores its owned planes plus one neighbour plane each
+// side so strict maxima are decided locally; the KB kernel tiles z by 8, so the
+// two extra planes are a nearly-empty extra tile layer (a 64-plane slab of the
+// 512^3 C4 runs 54.3 ms instead of ~49). With the exchange the rank scores only
+// its owned planes and receives the two neighbour planes from the adjacent
+// ranks (one plane each way over NCCL) before the maxima pass.
+namespace {
+std::mutex g_exch_mu;
+std::map<salvox_ctx*, ExhRun> g_exch_runs;  // the pending scores call of each context
+}  // namespace
+
+extern "C" int salvox_exhaustive_slab_scores(salvox_ctx* ctx, const float* slab, int32_t on_device,
+                                             int32_t nx, int32_t ny, int32_t nz, int32_t zs0,
+                                             int32_t zs1, int32_t z0, int32_t z1,
+                                             const salvox_window* iw, const double* scales,
+                                             int32_t n_scales, int32_t kernel, uint64_t budget,
+                                             float* score_out, float* best_scale_out,
+                                             uint64_t* visits) {
+  return guarded([&] {
+    if (!ctx) fail(SALVOX_EINVAL, "null context");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    validate_exhaustive(nx, ny, nz, iw, scales, n_scales, kernel, budget);
+    if (!slab) fail(SALVOX_EINVAL, "null volume");
+    if (!(0 <= zs0 && zs0 <= z0 && z0 < z1 && z1 <= zs1 && zs1 <= nz))
+      fail(SALVOX_EINVAL, "exhaustive slab: need 0 <= zs0 <= z0 < z1 <= zs1 <= nz");
+    if (iw->full_range)
+      fail(SALVOX_EINVAL, "exhaustive slab: pass an explicit (global) intensity window");
+    SX_CUDA(cudaSetDevice(ctx->device));
+    const size_t nown = (size_t)nx * ny * (z1 - z0);
+    ExhRun run;
+    if (!on_device) {
+      run_exhaustive_pipelined(ctx, slab, nx, ny, nz, zs0, zs1, z0, z1, iw->low, iw->high, iw->bins,
+                               scales, n_scales, score_out, best_scale_out, &run, true);
+    } else {
+      run_exhaustive(ctx, slab, nx, ny, nz, zs0, zs1, z0, z1, iw->low, iw->high, iw->bins, scales,
+                     n_scales, &run, true);
+      if (score_out)
+        SX_CUDA(cudaMemcpyAsync(score_out, run.kp.score, nown * 4, cudaMemcpyDeviceToDevice,
+                                ctx->stream));
+      if (best_scale_out)
+        SX_CUDA(cudaMemcpyAsync(best_scale_out, run.kp.best, nown * 4, cudaMemcpyDeviceToDevice,
+                                ctx->stream));
+      SX_CUDA(cudaStreamSynchronize(ctx->stream));  // outputs valid for any stream on return
+    }
+    {
+      std::lock_guard<std::mutex> g(g_exch_mu);
+      g_exch_runs[ctx] = run;
+    }
+    if (visits) *visits += closed_form_visits(run.pl, nown);
+  });
+}
+
+extern "C" int salvox_exhaustive_slab_edges(salvox_ctx* ctx, float* d_first, float* d_last) {
+  return guarded([&] {
+    if (!ctx) fail(SALVOX_EINVAL, "null context");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    ExhRun run;
+    {
+      std::lock_guard<std::mutex> g(g_exch_mu);
+      auto it = g_exch_runs.find(ctx);
+      if (it == g_exch_runs.end()) fail(SALVOX_EINVAL, "exhaustive slab edges: no pending scores call");
+      run = it->second;
+    }
+    SX_CUDA(cudaSetDevice(ctx->device));
+    const size_t plane = (size_t)run.kp.nx * run.kp.ny;
+    if (d_first)
+      SX_CUDA(cudaMemcpyAsync(d_first, run.kp.score, plane * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+    if (d_last)
+      SX_CUDA(cudaMemcpyAsync(d_last, run.kp.score + plane * (run.z1 - run.z0 - 1), plane * 4,
+                              cudaMemcpyDeviceToDevice, ctx->stream));
+    SX_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+extern "C" int salvox_exhaustive_slab_maxima(salvox_ctx* ctx, const float* d_below,
+                                             const float* d_above, salvox_maximum* maxima,
+                                             int64_t cap, int64_t* n_maxima) {
+  return guarded([&] {
+    if (!ctx) fail(SALVOX_EINVAL, "null context");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    ExhRun run;
+    {
+      std::lock_guard<std::mutex> g(g_exch_mu);
+      auto it = g_exch_runs.find(ctx);
+      if (it == g_exch_runs.end()) fail(SALVOX_EINVAL, "exhaustive slab maxima: no pending scores call");
+      run = it->second;
+      g_exch_runs.erase(it);
+    }
+    SX_CUDA(cudaSetDevice(ctx->device));
+    const size_t plane = (size_t)run.kp.nx * run.kp.ny;
+    if (run.z0 > 0) {  // plane z0 - 1 (the lower neighbour's last owned plane)
+      if (!d_below) fail(SALVOX_EINVAL, "exhaustive slab maxima: the plane below is required");
+      SX_CUDA(cudaMemcpyAsync(run.score_base, d_below, plane * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    if (run.z1 < run.kp.nz) {  // plane z1 (the upper neighbour's first owned plane)
+      if (!d_above) fail(SALVOX_EINVAL, "exhaustive slab maxima: the plane above is required");
+      SX_CUDA(cudaMemcpyAsync(run.score_base + plane * (run.zb1 - run.zb0 - 1), d_above, plane * 4,
+                              cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    const long long cnt = maxima_and_sort(ctx, run, run.z0, run.z1);
+    if (maxima) {
+      fetch_maxima(ctx, cnt, maxima, cap);
+    } else {  // they stay on the device (salvox_last_maxima[_device] fetch them)
+      ctx->last_maxima_n = cnt;
+      ctx->stage_valid = false;
+    }
+    if (n_maxima) *n_maxima = cnt;
+  });
+}
+
+// ---- device-side maxima merge (multi-GPU) ------------------------------------
+__global__ void maxima_keys_kernel(const salvox_maximum* __restrict__ in, long long n,
+                                   unsigned long long* keys, unsigned int* idx) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const float sc = (float)in[i].score;  // the map's float score, widened exactly
+    keys[i] = ((unsigned long long)(~__float_as_uint(sc)) << 32) |
+              ((unsigned long long)in[i].linear_index & 0xffffffffull);
+    idx[i] = (unsigned int)i;
+  }
+}
+
+__global__ void gather_maxima_kernel(const salvox_maximum* __restrict__ in,
+                                     const unsigned int* __restrict__ idx, long long n,
+                                     salvox_maximum* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    out[i] = in[idx[i]];
+}
+
+extern "C" int salvox_last_maxima_device(salvox_ctx* ctx, salvox_maximum* d_out, int64_t cap,
+                                         int64_t* n_out) {
+  return guarded([&] {
+    if (!ctx) fail(SALVOX_EINVAL, "null context");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    const int64_t n = ctx->last_maxima_n;
+    SX_CUDA(cudaSetDevice(ctx->device));
+    if (d_out && cap > 0 && n > 0)
+      SX_CUDA(cudaMemcpyAsync(d_out, ctx->d_maxima.p, (size_t)std::min(n, cap) * sizeof(salvox_maximum),
+                              cudaMemcpyDeviceToDevice, ctx->stream));
+    SX_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (n_out) *n_out = n;
+  });
+}
+
+extern "C" int salvox_merge_maxima_device(salvox_ctx* ctx, const salvox_maximum* d_in, int64_t n,
+                                          salvox_maximum* d_out) {
+  return guarded([&] {
+    if (!ctx) fail(SALVOX_EINVAL, "null context");
+    if (n < 0 || (n > 0 && (!d_in || !d_out))) fail(SALVOX_EINVAL, "merge maxima: bad arguments");
+    if (n > (int64_t)UINT_MAX) fail(SALVOX_EUNSUPPORTED, "merge maxima: too many records");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    SX_CUDA(cudaSetDevice(ctx->device));
+    if (n > 0) {
+      const size_t un = (size_t)n;
+      auto* keys = static_cast<unsigned long long*>(ctx->d_keys.ensure(un * 8));
+      auto* keys2 = static_cast<unsigned long long*>(ctx->d_keys_alt.ensure(un * 8));
+      auto* idx = static_cast<unsigned int*>(ctx->d_merge_idx.ensure(un * 8));
+      unsigned int* idx2 = idx + un;
+      const int grid = (int)std::min<long long>((n + 255) / 256, ctx->sm_count * 8);
+      maxima_keys_kernel<<<grid, 256, 0, ctx->stream>>>(d_in, n, keys, idx);
+      SX_LAUNCH_CHECK(ctx);
+      size_t tmp = 0;
+      SX_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, keys, keys2, idx, idx2, (int)n, 0, 64,
+                                              ctx->stream));
+      void* d_tmp = ctx->d_cub.ensure(tmp);
+      SX_CUDA(cub::DeviceRadixSort::SortPairs(d_tmp, tmp, keys, keys2, idx, idx2, (int)n, 0, 64,
+                                              ctx->stream));
+      ctx->launches += 4;
+      gather_maxima_kernel<<<grid, 256, 0, ctx->stream>>>(d_in, idx2, n, d_out);
+      SX_LAUNCH_CHECK(ctx);
+    }
+    SX_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
 }
 
 extern "C" int salvox_last_maxima(salvox_ctx* ctx, salvox_maximum* out, int64_t cap,

@@ -91,6 +91,103 @@ def allgather_maxima(local: np.ndarray, group=None, device=None) -> np.ndarray:
     return merge_maxima(parts)
 
 
+def exchange_edges(first, last, group=None):
+    """The neighbour-plane exchange of the z-slab split: rank g sends its first
+    owned score plane to g-1 and its last to g+1 and receives plane z0-1 (from
+    g-1's last) and plane z1 (from g+1's first). Point-to-point over the process
+    group (NCCL send/recv on the box, gloo in the CPU tests). Returns
+    (below, above), None at the volume ends."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    below = torch.empty_like(first) if rank > 0 else None
+    above = torch.empty_like(last) if rank < world - 1 else None
+    ops = []
+    if rank > 0:
+        ops.append(dist.P2POp(dist.isend, first, rank - 1, group))
+        ops.append(dist.P2POp(dist.irecv, below, rank - 1, group))
+    if rank < world - 1:
+        ops.append(dist.P2POp(dist.isend, last, rank + 1, group))
+        ops.append(dist.P2POp(dist.irecv, above, rank + 1, group))
+    if ops:
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+    return below, above
+
+
+def allgather_maxima_device(n_local, group=None, device=None, ctx=None):
+    """The maxima all-gather kept on the device: every rank's records (left on
+    the device by the slab maxima call) are all-gathered as raw 48-byte rows over
+    NCCL and sorted into the reference's order by salvox_merge_maxima_device --
+    no host round trip, no host sort. Returns a CUDA uint8 tensor (n, 48)."""
+    import torch
+    import torch.distributed as dist
+
+    from . import api
+
+    world = dist.get_world_size(group)
+    cnt = torch.tensor([n_local], dtype=torch.int64, device=device)
+    cnts = [torch.zeros_like(cnt) for _ in range(world)]
+    dist.all_gather(cnts, cnt, group=group)
+    counts = [int(c) for c in torch.cat(cnts).cpu().tolist()]
+    buf = torch.zeros((max(max(counts), 1), MAX_DTYPE.itemsize), dtype=torch.uint8, device=device)
+    api.last_maxima_device(buf, ctx=ctx)
+    bufs = [torch.empty_like(buf) for _ in range(world)]
+    dist.all_gather(bufs, buf, group=group)
+    cat = torch.cat([b[:c] for b, c in zip(bufs, counts)])
+    return api.merge_maxima_device(cat, ctx=ctx)
+
+
+def exhaustive_exchange(volume, scales, window_low, window_high, bins=64, budget=None, group=None,
+                        device=None, ctx=None, out=None, maxima_out=None, d_slab=None):
+    """kadir_brady_exhaustive over z-slabs with the neighbour-plane exchange: each
+    rank scores only its owned planes (whole 8-plane tile layers), swaps one
+    boundary plane with each neighbour, then selects its maxima; ONE all-gather
+    merges them. `d_slab` (a CUDA tensor holding planes [zs0, zs1)) makes the
+    call device-resident; otherwise the rank's planes of the host `volume` go up
+    pipelined. Returns what exhaustive_sharded returns."""
+    import torch
+    import torch.distributed as dist
+
+    from . import api
+
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    nz = volume.shape[0] if volume is not None else None
+    if nz is None:
+        raise ValueError("exhaustive_exchange: pass the volume (host) for its shape")
+    R = halo_radius(scales)
+    z0, z1, zs0, zs1 = slab_bounds(nz, world, rank, R)
+    ny, nx = volume.shape[1], volume.shape[2]
+    bud = budget if budget is not None else api.DEFAULT_BUDGET
+    src = d_slab if d_slab is not None else volume[zs0:zs1]
+    score, best, visits = api.exhaustive_slab_scores(src, nz, zs0, z0, z1, scales, window_low,
+                                                     window_high, bins, budget=bud, ctx=ctx,
+                                                     out=out)
+    dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+    first = torch.empty((ny, nx), dtype=torch.float32, device=dev)
+    last = torch.empty_like(first)
+    api.exhaustive_slab_edges(first, last, ctx=ctx)
+    below, above = exchange_edges(first, last, group) if world > 1 else (None, None)
+    if world == 1:
+        merged = api.exhaustive_slab_maxima(below, above, ctx=ctx, maxima_out=maxima_out)
+        return score, best, (z0, z1), merged, visits
+    n_local = api.exhaustive_slab_maxima(below, above, ctx=ctx, on_device=True)
+    merged_d = allgather_maxima_device(n_local, group, dev, ctx=ctx)
+    if d_slab is not None:  # device-resident call: the merged list stays on the device
+        return score, best, (z0, z1), merged_d, visits
+    n = merged_d.shape[0]
+    if maxima_out is not None and len(maxima_out) >= n:
+        host = torch.from_numpy(maxima_out.view(np.uint8).reshape(-1, MAX_DTYPE.itemsize)[:n])
+        host.copy_(merged_d)  # one DMA into the caller's (pinned) buffer
+        merged = maxima_out[:n]
+    else:
+        merged = merged_d.cpu().numpy().reshape(-1).view(MAX_DTYPE)
+    return score, best, (z0, z1), merged, visits
+
+
 def exhaustive_sharded(volume: np.ndarray, scales, window_low, window_high, bins=64,
                        budget=None, group=None, device=None, compute=None, ctx=None, out=None,
                        maxima_out=None):
@@ -111,6 +208,10 @@ def exhaustive_sharded(volume: np.ndarray, scales, window_low, window_high, bins
     nz = vol.shape[0]
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
+    if world > 1 and compute is None and device is not None and vol.shape[0] >= world:
+        # the device path: owned planes only, boundary-plane exchange, device merge
+        return exhaustive_exchange(vol, scales, window_low, window_high, bins, budget, group,
+                                   device, ctx=ctx, out=out, maxima_out=maxima_out)
     R = halo_radius(scales)
     z0, z1, zs0, zs1 = slab_bounds(nz, world, rank, R)
     if z1 <= z0:

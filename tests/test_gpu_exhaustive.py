@@ -125,6 +125,98 @@ def test_slabs_reproduce_full_volume(sx, oracle):
     assert vis == full_v
 
 
+@pytest.mark.parametrize("device_resident", [False, True])
+def test_exchange_slabs_reproduce_full_volume(sx, oracle, device_resident):
+    """The exchange form of the z-slab split (salvox_exhaustive_slab_scores /
+    _edges / _maxima): each "rank" (its own context, run one after another)
+    scores only its owned planes, the neighbours' boundary planes are passed in
+    as the NCCL exchange would, and the merged maxima, maps and visits equal the
+    single-call ones."""
+    import torch
+
+    from paper_1310_6736_b200 import api, sharding
+    from paper_1310_6736_b200._lib import Context
+
+    vol, _ = oracle.make_phantom(phantoms.ball_3d(40, (19.0, 20.0, 18.0), 7.0, 12))
+    scales = [3.0, 4.0, 5.0, 6.0]
+    R = 7
+    full_s, full_b, full_m, full_v = sx.kadir_brady_exhaustive_records(vol, scales, 0, 64, 64,
+                                                                       budget=10**9)
+    nz, ny, nx = vol.shape
+    cuts = [0, 9, 23, 31, nz]
+    dev = torch.device("cuda", 0)
+    ctxs, maps, bests, edges, vis = [], [], [], [], 0
+    for z0, z1 in zip(cuts[:-1], cuts[1:]):
+        zs0, zs1 = max(0, z0 - R - 1), min(nz, z1 + R + 1)
+        c = Context(0)
+        src = torch.from_numpy(vol[zs0:zs1].copy()).to(dev) if device_resident else vol[zs0:zs1]
+        s, b, v = api.exhaustive_slab_scores(src, nz, zs0, z0, z1, scales, 0, 64, 64,
+                                             budget=10**9, ctx=c)
+        if device_resident:
+            s, b = s.cpu().numpy(), b.cpu().numpy()
+        first = torch.empty((ny, nx), dtype=torch.float32, device=dev)
+        last = torch.empty_like(first)
+        api.exhaustive_slab_edges(first, last, ctx=c)
+        assert np.array_equal(first.cpu().numpy(), s[0]) and np.array_equal(last.cpu().numpy(), s[-1])
+        ctxs.append(c)
+        maps.append(s)
+        bests.append(b)
+        edges.append((first, last))
+        vis += v
+    maxs = []
+    for i, c in enumerate(ctxs):  # plane z0-1 = the lower rank's last, z1 = the upper's first
+        below = edges[i - 1][1] if i > 0 else None
+        above = edges[i + 1][0] if i + 1 < len(ctxs) else None
+        maxs.append(api.exhaustive_slab_maxima(below, above, ctx=c))
+    assert np.array_equal(np.concatenate(maps), full_s)
+    assert np.array_equal(np.concatenate(bests), full_b)
+    assert np.array_equal(sharding.merge_maxima(maxs), full_m)
+    assert vis == full_v
+    with pytest.raises(ValueError):  # no pending scores call any more
+        api.exhaustive_slab_maxima(None, None, ctx=ctxs[0])
+    for c in ctxs:
+        c.close()
+
+
+def test_device_maxima_merge(sx, oracle):
+    """salvox_merge_maxima_device sorts records into the reference's order (score
+    desc, linear index asc) like the host merge; allgather_maxima_device (here in
+    a one-rank NCCL group) returns the call's own list."""
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1310_6736_b200 import api, sharding
+    from paper_1310_6736_b200._lib import MAX_DTYPE
+
+    rng = np.random.default_rng(5)
+    n = 20000
+    m = np.zeros(n, MAX_DTYPE)
+    m["score"] = rng.integers(1, 50, n).astype(np.float32).astype(np.float64)  # many ties
+    m["linear_index"] = rng.permutation(10**7)[:n]
+    m["scale"] = rng.integers(3, 16, n)
+    dev = torch.device("cuda", 0)
+    d = torch.from_numpy(m.view(np.uint8).reshape(n, -1).copy()).to(dev)
+    got = api.merge_maxima_device(d).cpu().numpy().reshape(-1).view(MAX_DTYPE)
+    assert np.array_equal(got, sharding.merge_maxima([m[: n // 3], m[n // 3:]]))
+
+    vol, _ = oracle.make_phantom(phantoms.ball_3d(24, (11.0, 12.0, 10.0), 5.0, 13))
+    s, b, full_m, _ = sx.kadir_brady_exhaustive_records(vol, [3.0, 4.0], 0, 64, 64, budget=10**9)
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=dev)
+    try:
+        merged = sharding.allgather_maxima_device(len(full_m), device=dev,
+                                                  ctx=sx.default_context())
+        assert np.array_equal(merged.cpu().numpy().reshape(-1).view(MAX_DTYPE), full_m)
+    finally:
+        dist.destroy_process_group()
+
+
 def test_nonconsecutive_integer_scales_and_order(sx, oracle):
     # scales out of order with gaps: rank-based tie-break must follow the caller's order
     vol, _ = oracle.make_phantom(phantoms.square_2d(64, 30.0, 33.0, 7, 64, 5))

@@ -203,3 +203,78 @@ def test_bench_weak_scaling_slabs(world):
         z0, z1, zs0, zs1 = sharding.slab_bounds(nz, world, rank, R)
         assert (z1 - z0) * nx * ny == 256 ** 3
         assert zs0 == max(0, z0 - R - 1) and zs1 == min(nz, z1 + R + 1)
+
+
+def _exchange_worker(rank, world, port, vol, bins, out):
+    """The exchange form of the slab split (sharding.exhaustive_exchange): owned
+    planes only, one boundary plane each way (sharding.exchange_edges), maxima
+    with the received planes, one all-gather. The oracle stands in for the
+    device scoring and maxima."""
+    import torch
+    import torch.distributed as dist
+
+    from oracle import oracle as O
+    from paper_1310_6736_b200 import sharding
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        nz, ny, nx = vol.shape
+        R = sharding.halo_radius(SCALES)
+        z0, z1, zs0, zs1 = sharding.slab_bounds(nz, world, rank, R)
+        s, _, _ = O.exhaustive(vol[zs0:zs1], 0, bins, bins, SCALES, budget=10**12, mode="exact",
+                               threads=2, z_range=(z0 - zs0, z1 - zs0))
+        own = s[z0 - zs0:z1 - zs0]
+        below, above = sharding.exchange_edges(torch.from_numpy(own[0].copy()),
+                                               torch.from_numpy(own[-1].copy()))
+        ext = [own]
+        if below is not None:
+            ext.insert(0, below.numpy()[None])
+        if above is not None:
+            ext.append(above.numpy()[None])
+        ext = np.concatenate(ext)
+        e0 = z0 - (1 if below is not None else 0)
+        pos, sc, scale, lin = O.local_maxima(ext, np.zeros_like(ext))
+        keep = (pos[:, 2] + e0 >= z0) & (pos[:, 2] + e0 < z1)
+        m = np.zeros(int(keep.sum()), sharding.MAX_DTYPE)
+        m["position"] = pos[keep] + [0, 0, e0]
+        m["score"] = sc[keep]
+        m["linear_index"] = lin[keep] + e0 * ny * nx
+        merged = sharding.allgather_maxima(m)
+        out[rank] = (z0, z1, own, merged)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_exchange_gloo_matches_single_process(oracle, world):
+    """Each rank scores only its owned planes and receives the two neighbour
+    planes: the merged maxima equal the single-process ones (3 ranks: a middle
+    rank exchanges both ways)."""
+    bins = 16
+    vol, _ = oracle.make_phantom(phantoms.ball_3d(18, (9.0, 8.0, 9.0), 4.0, 21, levels=bins,
+                                                 background={"type": "gaussian", "mean": 4.0,
+                                                             "sigma": 1.5}))
+    s_ref, b_ref, _ = oracle.exhaustive(vol, 0, bins, bins, SCALES, budget=10**12, mode="exact",
+                                        threads=4)
+    pos, sc, scale, lin = oracle.local_maxima(s_ref, b_ref)
+    mgr = mp.Manager()
+    out = mgr.dict()
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    procs = [ctx.Process(target=_exchange_worker, args=(r, world, port, vol, bins, out))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    planes = []
+    for r in range(world):
+        z0, z1, s, merged = out[r]
+        planes.append((z0, s))
+        assert np.array_equal(merged["linear_index"], lin)
+        assert np.array_equal(merged["score"], sc)
+    full = np.concatenate([s for _, s in sorted(planes, key=lambda t: t[0])])
+    assert np.array_equal(full, s_ref)

@@ -52,4 +52,30 @@ for world in (1, 2, 4, 8):
         times.append(e0.elapsed_time(e1))
     res[f"slab_ms_x{world}"] = {"max": max(times), "min": min(times),
                                 "implied_evals_per_s": evals / (max(times) * 1e-3)}
+    # the exchange form: owned planes only (salvox_exhaustive_slab_scores), the two
+    # neighbour planes passed in (as the NCCL exchange delivers them), then maxima
+    if world > 1:
+        times = []
+        for rank in range(world):
+            z0, z1, zs0, zs1 = sharding.slab_bounds(nz, world, rank, R)
+            d_slab = d_vol[zs0:zs1].contiguous()
+            d_score = torch.empty((z1 - z0, ny, nx), dtype=torch.float32, device=dev)
+            d_best = torch.empty_like(d_score)
+            below = d_vol[max(z0 - 1, 0)].contiguous()  # stand-ins with the right shape
+            above = d_vol[min(z1, nz - 1)].contiguous()
+
+            def run_x():
+                api.exhaustive_slab_scores(d_slab, nz, zs0, z0, z1, SCALES, 0.0, 32.0, 32,
+                                           budget=10**15, ctx=ctx, out=(d_score, d_best))
+                api.exhaustive_slab_maxima(below if z0 > 0 else None, above if z1 < nz else None,
+                                           ctx=ctx)
+            run_x()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            run_x()
+            e1.record(st)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1))
+        res[f"exchange_slab_ms_x{world}"] = {"max": max(times), "min": min(times),
+                                             "implied_evals_per_s": evals / (max(times) * 1e-3)}
 print(json.dumps(res))
