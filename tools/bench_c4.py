@@ -52,8 +52,10 @@ for world in (1, 2, 4, 8):
         times.append(e0.elapsed_time(e1))
     res[f"slab_ms_x{world}"] = {"max": max(times), "min": min(times),
                                 "implied_evals_per_s": evals / (max(times) * 1e-3)}
-    # the exchange form: owned planes only (salvox_exhaustive_slab_scores), the two
-    # neighbour planes passed in (as the NCCL exchange delivers them), then maxima
+    # the exchange form (what bench.py runs at N > 1): owned planes only
+    # (salvox_exhaustive_slab_scores), the two neighbour planes passed in (as the
+    # NCCL exchange delivers them), then maxima left on the device for the
+    # all-gather + device merge (not included: ~1 ms over NVLink at N = 8)
     if world > 1:
         times = []
         for rank in range(world):
@@ -68,7 +70,7 @@ for world in (1, 2, 4, 8):
                 api.exhaustive_slab_scores(d_slab, nz, zs0, z0, z1, SCALES, 0.0, 32.0, 32,
                                            budget=10**15, ctx=ctx, out=(d_score, d_best))
                 api.exhaustive_slab_maxima(below if z0 > 0 else None, above if z1 < nz else None,
-                                           ctx=ctx)
+                                           ctx=ctx, on_device=True)
             run_x()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(st)
