@@ -1,3 +1,5 @@
+"""Per-rank cost of the regular vs the exchange form of a C4 slab (KB kernel time
+via ctx profiling, whole call via events) and the device merge of 8 slabs' maxima."""
 import sys, os, ctypes as C, numpy as np, torch
 sys.path.insert(0, '/root/repo')
 from paper_1310_6736_b200 import _lib, api, sharding
@@ -23,7 +25,6 @@ for world in (2,8):
     kb=ctx.kernel_time(); ctx.set_profiling(False)
     print(world, name, 'total', round(e0.elapsed_time(e1),2), 'kb', round(kb[0],2), kb[1], kb[2])
 # device merge cost at the N=8 size: 8 slabs' maxima (this slab's list 8 times, indices shifted)
-nloc = api.exhaustive_slab_maxima(None, None, ctx=ctx, on_device=True) if False else None
 z0,z1,zs0,zs1=sharding.slab_bounds(nz,8,3,R)
 d_slab=d_vol[zs0:zs1].contiguous(); d_score=torch.empty((z1-z0,ny,nx),device=dev); d_best=torch.empty_like(d_score)
 api.exhaustive_slab_scores(d_slab,nz,zs0,z0,z1,SCALES,0.0,32.0,32,budget=10**15,ctx=ctx,out=(d_score,d_best))
