@@ -734,6 +734,8 @@ __global__ void __launch_bounds__(1024, 1)
       for (int j = 0; j < 8; ++j) cur[j] = hc[(1 + c + j) * NT];
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
+      for (int j = 0; j < 8; ++j) asm volatile("" : "+r"(a[j]));  // no use before the wait
+#pragma unroll
       for (int j = 0; j < 8; ++j) {
         const uint32_t cv = cur[j];
 #ifndef KB_SKIP_MATH
@@ -1165,6 +1167,8 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
       for (int c = 0; c < NS; c += 8) tm_ld8(slot + c, a + c);
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+      for (int j = 0; j < NS; ++j) asm volatile("" : "+r"(a[j]));  // no use before the wait
 #pragma unroll
       for (int c = 0; c < NS; c += 8) tm_st8(slot + c, cur + c);  // the older slot becomes the newest
       {
