@@ -602,16 +602,24 @@ __device__ __forceinline__ void cta_produce(const PassIn& in, const Box& bb, int
   bool inb[kG];
   int bin[kG], xs[kG], ys[kG], zs[kG];
   double val[kG];
+  uint8_t raw[kG];
+  // the bin of every voxel of the chunk is fetched first (the bounding box lies
+  // inside the volume, so the loads are always valid): their L2 latency then
+  // overlaps the Mahalanobis tests instead of following them
 #pragma unroll
   for (int j = 0; j < kG; ++j) {
     const int L = base + 32 * j + lane;
-    const bool act = L < total;
-    const int Lc = act ? L : 0;
+    const int Lc = L < total ? L : 0;
     const int t = Lc / Lx;
     xs[j] = bb.x0 + (Lc - t * Lx);
     const int zz = t / Ly;
     ys[j] = bb.y0 + (t - zz * Ly);
     zs[j] = bb.z0 + zz;
+    raw[j] = __ldg(in.vb + ((size_t)zs[j] * in.ny + ys[j]) * in.nx + xs[j]);
+  }
+#pragma unroll
+  for (int j = 0; j < kG; ++j) {
+    const bool act = base + 32 * j + lane < total;
     inb[j] = false;
     bin[j] = 0;
     val[j] = 0.0;
@@ -619,7 +627,7 @@ __device__ __forceinline__ void cta_produce(const PassIn& in, const Box& bb, int
       const double d = maha(g, in.c, xs[j], ys[j], zs[j]);
       inb[j] = d <= 1.0;
       if (inb[j]) {
-        bin[j] = (int)__ldg(in.vb + ((size_t)zs[j] * in.ny + ys[j]) * in.nx + xs[j]) - 1;
+        bin[j] = (int)raw[j] - 1;
         if (MODE == PASS_HIST) val[j] = __dmul_rn(g.det_fac, kernel_value(in.kernel, d));
         if (MODE == PASS_CENT) val[j] = __dmul_rn(kernel_step_weight(in.kernel, d), w[bin[j]]);
         if (MODE == PASS_MOM) val[j] = w[bin[j]];
