@@ -240,6 +240,10 @@ __device__ __noinline__ HistRes warp_candidate_hist_impl(const uint8_t* vb, int 
     bool in[kG];
     int bin[kG];
     double val[kG];
+    uint8_t raw[kG];  // bins fetched before the Mahalanobis tests (latency overlap)
+#pragma unroll
+    for (int j = 0; j < kG; ++j)
+      raw[j] = act[j] ? __ldg(vb + ((size_t)z[j] * ny + y[j]) * nx + x[j]) : (uint8_t)0;
 #pragma unroll
     for (int j = 0; j < kG; ++j) {
       in[j] = false;
@@ -249,7 +253,7 @@ __device__ __noinline__ HistRes warp_candidate_hist_impl(const uint8_t* vb, int 
         const double d = maha(g, c, x[j], y[j], z[j]);
         in[j] = d <= 1.0;
         if (in[j]) {
-          bin[j] = (int)__ldg(vb + ((size_t)z[j] * ny + y[j]) * nx + x[j]) - 1;
+          bin[j] = (int)raw[j] - 1;
           val[j] = __dmul_rn(g.det_fac, kernel_value(kernel, d));
         }
       }
@@ -405,6 +409,10 @@ __device__ __noinline__ CentRes warp_centroid_impl(const uint8_t* vb, int nx, in
   warp_box_iter_g(bb, lane, [&](const bool* act, const int* x, const int* y, const int* z) {
     bool in[kG];
     double g[kG];
+    uint8_t raw[kG];  // bins fetched before the Mahalanobis tests (latency overlap)
+#pragma unroll
+    for (int j = 0; j < kG; ++j)
+      raw[j] = act[j] ? __ldg(vb + ((size_t)z[j] * ny + y[j]) * nx + x[j]) : (uint8_t)0;
 #pragma unroll
     for (int j = 0; j < kG; ++j) {
       in[j] = false;
@@ -413,7 +421,7 @@ __device__ __noinline__ CentRes warp_centroid_impl(const uint8_t* vb, int nx, in
         const double dd = maha(wg, c, x[j], y[j], z[j]);
         in[j] = dd <= 1.0;
         if (in[j]) {
-          const int b = (int)__ldg(vb + ((size_t)z[j] * ny + y[j]) * nx + x[j]) - 1;
+          const int b = (int)raw[j] - 1;
           g[j] = __dmul_rn(kernel_step_weight(step_kernel, dd), s.w[b]);
         }
       }
@@ -981,6 +989,9 @@ __device__ __noinline__ long long warp_moment(const SeekParams& P, const uint8_t
   warp_box_iter_g(bb, lane, [&](const bool* act, const int* x, const int* y, const int* z) {
     bool in[kG];
     double w[kG];
+    int braw[kG];  // bins fetched before the Mahalanobis tests (latency overlap)
+#pragma unroll
+    for (int j = 0; j < kG; ++j) braw[j] = act[j] ? bin_at(P, vb, x[j], y[j], z[j]) : 0;
 #pragma unroll
     for (int j = 0; j < kG; ++j) {
       in[j] = false;
@@ -988,7 +999,7 @@ __device__ __noinline__ long long warp_moment(const SeekParams& P, const uint8_t
       if (act[j]) {
         const double dd = maha(wg, xn, x[j], y[j], z[j]);
         in[j] = dd <= 1.0;
-        if (in[j]) w[j] = s.w[bin_at(P, vb, x[j], y[j], z[j])];
+        if (in[j]) w[j] = s.w[braw[j]];
       }
     }
     int off = 0;
