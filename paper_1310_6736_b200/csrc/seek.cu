@@ -203,6 +203,42 @@ __device__ __forceinline__ double kernel_step_weight(int k, double d) {  // kern
   return 1.0;
 }
 
+// Sequential fp64 sums in the reference's order (acc += src[0], src[1], ...):
+// the terms are staged W at a time in registers so their shared-memory loads
+// (and, for the moment, the products) are in flight together and only the
+// dependent DADD chain remains serial. W = 16 for the CTA engine's consumer
+// warp (C3 10.8 -> 10.1 ms); the warp engine keeps its unroll-4 loops (its
+// 80-register occupancy variant got slower with the staging: 72 -> 74-77 ms).
+template <int W>
+__device__ __forceinline__ double chain_sum(double acc, const double* src, int n) {
+  int k = 0;
+  for (; k + W <= n; k += W) {
+    double t[W];
+#pragma unroll
+    for (int u = 0; u < W; ++u) t[u] = src[k + u];
+#pragma unroll
+    for (int u = 0; u < W; ++u) acc = __dadd_rn(acc, t[u]);
+  }
+  for (; k < n; ++k) acc = __dadd_rn(acc, src[k]);
+  return acc;
+}
+
+// acc += (v[k] * di[k]) * dj[k] in order (the bandwidth moment's outer products)
+template <int W>
+__device__ __forceinline__ double chain_sum_mom(double acc, const double* v, const double* di,
+                                                const double* dj, int n) {
+  int k = 0;
+  for (; k + W <= n; k += W) {
+    double t[W];
+#pragma unroll
+    for (int u = 0; u < W; ++u) t[u] = __dmul_rn(__dmul_rn(v[k + u], di[k + u]), dj[k + u]);
+#pragma unroll
+    for (int u = 0; u < W; ++u) acc = __dadd_rn(acc, t[u]);
+  }
+  for (; k < n; ++k) acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(v[k], di[k]), dj[k]));
+  return acc;
+}
+
 __device__ __forceinline__ int bin_at(const SeekParams& P, const uint8_t* vb, int x, int y, int z) {
   return (int)__ldg(vb + ((size_t)z * P.ny + y) * P.nx + x) - 1;
 }
@@ -710,23 +746,11 @@ __device__ __forceinline__ void cta_consume(const CtaSlot& sl, int M, int lane, 
     }
     support += (unsigned)sl.n;
   } else if (MODE == PASS_CENT) {
-    if (lane < 4) {
-      const double* src = lane == 3 ? sl.v : sl.t[lane];
-      const int n = sl.n;
-#pragma unroll 4
-      for (int k = 0; k < n; ++k) a0 = __dadd_rn(a0, src[k]);
-    }
+    if (lane < 4) a0 = chain_sum<16>(a0, lane == 3 ? sl.v : sl.t[lane], sl.n);
   } else {
     const int n = sl.n;
-    if (lane < 9) {
-      const double* di = sl.t[lane / 3];
-      const double* dj = sl.t[lane % 3];
-#pragma unroll 4
-      for (int k = 0; k < n; ++k) a0 = __dadd_rn(a0, __dmul_rn(__dmul_rn(sl.v[k], di[k]), dj[k]));
-    } else if (lane == 9) {
-#pragma unroll 4
-      for (int k = 0; k < n; ++k) a0 = __dadd_rn(a0, sl.v[k]);
-    }
+    if (lane < 9) a0 = chain_sum_mom<16>(a0, sl.v, sl.t[lane / 3], sl.t[lane % 3], n);
+    else if (lane == 9) a0 = chain_sum<16>(a0, sl.v, n);
   }
 }
 
