@@ -583,6 +583,28 @@ __device__ __forceinline__ void tm_st8(uint32_t taddr, const uint32_t* r) {
                : "memory");
 }
 
+__device__ __forceinline__ void tm_ld32(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]),
+        "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]),
+        "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tm_st32(uint32_t taddr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]),
+      "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]),
+      "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+
 template <int NB, bool DBG>
 __global__ void __launch_bounds__(1024, 1)
     kb_tmem_kernel(const __grid_constant__ CUtensorMap tmap, const KbParams p) {
@@ -1164,13 +1186,21 @@ __global__ void __launch_bounds__(256, 1)
       // sums (the boundary was ~30% of the kernel's time with the serial,
       // branchy per-bin loop: KB_SKIP_BOUNDARY A/B, r01)
       uint32_t a[NS];
+      if constexpr (NS == 32) {
+        tm_ld32(slot, a);
+      } else {
 #pragma unroll
-      for (int c = 0; c < NS; c += 8) tm_ld8(slot + c, a + c);
+        for (int c = 0; c < NS; c += 8) tm_ld8(slot + c, a + c);
+      }
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
       for (int j = 0; j < NS; ++j) asm volatile("" : "+r"(a[j]));  // no use before the wait
+      if constexpr (NS == 32) {
+        tm_st32(slot, cur);  // the older slot becomes the newest
+      } else {
 #pragma unroll
-      for (int c = 0; c < NS; c += 8) tm_st8(slot + c, cur + c);  // the older slot becomes the newest
+        for (int c = 0; c < NS; c += 8) tm_st8(slot + c, cur + c);
+      }
       {
         // per bin: the entropy term (radii that are scales) and the exact L1 term
         // (radii s+1), branch-free inside chunks of 8 bins; a chunk empty at r in
