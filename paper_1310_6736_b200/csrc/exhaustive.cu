@@ -1228,10 +1228,12 @@ __global__ void __launch_bounds__(256, 1)
 #endif
             // L1 numerator sum_b |S_b(hi) T_lo - S_b(lo) T_hi| exactly: the signed
             // terms sum to T_hi T_lo - T_lo T_hi = 0, so it is twice their positive part
+#ifndef KB_SKIP_L1  // profiling knob (results wrong)
             if (wE) {
               if (j & 1) l1_pos_acc(q1, (int)cv, ta, (int)a[j], nt);
               else l1_pos_acc(q0, (int)cv, ta, (int)a[j], nt);
             }
+#endif
           }
         }
         if (wH) hacc = (h4[0] + h4[1]) + (h4[2] + h4[3]);
