@@ -217,9 +217,15 @@ def main():
     import torch
     import torch.distributed as dist
 
+    # SALVOX_BENCH_FUNCTIONAL=1: ranks share the visible GPUs round-robin over gloo
+    # -- a functional check of the N>1 orchestration on a 1-GPU box, never a
+    # measurement (tools/mgpu_functional.sh)
+    functional = os.environ.get("SALVOX_BENCH_FUNCTIONAL") == "1"
+    if functional and args.impl == "b200":
+        local = local % max(torch.cuda.device_count(), 1)
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        if args.impl == "b200":
+        if args.impl == "b200" and not functional:
             torch.cuda.set_device(local)
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
@@ -299,7 +305,7 @@ def main():
     ms_local = float(np.mean(times))
     ms = ms_local
     if world > 1:
-        t = torch.tensor([ms_local], dtype=torch.float64, device=dev)
+        t = torch.tensor([ms_local], dtype=torch.float64, device="cpu" if functional else dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
         dist.barrier()
@@ -334,7 +340,7 @@ def main():
             d2h = score.nbytes + best.nbytes + len(merged) * sx.MAX_DTYPE.itemsize
     e2e_ms = float(np.mean(e2e_times))
     if world > 1:
-        t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        t = torch.tensor([e2e_ms], dtype=torch.float64, device="cpu" if functional else dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
 

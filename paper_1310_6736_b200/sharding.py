@@ -102,6 +102,12 @@ def exchange_edges(first, last, group=None):
 
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
+    if first.is_cuda and dist.get_backend(group) != "nccl":
+        # gloo cannot send device memory: stage through the host (functional
+        # multi-process tests on one GPU; the product path is NCCL)
+        b, a = exchange_edges(first.cpu(), last.cpu(), group)
+        return (b.to(first.device) if b is not None else None,
+                a.to(first.device) if a is not None else None)
     below = torch.empty_like(first) if rank > 0 else None
     above = torch.empty_like(last) if rank < world - 1 else None
     ops = []
@@ -128,15 +134,19 @@ def allgather_maxima_device(n_local, group=None, device=None, ctx=None):
     from . import api
 
     world = dist.get_world_size(group)
-    cnt = torch.tensor([n_local], dtype=torch.int64, device=device)
+    # gloo cannot move device memory: its collectives run on host copies
+    # (functional multi-process tests on one GPU; the product path is NCCL)
+    coll = device if dist.get_backend(group) == "nccl" else torch.device("cpu")
+    cnt = torch.tensor([n_local], dtype=torch.int64, device=coll)
     cnts = [torch.zeros_like(cnt) for _ in range(world)]
     dist.all_gather(cnts, cnt, group=group)
     counts = [int(c) for c in torch.cat(cnts).cpu().tolist()]
     buf = torch.zeros((max(max(counts), 1), MAX_DTYPE.itemsize), dtype=torch.uint8, device=device)
     api.last_maxima_device(buf, ctx=ctx)
-    bufs = [torch.empty_like(buf) for _ in range(world)]
-    dist.all_gather(bufs, buf, group=group)
-    cat = torch.cat([b[:c] for b, c in zip(bufs, counts)])
+    buf_c = buf if coll == device else buf.cpu()
+    bufs = [torch.empty_like(buf_c) for _ in range(world)]
+    dist.all_gather(bufs, buf_c, group=group)
+    cat = torch.cat([b[:c] for b, c in zip(bufs, counts)]).to(device)
     return api.merge_maxima_device(cat, ctx=ctx)
 
 
