@@ -71,6 +71,7 @@ extern "C" int salvox_ctx_destroy(salvox_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
+    forget_exchange_run(ctx);
     delete ctx;
   });
 }

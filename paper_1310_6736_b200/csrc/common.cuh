@@ -159,5 +159,7 @@ void launch_bin_volume(salvox_ctx* ctx, const float* d_vol, uint8_t* d_bins, int
                        int nzs, int pitch, double low, double high, int bins);
 // Observed intensity range (IntensityWindow::full_range, volume.hpp:108-112).
 void device_full_range(salvox_ctx* ctx, const float* d_vol, size_t n, double* low, double* high);
+// Drops a context's pending exchange-form scores call (salvox_ctx_destroy).
+void forget_exchange_run(salvox_ctx* ctx);
 
 }  // namespace sx

@@ -2240,6 +2240,11 @@ std::mutex g_exch_mu;
 std::map<salvox_ctx*, ExhRun> g_exch_runs;  // the pending scores call of each context
 }  // namespace
 
+void sx::forget_exchange_run(salvox_ctx* ctx) {
+  std::lock_guard<std::mutex> g(g_exch_mu);
+  g_exch_runs.erase(ctx);
+}
+
 extern "C" int salvox_exhaustive_slab_scores(salvox_ctx* ctx, const float* slab, int32_t on_device,
                                              int32_t nx, int32_t ny, int32_t nz, int32_t zs0,
                                              int32_t zs1, int32_t z0, int32_t z1,
