@@ -2204,7 +2204,11 @@ static int exhaustive_device_impl(salvox_ctx* ctx, const float* d_slab, int32_t 
     if (d_best_scale)
       SX_CUDA(cudaMemcpyAsync(d_best_scale, ctx->d_best.as<float>() + off, nown * 4,
                               cudaMemcpyDeviceToDevice, ctx->stream));
-    fetch_maxima(ctx, cnt, nullptr, 0);
+    // device-resident form: the maxima stay in HBM (salvox_last_maxima[_device]
+    // copy them on request); no host staging inside the call
+    ctx->last_maxima_n = cnt;
+    ctx->stage_valid = false;
+    SX_CUDA(cudaStreamSynchronize(ctx->stream));
     if (n_maxima) *n_maxima = cnt;
   });
 }

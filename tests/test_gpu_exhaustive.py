@@ -217,6 +217,44 @@ def test_device_maxima_merge(sx, oracle):
         dist.destroy_process_group()
 
 
+def test_device_resident_call_keeps_maxima_on_device(sx, oracle):
+    """salvox_exhaustive_device leaves the maxima in HBM; salvox_last_maxima and
+    salvox_last_maxima_device return the same list as the host-buffer call."""
+    import ctypes as C
+
+    import torch
+
+    from paper_1310_6736_b200 import _lib, api
+    from paper_1310_6736_b200._lib import MAX_DTYPE, Context
+
+    vol, _ = oracle.make_phantom(phantoms.ball_3d(32, (15.0, 16.0, 14.0), 6.0, 17))
+    scales = [3.0, 4.0, 5.0]
+    s, b, full_m, _ = sx.kadir_brady_exhaustive_records(vol, scales, 0, 64, 64, budget=10**9)
+    ctx = Context(0)
+    dev = torch.device("cuda", 0)
+    d_vol = torch.from_numpy(vol).to(dev)
+    d_s = torch.empty_like(d_vol)
+    d_b = torch.empty_like(d_vol)
+    nz, ny, nx = vol.shape
+    sc = np.asarray(scales, np.float64)
+    iw = _lib.Window(0.0, 64.0, 64, 0)
+    n = C.c_int64(0)
+    _lib.check(_lib.load().salvox_exhaustive_device(
+        ctx.handle, C.c_void_p(d_vol.data_ptr()), nx, ny, nz, C.byref(iw),
+        sc.ctypes.data_as(C.c_void_p), len(sc), 0, 10**9, C.c_void_p(d_s.data_ptr()),
+        C.c_void_p(d_b.data_ptr()), C.byref(n)))
+    assert n.value == len(full_m)
+    assert np.array_equal(d_s.cpu().numpy(), s) and np.array_equal(d_b.cpu().numpy(), b)
+    host = np.empty(n.value, MAX_DTYPE)
+    _lib.check(_lib.load().salvox_last_maxima(ctx.handle, host.ctypes.data_as(C.c_void_p),
+                                              n.value, C.byref(n)))
+    assert np.array_equal(host, full_m)
+    d = torch.zeros((n.value, MAX_DTYPE.itemsize), dtype=torch.uint8, device=dev)
+    assert api.last_maxima_device(d, ctx=ctx) == n.value
+    assert np.array_equal(d.cpu().numpy().reshape(-1).view(MAX_DTYPE), full_m)
+    ctx.close()
+
+
 def test_nonconsecutive_integer_scales_and_order(sx, oracle):
     # scales out of order with gaps: rank-based tie-break must follow the caller's order
     vol, _ = oracle.make_phantom(phantoms.square_2d(64, 30.0, 33.0, 7, 64, 5))
