@@ -1400,16 +1400,17 @@ TileCfg pick_tile(int bins, bool two_d) {
   return two_d ? TileCfg{nb, 32, 16, 1, false} : TileCfg{nb, 8, 8, 8, false};
 }
 
-// kb_quad_kernel: warps 4-7 start their walk ~6 us late, so each sub-partition's
+// kb_quad_kernel: warps 4-7 start their walk ~4 us late, so each sub-partition's
 // two warps reach their radius boundaries (entropy/L1 math, TMEM snapshots:
 // little shared-pipe work) at different times and the other warp keeps the
 // atomics flowing. C2 sweeps (r01, cycles -> ms): 0 53.1, 4k 53.1, 10k 52.0,
 // 20k 51.1, 40k 51.3; after the boundary rework: 0 51.7, 12k 49.5, 20k 49.8,
-// 28k 50.0. A/B knob SALVOX_KB_LAG.
+// 28k 50.0; final: 0 51.3, 4k 49.5, 6k 49.15, 8k 49.02, 10k 49.09, 12k 49.18.
+// A/B knob SALVOX_KB_LAG.
 int kb_lag() {
   static const int lag = [] {
     const char* e = std::getenv("SALVOX_KB_LAG");
-    return e ? std::atoi(e) : 12000;
+    return e ? std::atoi(e) : 8000;
   }();
   return lag;
 }
