@@ -929,6 +929,9 @@ __global__ void __launch_bounds__(32 * (NP + 1)) shift_cta_kernel(const SeekPara
   }
   if (degenerate) d.flags |= SALVOX_FLAG_DEGENERATE;
   d.center[0] = c[0], d.center[1] = c[1], d.center[2] = c[2];
+#ifdef SEEK_SKIP_FINAL  // profiling knob: no final scoring (results wrong)
+  degenerate = true;
+#endif
   if (!degenerate) {  // final scores (shift.cpp:89-105), as warp_final_scores
     unsigned sup;
     long long v2;
