@@ -38,7 +38,10 @@
 namespace sx {
 
 constexpr int kMaxBins = 64;
-constexpr int kG = 4;            // bounding-box chunks of 32 voxels per warp step (ILP)
+#ifndef SEEK_KG
+#define SEEK_KG 4
+#endif
+constexpr int kG = SEEK_KG;      // bounding-box chunks of 32 voxels per warp step (ILP)
 constexpr int kStep = 32 * kG;
 constexpr unsigned kFull = 0xffffffffu;
 constexpr double kLn2 = 0.693147180559945309417232121458176568;  // std::numbers::ln2
