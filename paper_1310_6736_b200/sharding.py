@@ -147,6 +147,8 @@ def allgather_maxima_device(n_local, group=None, device=None, ctx=None):
     bufs = [torch.empty_like(buf_c) for _ in range(world)]
     dist.all_gather(bufs, buf_c, group=group)
     cat = torch.cat([b[:c] for b, c in zip(bufs, counts)]).to(device)
+    # the context may run on its own stream: the gathered records must be complete
+    torch.cuda.current_stream(device).synchronize()
     return api.merge_maxima_device(cat, ctx=ctx)
 
 
@@ -181,6 +183,8 @@ def exhaustive_exchange(volume, scales, window_low, window_high, bins=64, budget
     last = torch.empty_like(first)
     api.exhaustive_slab_edges(first, last, ctx=ctx)
     below, above = exchange_edges(first, last, group) if world > 1 else (None, None)
+    if world > 1:  # NCCL's wait orders torch's stream only; the context may have its own
+        torch.cuda.current_stream(dev).synchronize()
     if world == 1:
         merged = api.exhaustive_slab_maxima(below, above, ctx=ctx, maxima_out=maxima_out)
         return score, best, (z0, z1), merged, visits
