@@ -113,9 +113,9 @@ static void region_H(int shape, const double* half, double radius, const double*
     H[0] = H[4] = H[8] = (1.0 * radius) * radius; /* Identity() * r * r */
   } else {
     for (int i = 0; i < 3; ++i)
-      for (int j = 0; j < 3; ++j) /* axes * axes^T, k = 0,1,2 in order */
-        H[i * 3 + j] = (axes[i * 3 + 0] * axes[j * 3 + 0] + axes[i * 3 + 1] * axes[j * 3 + 1]) +
-                       axes[i * 3 + 2] * axes[j * 3 + 2];
+      for (int j = 0; j < 3; ++j) /* axes * axes^T: Eigen's lazy-product redux t0 + (t1 + t2) */
+        H[i * 3 + j] = axes[i * 3 + 0] * axes[j * 3 + 0] +
+                       (axes[i * 3 + 1] * axes[j * 3 + 1] + axes[i * 3 + 2] * axes[j * 3 + 2]);
   }
 }
 
@@ -170,7 +170,7 @@ int sxo_make_phantom(int nx, int ny, int nz, int bg_type, double bg_value, doubl
           } else {
             double hd[3];
             for (int i = 0; i < 3; ++i)
-              hd[i] = (Hinv[i * 3 + 0] * d[0] + Hinv[i * 3 + 1] * d[1]) + Hinv[i * 3 + 2] * d[2];
+              hd[i] = Hinv[i * 3 + 0] * d[0] + (Hinv[i * 3 + 1] * d[1] + Hinv[i * 3 + 2] * d[2]);
             inside = ((d[0] * hd[0] + d[1] * hd[1]) + d[2] * hd[2]) <= 1.0;
           }
           if (!inside) continue;

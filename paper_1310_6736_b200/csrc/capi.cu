@@ -25,11 +25,12 @@ using namespace sx;
 
 salvox_ctx::~salvox_ctx() {
   for (DevBuf* b : {&d_vol, &d_bins, &d_score, &d_best, &d_keys, &d_keys_alt, &d_cub, &d_counter,
-                    &d_maxima, &d_minmax, &d_dbg, &d_seeds, &d_dets, &d_geom, &d_sel_a, &d_sel_b,
+                    &d_maxima, &d_merge_idx, &d_minmax, &d_dbg, &d_seeds, &d_dets, &d_geom, &d_sel_a, &d_sel_b,
                     &d_sel_c, &d_sel_d, &d_visits, &d_target, &d_seek_vol, &d_seek_bins})
     b->release();
   h_stage.release();
   for (cudaEvent_t e : events) cudaEventDestroy(e);
+  if (order_event) cudaEventDestroy(order_event);
   if (copy_stream) cudaStreamDestroy(copy_stream);
   if (own_stream) cudaStreamDestroy(own_stream);
 }
@@ -81,6 +82,20 @@ extern "C" int salvox_ctx_set_stream(salvox_ctx* ctx, void* stream) {
     if (!ctx) fail(SALVOX_EINVAL, "null context");
     std::lock_guard<std::mutex> lk(ctx->mu);
     ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
+  });
+}
+
+extern "C" int salvox_ctx_wait_stream(salvox_ctx* ctx, void* stream) {
+  return guarded([&] {
+    if (!ctx) fail(SALVOX_EINVAL, "null context");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    cudaStream_t other = static_cast<cudaStream_t>(stream);
+    if (other == ctx->stream) return;  // same stream: already ordered
+    SX_CUDA(cudaSetDevice(ctx->device));
+    if (!ctx->order_event)
+      SX_CUDA(cudaEventCreateWithFlags(&ctx->order_event, cudaEventDisableTiming));
+    SX_CUDA(cudaEventRecord(ctx->order_event, other));
+    SX_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->order_event, 0));
   });
 }
 
@@ -147,7 +162,7 @@ extern "C" int salvox_make_phantom(int32_t nx, int32_t ny, int32_t nz, int32_t b
             } else {
               double hd[3];
               for (int i = 0; i < 3; ++i)
-                hd[i] = (Hi.m[i * 3] * d[0] + Hi.m[i * 3 + 1] * d[1]) + Hi.m[i * 3 + 2] * d[2];
+                hd[i] = Hi.m[i * 3] * d[0] + (Hi.m[i * 3 + 1] * d[1] + Hi.m[i * 3 + 2] * d[2]);
               inside = ((d[0] * hd[0] + d[1] * hd[1]) + d[2] * hd[2]) <= 1.0;
             }
             if (!inside) continue;

@@ -188,11 +188,11 @@ inline PhRegion phantom_region(int ri, const int dims[3], const int32_t* shape, 
     H.m[8] = half[2] * half[2];
   } else if (g.shape == 1) {  // Identity() * r * r
     H.m[0] = H.m[4] = H.m[8] = (1.0 * radius[ri]) * radius[ri];
-  } else {  // axes * axes^T
+  } else {  // axes * axes^T (Eigen's lazy-product redux: t0 + (t1 + t2))
     const double* a = axes + 9 * ri;
     for (int i = 0; i < 3; ++i)
       for (int j = 0; j < 3; ++j)
-        H.m[i * 3 + j] = (a[i * 3] * a[j * 3] + a[i * 3 + 1] * a[j * 3 + 1]) + a[i * 3 + 2] * a[j * 3 + 2];
+        H.m[i * 3 + j] = a[i * 3] * a[j * 3] + (a[i * 3 + 1] * a[j * 3 + 1] + a[i * 3 + 2] * a[j * 3 + 2]);
   }
   double ext[3];
   for (int i = 0; i < 3; ++i) ext[i] = g.shape == 0 ? half[i] : std::sqrt(std::max(H.m[i * 4], 0.0));

@@ -405,8 +405,8 @@ __device__ __forceinline__ bool ph_inside(const PhDev& g, int x, int y, int z) {
   double hd[3];
 #pragma unroll
   for (int i = 0; i < 3; ++i)
-    hd[i] = __dadd_rn(__dadd_rn(__dmul_rn(g.Hi[i * 3], d0), __dmul_rn(g.Hi[i * 3 + 1], d1)),
-                      __dmul_rn(g.Hi[i * 3 + 2], d2));
+    hd[i] = __dadd_rn(__dmul_rn(g.Hi[i * 3], d0),  // Eigen's lazy-product redux t0 + (t1 + t2)
+                      __dadd_rn(__dmul_rn(g.Hi[i * 3 + 1], d1), __dmul_rn(g.Hi[i * 3 + 2], d2)));
   return __dadd_rn(__dadd_rn(__dmul_rn(d0, hd[0]), __dmul_rn(d1, hd[1])), __dmul_rn(d2, hd[2])) <= 1.0;
 }
 
