@@ -153,8 +153,9 @@ class ClockSampler:
 # ------------------------------------------------------------------ reference arm
 def cpu_sample_run(vol, threads, planes):
     """The oracle's literal restatement of pipeline.cpp:63-166 (fp64, the reference's loop
-    order) on a bounded sample: `planes` full central z-planes of the same volume, split
-    row-wise over `threads` host threads."""
+    order; its maps are bit-identical to the reference's own, tests/test_ref_pin.py) on a
+    bounded sample: `planes` full central z-planes of the same volume, split row-wise over
+    `threads` host threads."""
     from oracle import oracle as O
     nz, ny, nx = vol.shape
     z0 = nz // 2 - planes // 2
@@ -167,14 +168,68 @@ def cpu_sample_run(vol, threads, planes):
                         f"({nx * ny * planes} voxels x 13 scales, {dt:.1f} s)")
 
 
+def reference_calibration(vol, n=16):
+    """The timed port against the reference ITSELF (oracle/_ref/libsalvox_ref.so: the
+    reference's own pipeline.cpp compiled here) on the same whole n^3 sub-volume, one
+    thread each: the maps must be bit-identical and the ratio says how the port's
+    speed relates to the reference's (the reference's exhaustive pass is
+    single-threaded; the port's plane samples are what the arm can afford)."""
+    from oracle import oracle as O
+    from oracle import ref as R
+    if not R.available():
+        return {"available": False, "why": "oracle/_ref/libsalvox_ref.so not built"}
+    nz, ny, nx = vol.shape
+    c = np.ascontiguousarray(vol[nz // 2 - n // 2: nz // 2 + n // 2,
+                                 ny // 2 - n // 2: ny // 2 + n // 2,
+                                 nx // 2 - n // 2: nx // 2 + n // 2])
+    tr = tp = float("inf")
+    for _ in range(2):  # alternating, best of 2 each (shared host cores are noisy)
+        t0 = time.perf_counter()
+        rs, rb, _, _ = R.exhaustive(c, LOW, HIGH, BINS, SCALES, budget=10**15)
+        tr = min(tr, time.perf_counter() - t0)
+        t0 = time.perf_counter()
+        ps, pb, _ = O.exhaustive(c, LOW, HIGH, BINS, SCALES, budget=10**15, mode="literal",
+                                 threads=1)
+        tp = min(tp, time.perf_counter() - t0)
+    evals = c.size * len(SCALES)
+    return {"sample": f"central {n}^3 sub-volume of the same volume, whole-volume call, 1 thread",
+            "reference_evals_per_s": evals / tr, "port_evals_per_s": evals / tp,
+            "port_speed_over_reference": tr / tp,
+            "maps_bit_identical": bool(rs.tobytes() == ps.tobytes() and
+                                       rb.tobytes() == pb.tobytes())}
+
+
+def reference_seed_grid(steps, threads):
+    """The reference's own detect() (oracle/_ref; pipeline.cpp:311-402, shift, its
+    parallel_for over `threads` workers) on the C3 seed grid: volumes/s."""
+    from oracle import ref as R
+    if not R.available():
+        return None
+    vol, _ = R.make_phantom(c3_spec())
+    kw = dict(method="shift", seed_spacing=16.0, scales=[8.0, 12.0], top_k=20, dedupe_radius=5.0,
+              workers=threads)
+    R.detect(vol, 0.0, 64.0, 64, **kw)
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        sel, _ = R.detect(vol, 0.0, 64.0, 64, **kw)
+        times.append(time.perf_counter() - t0)
+    ms = float(np.mean(times)) * 1e3
+    return {"metric": "seed-grid volumes/sec", "value": 1e3 / ms, "unit": "volumes/s",
+            "ms_per_volume": ms, "kind": "reference", "cores": threads,
+            "config": {"workload": "C3 256x256x160 MR phantom, shift mean-shift, 64 bins, "
+                                   "lattice 16 x scales {8, 12} = 5120 seeds",
+                       "selected": int(len(sel))}}
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return
     from paper_1310_6736_b200 import api
     vol, _ = api.make_phantom(weak_spec(world))
     threads = os.cpu_count() or 1
-    # ~5-10 s per step on the box's cores: threads/2 planes of 256^2 voxels
-    planes = max(1, (threads // 2) * 65536 // (vol.shape[1] * vol.shape[2]))
+    # ~4-8 s per step on the box's cores: threads/4 planes of 256^2 voxels
+    planes = max(1, (threads // 4) * 65536 // (vol.shape[1] * vol.shape[2]))
     for _ in range(min(args.warmup, 1)):
         cpu_sample_run(vol, threads, 1)
     vals = []
@@ -183,6 +238,7 @@ def run_reference(args, rank, world):
         vals.append(v)
     value = float(np.mean(vals))
     total_evals = float(np.prod(vol.shape)) * len(SCALES)
+    cal = reference_calibration(vol)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup,
@@ -191,12 +247,20 @@ def run_reference(args, rank, world):
         "config": {"workload": weak_workload(world, vol.shape[::-1]),
                    "sample_per_step": sample},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": sample},
+                         "sample": sample, "reference_calibration": cal},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "note": "reference C++ is unbuildable here (Eigen3/vendor absent); the literal oracle "
-                "restatement (oracle/salvox_oracle.c, fp64, reference loop order) is timed on "
-                "rank 0's host cores; ms_per_step extrapolates the sample to one full pass",
+        "note": "the reference's exhaustive pass (pipeline.cpp:63-166) is single-threaded and "
+                "can only score whole volumes, so each step times the literal port "
+                "(oracle/salvox_oracle.c: fp64, the reference's loop order, bit-identical maps) "
+                "on a plane sample of the same volume on ALL of rank 0's host cores; "
+                "reference_calibration times the reference itself (oracle/_ref, compiled from "
+                "its own sources) against the port on one identical sub-volume, single-threaded "
+                "(port_speed_over_reference > 1: this arm overstates the reference). "
+                "ms_per_step extrapolates the sample to one full pass",
     }
+    sg = reference_seed_grid(3, threads)
+    if sg is not None:
+        line["seed_grid"] = sg
     print(json.dumps(line), flush=True)
 
 
@@ -355,7 +419,8 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
         val, sample = cpu_sample_run(vol, threads, threads)
-        cpu = {"value": val, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample}
+        cpu = {"value": val, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample,
+               "reference_calibration": reference_calibration(vol)}
 
     if rank == 0:
         achieved = kb_updates / (kb_ms * 1e-3) if kb_ms > 0 else None

@@ -157,6 +157,11 @@ SALVOX_API int salvox_ctx_destroy(salvox_ctx* ctx);
 /* Binds the context to an external CUDA stream (cudaStream_t as void*); NULL
  * restores the context's own stream. Device-pointer entry points run on it. */
 SALVOX_API int salvox_ctx_set_stream(salvox_ctx* ctx, void* stream);
+/* Orders the context's stream after the work already queued on `stream`
+ * (cudaStream_t as void*): an event recorded on `stream`, waited on by the
+ * context's stream (no host synchronisation). Callers that produce device
+ * inputs on another stream call this before a device-pointer entry point. */
+SALVOX_API int salvox_ctx_wait_stream(salvox_ctx* ctx, void* stream);
 /* Number of this library's kernel launches issued through ctx so far. */
 SALVOX_API int salvox_ctx_launch_count(salvox_ctx* ctx, uint64_t* out);
 

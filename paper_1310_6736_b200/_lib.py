@@ -113,7 +113,8 @@ ABMSOD_ITER_DTYPE = np.dtype([("position", "<f8", (3,)), ("H", "<f8", (9,)),
 # Every symbol include/salvox_capi.h declares (checked by tests/test_capi_symbols.py).
 EXPORTS = [
     "salvox_last_error", "salvox_version", "salvox_ctx_create", "salvox_ctx_destroy",
-    "salvox_ctx_set_stream", "salvox_ctx_launch_count", "salvox_exhaustive",
+    "salvox_ctx_set_stream", "salvox_ctx_wait_stream", "salvox_ctx_launch_count",
+    "salvox_exhaustive",
     "salvox_exhaustive_slab", "salvox_exhaustive_device", "salvox_exhaustive_slab_device",
     "salvox_exhaustive_slab_scores", "salvox_exhaustive_slab_edges",
     "salvox_exhaustive_slab_maxima", "salvox_last_maxima", "salvox_last_maxima_device",
@@ -161,6 +162,7 @@ def _declare(L):
     L.salvox_ctx_create.argtypes = [C.c_int, C.POINTER(_vp)]
     L.salvox_ctx_destroy.argtypes = [_vp]
     L.salvox_ctx_set_stream.argtypes = [_vp, _vp]
+    L.salvox_ctx_wait_stream.argtypes = [_vp, _vp]
     L.salvox_ctx_launch_count.argtypes = [_vp, _pu64]
     L.salvox_exhaustive.argtypes = [_vp, _vp, _i32, _i32, _i32, C.POINTER(Window), _vp, _i32, _i32,
                                     _u64, _vp, _vp, _vp, _i64, _pi64, _pu64]
@@ -236,6 +238,23 @@ class Context:
 
     def set_stream(self, stream_ptr):
         check(load().salvox_ctx_set_stream(self._h, _vp(stream_ptr) if stream_ptr else None))
+
+    def wait_stream(self, stream_ptr):
+        """Orders this context's stream after the work queued on `stream_ptr`."""
+        check(load().salvox_ctx_wait_stream(self._h, _vp(stream_ptr)))
+
+    def after_torch(self, *tensors):
+        """Device-tensor entry points read torch tensors that torch's current stream
+        may still be producing (.contiguous(), non_blocking copies, torch.cat, ...):
+        order the context's stream after it (no-op when the context is bound to it
+        or no tensor is on the GPU)."""
+        dev = next((t.device for t in tensors if t is not None and getattr(t, "is_cuda", False)),
+                   None)
+        if dev is None:
+            return
+        import torch
+
+        self.wait_stream(torch.cuda.current_stream(dev).cuda_stream)
 
     def launch_count(self) -> int:
         out = C.c_uint64(0)

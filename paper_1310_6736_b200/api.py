@@ -172,6 +172,7 @@ def exhaustive_slab_scores(slab, nz_total, zs0, z0, z1, scales, window_low, wind
         else:
             score = torch.empty((z1 - z0, ny, nx), dtype=torch.float32, device=s.device)
             best = torch.empty_like(score)
+        c.after_torch(s, score, best)  # inputs/outputs may still be in use on torch's stream
         sp, op, bp = C.c_void_p(s.data_ptr()), C.c_void_p(score.data_ptr()), C.c_void_p(best.data_ptr())
     else:
         s = np.ascontiguousarray(slab, dtype=np.float32)
@@ -193,6 +194,7 @@ def exhaustive_slab_scores(slab, nz_total, zs0, z0, z1, scales, window_low, wind
 def exhaustive_slab_edges(first, last, ctx=None):
     """Step 2: the first / last owned score planes into device tensors (nx*ny floats)."""
     c = _ctx(ctx)
+    c.after_torch(first, last)
     check(_lib.load().salvox_exhaustive_slab_edges(
         c.handle, C.c_void_p(first.data_ptr()) if first is not None else None,
         C.c_void_p(last.data_ptr()) if last is not None else None))
@@ -203,6 +205,7 @@ def exhaustive_slab_maxima(below, above, ctx=None, maxima_out=None, on_device=Fa
     (`below`) and z1 (`above`) as device tensors (None at the volume ends).
     on_device=True leaves them on the device and returns their count."""
     c = _ctx(ctx)
+    c.after_torch(below, above)  # e.g. planes just received by NCCL on torch's stream
     if on_device:
         n = C.c_int64(0)
         check(_lib.load().salvox_exhaustive_slab_maxima(
@@ -231,6 +234,7 @@ def last_maxima_device(out, ctx=None):
     """The last exhaustive call's maxima into a CUDA uint8 tensor of shape (cap, 48)
     (salvox_last_maxima_device); returns the full count."""
     c = _ctx(ctx)
+    c.after_torch(out)
     n = C.c_int64(0)
     check(_lib.load().salvox_last_maxima_device(c.handle, C.c_void_p(out.data_ptr()),
                                                 int(out.shape[0]), C.byref(n)))
@@ -243,6 +247,7 @@ def merge_maxima_device(records, ctx=None):
     import torch
     c = _ctx(ctx)
     out = torch.empty_like(records)
+    c.after_torch(records, out)
     check(_lib.load().salvox_merge_maxima_device(c.handle, C.c_void_p(records.data_ptr()),
                                                  int(records.shape[0]), C.c_void_p(out.data_ptr())))
     return out
@@ -360,7 +365,8 @@ def detect_batch_device(d_volumes, batch, shape_zyx, method="shift", seed_spacin
                         window_high=None, bins=64, entropy_quantile=0.9, pdf_quantile=0.0,
                         workers=1, ctx=None, **extra):
     """detect() over `batch` device-resident volumes stored back to back at the
-    device address d_volumes (an int, e.g. torch_tensor.data_ptr()): one seek
+    device address d_volumes (a CUDA tensor, or an int address whose producer the
+    caller has already synchronised): one seek
     launch covers every volume -> ([selected DET_DTYPE per volume], visits)."""
     nz, ny, nx = shape_zyx if len(shape_zyx) == 3 else (1,) + tuple(shape_zyx)
     iw = _window(window_low, window_high, bins)
@@ -370,8 +376,12 @@ def detect_batch_device(d_volumes, batch, shape_zyx, method="shift", seed_spacin
     out = np.empty(max(batch, 1) * kk, DET_DTYPE)
     n_out = np.zeros(max(batch, 1), np.int64)
     visits = C.c_uint64(0)
+    c = _ctx(ctx)
+    if hasattr(d_volumes, "data_ptr"):  # a torch tensor: order after its producer
+        c.after_torch(d_volumes)
+        d_volumes = d_volumes.data_ptr()
     check(_lib.load().salvox_detect_batch_device(
-        _ctx(ctx).handle, C.c_void_p(int(d_volumes)), int(batch), nx, ny, nz, C.byref(iw),
+        c.handle, C.c_void_p(int(d_volumes)), int(batch), nx, ny, nz, C.byref(iw),
         C.byref(P), ptr(out), kk, ptr(n_out), C.byref(visits)))
     del keep
     return [out[v * kk: v * kk + n_out[v]].copy() for v in range(batch)], int(visits.value)
@@ -720,7 +730,9 @@ def make_phantom_device(spec, device=0, out=None, ctx=None):
           or not out.is_contiguous()):
         raise ValueError("make_phantom_device: out must be a contiguous CUDA float32 [z, y, x] tensor")
     cent = np.zeros(3 * max(nreg, 1))
-    check(_lib.load().salvox_make_phantom_device(_ctx(ctx).handle, *head,
+    c = _ctx(ctx)
+    c.after_torch(out)
+    check(_lib.load().salvox_make_phantom_device(c.handle, *head,
                                                  *(ptr(a) for a in arrays), seed,
                                                  C.c_void_p(out.data_ptr()), ptr(cent)))
     gt = [{"center": tuple(cent[3 * i:3 * i + 3]), "H": Hs[i]} for i in range(nreg)]

@@ -115,6 +115,11 @@ struct salvox_ctx {
   std::vector<cudaEvent_t> events;     // pipeline events (grown on demand)
   std::mutex mu;
   uint64_t launches = 0;
+  cudaEvent_t order_event = nullptr;  // salvox_ctx_wait_stream
+  // bumped by every exhaustive setup: a pending exchange-form scores call
+  // (salvox_exhaustive_slab_scores) is valid only while nothing else has reused
+  // d_score / d_best on this context
+  uint64_t exh_generation = 0;
   // kb_kernel timing (salvox_ctx_set_profiling)
   bool profiling = false;
   double kb_ms_total = 0.0;

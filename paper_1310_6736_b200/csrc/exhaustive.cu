@@ -1739,6 +1739,7 @@ struct ExhRun {
   float* score_base = nullptr;
   float* best_base = nullptr;
   bool exch = false;
+  uint64_t generation = 0;  // ctx->exh_generation when this run was set up
 };
 
 void upload_tables(salvox_ctx* ctx, const Plan& pl, bool quad = false) {
@@ -1825,6 +1826,7 @@ ExhRun setup_exhaustive(salvox_ctx* ctx, int nx, int ny, int nz, int zs0, int zs
                         int bins, const double* scales, int n_scales, bool exch = false) {
   const bool two_d = nz == 1;
   ExhRun run;
+  run.generation = ++ctx->exh_generation;  // invalidates any pending exchange-form run
   run.tc = pick_tile(bins, two_d);
   int SY = 0, SZ = 0;
   run.pl = cached_plan(scales, n_scales, two_d, run.tc, &SY, &SZ);
@@ -2301,6 +2303,12 @@ extern "C" int salvox_exhaustive_slab_edges(salvox_ctx* ctx, float* d_first, flo
       auto it = g_exch_runs.find(ctx);
       if (it == g_exch_runs.end()) fail(SALVOX_EINVAL, "exhaustive slab edges: no pending scores call");
       run = it->second;
+      if (run.generation != ctx->exh_generation) {
+        g_exch_runs.erase(it);
+        fail(SALVOX_EINVAL,
+             "exhaustive slab edges: another exhaustive call on this context replaced the pending "
+             "scores");
+      }
     }
     SX_CUDA(cudaSetDevice(ctx->device));
     const size_t plane = (size_t)run.kp.nx * run.kp.ny;
@@ -2326,6 +2334,10 @@ extern "C" int salvox_exhaustive_slab_maxima(salvox_ctx* ctx, const float* d_bel
       if (it == g_exch_runs.end()) fail(SALVOX_EINVAL, "exhaustive slab maxima: no pending scores call");
       run = it->second;
       g_exch_runs.erase(it);
+      if (run.generation != ctx->exh_generation)
+        fail(SALVOX_EINVAL,
+             "exhaustive slab maxima: another exhaustive call on this context replaced the pending "
+             "scores");
     }
     SX_CUDA(cudaSetDevice(ctx->device));
     const size_t plane = (size_t)run.kp.nx * run.kp.ny;

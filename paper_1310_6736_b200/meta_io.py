@@ -94,6 +94,7 @@ def load_volume_device(path, device=0, ctx=None):
     out = torch.empty((dims[2], dims[1], dims[0]), dtype=torch.float32,
                       device=torch.device("cuda", device))
     c = _ctx(ctx)
+    c.after_torch(out)
     raw = np.ascontiguousarray(data)
     _lib.check(_lib.load().salvox_upload_widen(c.handle, C.c_int32(code),
                                                raw.ctypes.data_as(C.c_void_p),

@@ -4,12 +4,14 @@ seed interleave for the seed-grid detector.
 One process per GPU (torch.distributed, NCCL over NVLink on the box; gloo in the
 CPU tests). Rank g owns planes [z_g, z_{g+1}); it bins the planes
 [z_g - R - 1, z_{g+1} + R + 1) (halo R = max scale + 1), scores its owned planes
-plus one neighbour plane each side (so strict 26-neighbour maxima are decided
-locally, no score exchange) and selects its maxima. The only collective is ONE
-all-gather of the per-slab maxima records (fixed-capacity tensors: counts first,
-then the padded records), followed by a merge in the reference's stable order
-(score descending, linear index ascending -- pipeline.cpp:163-164), so every
-N-GPU result is byte-identical to the 1-GPU one.
+only (whole 8-plane tile layers), swaps one boundary score plane with each
+neighbour (exchange_edges: NCCL send/recv) so strict 26-neighbour maxima are
+decided locally, and selects its maxima. ONE all-gather of the per-slab maxima
+records (counts first, then the padded records) and a merge in the reference's
+stable order (score descending, linear index ascending -- pipeline.cpp:163-164)
+give every rank the 1-GPU list. (Byte-identity with the 1-GPU call is tested on
+CPU with gloo and on one GPU with the ranks' slabs run one after another and
+gloo staging; a real multi-GPU NCCL run has not been available.)
 
 detect_sharded replicates the volume and gives rank g the plan positions
 j % N == g (interleaved for balance: neighbouring seeds have similar
@@ -25,6 +27,19 @@ import math
 import numpy as np
 
 from ._lib import DET_DTYPE, MAX_DTYPE
+
+
+def collective_device(group=None, device=None):
+    """Where a collective's tensors must live: NCCL moves device memory only
+    (the given device, else the current CUDA device), gloo host memory only."""
+    import torch
+    import torch.distributed as dist
+
+    if dist.get_backend(group) == "nccl":
+        if device is not None and torch.device(device).type == "cuda":
+            return torch.device(device)
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cpu")
 
 
 def halo_radius(scales) -> int:
@@ -77,7 +92,7 @@ def allgather_maxima(local: np.ndarray, group=None, device=None) -> np.ndarray:
     import torch.distributed as dist
 
     world = dist.get_world_size(group)
-    dev = device if device is not None else torch.device("cpu")
+    dev = collective_device(group, device)
     cnt = torch.tensor([len(local)], dtype=torch.int64, device=dev)
     cnts = [torch.zeros_like(cnt) for _ in range(world)]
     dist.all_gather(cnts, cnt, group=group)
@@ -141,15 +156,15 @@ def allgather_maxima_device(n_local, group=None, device=None, ctx=None):
     cnts = [torch.zeros_like(cnt) for _ in range(world)]
     dist.all_gather(cnts, cnt, group=group)
     counts = [int(c) for c in torch.cat(cnts).cpu().tolist()]
-    buf = torch.zeros((max(max(counts), 1), MAX_DTYPE.itemsize), dtype=torch.uint8, device=device)
+    # rows past each rank's count are never read: no fill needed. The context
+    # orders its stream after torch's (Context.after_torch) before writing it.
+    buf = torch.empty((max(max(counts), 1), MAX_DTYPE.itemsize), dtype=torch.uint8, device=device)
     api.last_maxima_device(buf, ctx=ctx)
     buf_c = buf if coll == device else buf.cpu()
     bufs = [torch.empty_like(buf_c) for _ in range(world)]
     dist.all_gather(bufs, buf_c, group=group)
     cat = torch.cat([b[:c] for b, c in zip(bufs, counts)]).to(device)
-    # the context may run on its own stream: the gathered records must be complete
-    torch.cuda.current_stream(device).synchronize()
-    return api.merge_maxima_device(cat, ctx=ctx)
+    return api.merge_maxima_device(cat, ctx=ctx)  # ordered after the gather on torch's stream
 
 
 def exhaustive_exchange(volume, scales, window_low, window_high, bins=64, budget=None, group=None,
@@ -182,9 +197,9 @@ def exhaustive_exchange(volume, scales, window_low, window_high, bins=64, budget
     first = torch.empty((ny, nx), dtype=torch.float32, device=dev)
     last = torch.empty_like(first)
     api.exhaustive_slab_edges(first, last, ctx=ctx)
+    # NCCL's wait orders torch's stream; the maxima call orders the context's
+    # stream after it (Context.after_torch), so no host synchronisation here
     below, above = exchange_edges(first, last, group) if world > 1 else (None, None)
-    if world > 1:  # NCCL's wait orders torch's stream only; the context may have its own
-        torch.cuda.current_stream(dev).synchronize()
     if world == 1:
         merged = api.exhaustive_slab_maxima(below, above, ctx=ctx, maxima_out=maxima_out)
         return score, best, (z0, z1), merged, visits
@@ -259,7 +274,7 @@ def allgather_detections(local: np.ndarray, n_total: int, group=None, device=Non
     import torch.distributed as dist
 
     world = dist.get_world_size(group)
-    dev = device if device is not None else torch.device("cpu")
+    dev = collective_device(group, device)
     cap = (n_total + world - 1) // world
     raw = np.zeros((max(cap, 1), DET_DTYPE.itemsize), np.uint8)
     if len(local):
@@ -297,7 +312,7 @@ def detect_sharded(volume: np.ndarray, method="shift", seed_spacing=16.0, scales
     local, n_total, visits = compute(rank, world)
     if world > 1:
         all_dets = allgather_detections(local, n_total, group, device)
-        dev = device if device is not None else torch.device("cpu")
+        dev = collective_device(group, device)
         v = torch.tensor([visits], dtype=torch.int64, device=dev)
         dist.all_reduce(v, group=group)
         visits = int(v.item())

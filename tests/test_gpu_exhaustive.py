@@ -178,6 +178,67 @@ def test_exchange_slabs_reproduce_full_volume(sx, oracle, device_resident):
         c.close()
 
 
+def test_exchange_pending_run_invalidated_by_other_call(sx, oracle):
+    """A scores call leaves a pending run that points into the context's score
+    buffers; any other exhaustive call on the same context reuses them, so the
+    edges / maxima steps must then fail (generation check) instead of reading
+    stale or freed device memory."""
+    import torch
+
+    from paper_1310_6736_b200 import api
+    from paper_1310_6736_b200._lib import Context
+
+    vol, _ = oracle.make_phantom(phantoms.ball_3d(24, (12.0, 11.0, 12.0), 5.0, 3))
+    other, _ = oracle.make_phantom(phantoms.ball_3d(40, (19.0, 20.0, 18.0), 7.0, 12))
+    nz, ny, nx = vol.shape
+    c = Context(0)
+    first = torch.empty((ny, nx), dtype=torch.float32, device="cuda")
+    for step in ("edges", "maxima"):
+        api.exhaustive_slab_scores(vol, nz, 0, 0, nz, [3.0, 4.0], 0, 64, 64, budget=10**9, ctx=c)
+        sx.kadir_brady_exhaustive_records(other, [3.0, 5.0, 7.0], 0, 64, 64, budget=10**9, ctx=c)
+        with pytest.raises(ValueError, match="replaced the pending scores"):
+            if step == "edges":
+                api.exhaustive_slab_edges(first, first, ctx=c)
+            else:
+                api.exhaustive_slab_maxima(None, None, ctx=c)
+    # an uninterrupted sequence still works on the same context
+    s, _, _ = api.exhaustive_slab_scores(vol, nz, 0, 0, nz, [3.0, 4.0], 0, 64, 64, budget=10**9,
+                                         ctx=c)
+    api.exhaustive_slab_edges(first, first, ctx=c)
+    m = api.exhaustive_slab_maxima(None, None, ctx=c)
+    ref_s, _, ref_m, _ = sx.kadir_brady_exhaustive_records(vol, [3.0, 4.0], 0, 64, 64,
+                                                           budget=10**9)
+    assert np.array_equal(s, ref_s) and np.array_equal(m, ref_m)
+    c.close()
+
+
+def test_device_inputs_ordered_after_torch_stream(sx, oracle):
+    """Device-tensor entry points on a context with its OWN stream read tensors
+    that torch's current stream is still producing: the context orders its stream
+    after torch's (Context.after_torch) -- here the slab is written by a torch op
+    queued behind a ~0.3 s sleep kernel, so an unordered read would see garbage."""
+    import torch
+
+    from paper_1310_6736_b200 import api
+    from paper_1310_6736_b200._lib import Context
+
+    vol, _ = oracle.make_phantom(phantoms.ball_3d(32, (16.0, 15.0, 14.0), 6.0, 7))
+    nz = vol.shape[0]
+    ref_s, ref_b, _ = api.exhaustive_slab_scores(vol, nz, 0, 0, nz, [3.0, 5.0], 0, 64, 64,
+                                                 budget=10**9)
+    c = Context(0)  # own non-blocking stream, not torch's
+    src = torch.from_numpy(vol).cuda()
+    torch.cuda.synchronize()
+    for _ in range(3):
+        torch.cuda._sleep(600_000_000)
+        slab = src * 1.0  # produced on torch's stream after the sleep
+        s, b, _ = api.exhaustive_slab_scores(slab, nz, 0, 0, nz, [3.0, 5.0], 0, 64, 64,
+                                             budget=10**9, ctx=c)
+        assert np.array_equal(s.cpu().numpy(), ref_s) and np.array_equal(b.cpu().numpy(), ref_b)
+        del slab
+    c.close()
+
+
 def test_device_maxima_merge(sx, oracle):
     """salvox_merge_maxima_device sorts records into the reference's order (score
     desc, linear index asc) like the host merge; allgather_maxima_device (here in
