@@ -151,6 +151,7 @@ struct KbParams {
   int bins;
   uint32_t tile_bytes;
   int lag;          // kb_quad_kernel: warps 4-7 start the walk this many cycles late
+  int lagmode;      // 0: warps 4-7 by lag; 1: warp w by w*lag/4; 3: (w%4)*lag/8 + (w/4)*lag
   float* score;     // planes [zc0, zc1)
   float* best;
   const long long* dbg_vox;  // debug launch: one block per voxel
@@ -1014,8 +1015,10 @@ __device__ __noinline__ void quad_walk_dbl(const uint8_t* tb, uint32_t c, int g,
   quad_run_t<NB, G, QuadDbl<1>>(tb, c, d.x, d.y);
 }
 
-// DBL: singles + x-adjacent doubles (variant 4, the default) or singles only (3)
-template <int NB, bool DBG, bool DBL>
+// DBL: singles + x-adjacent doubles (variant 4, the default) or singles only (3).
+// VB: voxels per boundary iteration (1: one voxel's math at a time, the state
+// rotating through slot 0; 2: two voxels' bins interleaved for ILP)
+template <int NB, bool DBG, bool DBL, int VB = 1>
 __global__ void __launch_bounds__(256, 1)
     kb_quad_kernel(const __grid_constant__ CUtensorMap tmap, const KbParams p) {
   constexpr int TX = 16, TY = 8, TZ = 8, NT = 256, NV = 1024;
@@ -1120,10 +1123,15 @@ __global__ void __launch_bounds__(256, 1)
   int g = 0;
   const bool warp_live = __any_sync(0xffffffffu, rowv && gx < p.nx);
   const int n_radii = warp_live ? p.n_radii : 0;
-  if (warp >= 4 && p.lag > 0) {  // offset the two warps of each sub-partition so their
-    // radius boundaries (little shared-pipe work) overlap the other warp's walk
-    const long long t0 = clock64();
-    while (clock64() - t0 < p.lag) __nanosleep(256);
+  {  // offset the two warps of each sub-partition so their radius boundaries
+    // (little shared-pipe work) overlap the other warp's walk
+    const int lag = p.lagmode == 1   ? warp * p.lag / 4
+                    : p.lagmode == 3 ? (warp & 3) * p.lag / 8 + (warp >> 2) * p.lag
+                                     : (warp >= 4 ? p.lag : 0);
+    if (lag > 0) {
+      const long long t0 = clock64();
+      while (clock64() - t0 < lag) __nanosleep(256);
+    }
   }
   for (int i = 0; i < n_radii; ++i) {
     const KbBound bd = c_bounds[i];
@@ -1156,6 +1164,121 @@ __global__ void __launch_bounds__(256, 1)
     // state rotates through slot 0 and is back in place after the 4 voxels
     // The live columns of voxel v + 1 are loaded while voxel v's math runs
     // (their loads queue behind the other warps' atomics).
+    if constexpr (VB == 2) {
+      // two voxels per iteration: their columns, TMEM slots and per-bin terms are
+      // independent, so the two chains interleave (the boundary is latency-bound)
+#pragma unroll 1
+      for (int vp = 0; vp < 4; vp += 2) {
+        uint32_t cur[2][NS], T[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const uint32_t* hc =
+              reinterpret_cast<const uint32_t*>(hist + ((vp + u) * 4 + G) * PANEL) + col;
+          T[u] = bd.W - hc[0];
+#pragma unroll
+          for (int j = 0; j < NS; ++j) cur[u][j] = hc[(1 + j) * 64];
+        }
+        bool doH[2], doE[2];
+        float invT[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          doH[u] = (bd.flags & 1) && T[u] > 0u;
+          doE[u] = (bd.flags & 2) && T[u] > 0u && TA[u] > 0u && TB[u] > 0u;
+          invT[u] = doH[u] ? 1.0f / (float)T[u] : 0.f;
+        }
+        uint32_t a[2][NS];
+        const uint32_t slot0 = lane_base + 64u * vp + (uint32_t)(32 * older);
+        if constexpr (NS == 32) {
+          tm_ld32(slot0, a[0]);
+          tm_ld32(slot0 + 64u, a[1]);
+        } else {
+#pragma unroll
+          for (int c = 0; c < NS; c += 8) {
+            tm_ld8(slot0 + c, a[0] + c);
+            tm_ld8(slot0 + 64u + c, a[1] + c);
+          }
+        }
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+          for (int j = 0; j < NS; ++j) asm volatile("" : "+r"(a[u][j]));
+        if constexpr (NS == 32) {
+          tm_st32(slot0, cur[0]);
+          tm_st32(slot0 + 64u, cur[1]);
+        } else {
+#pragma unroll
+          for (int c = 0; c < NS; c += 8) {
+            tm_st8(slot0 + c, cur[0] + c);
+            tm_st8(slot0 + 64u + c, cur[1] + c);
+          }
+        }
+        float hacc[2] = {0.f, 0.f};
+        uint32_t dom[2] = {0u, 0u};
+        unsigned long long num[2] = {0ull, 0ull};
+        {
+          const bool wH = bd.flags & 1, wE = bd.flags & 2;  // warp-uniform
+          float h4[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+          long long q[2][2] = {{0, 0}, {0, 0}};
+          const int ta[2] = {(int)TA[0], (int)TA[1]}, nt[2] = {-(int)T[0], -(int)T[1]};
+#pragma unroll
+          for (int c = 0; c < NS; c += 8) {
+            uint32_t orv = 0u;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) orv |= cur[0][c + j] | cur[1][c + j];
+            if (!__any_sync(0xffffffffu, orv != 0u)) continue;
+#pragma unroll
+            for (int j = c; j < c + 8; ++j) {
+#pragma unroll
+              for (int u = 0; u < 2; ++u) {
+                const uint32_t cv = cur[u][j];
+#ifndef KB_SKIP_MATH
+                if (wH) {
+                  dom[u] = max(dom[u], cv);
+                  h4[u][j & 3] -= ent_term((float)cv * invT[u]);
+                }
+#endif
+#ifndef KB_SKIP_L1
+                if (wE) l1_pos_acc(q[u][j & 1], (int)cv, ta[u], (int)a[u][j], nt[u]);
+#endif
+              }
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            if (wH) hacc[u] = (h4[u][0] + h4[u][1]) + (h4[u][2] + h4[u][3]);
+            if (doE[u]) num[u] = 2ull * (unsigned long long)(q[u][0] + q[u][1]);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          if (DBG && vp + u == dbg_v) {
+            for (int j = 0; j < NS && j < p.bins; ++j)
+              p.dbg_out[(size_t)i * (p.bins + 1) + j] = cur[u][j];
+            p.dbg_out[(size_t)i * (p.bins + 1) + p.bins] = T[u];
+          }
+          if (doH[u] && 2u * dom[u] > T[u]) {  // dominant bin: its term again, accurately
+            const float pb = (float)dom[u] * invT[u];
+            hacc[u] += ent_term(pb);
+            hacc[u] -= pb * (log1pf(-(float)(T[u] - dom[u]) * invT[u]) * 1.4426950408889634f);
+          }
+          if (doE[u]) {
+            const double y = ((double)Hb[u] * bd.fac) *
+                             ((double)num[u] * __drcp_rn((double)T[u] * (double)TA[u]));
+            if (y > best[u] || (y == best[u] && y > 0.0 && bd.rank < best_rank[u])) {
+              best[u] = y;
+              best_s[u] = bd.scale;
+              best_rank[u] = bd.rank;
+            }
+          }
+          TA[u] = TB[u];
+          TB[u] = T[u];
+          Hb[u] = doH[u] ? fmaxf(hacc[u], 0.f) : 0.f;
+        }
+        rot4(TA), rot4(TB), rot4(Hb), rot4(best), rot4(best_s), rot4(best_rank);
+        rot4(TA), rot4(TB), rot4(Hb), rot4(best), rot4(best_s), rot4(best_rank);
+      }
+    } else {
     uint32_t nxt[NS + 1];
     {
       const uint32_t* hc = reinterpret_cast<const uint32_t*>(hist + G * PANEL) + col;
@@ -1267,6 +1390,7 @@ __global__ void __launch_bounds__(256, 1)
       rot4(best_s);
       rot4(best_rank);
     }
+    }
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");  // before the next radius' loads
     older ^= 1;
   }
@@ -1371,6 +1495,7 @@ struct TileCfg {
   bool tmem = false;  // kb_tmem_kernel (1024 threads, snapshots in TMEM)
   bool quad = false;  // kb_quad_kernel (256 threads x 4 voxels, snapshots in TMEM)
   bool dbl = false;  // kb_quad_kernel<DBL>: x-adjacent offset doubles share bin words
+  bool vb2 = false;  // kb_quad_kernel<.., VB = 2>: two voxels per boundary iteration
 };
 
 TileCfg pick_tile(int bins, bool two_d) {
@@ -1396,7 +1521,11 @@ TileCfg pick_tile(int bins, bool two_d) {
   if (mode == 1) return two_d ? TileCfg{nb, 8, 64, 1, true} : TileCfg{nb, 8, 8, 8, true};
   if (mode == 2 && !two_d) return TileCfg{nb, 16, 8, 8, false, true};
   if (mode == 3 && !two_d) return TileCfg{nb, 16, 8, 8, false, false, true};
-  if (mode == 4 && !two_d) return TileCfg{nb, 16, 8, 8, false, false, true, true};
+  static const bool vb2 = [] {  // A/B knob SALVOX_KB_VB (1 or 2)
+    const char* e = std::getenv("SALVOX_KB_VB");
+    return e && std::atoi(e) == 2;
+  }();
+  if (mode == 4 && !two_d) return TileCfg{nb, 16, 8, 8, false, false, true, true, vb2};
   return two_d ? TileCfg{nb, 32, 16, 1, false} : TileCfg{nb, 8, 8, 8, false};
 }
 
@@ -1413,6 +1542,13 @@ int kb_lag() {
     return e ? std::atoi(e) : 8000;
   }();
   return lag;
+}
+int kb_lagmode() {  // A/B knob SALVOX_KB_LAGMODE (see KbParams::lagmode)
+  static const int m = [] {
+    const char* e = std::getenv("SALVOX_KB_LAGMODE");
+    return e ? std::atoi(e) : 0;
+  }();
+  return m;
 }
 
 // Dynamic shared memory of one CTA: histogram columns, tile(s), mbarrier.
@@ -1702,7 +1838,8 @@ void dispatch_kb(salvox_ctx* ctx, const TileCfg& tc, const CUtensorMap& map, con
     return;                                                                                  \
   }
   if (tc.quad) {
-    auto k = tc.dbl ? (tc.nb == 17 ? kb_quad_kernel<17, DBG, true> : kb_quad_kernel<33, DBG, true>)
+    auto k = tc.dbl ? (tc.nb == 17 ? (tc.vb2 ? kb_quad_kernel<17, DBG, true, 2> : kb_quad_kernel<17, DBG, true, 1>)
+                                   : (tc.vb2 ? kb_quad_kernel<33, DBG, true, 2> : kb_quad_kernel<33, DBG, true, 1>))
                     : (tc.nb == 17 ? kb_quad_kernel<17, DBG, false> : kb_quad_kernel<33, DBG, false>);
     SX_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k<<<grid, 256, smem, ctx->stream>>>(map, kp);
@@ -1869,6 +2006,7 @@ ExhRun setup_exhaustive(salvox_ctx* ctx, int nx, int ny, int nz, int zs0, int zs
   kp.zc1 = zc1;
   kp.R = R;
   kp.lag = kb_lag();
+  kp.lagmode = kb_lagmode();
   kp.Rz = two_d ? 0 : R;
   kp.SY = SY;
   kp.SZ = SZ;
@@ -2488,6 +2626,7 @@ extern "C" int salvox_exhaustive_debug_hist(salvox_ctx* ctx, const int64_t* voxe
     kp.zc1 = std::min(st.nz, st.z1 + 1);
     kp.R = R;
   kp.lag = kb_lag();
+  kp.lagmode = kb_lagmode();
     kp.Rz = two_d ? 0 : R;
     kp.SY = SY;
     kp.SZ = SZ;
