@@ -83,6 +83,15 @@ std::vector<Seed> plan_seeds(const Volume& v, const SeedPlan& plan) {
 ExhaustiveResult kadir_brady_exhaustive(const Volume& v, const IntensityWindow& iw,
                                         const std::vector<double>& scales, Kernel kernel,
                                         EvalCounter* counter, uint64_t budget) {
+  // argument checks first, with the reference's messages (pipeline.cpp:66-72),
+  // so invalid calls fail the same way with or without a device
+  if (scales.empty()) throw std::invalid_argument("exhaustive scan: no scales");
+  for (double s : scales)
+    if (s < 2.0) throw std::invalid_argument("exhaustive scan: scales must be >= 2 voxels");
+  const uint64_t evals = uint64_t(v.size()) * scales.size();
+  if (evals > budget)
+    throw std::invalid_argument("exhaustive scan: budget exceeded (" + std::to_string(evals) +
+                                " voxel-scale evaluations)");
   ExhaustiveResult res;
   res.map.dims = Eigen::Vector3i(v.nx(), v.ny(), v.nz());
   res.map.score.resize(v.size());

@@ -46,10 +46,13 @@ std::vector<Detection> saliency_shift_many(const Volume& v, const std::vector<Ei
   return dets;
 }
 
+ShiftResult saliency_shift_traced(const Volume& v, const Eigen::Vector3d& seed,
+                                  const ShiftParams& params, const IntensityWindow& iw,
+                                  EvalCounter* counter);  // window.cpp
+
 ShiftResult saliency_shift(const Volume& v, const Eigen::Vector3d& seed, const ShiftParams& params,
                            const IntensityWindow& iw, EvalCounter* counter) {
-  if (params.record_trace)
-    throw unsupported_error("saliency_shift (device): record_trace is not produced on the device");
+  if (params.record_trace) return saliency_shift_traced(v, seed, params, iw, counter);
   ShiftResult r;
   r.det = saliency_shift_many(v, {seed}, params, iw, counter).front();
   r.det.seed_index = -1;

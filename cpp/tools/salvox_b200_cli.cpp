@@ -8,7 +8,9 @@
 //   salvox-b200 exhaustive --volume V.mhd --scales a,b --out MAXIMA.json [--window L:H]
 //                          [--bins N] [--budget B]
 //   salvox-b200 eval DETS.json GT.json [--out METRICS.json]   (tools/main.cpp:161-229)
+//   salvox-b200 bench [detect flags] [--repeat R]              (tools/main.cpp:231-282)
 // Exit codes: 0 success, 1 config/IO/device error, 2 detect found nothing.
+#include <algorithm>
 #include <chrono>
 #include <cstdio>
 #include <iostream>
@@ -18,6 +20,7 @@
 #include "../src/json_min.hpp"
 #include "salvox/config.hpp"
 #include "salvox/meta_io.hpp"
+#include "salvox/parallel.hpp"
 #include "salvox/phantom.hpp"
 #include "salvox/pipeline.hpp"
 #include "salvox/report.hpp"
@@ -151,6 +154,62 @@ int cmd_exhaustive(const std::map<std::string, std::string>& f) {
   return 0;
 }
 
+// bench (tools/main.cpp:231-282): detect timed per worker count {1, 2, 4, all};
+// the device path ignores the count, so every row must carry the same
+// detections checksum (FNV-1a of the compact detections array).
+int cmd_bench(std::map<std::string, std::string> f) {
+  int repeat = 3;
+  if (f.count("repeat")) {
+    repeat = std::stoi(f.at("repeat"));
+    f.erase("repeat");
+  }
+  RunConfig cfg = resolve(f);
+  if (cfg.volume_path.empty()) throw std::invalid_argument("bench: --volume is required");
+  if (repeat < 1) throw std::invalid_argument("bench: --repeat must be >= 1");
+  const Volume v = load_volume(cfg.volume_path);
+  std::vector<unsigned> counts = {1, 2, 4};
+  if (std::find(counts.begin(), counts.end(), hardware_workers()) == counts.end())
+    counts.push_back(hardware_workers());
+  json::Value rows = json::Value::array();
+  for (unsigned w : counts) {
+    RunConfig run = cfg;
+    run.workers = w;
+    std::vector<double> ms;
+    std::string checksum;
+    for (int r = 0; r < repeat; ++r) {
+      const auto t0 = std::chrono::steady_clock::now();
+      const auto dets = detect(v, run.intensity_window(v), run.detect_params());
+      ms.push_back(std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)
+                       .count());
+      const std::string body =
+          json::dump(json::parse(detection_report_json(run, v, dets, 0.0)).at("detections"));
+      checksum = fnv1a64_hex(body.data(), body.size());
+    }
+    std::sort(ms.begin(), ms.end());
+    json::Value row = json::Value::object();
+    row.set("workers", json::Value::number(double(w)));
+    json::Value runs = json::Value::array();
+    for (double t : ms) runs.push(json::Value::number(t));
+    row.set("runs_ms", runs);
+    row.set("median_ms", json::Value::number(ms[ms.size() / 2]));
+    row.set("detections_checksum", json::Value::string(checksum));
+    rows.push(row);
+  }
+  json::Value out = json::Value::object();
+  out.set("method", json::Value::string(cfg.method));
+  out.set("volume", json::Value::string(cfg.volume_path));
+  out.set("repeat", json::Value::number(double(repeat)));
+  out.set("low_confidence", json::Value::boolean(repeat < 2));
+  out.set("results", rows);
+  out.set("config", json::parse(cfg.to_json_text()));
+  const std::string text = json::dump(out, 2) + "\n";
+  if (cfg.out_path.empty())
+    std::cout << text;
+  else
+    write_file_atomic(cfg.out_path, text);
+  return 0;
+}
+
 int cmd_phantom(const std::string& spec_path, const std::string& out_path) {
   const auto [v, gt] = make_phantom(PhantomSpec::from_json_text(read_file(spec_path)));
   save_volume(v, out_path);
@@ -232,13 +291,14 @@ int cmd_eval(const std::string& dets_path, const std::string& gt_path, const std
 
 int main(int argc, char** argv) {
   if (argc < 2) {
-    std::cerr << "usage: salvox-b200 {detect|exhaustive|phantom|eval} ...\n";
+    std::cerr << "usage: salvox-b200 {detect|exhaustive|phantom|eval|bench} ...\n";
     return 1;
   }
   const std::string cmd = argv[1];
   try {
     if (cmd == "detect") return cmd_detect(parse_flags(argc, argv, 2));
     if (cmd == "exhaustive") return cmd_exhaustive(parse_flags(argc, argv, 2));
+    if (cmd == "bench") return cmd_bench(parse_flags(argc, argv, 2));
     if (cmd == "eval") {
       if (argc != 4 && argc != 6) throw std::invalid_argument("usage: salvox-b200 eval DETS.json GT.json [--out M.json]");
       std::string out;

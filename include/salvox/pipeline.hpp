@@ -10,6 +10,7 @@
 
 #include "salvox/abmsod.hpp"
 #include "salvox/detection.hpp"
+#include "salvox/phantom.hpp"
 #include "salvox/quadrant.hpp"
 #include "salvox/seeds.hpp"
 #include "salvox/shift.hpp"
@@ -82,5 +83,15 @@ std::vector<uint64_t> rasterize_window(const Volume& frame, const EllipsoidWindo
 /// Jaccard index |A∩B| / |A∪B| over sorted voxel index sets (pipeline.cpp:194-211).
 double jaccard(const std::vector<uint64_t>& a, const std::vector<uint64_t>& b);
 double jaccard(const Volume& frame, const EllipsoidWindow& win, const std::vector<uint64_t>& mask);
+
+/// The evaluation-only comparison detector of the reference (pipeline.cpp:272-309):
+/// 6-connected components of the voxels >= threshold, largest first (stable),
+/// each with its voxel count and centroid. A host utility off the hot path
+/// (DESIGN.md §7), kept so callers of the reference API find it.
+struct ThresholdComponent {
+  Eigen::Vector3d centroid = Eigen::Vector3d::Zero();
+  uint64_t voxels = 0;
+};
+std::vector<ThresholdComponent> threshold_baseline(const Volume& v, double threshold);
 
 }  // namespace salvox

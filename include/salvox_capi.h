@@ -343,6 +343,67 @@ SALVOX_API int salvox_ascent_seek(salvox_ctx* ctx, const float* volume, int32_t 
                                   int32_t max_iters, const double* seeds, int64_t n,
                                   salvox_ascent_result* out, uint64_t* visits);
 
+/* One ascent STEP per point: quadrant_step (quadrant.hpp:66-71,
+ * src/quadrant.cpp:37-81; dims = 2, nz must be 1) or the octant step (dims = 3):
+ * the moved (clamped) position in moved[3 * i] and the step's state. */
+typedef struct {
+  double entropy[8];      /* best entropy per quadrant (NE, NW, SW, SE) / octant (bits) */
+  int32_t best_scale[8];  /* its argmax scale (smallest wins ties) */
+  double norm_entropy[8]; /* entropies normalised to sum 1 (0 when degenerate) */
+  double displacement[3];
+  int32_t degenerate;     /* every quadrant carried zero entropy */
+  int32_t pad_;
+} salvox_ascent_state;
+
+SALVOX_API int salvox_ascent_step(salvox_ctx* ctx, const float* volume, int32_t nx, int32_t ny,
+                                  int32_t nz, const salvox_window* iw, int32_t dims,
+                                  const int32_t* scales, int32_t n_scales, const double* points,
+                                  int64_t n, double* moved, salvox_ascent_state* states,
+                                  uint64_t* visits);
+
+/* Window operations of the seek path, one warp per op, all ops of a call in one
+ * launch, each with the reference's fp64 operation order (bit-exact sums):
+ *   SALVOX_WOP_HIST        try_candidate_histogram (window.hpp:115-117,
+ *                          src/window.cpp:5-19): pmf -> pmf_out row, ok = 0 for
+ *                          nullopt; support = the support voxel count (the
+ *                          numerator of inbounds_support_fraction, window.cpp:54-60)
+ *   SALVOX_WOP_SHIFT_STEP  shift_step (shift.hpp:49-52, src/shift.cpp:15-34):
+ *                          value = the new position, ok = 0 for nullopt; pmf_out
+ *                          row = the candidate pmf at the old position
+ *   SALVOX_WOP_PDF_DIFF    pdf_difference (window.hpp:127-135, src/window.cpp:30-46):
+ *                          value[0]; ok = -1 degenerate scale, 0 degenerate
+ *                          flank (both thrown as std::invalid_argument)
+ *   SALVOX_WOP_BOX_ENTROPY box_entropy_bits (quadrant.hpp:58-60,
+ *                          src/quadrant.cpp:18-35) of the inclusive integer box
+ *                          inside the real corners box[6] = (x0, x1, y0, y1, z0, z1),
+ *                          0 below min_voxels; value[0]
+ * visits = what the reference call adds to its EvalCounter. */
+#define SALVOX_WOP_HIST 0
+#define SALVOX_WOP_SHIFT_STEP 1
+#define SALVOX_WOP_PDF_DIFF 2
+#define SALVOX_WOP_BOX_ENTROPY 3
+typedef struct {
+  int32_t op;
+  int32_t kernel;      /* histogram kernel (HIST, SHIFT_STEP, PDF_DIFF) */
+  int32_t step_kernel; /* SHIFT_STEP */
+  int32_t min_voxels;  /* BOX_ENTROPY */
+  double center[3];
+  double H[9];         /* bandwidth matrix, row-major (HIST, SHIFT_STEP, PDF_DIFF) */
+  double box[6];       /* BOX_ENTROPY */
+} salvox_window_op;
+typedef struct {
+  double value[3];
+  uint64_t support;
+  uint64_t visits;
+  int32_t ok;
+  int32_t pad_;
+} salvox_window_result;
+
+SALVOX_API int salvox_window_ops(salvox_ctx* ctx, const float* volume, int32_t nx, int32_t ny,
+                                 int32_t nz, const salvox_window* iw, const double* target,
+                                 const salvox_window_op* ops, int64_t n, salvox_window_result* out,
+                                 double* pmf_out);
+
 /* Thresholds + dedupe (pipeline.cpp:383-401, :54-59, :168-183) on the device. */
 SALVOX_API int salvox_select(salvox_ctx* ctx, const salvox_detection* dets, int64_t n, double q_entropy,
                   double q_pdf, int32_t k, double radius, salvox_detection* out,

@@ -13,6 +13,9 @@ from .api import (DEFAULT_BUDGET, abmsod, abmsod_records, bandwidth_from_moment,
                   saliency_shift, seek_records, select)
 
 from .api import hu_filter, hu_moments, hu_template_distance, jaccard, rasterize_window
+from .api import (ascent_step, bhattacharyya, box_entropy_bits, candidate_histogram, entropy_bits,
+                  entropy_nats, mixture_entropy, mixture_entropy_derivative, pdf_difference,
+                  shift_step, window_ops)
 from .meta_io import load_volume, load_volume_device, save_volume
 
 __version__ = "0.1.0"

@@ -105,6 +105,17 @@ class AbmsodParams(C.Structure):
     ]
 
 
+# salvox_window_op / salvox_window_result / salvox_ascent_state (include/salvox_capi.h)
+WINDOW_OP_DTYPE = np.dtype([("op", "<i4"), ("kernel", "<i4"), ("step_kernel", "<i4"),
+                            ("min_voxels", "<i4"), ("center", "<f8", (3,)), ("H", "<f8", (9,)),
+                            ("box", "<f8", (6,))])
+WINDOW_RESULT_DTYPE = np.dtype([("value", "<f8", (3,)), ("support", "<u8"), ("visits", "<u8"),
+                                ("ok", "<i4"), ("pad_", "<i4")])
+ASCENT_STATE_DTYPE = np.dtype([("entropy", "<f8", (8,)), ("best_scale", "<i4", (8,)),
+                               ("norm_entropy", "<f8", (8,)), ("displacement", "<f8", (3,)),
+                               ("degenerate", "<i4"), ("pad_", "<i4")])
+WOP_HIST, WOP_SHIFT_STEP, WOP_PDF_DIFF, WOP_BOX_ENTROPY = 0, 1, 2, 3
+
 ABMSOD_ITER_DTYPE = np.dtype([("position", "<f8", (3,)), ("H", "<f8", (9,)),
                               ("bhattacharyya", "<f8"), ("max_bhattacharyya", "<f8"),
                               ("eig_min", "<f8"), ("eig_max", "<f8")])
@@ -123,7 +134,8 @@ EXPORTS = [
     "salvox_detect_shard", "salvox_seek",
     "salvox_select", "salvox_dedupe_top_k", "salvox_plan_seeds", "salvox_make_phantom",
     "salvox_make_phantom_device",
-    "salvox_ascent_seek", "salvox_abmsod_run", "salvox_bandwidth_from_moment",
+    "salvox_ascent_seek", "salvox_ascent_step", "salvox_window_ops", "salvox_abmsod_run",
+    "salvox_bandwidth_from_moment",
     "salvox_upload_widen", "salvox_widen_device", "salvox_rasterize_window",
     "salvox_hu_moments", "salvox_hu_template_distance",
 ]
@@ -191,6 +203,10 @@ def _declare(L):
                               C.POINTER(DetectParams), _vp, _vp, _vp, _vp, _i64, _vp, _pu64]
     L.salvox_ascent_seek.argtypes = [_vp, _vp, _i32, _i32, _i32, C.POINTER(Window), _i32, _vp,
                                      _i32, _dbl, _i32, _vp, _i64, _vp, _pu64]
+    L.salvox_ascent_step.argtypes = [_vp, _vp, _i32, _i32, _i32, C.POINTER(Window), _i32, _vp,
+                                     _i32, _vp, _i64, _vp, _vp, _pu64]
+    L.salvox_window_ops.argtypes = [_vp, _vp, _i32, _i32, _i32, C.POINTER(Window), _vp, _vp, _i64,
+                                    _vp, _vp]
     L.salvox_select.argtypes = [_vp, _vp, _i64, _dbl, _dbl, _i32, _dbl, _vp, _pi64]
     L.salvox_dedupe_top_k.argtypes = [_vp, _vp, _i64, _i32, _dbl, _vp, _pi64]
     L.salvox_plan_seeds.argtypes = [_i32, _i32, _i32, _i32, _dbl, _i32, _vp, _i32, _u64, _vp, _vp,

@@ -268,6 +268,186 @@ def exhaustive_debug_hist(voxels, bins, n_scales, ctx=None):
 
 
 # --------------------------------------------------------------------- detect (E2/E3)
+# ------------------------------------------------- window operations (device)
+def window_ops(volume, ops, window_low=None, window_high=None, bins=64, target=None, ctx=None,
+               want_pmf=False):
+    """Runs WINDOW_OP_DTYPE records through salvox_window_ops (one warp per op) ->
+    (WINDOW_RESULT_DTYPE[n], pmf[n, bins] or None)."""
+    from ._lib import WINDOW_RESULT_DTYPE
+
+    v, nx, ny, nz = _volume(volume)
+    iw = _window(window_low, window_high, bins)
+    o = np.ascontiguousarray(ops)
+    out = np.zeros(max(len(o), 1), WINDOW_RESULT_DTYPE)
+    pmf = np.zeros((max(len(o), 1), int(bins))) if want_pmf else None
+    t = None if target is None else np.ascontiguousarray(histogram_from_array(target))
+    check(_lib.load().salvox_window_ops(_ctx(ctx).handle, ptr(v), nx, ny, nz, C.byref(iw), ptr(t),
+                                        ptr(o), len(o), ptr(out), ptr(pmf)))
+    return out[: len(o)], (pmf[: len(o)] if want_pmf else None)
+
+
+def _op(kind, center=(0.0, 0.0, 0.0), H=None, kernel="identity", step_kernel="identity"):
+    from ._lib import WINDOW_OP_DTYPE
+
+    o = np.zeros(1, WINDOW_OP_DTYPE)
+    o["op"] = kind
+    o["kernel"] = KERNELS[kernel]
+    o["step_kernel"] = KERNELS[step_kernel]
+    c = np.zeros(3)
+    c[: len(center)] = center
+    o["center"] = c
+    if H is not None:
+        o["H"] = np.asarray(H, np.float64).reshape(9)
+    return o
+
+
+def candidate_histogram(volume, center, H, window_low=None, window_high=None, bins=64,
+                        kernel="epanechnikov", ctx=None):
+    """candidate_histogram (py_module.cpp:125-137, window.cpp:5-27) on the device."""
+    from ._lib import WOP_HIST
+
+    r, pmf = window_ops(volume, _op(WOP_HIST, center, H, kernel), window_low, window_high, bins,
+                        ctx=ctx, want_pmf=True)
+    if not r[0]["ok"]:
+        raise ValueError("candidate_histogram: window support holds no usable in-bounds voxel")
+    return pmf[0].copy()
+
+
+def pdf_difference(volume, center, scale, window_low=None, window_high=None, bins=64,
+                   kernel="identity", ctx=None):
+    """pdf_difference (py_module.cpp:139-147, window.cpp:30-51) on the device: isotropic
+    window of the given scale (z pinned to 1 voxel for 2D arrays)."""
+    from ._lib import WOP_PDF_DIFF
+
+    v = np.asarray(volume)
+    two_d = v.ndim == 2 or v.shape[0] == 1
+    s2 = float(scale) ** 2
+    H = np.diag([s2, s2, 1.0 if two_d else s2])
+    r, _ = window_ops(volume, _op(WOP_PDF_DIFF, center, H, kernel), window_low, window_high, bins,
+                      ctx=ctx)
+    if r[0]["ok"] < 0:
+        raise ValueError("pdf_difference: degenerate scale (inner flank below 1 voxel)")
+    if r[0]["ok"] == 0:
+        raise ValueError("pdf_difference: degenerate flanking support")
+    return float(r[0]["value"][0])
+
+
+def shift_step(volume, x, half_extents, window_low=None, window_high=None, bins=64,
+               step_kernel="identity", hist_kernel="identity", target=None, ctx=None):
+    """shift_step (shift.hpp:49-52, shift.cpp:15-34) on the device -> new position or None."""
+    from ._lib import WOP_SHIFT_STEP
+
+    v = np.asarray(volume)
+    half = np.asarray(half_extents, np.float64).copy()
+    if v.ndim == 2 or v.shape[0] == 1:
+        half[2] = 1.0  # shift.cpp:9
+    H = np.diag(half * half)
+    r, _ = window_ops(volume, _op(WOP_SHIFT_STEP, x, H, hist_kernel, step_kernel), window_low,
+                      window_high, bins, target=target, ctx=ctx)
+    return r[0]["value"].copy() if r[0]["ok"] else None
+
+
+def box_entropy_bits(volume, x0, x1, y0, y1, z0=0.0, z1=0.0, window_low=None, window_high=None,
+                     bins=64, min_voxels=4, ctx=None):
+    """box_entropy_bits (quadrant.hpp:58-60, quadrant.cpp:18-35) on the device; the z
+    range generalises it to the octant boxes."""
+    from ._lib import WOP_BOX_ENTROPY
+
+    o = _op(WOP_BOX_ENTROPY)
+    o["box"] = [x0, x1, y0, y1, z0, z1]
+    o["min_voxels"] = int(min_voxels)
+    r, _ = window_ops(volume, o, window_low, window_high, bins, ctx=ctx)
+    return float(r[0]["value"][0])
+
+
+def ascent_step(volume, points, scale_range, window_low=None, window_high=None, bins=64, dims=2,
+                ctx=None):
+    """quadrant_step (quadrant.cpp:37-81; dims = 2) or the octant step (dims = 3) for many
+    points in one launch -> (moved[n, 3], ASCENT_STATE_DTYPE[n], visits)."""
+    from ._lib import ASCENT_STATE_DTYPE
+
+    v, nx, ny, nz = _volume(volume)
+    iw = _window(window_low, window_high, bins)
+    pts = np.asarray(points, np.float64)
+    if pts.ndim == 1:
+        pts = pts[None]
+    if pts.shape[-1] == 2:
+        pts = np.concatenate([pts, np.zeros(pts.shape[:-1] + (1,))], axis=-1)
+    pts = np.ascontiguousarray(pts)
+    sc = np.ascontiguousarray(scale_range, np.int32)
+    moved = np.zeros((max(len(pts), 1), 3))
+    st = np.zeros(max(len(pts), 1), ASCENT_STATE_DTYPE)
+    visits = C.c_uint64(0)
+    check(_lib.load().salvox_ascent_step(_ctx(ctx).handle, ptr(v), nx, ny, nz, C.byref(iw),
+                                         int(dims), ptr(sc), len(sc), ptr(pts), len(pts),
+                                         ptr(moved), ptr(st), C.byref(visits)))
+    return moved[: len(pts)], st[: len(pts)], int(visits.value)
+
+
+# -------------------------------------------------- pmf functionals (host)
+def entropy_nats(pmf):
+    """entropy_nats (py_module.cpp:86-88, histogram.hpp:56-62): normalises the input,
+    max(-sum p ln p, 0) in bin order."""
+    import math
+
+    p = histogram_from_array(pmf)
+    h = 0.0
+    for v in p.tolist():
+        if v > 0.0:
+            h -= v * math.log(v)
+    return max(h, 0.0)
+
+
+def entropy_bits(pmf):
+    """entropy_bits (py_module.cpp:82-84, histogram.hpp:65-67)."""
+    import math
+
+    return entropy_nats(pmf) / math.log(2.0)
+
+
+def bhattacharyya(p, q):
+    """bhattacharyya (py_module.cpp:95-97, histogram.hpp:95-103), capped at 1."""
+    import math
+
+    a, b = histogram_from_array(p), histogram_from_array(q)
+    if len(a) != len(b):
+        raise ValueError("bhattacharyya: bin count mismatch")
+    rho = 0.0
+    for x, y in zip(a.tolist(), b.tolist()):
+        rho += math.sqrt(x * y)
+    return min(rho, 1.0)
+
+
+def mixture_entropy(alpha, bins):
+    """mixture_entropy (py_module.cpp:90-91, histogram.hpp:73-83): entropy (nats) of M bins
+    blended with fraction alpha into one background bin,
+    -(a/M + 1-a) ln(a/M + 1-a) - a (M-1)/M ln(a/M)."""
+    import math
+
+    if bins < 2:
+        raise ValueError("mixture_entropy: bins must be >= 2")
+    if alpha < 0.0 or alpha > 1.0:
+        raise ValueError("mixture_entropy: alpha outside [0,1]")
+    if alpha == 0.0:
+        return 0.0
+    m = float(bins)
+    shared = alpha / m + (1.0 - alpha)
+    return -shared * math.log(shared) - alpha * (m - 1.0) / m * math.log(alpha / m)
+
+
+def mixture_entropy_derivative(alpha, bins):
+    """mixture_entropy_derivative (py_module.cpp:92-93, histogram.hpp:86-93):
+    (M-1)/M ln((a + M(1-a)) / a) on (0, 1]."""
+    import math
+
+    if bins < 2:
+        raise ValueError("mixture_entropy_derivative: bins must be >= 2")
+    if alpha <= 0.0 or alpha > 1.0:
+        raise ValueError("mixture_entropy_derivative: alpha outside (0,1]")
+    m = float(bins)
+    return (m - 1.0) / m * math.log((alpha + m * (1.0 - alpha)) / alpha)
+
+
 def histogram_from_array(arr):
     """histogram_from_array (py_module.cpp:46-54): 1D, normalised by the sequential
     bin-order mass (Histogram::normalize, histogram.hpp:21-33)."""

@@ -87,6 +87,7 @@ struct SeekParams {
   salvox_detection* out;
   unsigned long long* visits;
   salvox_ascent_result* ascent_out;  // raw ascent results (salvox_ascent_seek), nullable
+  salvox_ascent_state* ascent_state; // the last step's state per slot (salvox_ascent_step), nullable
   int post_score;                    // ascent: score the converged window (detect)
   // ABMSOD (abmsod.hpp:19-40)
   const double* seed_H;              // 9 per output slot (row-major)
@@ -1701,16 +1702,24 @@ __global__ void __launch_bounds__(32 * NQ, 24 / NQ) ascent_kernel(const SeekPara
       double total = 0.0;
       for (int r = 0; r < NQ; ++r) total = __dadd_rn(total, ent[r]);
       ctl[0] = ctl[1] = ctl[2] = 0;
+      salvox_ascent_state* st = P.ascent_state ? &P.ascent_state[si.slot] : nullptr;
+      if (st) {  // QuadrantState (quadrant.hpp:32-38) of this step
+        memset(st, 0, sizeof *st);
+        for (int r = 0; r < NQ; ++r) st->entropy[r] = ent[r], st->best_scale[r] = bk[r];
+      }
       if (total <= 0.0) {
         ctl[0] = ctl[2] = 1;
         pos[0] = p[0], pos[1] = p[1], pos[2] = p[2];
+        if (st) st->degenerate = 1;
       } else {
         double ed[3] = {0.0, 0.0, 0.0};
         for (int r = 0; r < NQ; ++r) {
           const double ne = __ddiv_rn(ent[r], total);
+          if (st) st->norm_entropy[r] = ne;
           for (int a = 0; a < (two_d ? 2 : 3); ++a)
             ed[a] = __dadd_rn(ed[a], __dmul_rn(__dmul_rn(ne, (double)c_dirs[r][a]), (double)bk[r]));
         }
+        if (st) st->displacement[0] = ed[0], st->displacement[1] = ed[1], st->displacement[2] = ed[2];
         pos[0] = p[0], pos[1] = p[1], pos[2] = p[2];
         for (int a = 0; a < (two_d ? 2 : 3); ++a) pos[a] = dclamp(__dadd_rn(p[a], ed[a]), lim[a]);
         const double nrm =
@@ -1807,6 +1816,118 @@ __global__ void __launch_bounds__(32 * NQ, 24 / NQ) ascent_kernel(const SeekPara
       P.ascent_out[si.slot] = r;
     }
   }
+}
+
+// ------------------------------------------------------------- window ops
+// The building blocks of the seek path as callable operations (salvox_window_ops):
+// the same warp routines as the seek kernels, so a pmf, a mean-shift step or a
+// pdf difference computed here is the one a trajectory would compute.
+struct WinOpDev {
+  int op, kernel, step_kernel, min_vox;
+  double c[3];
+  double box[6];
+  int geom;  // ScaleGeom of the op's window (HIST, SHIFT_STEP, PDF_DIFF)
+  int pad_;
+};
+
+struct WinOpParams {
+  int nx, ny, nz, bins, n;
+  const uint8_t* binvol;
+  const double* q;
+  const ScaleGeom* geoms;
+  const WinOpDev* ops;
+  salvox_window_result* out;
+  double* pmf;  // n x bins, nullable
+};
+
+// box_entropy_bits (quadrant.cpp:18-35) over an inclusive integer box: exact
+// counts, p_b = count_b / count, entropy in bin order (sx_log)
+__device__ double warp_box_entropy(const WinOpParams& P, const uint8_t* vb, WarpScratch& s,
+                                   unsigned* cnt, const double* bx, int min_vox, int lane,
+                                   unsigned long long* visits) {
+  auto range = [](double a, double b, int n, int* lo, int* hi) {
+    *lo = max(0, (int)ceil(a < b ? a : b));
+    *hi = min(n - 1, (int)floor(a < b ? b : a));
+  };
+  Box B;
+  range(bx[0], bx[1], P.nx, &B.x0, &B.x1);
+  range(bx[2], bx[3], P.ny, &B.y0, &B.y1);
+  range(bx[4], bx[5], P.nz, &B.z0, &B.z1);
+  const long long count = box_size(B);
+  if (count <= 0 || count < min_vox) return 0.0;
+  for (int b = lane; b < P.bins; b += 32) cnt[b] = 0u;
+  __syncwarp();
+  warp_box_iter(B, lane, [&](bool act, int x, int y, int z) {
+    if (act) atomicAdd(&cnt[(int)__ldg(vb + ((size_t)z * P.ny + y) * P.nx + x) - 1], 1u);
+  });
+  __syncwarp();
+  *visits = (unsigned long long)count;
+  for (int b = lane; b < P.bins; b += 32) s.p[b] = __ddiv_rn((double)cnt[b], (double)count);
+  __syncwarp();
+  return warp_entropy_bits(s.p, P.bins, lane, s.w);
+}
+
+template <int NW>
+__global__ void __launch_bounds__(32 * NW) window_ops_kernel(const WinOpParams P) {
+  __shared__ WarpScratch scratch[NW];
+  __shared__ unsigned counts[NW][kMaxBins];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int job = blockIdx.x * NW + wid;
+  if (job >= P.n) return;
+  const WinOpDev op = P.ops[job];
+  WarpScratch& s = scratch[wid];
+  const uint8_t* vb = P.binvol;
+  const int M = P.bins;
+  salvox_window_result r;
+  memset(&r, 0, sizeof r);
+  if (op.op == SALVOX_WOP_BOX_ENTROPY) {
+    unsigned long long v = 0;
+    r.value[0] = warp_box_entropy(P, vb, s, counts[wid], op.box, op.min_vox, lane, &v);
+    r.visits = v;
+    r.ok = 1;
+  } else if (op.op == SALVOX_WOP_PDF_DIFF) {
+    const ScaleGeom& sg = P.geoms[op.geom];
+    if (!sg.pdf_ok) {
+      r.ok = -1;  // s - ds < 1: the reference throws before any pass
+    } else {     // both flanks are evaluated before the check (window.cpp:37-39)
+      const HistRes lo = warp_candidate_hist_impl(vb, P.nx, P.ny, P.nz, M, &s, op.c[0], op.c[1],
+                                                  op.c[2], &sg.lo, op.kernel);
+      for (int b = lane; b < M; b += 32) s.w[b] = s.p[b];
+      __syncwarp();
+      const HistRes hi = warp_candidate_hist_impl(vb, P.nx, P.ny, P.nz, M, &s, op.c[0], op.c[1],
+                                                  op.c[2], &sg.hi, op.kernel);
+      r.visits = (unsigned long long)(lo.visited + hi.visited);
+      r.ok = lo.ok && hi.ok;
+      if (r.ok && lane == 0) {
+        double l1 = 0.0;
+        for (int b = 0; b < M; ++b) l1 = __dadd_rn(l1, fabs(__dsub_rn(s.p[b], s.w[b])));
+        r.value[0] = __dmul_rn(sg.pdf_fac, l1);
+      }
+    }
+  } else {  // HIST, SHIFT_STEP: the candidate histogram at c first
+    const ScaleGeom& sg = P.geoms[op.geom];
+    const HistRes h = warp_candidate_hist_impl(vb, P.nx, P.ny, P.nz, M, &s, op.c[0], op.c[1],
+                                               op.c[2], &sg.main, op.kernel);
+    r.support = h.support;
+    r.visits = (unsigned long long)h.visited;
+    r.ok = h.ok;
+    if (h.ok && P.pmf)
+      for (int b = lane; b < M; b += 32) P.pmf[(size_t)job * M + b] = s.p[b];
+    if (op.op == SALVOX_WOP_SHIFT_STEP && h.ok) {  // shift.cpp:21-33
+      for (int b = lane; b < M; b += 32) {  // weight_for_bin (histogram.hpp:107-113)
+        const double pb = s.p[b] > 1e-6 ? s.p[b] : 1e-6;
+        s.w[b] = __dsqrt_rn(__ddiv_rn(P.q[b], pb));
+      }
+      __syncwarp();
+      const CentRes cr = warp_centroid_impl(vb, P.nx, P.ny, P.nz, &s, op.c[0], op.c[1], op.c[2],
+                                            &sg.main, op.step_kernel);
+      r.visits += (unsigned long long)cr.visited;
+      r.ok = cr.den > 0.0;
+      if (r.ok)
+        for (int a = 0; a < 3; ++a) r.value[a] = __ddiv_rn(cr.num[a], cr.den);
+    }
+  }
+  if (lane == 0) P.out[job] = r;
 }
 
 // ------------------------------------------------------------------ selection
@@ -2530,6 +2651,128 @@ extern "C" int salvox_ascent_seek(salvox_ctx* ctx, const float* volume, int32_t 
                             cudaMemcpyDeviceToHost, ctx->stream));
     const unsigned long long v = sum_visits(ctx, d_vis, (int)n);
     if (visits) *visits += v;
+  });
+}
+
+extern "C" int salvox_ascent_step(salvox_ctx* ctx, const float* volume, int32_t nx, int32_t ny,
+                                  int32_t nz, const salvox_window* iw, int32_t dims,
+                                  const int32_t* scales, int32_t n_scales, const double* points,
+                                  int64_t n, double* moved, salvox_ascent_state* states,
+                                  uint64_t* visits) {
+  return guarded([&] {
+    if (!ctx) fail(SALVOX_EINVAL, "null context");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (nx < 1 || ny < 1 || nz < 1) fail(SALVOX_EINVAL, "Volume: dims must be >= 1");
+    if (dims != 2 && dims != 3) fail(SALVOX_EINVAL, "ascent: dims must be 2 or 3");
+    if (dims == 2 && nz != 1)
+      fail(SALVOX_EINVAL, "quadrant_step: volume must be 2D (nz == 1)");  // quadrant.cpp:42
+    check_window(iw);
+    if (n < 0 || (n > 0 && !points)) fail(SALVOX_EINVAL, "bad point arrays");
+    salvox_detect_params prm{};
+    prm.method = dims == 2 ? SALVOX_METHOD_QUADRANT : SALVOX_METHOD_OCTANT;
+    prm.quadrant_scales = scales;
+    prm.n_quadrant_scales = n_scales;
+    prm.quadrant_eta = 1.0;
+    prm.quadrant_max_iters = 1;  // one step (quadrant.cpp:37-81)
+    if (n_scales < 1 || !scales) fail(SALVOX_EINVAL, "quadrant: empty scale range");
+    std::vector<SeedRec> recs((size_t)n);
+    std::vector<int> index((size_t)n);
+    for (int64_t i = 0; i < n; ++i) {
+      std::memcpy(recs[i].pos, points + 3 * i, 3 * sizeof(double));
+      recs[i].scale = 0.0;
+      index[i] = (int)i;
+    }
+    SeekJob job;
+    build_job(nx, ny, nz, &prm, recs, index, job);
+    if (n == 0) return;
+    SX_CUDA(cudaSetDevice(ctx->device));
+    const size_t nv = (size_t)nx * ny * nz;
+    float* d_vol = static_cast<float*>(ctx->d_seek_vol.ensure(nv * 4));
+    SX_CUDA(cudaMemcpyAsync(d_vol, volume, nv * 4, cudaMemcpyHostToDevice, ctx->stream));
+    double* d_q = nullptr;
+    const uint8_t* d_bins = prepare_volume(ctx, d_vol, nx, ny, nz, iw, nullptr, &d_q);
+    char* d_dets = static_cast<char*>(ctx->d_dets.ensure(
+        (size_t)(n + 1) * (sizeof(salvox_detection) + 8 + sizeof(salvox_ascent_result) +
+                           sizeof(salvox_ascent_state)) + 1024));
+    salvox_detection* d_all = reinterpret_cast<salvox_detection*>(d_dets);
+    unsigned long long* d_vis = reinterpret_cast<unsigned long long*>(d_all + (n + 1));
+    salvox_ascent_result* d_res = reinterpret_cast<salvox_ascent_result*>(d_vis + (n + 1));
+    salvox_ascent_state* d_st = reinterpret_cast<salvox_ascent_state*>(d_res + (n + 1));
+    job.P.post_score = 0;
+    job.P.ascent_out = d_res;
+    job.P.ascent_state = d_st;
+    run_seek(ctx, job, d_bins, iw->bins, d_q, d_all, d_vis);
+    std::vector<salvox_ascent_result> res((size_t)n);
+    SX_CUDA(cudaMemcpyAsync(res.data(), d_res, (size_t)n * sizeof(salvox_ascent_result),
+                            cudaMemcpyDeviceToHost, ctx->stream));
+    if (states)
+      SX_CUDA(cudaMemcpyAsync(states, d_st, (size_t)n * sizeof(salvox_ascent_state),
+                              cudaMemcpyDeviceToHost, ctx->stream));
+    const unsigned long long v = sum_visits(ctx, d_vis, (int)n);
+    if (moved)
+      for (int64_t i = 0; i < n; ++i) std::memcpy(moved + 3 * i, res[i].position, 3 * sizeof(double));
+    if (visits) *visits += v;
+  });
+}
+
+extern "C" int salvox_window_ops(salvox_ctx* ctx, const float* volume, int32_t nx, int32_t ny,
+                                 int32_t nz, const salvox_window* iw, const double* target,
+                                 const salvox_window_op* ops, int64_t n, salvox_window_result* out,
+                                 double* pmf_out) {
+  return guarded([&] {
+    if (!ctx) fail(SALVOX_EINVAL, "null context");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (nx < 1 || ny < 1 || nz < 1) fail(SALVOX_EINVAL, "Volume: dims must be >= 1");
+    check_window(iw);
+    if (n < 0 || (n > 0 && (!ops || !out))) fail(SALVOX_EINVAL, "bad op arrays");
+    if (n == 0) return;
+    const bool two_d = nz == 1;
+    std::vector<WinOpDev> dev((size_t)n);
+    std::vector<ScaleGeom> geoms;
+    for (int64_t i = 0; i < n; ++i) {
+      const salvox_window_op& o = ops[i];
+      if (o.op < SALVOX_WOP_HIST || o.op > SALVOX_WOP_BOX_ENTROPY) fail(SALVOX_EINVAL, "unknown window op");
+      if (o.kernel < 0 || o.kernel > 2 || o.step_kernel < 0 || o.step_kernel > 2)
+        fail(SALVOX_EINVAL, "unknown kernel");
+      WinOpDev& d = dev[i];
+      d.op = o.op, d.kernel = o.kernel, d.step_kernel = o.step_kernel, d.min_vox = o.min_voxels;
+      std::memcpy(d.c, o.center, sizeof d.c);
+      std::memcpy(d.box, o.box, sizeof d.box);
+      d.geom = 0;
+      if (o.op != SALVOX_WOP_BOX_ENTROPY) {  // window geometry on the host (glibc pow/sqrt,
+        Mat3 H;                             // Eigen's 3x3 inverse/determinant) like the seeds'
+        std::memcpy(H.m, o.H, sizeof H.m);
+        d.geom = (int)geoms.size();
+        geoms.push_back(make_scale_geom(H, two_d));
+      }
+    }
+    if (geoms.empty()) geoms.push_back(ScaleGeom{});
+    SX_CUDA(cudaSetDevice(ctx->device));
+    const size_t nv = (size_t)nx * ny * nz;
+    float* d_vol = static_cast<float*>(ctx->d_seek_vol.ensure(nv * 4));
+    SX_CUDA(cudaMemcpyAsync(d_vol, volume, nv * 4, cudaMemcpyHostToDevice, ctx->stream));
+    double* d_q = nullptr;
+    const uint8_t* d_bins = prepare_volume(ctx, d_vol, nx, ny, nz, iw, target, &d_q);
+    auto up = [](size_t b) { return ((b + 255) / 256) * 256; };
+    const size_t ob = dev.size() * sizeof(WinOpDev), gb = geoms.size() * sizeof(ScaleGeom);
+    const size_t rb = (size_t)n * sizeof(salvox_window_result);
+    const size_t pb = pmf_out ? (size_t)n * iw->bins * sizeof(double) : 0;
+    char* d = static_cast<char*>(ctx->d_geom.ensure(up(ob) + up(gb) + up(rb) + up(pb) + 256));
+    WinOpDev* d_ops = reinterpret_cast<WinOpDev*>(d);
+    ScaleGeom* d_geo = reinterpret_cast<ScaleGeom*>(d + up(ob));
+    salvox_window_result* d_out = reinterpret_cast<salvox_window_result*>(d + up(ob) + up(gb));
+    double* d_pmf = pmf_out ? reinterpret_cast<double*>(d + up(ob) + up(gb) + up(rb)) : nullptr;
+    SX_CUDA(cudaMemcpyAsync(d_ops, dev.data(), ob, cudaMemcpyHostToDevice, ctx->stream));
+    SX_CUDA(cudaMemcpyAsync(d_geo, geoms.data(), gb, cudaMemcpyHostToDevice, ctx->stream));
+    WinOpParams P{};
+    P.nx = nx, P.ny = ny, P.nz = nz, P.bins = iw->bins, P.n = (int)n;
+    P.binvol = d_bins, P.q = d_q, P.geoms = d_geo, P.ops = d_ops, P.out = d_out, P.pmf = d_pmf;
+    constexpr int NW = 2;
+    window_ops_kernel<NW><<<(unsigned)((n + NW - 1) / NW), 32 * NW, 0, ctx->stream>>>(P);
+    SX_LAUNCH_CHECK(ctx);
+    SX_CUDA(cudaMemcpyAsync(out, d_out, rb, cudaMemcpyDeviceToHost, ctx->stream));
+    if (pmf_out) SX_CUDA(cudaMemcpyAsync(pmf_out, d_pmf, pb, cudaMemcpyDeviceToHost, ctx->stream));
+    SX_CUDA(cudaStreamSynchronize(ctx->stream));
   });
 }
 

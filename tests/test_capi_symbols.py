@@ -37,12 +37,14 @@ def test_struct_layouts_match_header(sx, tmp_path):
 #include <stddef.h>
 #include "salvox_capi.h"
 int main(void) {
-  printf("%zu %zu %zu %zu %zu %zu %zu %zu %zu %zu %zu\\n", sizeof(salvox_window),
+  printf("%zu %zu %zu %zu %zu %zu %zu %zu %zu %zu %zu %zu %zu %zu %zu %zu\\n", sizeof(salvox_window),
          sizeof(salvox_detection), sizeof(salvox_maximum), sizeof(salvox_detect_params),
          offsetof(salvox_detect_params, shift_target), offsetof(salvox_detection, flags),
          offsetof(salvox_detect_params, quadrant_scales),
          offsetof(salvox_detect_params, abmsod_target), sizeof(salvox_abmsod_params),
-         offsetof(salvox_abmsod_params, target), sizeof(salvox_abmsod_iter));
+         offsetof(salvox_abmsod_params, target), sizeof(salvox_abmsod_iter),
+         sizeof(salvox_window_op), offsetof(salvox_window_op, box), sizeof(salvox_window_result),
+         sizeof(salvox_ascent_state), offsetof(salvox_ascent_state, displacement));
   return 0;
 }
 """)
@@ -56,7 +58,10 @@ int main(void) {
     assert got == [ctypes.sizeof(sx._lib.Window), sx.DET_DTYPE.itemsize, sx.MAX_DTYPE.itemsize,
                    ctypes.sizeof(P), P.shift_target.offset, sx.DET_DTYPE.fields["flags"][1],
                    P.quadrant_scales.offset, P.abmsod_target.offset, ctypes.sizeof(A),
-                   A.target.offset, sx._lib.ABMSOD_ITER_DTYPE.itemsize]
+                   A.target.offset, sx._lib.ABMSOD_ITER_DTYPE.itemsize,
+                   sx._lib.WINDOW_OP_DTYPE.itemsize, sx._lib.WINDOW_OP_DTYPE.fields["box"][1],
+                   sx._lib.WINDOW_RESULT_DTYPE.itemsize, sx._lib.ASCENT_STATE_DTYPE.itemsize,
+                   sx._lib.ASCENT_STATE_DTYPE.fields["displacement"][1]]
 
 
 def test_no_cpu_fallback_without_gpu(sx):
