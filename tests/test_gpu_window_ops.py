@@ -142,3 +142,28 @@ def test_box_entropy_and_quadrant_step_match_reference(sx, R, oracle):
         np.testing.assert_allclose(st[i]["entropy"][:4], list(s.entropy[:4]), rtol=1e-12)
         assert bool(st[i]["degenerate"]) == bool(s.degenerate)
     assert visits == total
+
+
+def test_octant_step_and_3d_box_bit_exact_vs_oracle_shared_log(sx, oracle, vol3):
+    """The octant step (NEW, no reference) and 3D boxes against the oracle's restatement
+    in the device's own math (shared sx_log): bit-identical."""
+    rng = np.random.default_rng(5)
+    pts = rng.uniform(0, 31, size=(16, 3))
+    scales = [3, 5, 7]
+    moved, st, visits = sx.ascent_step(vol3, pts, scales, 0.0, 64.0, 64, dims=3)
+    oracle.set_log_mode(1)
+    try:
+        for i, p in enumerate(pts):
+            m, s = oracle.ascent_step(vol3, 0.0, 64.0, 64, p, scales, dims=3)
+            assert moved[i].tobytes() == np.asarray(m).tobytes()
+            assert st[i]["entropy"].tobytes() == s["entropy"].tobytes()
+            assert list(st[i]["best_scale"]) == list(s["best_scale"])
+            assert st[i]["norm_entropy"].tobytes() == s["norm_entropy"].tobytes()
+        for _ in range(12):
+            b = rng.uniform(-4, 36, size=6)
+            got = sx.box_entropy_bits(vol3, *b, window_low=0.0, window_high=64.0, bins=64,
+                                      min_voxels=8)
+            want = oracle.box_entropy_bits(vol3, 0.0, 64.0, 64, *b, min_voxels=8)
+            assert got == want
+    finally:
+        oracle.set_log_mode(0)
