@@ -741,6 +741,11 @@ __device__ __forceinline__ void cta_produce(const PassIn& in, const Box& bb, int
 template <int MODE>
 __device__ __forceinline__ void cta_consume(const CtaSlot& sl, int M, int lane, double& a0,
                                             double& a1, unsigned& support) {
+#ifdef SEEK_SKIP_CHAINS  // profiling knob: no ordered fp64 chains (results wrong)
+  a0 = __dadd_rn(a0, (double)sl.n);
+  if (MODE == PASS_HIST) support += (unsigned)sl.n;
+  return;
+#endif
   if (MODE == PASS_HIST) {
     const int c0 = sl.cnt[lane], s0 = sl.start[lane];
     for (int k = 0; k < c0; ++k) a0 = __dadd_rn(a0, sl.v[s0 + k]);
@@ -863,8 +868,11 @@ __device__ double cta_entropy(const SeekParams& P, CtaShared<NP>& S) {
   return e;
 }
 
+#ifndef CTA_MINB  // A/B knob: resident CTAs per SM the register allocation must allow
+#define CTA_MINB 1
+#endif
 template <int NP>
-__global__ void __launch_bounds__(32 * (NP + 1)) shift_cta_kernel(const SeekParams P) {
+__global__ void __launch_bounds__(32 * (NP + 1), CTA_MINB) shift_cta_kernel(const SeekParams P) {
   extern __shared__ __align__(16) unsigned char cta_dyn[];
   CtaShared<NP>& S = *reinterpret_cast<CtaShared<NP>*>(cta_dyn);
   const int seed = blockIdx.x;
