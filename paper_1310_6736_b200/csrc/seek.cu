@@ -126,23 +126,41 @@ __device__ __forceinline__ int fdiv_small(int n, float inv_d) {
   return (int)(((float)n + 0.5f) * inv_d);
 }
 
+// Linear bounding-box index -> (x, y, z): two divisions by the box's row and
+// plane lengths, through fdiv_small while the box holds < 2^22 - 1 voxels (every
+// fixed-scale window; ABMSOD windows can grow past it and divide exactly).
+struct BoxDiv {
+  int Lx, Ly;
+  float ix, iy;
+  bool fast;
+  __device__ __forceinline__ BoxDiv(int lx, int ly, int total)
+      : Lx(lx), Ly(ly), ix(1.0f / (float)lx), iy(1.0f / (float)ly),
+#ifdef SEEK_INT_DIV  // A/B knob: integer division only
+        fast(false) {}
+#else
+        fast(total < (1 << 22) - 1) {}
+#endif
+  __device__ __forceinline__ void split(int L, const Box& b, int* x, int* y, int* z) const {
+    const int t = fast ? fdiv_small(L, ix) : L / Lx;
+    const int zz = fast ? fdiv_small(t, iy) : t / Ly;
+    *x = b.x0 + (L - t * Lx);
+    *y = b.y0 + (t - zz * Ly);
+    *z = b.z0 + zz;
+  }
+};
+
 // Visits a box in z->y->x order, 32 voxels per step (uniform control flow).
 template <class F>
 __device__ __forceinline__ void warp_box_iter(const Box& b, int lane, F&& f) {
   const int Lx = b.x1 - b.x0 + 1, Ly = b.y1 - b.y0 + 1, Lz = b.z1 - b.z0 + 1;
   if (Lx <= 0 || Ly <= 0 || Lz <= 0) return;
   const int total = Lx * Ly * Lz;
+  const BoxDiv dv(Lx, Ly, total);
   for (int base = 0; base < total; base += 32) {
     const int L = base + lane;
     const bool act = L < total;
     int x = 0, y = 0, z = 0;
-    if (act) {
-      const int t = L / Lx;
-      x = b.x0 + (L - t * Lx);
-      const int zz = t / Ly;
-      y = b.y0 + (t - zz * Ly);
-      z = b.z0 + zz;
-    }
+    if (act) dv.split(L, b, &x, &y, &z);
     f(act, x, y, z);
   }
 }
@@ -155,6 +173,7 @@ __device__ __forceinline__ void warp_box_iter_g(const Box& b, int lane, F&& f) {
   const int Lx = b.x1 - b.x0 + 1, Ly = b.y1 - b.y0 + 1, Lz = b.z1 - b.z0 + 1;
   if (Lx <= 0 || Ly <= 0 || Lz <= 0) return;
   const int total = Lx * Ly * Lz;
+  const BoxDiv dv(Lx, Ly, total);
   for (int base = 0; base < total; base += kStep) {
     bool act[kG];
     int x[kG], y[kG], z[kG];
@@ -162,12 +181,7 @@ __device__ __forceinline__ void warp_box_iter_g(const Box& b, int lane, F&& f) {
     for (int j = 0; j < kG; ++j) {
       const int L = base + 32 * j + lane;
       act[j] = L < total;
-      const int Lc = act[j] ? L : 0;
-      const int t = Lc / Lx;
-      x[j] = b.x0 + (Lc - t * Lx);
-      const int zz = t / Ly;
-      y[j] = b.y0 + (t - zz * Ly);
-      z[j] = b.z0 + zz;
+      dv.split(act[j] ? L : 0, b, &x[j], &y[j], &z[j]);
     }
     f(act, x, y, z);
   }
@@ -654,6 +668,8 @@ __device__ __forceinline__ void cta_produce(const PassIn& in, const Box& bb, int
   // the bin of every voxel of the chunk is fetched first (the bounding box lies
   // inside the volume, so the loads are always valid): their L2 latency then
   // overlaps the Mahalanobis tests instead of following them
+  // integer division here: the fp32-reciprocal form (BoxDiv) measured 2% slower in
+  // this engine (C3 10.48 vs 10.24 ms) while it helps the warp engine (C1 shift)
 #pragma unroll
   for (int j = 0; j < kG; ++j) {
     const int L = base + 32 * j + lane;
@@ -739,6 +755,10 @@ __device__ __forceinline__ void cta_produce(const PassIn& in, const Box& bb, int
 }
 
 template <int MODE>
+__device__ __forceinline__ void cta_consume_once(const CtaSlot& sl, int M, int lane, double& a0,
+                                                 double& a1, unsigned& support);
+
+template <int MODE>
 __device__ __forceinline__ void cta_consume(const CtaSlot& sl, int M, int lane, double& a0,
                                             double& a1, unsigned& support) {
 #ifdef SEEK_SKIP_CHAINS  // profiling knob: no ordered fp64 chains (results wrong)
@@ -746,6 +766,21 @@ __device__ __forceinline__ void cta_consume(const CtaSlot& sl, int M, int lane, 
   if (MODE == PASS_HIST) support += (unsigned)sl.n;
   return;
 #endif
+#ifdef SEEK_DOUBLE_CHAINS  // profiling knob: every chain twice (same results, 2x consumer latency)
+  {
+    double x0 = a0, x1 = a1;
+    unsigned sp = 0;
+    cta_consume_once<MODE>(sl, M, lane, x0, x1, sp);
+    // a fake dependence: the real chain starts only after the copy finished
+    asm volatile("" : "+d"(a0), "+d"(a1), "+r"(support) : "d"(x0), "d"(x1), "r"(sp));
+  }
+#endif
+  cta_consume_once<MODE>(sl, M, lane, a0, a1, support);
+}
+
+template <int MODE>
+__device__ __forceinline__ void cta_consume_once(const CtaSlot& sl, int M, int lane, double& a0,
+                                                 double& a1, unsigned& support) {
   if (MODE == PASS_HIST) {
     const int c0 = sl.cnt[lane], s0 = sl.start[lane];
     for (int k = 0; k < c0; ++k) a0 = __dadd_rn(a0, sl.v[s0 + k]);
@@ -868,11 +903,13 @@ __device__ double cta_entropy(const SeekParams& P, CtaShared<NP>& S) {
   return e;
 }
 
-#ifndef CTA_MINB  // A/B knob: resident CTAs per SM the register allocation must allow
-#define CTA_MINB 1
+#ifdef CTA_MINB  // A/B knob: resident CTAs per SM the register allocation must allow
+#define SX_CTA_BOUNDS(NT) __launch_bounds__(NT, CTA_MINB)
+#else             // default: no minimum (ptxas settles at 128 registers, 4 CTAs/SM)
+#define SX_CTA_BOUNDS(NT) __launch_bounds__(NT)
 #endif
 template <int NP>
-__global__ void __launch_bounds__(32 * (NP + 1), CTA_MINB) shift_cta_kernel(const SeekParams P) {
+__global__ void SX_CTA_BOUNDS(32 * (NP + 1)) shift_cta_kernel(const SeekParams P) {
   extern __shared__ __align__(16) unsigned char cta_dyn[];
   CtaShared<NP>& S = *reinterpret_cast<CtaShared<NP>*>(cta_dyn);
   const int seed = blockIdx.x;
