@@ -2770,6 +2770,7 @@ extern "C" int salvox_window_ops(salvox_ctx* ctx, const float* volume, int32_t n
     if (nx < 1 || ny < 1 || nz < 1) fail(SALVOX_EINVAL, "Volume: dims must be >= 1");
     check_window(iw);
     if (n < 0 || (n > 0 && (!ops || !out))) fail(SALVOX_EINVAL, "bad op arrays");
+    if (n > (int64_t)1 << 30) fail(SALVOX_EINVAL, "window ops: too many ops in one call");
     if (n == 0) return;
     const bool two_d = nz == 1;
     std::vector<WinOpDev> dev((size_t)n);
