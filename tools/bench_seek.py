@@ -9,7 +9,9 @@
       paper's shapes: 128x128x34 with 400 random seeds (16 bins) and 256x256x176
       with 700 random seeds (64 bins), seed windows isotropic r = 8 -- the paper
       reports 4.1 s and 7.8 s per volume on a Tesla C2050
-Prints one JSON object per config; --cpu adds the oracle's time on all host cores.
+Prints one JSON object per config; --cpu adds the oracle's time on all host cores,
+--ref the reference's OWN detect() (oracle/_ref, its parallel_for on all host
+cores; octant does not exist in the reference).
 """
 import argparse
 import ctypes as C
@@ -74,9 +76,21 @@ def time_batch(ctx, stream, d_vols, batch, shape, window, method, scales, spacin
     return float(np.mean(ts)), int(n_out.sum())
 
 
+def ref_ms(vol, low, high, bins, **kw):
+    """The reference's own detect() (oracle/_ref) on all host cores, best of 2."""
+    from oracle import ref as R
+    best = float("inf")
+    for _ in range(2):
+        t0 = time.perf_counter()
+        R.detect(vol, low, high, bins, workers=os.cpu_count() or 1, **kw)
+        best = min(best, time.perf_counter() - t0)
+    return best * 1e3
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--cpu", action="store_true")
+    ap.add_argument("--ref", action="store_true")
     ap.add_argument("--c5", type=int, default=64)
     ap.add_argument("--only", default="", help="substring filter on config names")
     args = ap.parse_args()
@@ -99,13 +113,22 @@ def main():
                      top_k=20, dedupe_radius=5.0, workers=os.cpu_count() or 1)
             r["cpu_ms"] = (time.perf_counter() - t0) * 1e3
             r["cpu_cores"] = os.cpu_count()
+        if args.ref and method == "shift":
+            r["ref_ms"] = ref_ms(v1, 0.0, 16.0, 16, method="shift", seed_spacing=8.0,
+                                 scales=C1_SCALES, top_k=20, dedupe_radius=5.0)
+            r["ref_cores"] = os.cpu_count()
         res.append(r)
     if want("C3 shift"):
         v3, _ = api.make_phantom(phantoms.config_c3())
         d3 = torch.from_numpy(v3).to(dev)
         ms, sel = time_batch(ctx, st, d3, 1, v3.shape, (0.0, 64.0, 64), "shift", [8.0, 12.0], 16.0)
-        res.append({"config": "C3 shift", "ms_per_volume": ms, "volumes_per_s": 1e3 / ms,
-                    "selected": sel})
+        r = {"config": "C3 shift", "ms_per_volume": ms, "volumes_per_s": 1e3 / ms,
+             "selected": sel}
+        if args.ref:
+            r["ref_ms"] = ref_ms(v3, 0.0, 64.0, 64, method="shift", seed_spacing=16.0,
+                                 scales=[8.0, 12.0], top_k=20, dedupe_radius=5.0)
+            r["ref_cores"] = os.cpu_count()
+        res.append(r)
     for name, spec, bins, n_seeds, paper_s in (("PAPER PET abmsod", phantoms.paper_pet(), 16, 400, 4.1),
                                                ("PAPER MR abmsod", phantoms.paper_mr(), 64, 700, 7.8)):
         if not want(name):
@@ -125,6 +148,11 @@ def main():
                      workers=os.cpu_count() or 1)
             r["cpu_ms"] = (time.perf_counter() - t0) * 1e3
             r["cpu_cores"] = os.cpu_count()
+        if args.ref:
+            r["ref_ms"] = ref_ms(vp, 0.0, float(bins), bins, method="abmsod", seed_mode="random",
+                                 seed_count=n_seeds, rng_seed=1310, scales=[8.0], top_k=20,
+                                 dedupe_radius=5.0)
+            r["ref_cores"] = os.cpu_count()
         res.append(r)
     if args.c5 > 0 and want("C5"):
         vols = np.stack([api.make_phantom(s)[0] for s in c5_specs(args.c5)])
