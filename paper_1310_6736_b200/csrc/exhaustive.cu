@@ -882,6 +882,12 @@ __device__ __forceinline__ uint32_t quad_prmt(uint32_t w0, uint32_t w1, uint32_t
 }
 
 template <int NB, int G, int V>
+__device__ __forceinline__ void quad_red1(uint32_t a, uint32_t n) {
+  constexpr uint32_t IMM = kDsmemBase + (uint32_t)((V * 4 + G) * NB * 256);
+  asm volatile("red.shared.add.u32 [%0+%2], %1;" ::"r"(a), "r"(n), "n"(IMM));
+}
+
+template <int NB, int G, int V>
 __device__ __forceinline__ void quad_red2(uint32_t ap, uint32_t am, uint32_t n) {
   constexpr uint32_t IMM = kDsmemBase + (uint32_t)((V * 4 + G) * NB * 256);
   asm volatile("red.shared.add.u32 [%0+%2], %1;" ::"r"(ap), "r"(n), "n"(IMM));
@@ -895,10 +901,24 @@ __device__ __forceinline__ void quad_entry_issue(uint32_t p0, uint32_t p1, uint3
   const uint32_t a1 = quad_prmt<1 + SP>(p0, p1, c), b1 = quad_prmt<1 + SM>(m0, m1, c);
   const uint32_t a2 = quad_prmt<2 + SP>(p0, p1, c), b2 = quad_prmt<2 + SM>(m0, m1, c);
   const uint32_t a3 = quad_prmt<3 + SP>(p0, p1, c), b3 = quad_prmt<3 + SM>(m0, m1, c);
+#ifdef KB_PAIR_ORDER  // A/B knob: +o and -o atomics of a voxel back to back
   quad_red2<NB, G, 0>(a0, b0, n);
   quad_red2<NB, G, 1>(a1, b1, n);
   quad_red2<NB, G, 2>(a2, b2, n);
   quad_red2<NB, G, 3>(a3, b3, n);
+#else
+  // the +o atomics of the four voxels, then the -o ones: the two atomics of one
+  // voxel hit the same word whenever bin(c+o) == bin(c-o) (homogeneous regions),
+  // and back-to-back same-address atomics replay
+  quad_red1<NB, G, 0>(a0, n);
+  quad_red1<NB, G, 1>(a1, n);
+  quad_red1<NB, G, 2>(a2, n);
+  quad_red1<NB, G, 3>(a3, n);
+  quad_red1<NB, G, 0>(b0, n);
+  quad_red1<NB, G, 1>(b1, n);
+  quad_red1<NB, G, 2>(b2, n);
+  quad_red1<NB, G, 3>(b3, n);
+#endif
 }
 
 // One int4 group = 4 table entries = 4 +-o pairs = 32 updates: all bin words
