@@ -1435,13 +1435,16 @@ __global__ void __launch_bounds__(256, 1)
 __global__ void maxima_kernel(const float* __restrict__ score, int nx, int ny, int nz, int zc0,
                               int z0, int z1, unsigned long long* keys, unsigned int* counter) {
   const long long rows = (long long)ny * (z1 - z0);
+  const unsigned lane = threadIdx.x & 31u;
   for (long long row = blockIdx.x; row < rows; row += gridDim.x) {
     const int y = (int)(row % ny);
     const int z = z0 + (int)(row / ny);
-    for (int x = threadIdx.x; x < nx; x += blockDim.x) {
-      const float s0 = score[((size_t)(z - zc0) * ny + y) * nx + x];
-      if (!(s0 > 0.0f)) continue;
-      bool is_max = true;
+    // every lane of a warp runs the same trips (blockDim is a multiple of 32), so
+    // the maxima of a warp take ONE counter atomic (the counter was the hot spot)
+    for (int xb = 0; xb < nx; xb += blockDim.x) {
+      const int x = xb + (int)threadIdx.x;
+      const float s0 = x < nx ? score[((size_t)(z - zc0) * ny + y) * nx + x] : 0.0f;
+      bool is_max = s0 > 0.0f;
       for (int dz = -1; dz <= 1 && is_max; ++dz) {
         const int sz = z + dz;
         if (sz < 0 || sz >= nz) continue;
@@ -1459,14 +1462,105 @@ __global__ void maxima_kernel(const float* __restrict__ score, int nx, int ny, i
           }
         }
       }
+      const unsigned found = __ballot_sync(0xffffffffu, is_max);
+      if (found == 0u) continue;
+      unsigned int base = 0;
+      if (lane == 0) base = atomicAdd(counter, (unsigned)__popc(found));
+      base = __shfl_sync(0xffffffffu, base, 0);
       if (is_max) {
         const unsigned long long lin =
             (unsigned long long)x + (unsigned long long)nx * ((unsigned long long)y + (unsigned long long)ny * z);
-        const unsigned int slot = atomicAdd(counter, 1u);
-        keys[slot] = ((unsigned long long)(~__float_as_uint(s0)) << 32) | (lin & 0xffffffffull);
+        keys[base + __popc(found & ((1u << lane) - 1u))] =
+            ((unsigned long long)(~__float_as_uint(s0)) << 32) | (lin & 0xffffffffull);
       }
     }
   }
+}
+
+// The same strict 26-neighbour test, tiled: a CTA owns a 32 x 8 column block
+// and walks a run of planes, keeping planes z-1, z, z+1 (+ a one-voxel halo) in a
+// shared-memory ring while plane z+2 is in flight in registers, so every score
+// is read from L2/HBM ~1.3 times instead of up to 27 times and the load latency
+// overlaps the tests. Out-of-volume neighbours are -inf (they never kill).
+constexpr int kMxTX = 32, kMxTY = 8, kMxZ = 16;
+constexpr int kMxPl = (kMxTY + 2) * (kMxTX + 2);  // one plane with its halo
+constexpr int kMxPer = (kMxPl + kMxTX * kMxTY - 1) / (kMxTX * kMxTY);  // elements per thread
+__global__ void __launch_bounds__(kMxTX * kMxTY)
+    maxima_tile_kernel(const float* __restrict__ score, int nx, int ny, int nz, int zc0, int z0,
+                       int z1, unsigned long long* keys, unsigned int* counter) {
+  __shared__ float pl[4][kMxTY + 2][kMxTX + 2];  // ring: z-1, z, z+1 and the plane in flight
+  // the CTA's maxima are gathered here and published with ONE global atomic: a
+  // single counter hit once per warp-step serialised the pass (~400k atomics).
+  // At most one strict maximum per 2x2x2 cube of the block: 32*8*16/8 slots.
+  __shared__ unsigned long long ckeys[kMxTX * kMxTY * kMxZ / 8];
+  __shared__ unsigned int ccount, cbase;
+  if (threadIdx.x == 0) ccount = 0u;
+  const int tx = threadIdx.x & (kMxTX - 1), ty = threadIdx.x / kMxTX;
+  const int x0 = blockIdx.x * kMxTX, y0 = blockIdx.y * kMxTY;
+  const int za = z0 + blockIdx.z * kMxZ, zb = min(z1, za + kMxZ);
+  const unsigned lane = threadIdx.x & 31u;
+  if (za >= zb) return;
+  float reg[kMxPer];
+  auto fetch = [&](int z) {  // this thread's elements of plane z (+ halo) into registers
+#pragma unroll
+    for (int k = 0; k < kMxPer; ++k) {
+      const int i = threadIdx.x + k * kMxTX * kMxTY;
+      const int ly = i / (kMxTX + 2), lx = i - ly * (kMxTX + 2);
+      const int x = x0 + lx - 1, y = y0 + ly - 1;
+      float v = -INFINITY;
+      if (i < kMxPl && z >= 0 && z < nz && x >= 0 && x < nx && y >= 0 && y < ny)
+        v = score[((size_t)(z - zc0) * ny + y) * nx + x];
+      reg[k] = v;
+    }
+  };
+  auto store = [&](int slot) {
+#pragma unroll
+    for (int k = 0; k < kMxPer; ++k) {
+      const int i = threadIdx.x + k * kMxTX * kMxTY;
+      if (i < kMxPl) (&pl[slot][0][0])[i] = reg[k];
+    }
+  };
+  fetch(za - 1);
+  store((za - 1 - za + 4) & 3);
+  fetch(za);
+  store(0);
+  fetch(za + 1);
+  store(1);
+  __syncthreads();
+  const int x = x0 + tx, y = y0 + ty;
+  for (int z = za; z < zb; ++z) {
+    const int r = z - za;
+    if (z + 1 < zb) fetch(z + 2);  // in flight while plane z is tested
+    const int s_lo = (r + 3) & 3, s_c = r & 3, s_hi = (r + 1) & 3;
+    const float s0 = pl[s_c][ty + 1][tx + 1];
+    bool is_max = x < nx && y < ny && s0 > 0.0f;
+#pragma unroll
+    for (int dz = 0; dz < 3; ++dz) {
+      const int sl = dz == 0 ? s_lo : (dz == 1 ? s_c : s_hi);
+#pragma unroll
+      for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+        for (int dx = 0; dx < 3; ++dx)
+          if (!(dz == 1 && dy == 1 && dx == 1) && pl[sl][ty + dy][tx + dx] >= s0) is_max = false;
+    }
+    const unsigned found = __ballot_sync(0xffffffffu, is_max);
+    if (found != 0u) {
+      unsigned int base = 0;
+      if (lane == 0) base = atomicAdd(&ccount, (unsigned)__popc(found));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (is_max) {
+        const unsigned long long lin =
+            (unsigned long long)x + (unsigned long long)nx * ((unsigned long long)y + (unsigned long long)ny * z);
+        ckeys[base + __popc(found & ((1u << lane) - 1u))] =
+            ((unsigned long long)(~__float_as_uint(s0)) << 32) | (lin & 0xffffffffull);
+      }
+    }
+    if (z + 1 < zb) store((r + 2) & 3);  // slot of z - 2: no longer read
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) cbase = ccount ? atomicAdd(counter, ccount) : 0u;
+  __syncthreads();
+  for (unsigned i = threadIdx.x; i < ccount; i += kMxTX * kMxTY) keys[cbase + i] = ckeys[i];
 }
 
 __global__ void decode_maxima_kernel(const unsigned long long* __restrict__ keys, long long n,
@@ -2085,9 +2179,19 @@ long long maxima_and_sort(salvox_ctx* ctx, const ExhRun& run, int z0, int z1) {
   unsigned int* d_cnt = static_cast<unsigned int*>(ctx->d_counter.ensure(64));
   SX_CUDA(cudaMemsetAsync(d_cnt, 0, 4, ctx->stream));
   const long long rows = (long long)ny * (z1 - z0);
-  maxima_kernel<<<(int)std::min<long long>(std::max<long long>(rows, 1), ctx->sm_count * 32),
-                  nx >= 128 ? 128 : 32, 0, ctx->stream>>>(d_score, nx, ny, nz, zc0, z0, z1, d_keys,
-                                                         d_cnt);
+  static const bool row_form = [] {  // A/B knob SALVOX_MAXIMA_ROWS=1: the per-row kernel
+    const char* e = std::getenv("SALVOX_MAXIMA_ROWS");
+    return e && e[0] == '1';
+  }();
+  if (row_form) {
+    maxima_kernel<<<(int)std::min<long long>(std::max<long long>(rows, 1), ctx->sm_count * 32),
+                    nx >= 128 ? 128 : 32, 0, ctx->stream>>>(d_score, nx, ny, nz, zc0, z0, z1, d_keys,
+                                                           d_cnt);
+  } else if (z1 > z0) {
+    const dim3 grid((nx + kMxTX - 1) / kMxTX, (ny + kMxTY - 1) / kMxTY, (z1 - z0 + kMxZ - 1) / kMxZ);
+    maxima_tile_kernel<<<grid, kMxTX * kMxTY, 0, ctx->stream>>>(d_score, nx, ny, nz, zc0, z0, z1,
+                                                                d_keys, d_cnt);
+  }
   SX_LAUNCH_CHECK(ctx);
   unsigned int cnt = 0;
   SX_CUDA(cudaMemcpyAsync(&cnt, d_cnt, 4, cudaMemcpyDeviceToHost, ctx->stream));
