@@ -2286,8 +2286,13 @@ long long run_exhaustive_pipelined(salvox_ctx* ctx, const float* h_slab, int nx,
   const int zc0 = run.kp.zc0, zc1 = run.kp.zc1;
   const int ntiles = (zc1 - zc0 + tz - 1) / tz;
   const int K = std::max(1, std::min(4, ntiles / 4));
+  // chunk boundaries in eighths of the tile layers: 1, 3, 3, 1 for K = 4 -- a
+  // short first chunk starts after fewer uploaded planes, a short last chunk
+  // leaves fewer maps to copy back after the compute ends
+  static const int kEighths[5][5] = {{0}, {0, 8}, {0, 4, 8}, {0, 2, 6, 8}, {0, 1, 4, 7, 8}};
   std::vector<int> cut(K + 1);
-  for (int k = 0; k <= K; ++k) cut[k] = std::min(zc1, zc0 + tz * (int)((long long)ntiles * k / K));
+  for (int k = 0; k <= K; ++k)
+    cut[k] = std::min(zc1, zc0 + tz * (int)((long long)ntiles * kEighths[K][k] / 8));
   cut[K] = zc1;
   const int npieces = std::max(1, std::min(8, nzs / 8));
   std::vector<int> pc(npieces + 1);
