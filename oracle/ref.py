@@ -355,6 +355,29 @@ def hu_template_distance(vol, center, H, tmpl, slices=5):
                                           t.shape[0], int(slices))
 
 
+def rasterize_windows(shape_zyx, centers, Hs):
+    """rasterize_window over many windows on ONE frame -> per-window support counts."""
+    nz, ny, nx = shape_zyx
+    c = np.ascontiguousarray(centers, np.float64).reshape(-1, 3)
+    h = np.ascontiguousarray(np.asarray(Hs, np.float64).reshape(-1, 9))
+    counts = np.zeros(max(len(c), 1), np.int64)
+    lib().sxr_rasterize_windows.restype = C.c_int64
+    lib().sxr_rasterize_windows(nx, ny, nz, _p(c), _p(h), C.c_int64(len(c)), _p(counts))
+    return counts[: len(c)]
+
+
+def hu_template_distances(vol, centers, Hs, tmpl, slices=5):
+    """hu_template_distance for many detections with ONE Volume built."""
+    v, nx, ny, nz = _vol(vol)
+    t = np.ascontiguousarray(tmpl, np.float32)
+    c = np.ascontiguousarray(centers, np.float64).reshape(-1, 3)
+    h = np.ascontiguousarray(np.asarray(Hs, np.float64).reshape(-1, 9))
+    out = np.zeros(max(len(c), 1))
+    lib().sxr_hu_template_distances(_p(v), nx, ny, nz, _p(c), _p(h), C.c_int64(len(c)), _p(t),
+                                    t.shape[1], t.shape[0], int(slices), _p(out))
+    return out[: len(c)]
+
+
 def load_volume(mhd_path):
     """meta_io.cpp:37-117 -> (volume zyx float32, spacing (3,))."""
     dims = np.zeros(3, np.int32)

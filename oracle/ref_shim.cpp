@@ -470,6 +470,34 @@ double sxr_hu_template_distance(const float* vol, int nx, int ny, int nz, const 
                               slices);
 }
 
+// the same two calls over many windows / detections with ONE Volume built (a
+// caller of the reference API holds its volume already; timing per-call copies
+// of it would charge the reference for this shim)
+int64_t sxr_rasterize_windows(int nx, int ny, int nz, const double* centers, const double* Hs,
+                              int64_t n, int64_t* counts) {
+  const Volume frame(nx, ny, nz);
+  int64_t total = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    counts[i] = int64_t(rasterize_window(frame, window_of(centers + 3 * i, Hs + 9 * i)).size());
+    total += counts[i];
+  }
+  return total;
+}
+
+void sxr_hu_template_distances(const float* vol, int nx, int ny, int nz, const double* centers,
+                               const double* Hs, int64_t n, const float* tmpl, int tnx, int tny,
+                               int slices, double* out) {
+  const Volume v = make_volume(vol, nx, ny, nz);
+  const Volume t = make_volume(tmpl, tnx, tny, 1);
+  for (int64_t i = 0; i < n; ++i) {
+    Detection d;
+    d.center = {centers[3 * i], centers[3 * i + 1], centers[3 * i + 2]};
+    for (int r = 0; r < 3; ++r)
+      for (int c = 0; c < 3; ++c) d.H(r, c) = Hs[9 * i + 3 * r + c];
+    out[i] = hu_template_distance(d, v, t, slices);
+  }
+}
+
 // meta_io.cpp:37-117 load_volume. Query dims with out == NULL.
 int sxr_load_volume(const char* mhd_path, float* out, int64_t cap, int* dims_out,
                     double* spacing_out, char* err, int err_len) {
