@@ -161,7 +161,8 @@ int guarded(F&& f) {
 
 // Bin volume pre-pass (volume.hpp:102-105): u8 (bin + 1), 0 = outside.
 void launch_bin_volume(salvox_ctx* ctx, const float* d_vol, uint8_t* d_bins, int nx, int ny,
-                       int nzs, int pitch, double low, double high, int bins);
+                       int nzs, int pitch, double low, double high, int bins,
+                       cudaStream_t stream = nullptr);  // null: ctx->stream
 // Observed intensity range (IntensityWindow::full_range, volume.hpp:108-112).
 void device_full_range(salvox_ctx* ctx, const float* d_vol, size_t n, double* low, double* high);
 // Drops a context's pending exchange-form scores call (salvox_ctx_destroy).

@@ -27,6 +27,7 @@
 
 #include <algorithm>
 #include <array>
+#include <chrono>
 #include <climits>
 #include <cmath>
 #include <map>
@@ -54,11 +55,12 @@ __global__ void bin_volume_kernel(const float* __restrict__ vol, uint8_t* __rest
 }
 
 void launch_bin_volume(salvox_ctx* ctx, const float* d_vol, uint8_t* d_bins, int nx, int ny,
-                       int nzs, int pitch, double low, double high, int bins) {
+                       int nzs, int pitch, double low, double high, int bins,
+                       cudaStream_t stream) {
   const long long rows = (long long)ny * nzs;
   const int grid = (int)std::min<long long>(rows, (long long)ctx->sm_count * 32);
   const int block = nx >= 256 ? 256 : ((nx + 31) / 32) * 32;
-  bin_volume_kernel<<<grid, block, 0, ctx->stream>>>(d_vol, d_bins, nx, rows, pitch, low,
+  bin_volume_kernel<<<grid, block, 0, stream ? stream : ctx->stream>>>(d_vol, d_bins, nx, rows, pitch, low,
                                                       high - low, (double)bins, bins);
   SX_LAUNCH_CHECK(ctx);
 }
@@ -154,6 +156,11 @@ struct KbParams {
   int lagmode;      // 0: warps 4-7 by lag; 1: warp w by w*lag/4; 3: (w%4)*lag/8 + (w/4)*lag
   float* score;     // planes [zc0, zc1)
   float* best;
+  // kb_quad_kernel: also store the planes [hz0, hz1) straight into the caller's
+  // pinned host maps (plane hz0 at h_score[0]); null = device maps only
+  float* h_score;
+  float* h_best;
+  int hz0, hz1;
   const long long* dbg_vox;  // debug launch: one block per voxel
   uint32_t* dbg_out;
 };
@@ -1066,6 +1073,9 @@ __global__ void __launch_bounds__(256, 1)
     tx0 = blockIdx.x * TX;
     ty0 = blockIdx.y * TY;
     tz0 = p.zc0 + blockIdx.z * TZ;
+    // a dependent chunk launched with programmatic serialization may take the
+    // SMs this grid's tail frees (it reads nothing this grid writes)
+    asm volatile("griddepcontrol.launch_dependents;");
   }
   if (tid == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)));
@@ -1422,6 +1432,15 @@ __global__ void __launch_bounds__(256, 1)
         p.score[o] = (float)best[v];
         p.best[o] = best_s[v];
       }
+    if (gz >= p.hz0 && gz < p.hz1) {  // mapped pinned host maps (hz0 == hz1: none)
+      const size_t h = ((size_t)(gz - p.hz0) * p.ny + gy) * p.nx + gx;
+#pragma unroll
+      for (int v = 0; v < 4; ++v)
+        if (gx + v < p.nx) {
+          if (p.h_score) p.h_score[h + v] = (float)best[v];
+          if (p.h_best) p.h_best[h + v] = best_s[v];
+        }
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -1429,6 +1448,9 @@ __global__ void __launch_bounds__(256, 1)
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tbase) : "memory");
   }
+  // launched as a programmatic dependent: complete only after the preceding
+  // grid has, so work ordered after this grid also follows that one (no-op otherwise)
+  if (!DBG) asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 // ----------------------------------------------------------------------------- K3
@@ -1928,9 +1950,11 @@ void launch_kb(salvox_ctx* ctx, const CUtensorMap& map, const KbParams& kp, dim3
   SX_LAUNCH_CHECK(ctx);
 }
 
+// pdl: launch kb_quad_kernel with programmatic stream serialization (its CTAs
+// may start while the preceding KB grid's last wave drains); other variants ignore it
 template <bool DBG>
 void dispatch_kb(salvox_ctx* ctx, const TileCfg& tc, const CUtensorMap& map, const KbParams& kp,
-                 dim3 grid, size_t smem) {
+                 dim3 grid, size_t smem, bool pdl = false) {
 #define SX_KB(NB, TX, TY, TZ)                                             \
   if (!tc.pair && !tc.tmem && !tc.quad && tc.nb == NB && tc.tx == TX && tc.ty == TY && tc.tz == TZ) { \
     launch_kb<NB, TX, TY, TZ, DBG>(ctx, map, kp, grid, smem);             \
@@ -1956,7 +1980,21 @@ void dispatch_kb(salvox_ctx* ctx, const TileCfg& tc, const CUtensorMap& map, con
                                    : (tc.vb2 ? kb_quad_kernel<33, DBG, true, 2> : kb_quad_kernel<33, DBG, true, 1>))
                     : (tc.nb == 17 ? kb_quad_kernel<17, DBG, false> : kb_quad_kernel<33, DBG, false>);
     SX_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k<<<grid, 256, smem, ctx->stream>>>(map, kp);
+    if (pdl && !DBG) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = grid;
+      cfg.blockDim = dim3(256);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = ctx->stream;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      SX_CUDA(cudaLaunchKernelEx(&cfg, k, map, kp));
+    } else {
+      k<<<grid, 256, smem, ctx->stream>>>(map, kp);
+    }
     SX_LAUNCH_CHECK(ctx);
     return;
   }
@@ -2131,6 +2169,9 @@ ExhRun setup_exhaustive(salvox_ctx* ctx, int nx, int ny, int nz, int zs0, int zs
   kp.best = d_best + (size_t)nx * ny * (zc0 - zb0);
   kp.dbg_vox = nullptr;
   kp.dbg_out = nullptr;
+  kp.h_score = nullptr;
+  kp.h_best = nullptr;
+  kp.hz0 = kp.hz1 = 0;
   run.smem = kb_smem(run.tc, kp.tile_bytes);
   run.grid = dim3((nx + run.tc.tx - 1) / run.tc.tx, (ny + run.tc.ty - 1) / run.tc.ty,
                   (zc1 - zc0 + run.tc.tz - 1) / run.tc.tz);
@@ -2139,8 +2180,15 @@ ExhRun setup_exhaustive(salvox_ctx* ctx, int nx, int ny, int nz, int zs0, int zs
 
 // KB kernel over the scored planes [a, b) (a subrange of [zc0, zc1)); the
 // constant-memory tables must already hold run.pl (caller holds g_const_mu).
-void launch_kb_chunk(salvox_ctx* ctx, const ExhRun& run, int a, int b) {
+// With h_score/h_best (device-accessible pinned host maps of the owned planes
+// [hz0, hz1)) the epilogue also stores there; pdl as dispatch_kb.
+void launch_kb_chunk(salvox_ctx* ctx, const ExhRun& run, int a, int b, float* h_score = nullptr,
+                     float* h_best = nullptr, int hz0 = 0, int hz1 = 0, bool pdl = false) {
   KbParams kp = run.kp;
+  kp.h_score = h_score;
+  kp.h_best = h_best;
+  kp.hz0 = hz0;
+  kp.hz1 = hz1;
   const size_t plane = (size_t)kp.nx * kp.ny;
   kp.score = run.kp.score + (size_t)(a - run.kp.zc0) * plane;
   kp.best = run.kp.best + (size_t)(a - run.kp.zc0) * plane;
@@ -2153,7 +2201,7 @@ void launch_kb_chunk(salvox_ctx* ctx, const ExhRun& run, int a, int b) {
     SX_CUDA(cudaEventCreate(&ev1));
     SX_CUDA(cudaEventRecord(ev0, ctx->stream));
   }
-  dispatch_kb<false>(ctx, run.tc, run.map, kp, grid, run.smem);
+  dispatch_kb<false>(ctx, run.tc, run.map, kp, grid, run.smem, pdl && !ctx->profiling);
   if (ctx->profiling) {
     SX_CUDA(cudaEventRecord(ev1, ctx->stream));
     SX_CUDA(cudaEventSynchronize(ev1));
@@ -2263,6 +2311,73 @@ cudaEvent_t ctx_event(salvox_ctx* ctx, size_t i) {
   return ctx->events[i];
 }
 
+// SALVOX_E2E_TRACE=1: device timeline of the direct host-buffer form (stderr);
+// the marks between the two chunks delay the second one's programmatic start.
+struct E2eTrace {
+  bool on = false;
+  std::vector<std::pair<cudaEvent_t, const char*>> marks;
+  std::chrono::steady_clock::time_point t0;
+  explicit E2eTrace(cudaStream_t s) {
+    static const bool env = [] {
+      const char* e = std::getenv("SALVOX_E2E_TRACE");
+      return e && e[0] == '1';
+    }();
+    on = env;
+    if (on) {
+      t0 = std::chrono::steady_clock::now();
+      mark(s, "entry");
+    }
+  }
+  void mark(cudaStream_t s, const char* what) {
+    if (!on) return;
+    cudaEvent_t e;
+    SX_CUDA(cudaEventCreate(&e));
+    SX_CUDA(cudaEventRecord(e, s));
+    marks.emplace_back(e, what);
+  }
+  void report() {
+    if (!on) return;
+    const double host_ms =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    for (auto& m : marks) {
+      float ms = 0.f;
+      SX_CUDA(cudaEventSynchronize(m.first));
+      SX_CUDA(cudaEventElapsedTime(&ms, marks[0].first, m.first));
+      std::fprintf(stderr, "[e2e] %8.3f ms  %s\n", ms, m.second);
+    }
+    std::fprintf(stderr, "[e2e] %8.3f ms  host return\n", host_ms);
+    for (auto& m : marks) cudaEventDestroy(m.first);
+    marks.clear();
+  }
+};
+
+// SALVOX_EXH_DIRECT=0 keeps the copy-back pipeline even for pinned host maps (A/B timing).
+bool direct_maps_disabled() {
+  static const bool off = [] {
+    const char* e = std::getenv("SALVOX_EXH_DIRECT");
+    return e && std::string(e) == "0";
+  }();
+  return off;
+}
+
+// The device address of host buffer [h, h + n) when it is pinned, mapped and one
+// allocation (torch pin_memory, cudaHostAlloc); null otherwise.
+float* mapped_host(float* h, size_t n) {
+  if (!h || n == 0) return nullptr;
+  cudaPointerAttributes a{}, b{};
+  if (cudaPointerGetAttributes(&a, h) != cudaSuccess ||
+      cudaPointerGetAttributes(&b, h + n - 1) != cudaSuccess) {
+    cudaGetLastError();  // clear: a pageable pointer is not an error here
+    return nullptr;
+  }
+  if (a.type != cudaMemoryTypeHost || b.type != cudaMemoryTypeHost || !a.devicePointer ||
+      !b.devicePointer)
+    return nullptr;
+  float* d = static_cast<float*>(a.devicePointer);
+  if (static_cast<float*>(b.devicePointer) != d + (n - 1)) return nullptr;
+  return d;
+}
+
 // Host-buffer form, pipelined: the slab goes up in pieces
 // on the copy stream; the compute stream bins each piece as it lands and runs
 // the KB kernel over K z-chunks of the scored planes; each chunk's owned
@@ -2273,7 +2388,14 @@ long long run_exhaustive_pipelined(salvox_ctx* ctx, const float* h_slab, int nx,
                                    int bins, const double* scales, int n_scales,
                                    float* score_out, float* best_out, ExhRun* run_out,
                                    bool exch = false) {
-  if (!ctx->copy_stream) SX_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+  if (!ctx->copy_stream) {
+    // highest priority: the bin kernels queued on it behind each uploaded piece
+    // get their CTAs dispatched beside a running KB chunk (which keeps the SMs
+    // saturated with pending CTAs) instead of after its last CTA is placed
+    int least = 0, greatest = 0;
+    SX_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    SX_CUDA(cudaStreamCreateWithPriority(&ctx->copy_stream, cudaStreamNonBlocking, greatest));
+  }
   cudaStream_t cs = ctx->stream, ps = ctx->copy_stream;
   ExhRun run = setup_exhaustive(ctx, nx, ny, nz, zs0, zs1, z0, z1, bins, scales, n_scales, exch);
   const int R = run.pl.R, tz = run.tc.tz;
@@ -2285,6 +2407,68 @@ long long run_exhaustive_pipelined(salvox_ctx* ctx, const float* h_slab, int nx,
   // K output chunks of whole tiles; the input in pieces of the same planes
   const int zc0 = run.kp.zc0, zc1 = run.kp.zc1;
   const int ntiles = (zc1 - zc0 + tz - 1) / tz;
+  const int npieces = std::max(1, std::min(8, nzs / 8));
+  std::vector<int> pc(npieces + 1);
+  for (int i = 0; i <= npieces; ++i) pc[i] = (int)((long long)nzs * i / npieces);
+  float* hs = mapped_host(score_out, (size_t)(z1 - z0) * plane);
+  float* hb = mapped_host(best_out, (size_t)(z1 - z0) * plane);
+  static const bool no_store = [] {  // trace knob: skip the host stores (maps NOT written)
+    const char* e = std::getenv("SALVOX_E2E_NOSTORE");
+    return e && e[0] == '1';
+  }();
+  if (run.tc.quad && !direct_maps_disabled() && (score_out || best_out) && (!score_out || hs) &&
+      (!best_out || hb)) {
+    // Direct form: the KB epilogue stores the owned maps straight into the
+    // caller's pinned host buffers (no copy-back at all), so the only reason
+    // to chunk is the upload: a small first chunk starts once its own planes
+    // have landed, the rest follows as a programmatic
+    // dependent that fills the SMs the first chunk's tail frees. Each piece
+    // is binned on the copy stream right after it lands.
+    // chunk 0: 1/16 of the tile layers (1/8 when there are fewer than 16)
+    const int c1 = ntiles >= 16   ? zc0 + tz * (ntiles / 16)
+                   : ntiles >= 8 ? zc0 + tz * (ntiles / 8)
+                                 : zc1;
+    const int need0 = std::min(nzs, c1 + R + 1 - zs0);  // local planes chunk 0 reads
+    // upload pieces: exactly chunk 0's planes first, then the rest in <= 7 parts
+    std::vector<int> dp{0, need0};
+    const int rest = nzs - need0;
+    const int nrest = rest > 0 ? std::max(1, std::min(7, rest / 8)) : 0;
+    for (int i = 1; i <= nrest; ++i) dp.push_back(need0 + (int)((long long)rest * i / nrest));
+    const int nd = (int)dp.size() - 1;
+    E2eTrace tr(cs);
+    SX_CUDA(cudaEventRecord(ctx_event(ctx, 0), cs));  // order after earlier work on cs
+    SX_CUDA(cudaStreamWaitEvent(ps, ctx_event(ctx, 0), 0));
+    for (int i = 0; i < nd; ++i) {
+      const size_t o = (size_t)dp[i] * plane, n = (size_t)(dp[i + 1] - dp[i]) * plane;
+      SX_CUDA(cudaMemcpyAsync(d_vol + o, h_slab + o, n * 4, cudaMemcpyHostToDevice, ps));
+      launch_bin_volume(ctx, d_vol + o, d_bins + (size_t)dp[i] * pitch * ny, nx, ny,
+                        dp[i + 1] - dp[i], pitch, low, high, bins, ps);
+      SX_CUDA(cudaEventRecord(ctx_event(ctx, 1 + i), ps));
+      tr.mark(ps, "piece uploaded+binned");
+    }
+    {
+      std::lock_guard<std::mutex> lk(g_const_mu);
+      upload_tables(ctx, run.pl, run.tc.quad);
+      SX_CUDA(cudaStreamWaitEvent(cs, ctx_event(ctx, 1), 0));  // chunk 0's planes binned
+      tr.mark(cs, "chunk 0 may start");
+      const int hz1 = no_store ? z0 : z1;
+      launch_kb_chunk(ctx, run, zc0, c1, hs, hb, z0, hz1);
+      tr.mark(cs, "chunk 0 done");
+      if (c1 < zc1) {
+        SX_CUDA(cudaStreamWaitEvent(cs, ctx_event(ctx, nd), 0));  // every piece binned
+        launch_kb_chunk(ctx, run, c1, zc1, hs, hb, z0, hz1, /*pdl=*/true);
+        tr.mark(cs, "chunk 1 done");
+      }
+      SX_CUDA(cudaEventRecord(g_const_done, cs));
+    }
+    const long long cnt = exch ? 0 : maxima_and_sort(ctx, run, z0, z1);
+    tr.mark(cs, "maxima sorted");
+    SX_CUDA(cudaStreamSynchronize(cs));  // the host maps are complete
+    tr.report();
+    if (run_out) *run_out = run;
+    remember_run(ctx, run, nx, ny, nz, zs0, zs1, z0, z1, bins, scales, n_scales);
+    return cnt;
+  }
   const int K = std::max(1, std::min(4, ntiles / 4));
   // chunk boundaries in eighths of the tile layers: 1, 3, 3, 1 for K = 4 -- a
   // short first chunk starts after fewer uploaded planes, a short last chunk
@@ -2294,9 +2478,6 @@ long long run_exhaustive_pipelined(salvox_ctx* ctx, const float* h_slab, int nx,
   for (int k = 0; k <= K; ++k)
     cut[k] = std::min(zc1, zc0 + tz * (int)((long long)ntiles * kEighths[K][k] / 8));
   cut[K] = zc1;
-  const int npieces = std::max(1, std::min(8, nzs / 8));
-  std::vector<int> pc(npieces + 1);
-  for (int i = 0; i <= npieces; ++i) pc[i] = (int)((long long)nzs * i / npieces);
   SX_CUDA(cudaEventRecord(ctx_event(ctx, 0), cs));  // order after earlier work on cs
   SX_CUDA(cudaStreamWaitEvent(ps, ctx_event(ctx, 0), 0));
   for (int i = 0; i < npieces; ++i) {

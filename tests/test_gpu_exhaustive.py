@@ -320,3 +320,32 @@ def test_nonconsecutive_integer_scales_and_order(sx, oracle):
     # scales out of order with gaps: rank-based tie-break must follow the caller's order
     vol, _ = oracle.make_phantom(phantoms.square_2d(64, 30.0, 33.0, 7, 64, 5))
     _check_maps(sx, oracle, vol, 0, 64, 64, [10.0, 4.0, 7.0], budget=10**9)
+
+
+@pytest.mark.parametrize("slab", [False, True])
+def test_pinned_host_maps_direct_equal_copy_back(sx, oracle, slab):
+    """Pinned host maps take the direct form (the KB epilogue stores the owned
+    planes straight into them; the second chunk runs as a programmatic dependent);
+    pageable maps, or one pinned and one pageable, take the copy-back pipeline.
+    All three are bit-identical, maxima included; the slab case checks the owned
+    plane offset (z0 > zs0) of the host stores."""
+    import torch
+
+    vol, _ = oracle.make_phantom(phantoms.ball_3d(64, (30.0, 33.0, 31.0), 12.0, 5))
+    nz, ny, nx = vol.shape
+    scales = [3.0, 5.0, 7.0]
+    zs0, zs1, z0, z1 = (3, 61, 14, 50) if slab else (0, nz, 0, nz)
+    args = (vol[zs0:zs1], nz, zs0, z0, z1, scales, 0, 64, 64)
+
+    def pinned():
+        return torch.empty((z1 - z0, ny, nx), dtype=torch.float32).pin_memory().numpy()
+
+    ref = sx.kadir_brady_exhaustive_slab(*args, budget=10**10)  # pageable: copy-back
+    for out in [(pinned(), pinned()), (pinned(), np.empty((z1 - z0, ny, nx), np.float32))]:
+        out[0].fill(-7.0)
+        out[1].fill(-7.0)
+        got = sx.kadir_brady_exhaustive_slab(*args, budget=10**10, out=out)
+        assert np.array_equal(got[0], ref[0]) and np.array_equal(got[1], ref[1])
+        assert np.array_equal(got[2], ref[2]) and got[3] == ref[3]
+    s, b, m, _ = sx.kadir_brady_exhaustive_records(vol, scales, 0, 64, 64, budget=10**10)
+    assert np.array_equal(ref[0], s[z0:z1]) and np.array_equal(ref[1], b[z0:z1])

@@ -15,7 +15,7 @@ for r in $(seq $ROUNDS); do
 import json, sys
 for l in open('gpurun_out/abe_bench.log'):
     if l.startswith('{'):
-        d=json.loads(l); print(sys.argv[1], 'kb_ms', round(d['roofline']['kb_ms_per_launch'],2), 'ms/step', round(d['ms_per_step'],2), 'frac', round(d['roofline']['frac'],3), 'clk', d['clocks']['sm_mhz'])
+        d=json.loads(l); print(sys.argv[1], 'kb_ms', round(d['roofline']['kb_ms_per_launch'],2), 'ms/step', round(d['ms_per_step'],2), 'frac', round(d['roofline']['frac'],3), 'e2e_ms', round(d['e2e'].get('ms_per_step', 0),2), 'clk', d['clocks']['sm_mhz'])
 P
   done
 done
