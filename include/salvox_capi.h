@@ -168,7 +168,8 @@ SALVOX_API int salvox_ctx_launch_count(salvox_ctx* ctx, uint64_t* out);
 /* ------------------------------------------------------- exhaustive pass (E1)
  * Replaces kadir_brady_exhaustive (include/salvox/pipeline.hpp:49-53,
  * src/pipeline.cpp:63-166). Same validation and messages (scales >= 2,
- * budget). kernel: identity only on device (others -> SALVOX_EUNSUPPORTED).
+ * budget). kernel: identity or Epanechnikov (exact integer forms); Gaussian
+ * -> SALVOX_EUNSUPPORTED (its weights have no exact shell form).
  * score_out / best_scale_out (nx*ny*nz floats, nullable) receive the dense map;
  * up to `cap` maxima (score-descending, ties by linear index -- the
  * reference's stable_sort order) go to `maxima`; *n_maxima is the full count

@@ -80,7 +80,7 @@ def kadir_brady_exhaustive_records(volume, scales, window_low=None, window_high=
     c = _ctx(ctx)
     score = np.empty(v.shape, np.float32) if want_maps else None
     best = np.empty(v.shape, np.float32) if want_maps else None
-    cap = 4096
+    cap = max(4096, int(_MAXIMA_HINT.get(id(c), 0) * 1.1))  # size from the last call
     maxima = np.empty(cap, MAX_DTYPE)
     n = C.c_int64(0)
     visits = C.c_uint64(0)

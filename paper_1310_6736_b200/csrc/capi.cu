@@ -29,6 +29,8 @@ salvox_ctx::~salvox_ctx() {
                     &d_sel_c, &d_sel_d, &d_visits, &d_target, &d_seek_vol, &d_seek_bins})
     b->release();
   h_stage.release();
+  h_maps.release();
+  h_vol.release();
   for (cudaEvent_t e : events) cudaEventDestroy(e);
   if (order_event) cudaEventDestroy(order_event);
   if (copy_stream) cudaStreamDestroy(copy_stream);

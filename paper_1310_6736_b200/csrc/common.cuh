@@ -129,6 +129,8 @@ struct salvox_ctx {
   sx::DevBuf d_vol, d_bins, d_score, d_best, d_keys, d_keys_alt, d_cub, d_counter, d_maxima,
       d_merge_idx, d_minmax, d_dbg;
   sx::HostBuf h_stage;       // pinned: the last call's maxima (salvox_last_maxima)
+  sx::HostBuf h_maps;        // pinned staging of the maps for pageable host outputs
+  sx::HostBuf h_vol;         // pinned staging of a pageable host volume
   int64_t last_maxima_n = 0;
   bool stage_valid = false;  // h_stage holds them (else read d_maxima again)
   sx::ExhState exh;

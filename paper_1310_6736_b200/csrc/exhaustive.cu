@@ -28,6 +28,8 @@
 #include <algorithm>
 #include <array>
 #include <chrono>
+#include <cstring>
+#include <thread>
 #include <climits>
 #include <cmath>
 #include <map>
@@ -119,7 +121,10 @@ struct KbBound {
   uint32_t W;     // sum of |o|^2 over B(r_i) \ {0}: T(r_i) = W - S_0 (bin 0 = outside)
   double fac;     // s * s / 2.0 (pipeline.cpp:131)
   float scale;    // (float) r_{i-1}
-  int32_t pad_;
+  // Epanechnikov (kb_kernel<EPA>): #B(r_i) incl. the centre, and q, q * r_i^2
+  // with q in {1, 4} the smallest making q * r_i^2 an integer (0: none)
+  uint32_t cnt;
+  uint32_t r2q, q;
 };
 
 // One |o|^2 level: the +-o representatives with that squared norm are
@@ -169,13 +174,19 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-template <int NB, int TX, int TY, int TZ, bool DBG>
+// EPA (Epanechnikov kernel, K(d) = 1 - d, kernel.hpp:21): a second column of
+// per-bin counts C_b(r) beside the sums S_b(r), so per bin the exact integer
+// q * h_b * r^2 = q r^2 C_b(r) - q S_b(r) (the centre, d = 0, weight 1, is
+// counted once up front); same walk, two 32-bit shared atomics per update (a
+// 64-bit count|sum word would compile to a CAS loop).
+template <int NB, int TX, int TY, int TZ, bool DBG, bool EPA = false>
 __global__ void __launch_bounds__(TX* TY* TZ, 1)
     kb_kernel(const __grid_constant__ CUtensorMap tmap, const KbParams p) {
   constexpr int NT = TX * TY * TZ;
+  constexpr int WB = EPA ? 8 : 4;  // bytes per histogram word
   extern __shared__ __align__(1024) uint8_t smem[];
-  uint32_t* hist = reinterpret_cast<uint32_t*>(smem);
-  uint8_t* tile = smem + NB * NT * 4;
+  uint32_t* hist = reinterpret_cast<uint32_t*>(smem);  // EPA: sums, then counts
+  uint8_t* tile = smem + NB * NT * WB;
   uint64_t* bar = reinterpret_cast<uint64_t*>(tile + ((p.tile_bytes + 15u) & ~15u));
   const int tid = threadIdx.x;
 
@@ -218,12 +229,13 @@ __global__ void __launch_bounds__(TX* TY* TZ, 1)
   }
   {
     uint4* h4 = reinterpret_cast<uint4*>(hist);
-    for (int i = tid; i < NB * NT / 4; i += NT) h4[i] = make_uint4(0u, 0u, 0u, 0u);
+    for (int i = tid; i < NB * NT * WB / 16; i += NT) h4[i] = make_uint4(0u, 0u, 0u, 0u);
   }
   const int lx = tid % TX, ly = (tid / TX) % TY, lz = tid / (TX * TY);
   const int gx = tx0 + lx, gy = ty0 + ly, gz = tz0 + lz;
   const uint8_t* tb = tile + (lz + p.Rz) * p.SZ + (ly + p.R) * p.SY + (lx + p.R + delta);
   uint32_t* hc = hist + tid;
+  uint32_t* hcc = hist + NB * NT + tid;  // EPA counts
   {
     uint32_t done = 0;
     while (!done) {
@@ -240,6 +252,7 @@ __global__ void __launch_bounds__(TX* TY* TZ, 1)
   const bool dbg_me =
       DBG && ((long long)gx + (long long)p.nx * ((long long)gy + (long long)p.ny * gz)) == dbg_lin;
   if (DBG && !dbg_me) return;
+  if (EPA) hcc[(uint32_t)tb[0] * NT] += 1u;  // the centre (private column)
 
   uint32_t A[NB], B[NB];
 #pragma unroll
@@ -264,20 +277,24 @@ __global__ void __launch_bounds__(TX* TY* TZ, 1)
     for (; lvl < bd.lend; ++lvl) {
       const KbLevel L = c_levels[lvl];
       const uint32_t n = (uint32_t)L.n;
+      auto upd = [&](uint32_t b) {
+        atomicAdd(hc + b * NT, n);
+        if (EPA) atomicAdd(hcc + b * NT, 1u);
+      };
       const int g0 = L.start0 >> 2, g1 = (L.start0 + L.count0) >> 2;
 #pragma unroll 2
       for (int g = g0; g < g1; ++g) {
         const int4 w = offs4[g];
         const uint32_t b0 = tb[w.x], b1 = tb[-w.x], b2 = tb[w.y], b3 = tb[-w.y];
         const uint32_t b4 = tb[w.z], b5 = tb[-w.z], b6 = tb[w.w], b7 = tb[-w.w];
-        atomicAdd(hc + b0 * NT, n);
-        atomicAdd(hc + b1 * NT, n);
-        atomicAdd(hc + b2 * NT, n);
-        atomicAdd(hc + b3 * NT, n);
-        atomicAdd(hc + b4 * NT, n);
-        atomicAdd(hc + b5 * NT, n);
-        atomicAdd(hc + b6 * NT, n);
-        atomicAdd(hc + b7 * NT, n);
+        upd(b0);
+        upd(b1);
+        upd(b2);
+        upd(b3);
+        upd(b4);
+        upd(b5);
+        upd(b6);
+        upd(b7);
       }
       const int rem = (L.count0 & 3);
       if (rem) {  // tail of the level (entries of the last group, in order)
@@ -285,13 +302,17 @@ __global__ void __launch_bounds__(TX* TY* TZ, 1)
         const int o[3] = {w.x, w.y, w.z};
         for (int j = 0; j < rem; ++j) {
           const uint32_t bp = tb[o[j]], bm = tb[-o[j]];
-          atomicAdd(hc + bp * NT, n);
-          atomicAdd(hc + bm * NT, n);
+          upd(bp);
+          upd(bm);
         }
       }
     }
     // ---- boundary: the column now holds S_b(r_i) for b = 0..NB-1 (0 = outside)
-    const uint32_t T = bd.W - hc[0];
+    // (EPA: and C_b(r_i); the bin value is q r^2 C_b - q S_b)
+    auto bin_value = [&](int b) -> uint32_t {
+      return EPA ? bd.r2q * hcc[b * NT] - bd.q * hc[b * NT] : hc[b * NT];
+    };
+    const uint32_t T = EPA ? bd.r2q * (bd.cnt - hcc[0]) - bd.q * (bd.W - hc[0]) : bd.W - hc[0];
     const bool doH = (bd.flags & 1) && T > 0u;
     const bool doE = (bd.flags & 2) && T > 0u && TA > 0u && TB > 0u;
     const float invT = doH ? 1.0f / (float)T : 0.f;
@@ -299,7 +320,7 @@ __global__ void __launch_bounds__(TX* TY* TZ, 1)
     unsigned long long num = 0ull;
 #pragma unroll
     for (int b = 1; b < NB; ++b) {
-      const uint32_t c = hc[b * NT];
+      const uint32_t c = bin_value(b);
       if (doH && c) {
         const float pb = (float)c * invT;
         float lg;
@@ -1632,10 +1653,17 @@ struct TileCfg {
   bool quad = false;  // kb_quad_kernel (256 threads x 4 voxels, snapshots in TMEM)
   bool dbl = false;  // kb_quad_kernel<DBL>: x-adjacent offset doubles share bin words
   bool vb2 = false;  // kb_quad_kernel<.., VB = 2>: two voxels per boundary iteration
+  bool epa = false;  // kb_kernel<.., EPA>: Epanechnikov, 64-bit count|sum words
 };
 
-TileCfg pick_tile(int bins, bool two_d) {
+TileCfg pick_tile(int bins, bool two_d, bool epa = false) {
   const int nb = bins <= 16 ? 17 : (bins <= 32 ? 33 : 65);
+  if (epa) {  // the plain kb_kernel tiles (64-bit words: 2x the histogram bytes)
+    TileCfg t = nb == 65 ? (two_d ? TileCfg{65, 32, 8, 1, false} : TileCfg{65, 8, 8, 4, false})
+                         : (two_d ? TileCfg{nb, 32, 16, 1, false} : TileCfg{nb, 8, 8, 8, false});
+    t.epa = true;
+    return t;
+  }
   if (nb == 65) return two_d ? TileCfg{65, 32, 8, 1, false} : TileCfg{65, 8, 8, 4, false};
   // Variants (A/B knob SALVOX_KB_VARIANT; measured at C2 on one B200, r01):
   //   4 (default, 3D): kb_quad_kernel<DBL> -- as 3, plus x-adjacent offset
@@ -1694,7 +1722,7 @@ size_t kb_smem(const TileCfg& tc, uint32_t tile_bytes) {
     return (size_t)tc.nb * voxels * 4 + 2 * (((size_t)tile_bytes + 127) & ~(size_t)127) + 16;
   if (tc.tmem || tc.quad)
     return (size_t)tc.nb * voxels * 4 + (((size_t)tile_bytes + 15) & ~(size_t)15) + 32;
-  return (size_t)tc.nb * voxels * 4 + (((size_t)tile_bytes + 15) & ~(size_t)15) + 16;
+  return (size_t)tc.nb * voxels * (tc.epa ? 8 : 4) + (((size_t)tile_bytes + 15) & ~(size_t)15) + 16;
 }
 
 // Offsets of make_sphere_offsets (pipeline.cpp:37-52) for every needed radius,
@@ -1819,6 +1847,17 @@ Plan make_plan(const double* scales, int n_scales, bool two_d, const TileCfg& tc
     KbBound b{};
     b.lend = (int)pl.levels.size();
     b.W = W;
+    b.cnt = (uint32_t)pl.ball_size[i];
+    {
+      const double r2 = pl.radii[i] * pl.radii[i];
+      if (r2 == std::floor(r2)) {
+        b.q = 1;
+        b.r2q = (uint32_t)r2;
+      } else if (4.0 * r2 == std::floor(4.0 * r2)) {
+        b.q = 4;
+        b.r2q = (uint32_t)(4.0 * r2);
+      }
+    }
     b.flags = (is_scale[i] ? 1 : 0) | (eval_rank[i] != INT_MAX ? 2 : 0);
     if (eval_rank[i] != INT_MAX) {
       const double s = pl.radii[i - 1];
@@ -1941,10 +1980,10 @@ Plan make_plan(const double* scales, int n_scales, bool two_d, const TileCfg& tc
 std::mutex g_const_mu;
 cudaEvent_t g_const_done = nullptr;
 
-template <int NB, int TX, int TY, int TZ, bool DBG>
+template <int NB, int TX, int TY, int TZ, bool DBG, bool EPA = false>
 void launch_kb(salvox_ctx* ctx, const CUtensorMap& map, const KbParams& kp, dim3 grid,
                size_t smem) {
-  auto k = kb_kernel<NB, TX, TY, TZ, DBG>;
+  auto k = kb_kernel<NB, TX, TY, TZ, DBG, EPA>;
   SX_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   k<<<grid, TX * TY * TZ, smem, ctx->stream>>>(map, kp);
   SX_LAUNCH_CHECK(ctx);
@@ -1957,7 +1996,12 @@ void dispatch_kb(salvox_ctx* ctx, const TileCfg& tc, const CUtensorMap& map, con
                  dim3 grid, size_t smem, bool pdl = false) {
 #define SX_KB(NB, TX, TY, TZ)                                             \
   if (!tc.pair && !tc.tmem && !tc.quad && tc.nb == NB && tc.tx == TX && tc.ty == TY && tc.tz == TZ) { \
-    launch_kb<NB, TX, TY, TZ, DBG>(ctx, map, kp, grid, smem);             \
+    if (tc.epa) {                                                         \
+      if (DBG) fail(SALVOX_EUNSUPPORTED, "exhaustive debug: identity kernel only"); \
+      launch_kb<NB, TX, TY, TZ, false, true>(ctx, map, kp, grid, smem);   \
+    } else {                                                              \
+      launch_kb<NB, TX, TY, TZ, DBG>(ctx, map, kp, grid, smem);           \
+    }                                                                     \
     return;                                                               \
   }
   SX_KB(17, 8, 8, 8)
@@ -2066,8 +2110,10 @@ void validate_exhaustive(int nx, int ny, int nz, const salvox_window* iw, const 
   if (evals > budget)
     fail(SALVOX_EINVAL, "exhaustive scan: budget exceeded (" + std::to_string(evals) +
                             " voxel-scale evaluations)");
-  if (kernel != SALVOX_KERNEL_IDENTITY)
-    fail(SALVOX_EUNSUPPORTED, "exhaustive (device): only the identity kernel is implemented");
+  if (kernel != SALVOX_KERNEL_IDENTITY && kernel != SALVOX_KERNEL_EPANECHNIKOV)
+    fail(SALVOX_EUNSUPPORTED,
+         "exhaustive (device): identity and Epanechnikov kernels only (the Gaussian weights have "
+         "no exact integer form)");
   if (iw->bins > 64) fail(SALVOX_EUNSUPPORTED, "exhaustive (device): bins must be <= 64");
   if ((uint64_t)nx * ny * nz > 0xffffffffull)
     fail(SALVOX_EUNSUPPORTED, "exhaustive (device): volume exceeds 2^32 voxels");
@@ -2112,13 +2158,19 @@ Plan cached_plan(const double* scales, int n_scales, bool two_d, const TileCfg& 
 // ctx->d_bins, pitch 16-aligned): plan, tensor map, kernel parameters for the
 // scored planes [zc0, zc1) = [z0-1, z1+1) clipped, score/best buffers.
 ExhRun setup_exhaustive(salvox_ctx* ctx, int nx, int ny, int nz, int zs0, int zs1, int z0, int z1,
-                        int bins, const double* scales, int n_scales, bool exch = false) {
+                        int bins, const double* scales, int n_scales, bool exch = false,
+                        bool epa = false) {
   const bool two_d = nz == 1;
   ExhRun run;
   run.generation = ++ctx->exh_generation;  // invalidates any pending exchange-form run
-  run.tc = pick_tile(bins, two_d);
+  run.tc = pick_tile(bins, two_d, epa);
   int SY = 0, SZ = 0;
   run.pl = cached_plan(scales, n_scales, two_d, run.tc, &SY, &SZ);
+  if (epa)
+    for (const KbBound& b : run.pl.bounds)
+      if (b.q == 0)
+        fail(SALVOX_EUNSUPPORTED,
+             "exhaustive (device): the Epanechnikov kernel needs integer or half-integer scales");
   if (run.tc.quad && run.pl.qtab.empty()) run.tc.quad = false, run.tc.tmem = true;  // table too big
   const int R = run.pl.R;
   if (zs0 > std::max(0, z0 - R - 1) || zs1 < std::min(nz, z1 + R + 1))
@@ -2285,8 +2337,9 @@ void remember_run(salvox_ctx* ctx, const ExhRun& run, int nx, int ny, int nz, in
 // Leaves: ctx->d_score/d_best (planes zc0..zc1), sorted keys, count.
 long long run_exhaustive(salvox_ctx* ctx, const float* d_slab, int nx, int ny, int nz, int zs0,
                          int zs1, int z0, int z1, double low, double high, int bins,
-                         const double* scales, int n_scales, ExhRun* run_out, bool exch = false) {
-  ExhRun run = setup_exhaustive(ctx, nx, ny, nz, zs0, zs1, z0, z1, bins, scales, n_scales, exch);
+                         const double* scales, int n_scales, ExhRun* run_out, bool exch = false,
+                         bool epa = false) {
+  ExhRun run = setup_exhaustive(ctx, nx, ny, nz, zs0, zs1, z0, z1, bins, scales, n_scales, exch, epa);
   const int pitch = (nx + 15) / 16 * 16;
   launch_bin_volume(ctx, d_slab, ctx->d_bins.as<uint8_t>(), nx, ny, zs1 - zs0, pitch, low, high,
                     bins);
@@ -2316,6 +2369,7 @@ cudaEvent_t ctx_event(salvox_ctx* ctx, size_t i) {
 struct E2eTrace {
   bool on = false;
   std::vector<std::pair<cudaEvent_t, const char*>> marks;
+  std::vector<std::pair<double, const char*>> hmarks;  // host-side phases
   std::chrono::steady_clock::time_point t0;
   explicit E2eTrace(cudaStream_t s) {
     static const bool env = [] {
@@ -2335,8 +2389,15 @@ struct E2eTrace {
     SX_CUDA(cudaEventRecord(e, s));
     marks.emplace_back(e, what);
   }
+  void host(const char* what) {
+    if (on)
+      hmarks.emplace_back(
+          std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(), what);
+  }
   void report() {
     if (!on) return;
+    for (auto& h : hmarks) std::fprintf(stderr, "[e2e host] %8.3f ms  %s\n", h.first, h.second);
+    hmarks.clear();
     const double host_ms =
         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     for (auto& m : marks) {
@@ -2348,6 +2409,88 @@ struct E2eTrace {
     std::fprintf(stderr, "[e2e] %8.3f ms  host return\n", host_ms);
     for (auto& m : marks) cudaEventDestroy(m.first);
     marks.clear();
+  }
+};
+
+// SALVOX_EXH_STAGED=0: pageable host maps take the plain (blocking) D2H (A/B timing).
+bool staged_maps_disabled() {
+  static const bool off = [] {
+    const char* e = std::getenv("SALVOX_EXH_STAGED");
+    return e && std::string(e) == "0";
+  }();
+  return off;
+}
+
+// Whether host buffer h is page-locked (any CUDA host allocation or registration).
+bool pinned_host(const void* h) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, h) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+// memcpy with up to 8 threads (page-sized splits): pageable buffers copy at a
+// few GB/s per thread.
+void parallel_memcpy(void* dst, const void* src, size_t bytes) {
+  static const int T = [] {
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    return (int)std::min(8u, std::max(1u, hw / 2));
+  }();
+  char* d = static_cast<char*>(dst);
+  const char* s = static_cast<const char*>(src);
+  const size_t per = std::max<size_t>(((bytes + T - 1) / T + 4095) & ~(size_t)4095, 1 << 20);
+  std::vector<std::thread> hs;
+  for (size_t o = per; o < bytes; o += per)
+    hs.emplace_back([=] { std::memcpy(d + o, s + o, std::min(per, bytes - o)); });
+  std::memcpy(d, s, std::min(per, bytes));
+  for (auto& h : hs) h.join();
+}
+
+// Host side of the staged copy-back: one thread walks the chunks in order,
+// waits for each chunk's DMA event and copies its (dst, src, bytes) parts into
+// the caller's pageable buffers with up to 8 helper threads (first-touch page
+// faults of a fresh buffer make one thread far slower than the DMA).
+struct StagedCopier {
+  std::thread th;
+  std::string err;
+  void start(int device, std::vector<std::pair<cudaEvent_t, std::vector<std::array<void*, 3>>>> jobs) {
+    th = std::thread([this, device, jobs = std::move(jobs)] {
+      cudaSetDevice(device);
+      const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+      const int T = (int)std::min(8u, std::max(1u, hw / 2));
+      {  // fault the destination pages in while the first chunks compute
+        std::vector<std::pair<char*, size_t>> ranges;
+        for (const auto& j : jobs)
+          for (const auto& part : j.second) ranges.emplace_back(static_cast<char*>(part[0]), (size_t)part[2]);
+        std::vector<std::thread> hs;
+        for (int t = 0; t < T; ++t)
+          hs.emplace_back([&ranges, t, T] {
+            for (const auto& r : ranges) {
+              const size_t pages = (r.second + 4095) / 4096;
+              for (size_t pg = pages * t / T; pg < pages * (t + 1) / T; ++pg)
+                reinterpret_cast<volatile char*>(r.first)[pg * 4096] = 0;
+            }
+          });
+        for (auto& h : hs) h.join();
+      }
+      for (const auto& j : jobs) {
+        const cudaError_t e = cudaEventSynchronize(j.first);
+        if (e != cudaSuccess) {
+          err = cudaGetErrorString(e);
+          return;
+        }
+        for (const auto& part : j.second) parallel_memcpy(part[0], part[1], (size_t)part[2]);
+      }
+    });
+  }
+  void finish() {
+    if (th.joinable()) th.join();
+    if (!err.empty()) fail(SALVOX_ECUDA, "staged map copy-back: " + err);
+  }
+  ~StagedCopier() {
+    if (th.joinable()) th.join();
   }
 };
 
@@ -2387,7 +2530,7 @@ long long run_exhaustive_pipelined(salvox_ctx* ctx, const float* h_slab, int nx,
                                    int zs0, int zs1, int z0, int z1, double low, double high,
                                    int bins, const double* scales, int n_scales,
                                    float* score_out, float* best_out, ExhRun* run_out,
-                                   bool exch = false) {
+                                   bool exch = false, bool epa = false) {
   if (!ctx->copy_stream) {
     // highest priority: the bin kernels queued on it behind each uploaded piece
     // get their CTAs dispatched beside a running KB chunk (which keeps the SMs
@@ -2397,7 +2540,7 @@ long long run_exhaustive_pipelined(salvox_ctx* ctx, const float* h_slab, int nx,
     SX_CUDA(cudaStreamCreateWithPriority(&ctx->copy_stream, cudaStreamNonBlocking, greatest));
   }
   cudaStream_t cs = ctx->stream, ps = ctx->copy_stream;
-  ExhRun run = setup_exhaustive(ctx, nx, ny, nz, zs0, zs1, z0, z1, bins, scales, n_scales, exch);
+  ExhRun run = setup_exhaustive(ctx, nx, ny, nz, zs0, zs1, z0, z1, bins, scales, n_scales, exch, epa);
   const int R = run.pl.R, tz = run.tc.tz;
   const int nzs = zs1 - zs0;
   const size_t plane = (size_t)nx * ny;
@@ -2410,6 +2553,22 @@ long long run_exhaustive_pipelined(salvox_ctx* ctx, const float* h_slab, int nx,
   const int npieces = std::max(1, std::min(8, nzs / 8));
   std::vector<int> pc(npieces + 1);
   for (int i = 0; i <= npieces; ++i) pc[i] = (int)((long long)nzs * i / npieces);
+  // A pageable slab would make each piece's cudaMemcpyAsync a blocking,
+  // driver-staged copy (the host could enqueue no kernel until the whole slab
+  // was up): host threads copy each piece into pinned staging right before its
+  // (then truly asynchronous) DMA, and pieces are enqueued only as the chunks
+  // need them, so those host copies overlap the first chunk's compute.
+  const bool stage_in = !staged_maps_disabled() && !pinned_host(h_slab);
+  float* h_in = stage_in ? static_cast<float*>(ctx->h_vol.ensure(plane * nzs * 4)) : nullptr;
+  auto upload = [&](int p0, int p1) {  // local planes [p0, p1) on the copy stream
+    const size_t o = (size_t)p0 * plane, n = (size_t)(p1 - p0) * plane;
+    const float* src = h_slab + o;
+    if (stage_in) {
+      parallel_memcpy(h_in + o, src, n * 4);
+      src = h_in + o;
+    }
+    SX_CUDA(cudaMemcpyAsync(d_vol + o, src, n * 4, cudaMemcpyHostToDevice, ps));
+  };
   float* hs = mapped_host(score_out, (size_t)(z1 - z0) * plane);
   float* hb = mapped_host(best_out, (size_t)(z1 - z0) * plane);
   static const bool no_store = [] {  // trace knob: skip the host stores (maps NOT written)
@@ -2438,14 +2597,14 @@ long long run_exhaustive_pipelined(salvox_ctx* ctx, const float* h_slab, int nx,
     E2eTrace tr(cs);
     SX_CUDA(cudaEventRecord(ctx_event(ctx, 0), cs));  // order after earlier work on cs
     SX_CUDA(cudaStreamWaitEvent(ps, ctx_event(ctx, 0), 0));
-    for (int i = 0; i < nd; ++i) {
-      const size_t o = (size_t)dp[i] * plane, n = (size_t)(dp[i + 1] - dp[i]) * plane;
-      SX_CUDA(cudaMemcpyAsync(d_vol + o, h_slab + o, n * 4, cudaMemcpyHostToDevice, ps));
-      launch_bin_volume(ctx, d_vol + o, d_bins + (size_t)dp[i] * pitch * ny, nx, ny,
-                        dp[i + 1] - dp[i], pitch, low, high, bins, ps);
+    auto piece = [&](int i) {
+      upload(dp[i], dp[i + 1]);
+      launch_bin_volume(ctx, d_vol + (size_t)dp[i] * plane, d_bins + (size_t)dp[i] * pitch * ny, nx,
+                        ny, dp[i + 1] - dp[i], pitch, low, high, bins, ps);
       SX_CUDA(cudaEventRecord(ctx_event(ctx, 1 + i), ps));
       tr.mark(ps, "piece uploaded+binned");
-    }
+    };
+    piece(0);
     {
       std::lock_guard<std::mutex> lk(g_const_mu);
       upload_tables(ctx, run.pl, run.tc.quad);
@@ -2454,6 +2613,7 @@ long long run_exhaustive_pipelined(salvox_ctx* ctx, const float* h_slab, int nx,
       const int hz1 = no_store ? z0 : z1;
       launch_kb_chunk(ctx, run, zc0, c1, hs, hb, z0, hz1);
       tr.mark(cs, "chunk 0 done");
+      for (int i = 1; i < nd; ++i) piece(i);
       if (c1 < zc1) {
         SX_CUDA(cudaStreamWaitEvent(cs, ctx_event(ctx, nd), 0));  // every piece binned
         launch_kb_chunk(ctx, run, c1, zc1, hs, hb, z0, hz1, /*pdl=*/true);
@@ -2478,45 +2638,85 @@ long long run_exhaustive_pipelined(salvox_ctx* ctx, const float* h_slab, int nx,
   for (int k = 0; k <= K; ++k)
     cut[k] = std::min(zc1, zc0 + tz * (int)((long long)ntiles * kEighths[K][k] / 8));
   cut[K] = zc1;
+  E2eTrace tr(cs);
   SX_CUDA(cudaEventRecord(ctx_event(ctx, 0), cs));  // order after earlier work on cs
   SX_CUDA(cudaStreamWaitEvent(ps, ctx_event(ctx, 0), 0));
-  for (int i = 0; i < npieces; ++i) {
-    const size_t o = (size_t)pc[i] * plane, n = (size_t)(pc[i + 1] - pc[i]) * plane;
-    SX_CUDA(cudaMemcpyAsync(d_vol + o, h_slab + o, n * 4, cudaMemcpyHostToDevice, ps));
-    SX_CUDA(cudaEventRecord(ctx_event(ctx, 1 + i), ps));
-  }
-  int binned = 0;  // pieces binned so far
+  int uploaded = 0, binned = 0;  // pieces enqueued for upload / binned so far
+  auto piece_up = [&] {
+    upload(pc[uploaded], pc[uploaded + 1]);
+    SX_CUDA(cudaEventRecord(ctx_event(ctx, 1 + uploaded), ps));
+    ++uploaded;
+  };
   {
     std::lock_guard<std::mutex> lk(g_const_mu);
     upload_tables(ctx, run.pl, run.tc.quad);
     for (int k = 0; k < K; ++k) {
       const int need = std::min(nzs, cut[k + 1] + R + 1 - zs0);  // local planes the chunk reads
       while (binned < npieces && pc[binned] < need) {
+        while (uploaded <= binned) piece_up();
         SX_CUDA(cudaStreamWaitEvent(cs, ctx_event(ctx, 1 + binned), 0));
         const int p0 = pc[binned], p1 = pc[binned + 1];
         launch_bin_volume(ctx, d_vol + (size_t)p0 * plane, d_bins + (size_t)p0 * pitch * ny, nx, ny,
                           p1 - p0, pitch, low, high, bins);
         ++binned;
       }
+      tr.host("chunk enqueue");
+      tr.mark(cs, "chunk start");
       launch_kb_chunk(ctx, run, cut[k], cut[k + 1]);
+      tr.mark(cs, "chunk done");
       SX_CUDA(cudaEventRecord(ctx_event(ctx, 1 + npieces + k), cs));
     }
     SX_CUDA(cudaEventRecord(g_const_done, cs));
   }
-  // owned planes of each chunk back to the host while later chunks compute
+  while (uploaded < npieces) piece_up();  // planes no chunk reads (keeps d_vol whole)
+  // Owned planes of each chunk back to the host while later chunks compute.
+  // Pinned (mapped or not) maps take the DMA directly. Pageable maps would make
+  // each cudaMemcpyAsync a blocking, driver-staged copy (C2: ~20 ms after the
+  // compute), so they go through pinned staging instead: one DMA per chunk into
+  // ctx->h_maps, and host threads copy each chunk into the caller's buffers as
+  // soon as its DMA lands, overlapped with the later chunks' compute.
+  const size_t nown = (size_t)(z1 - z0) * plane;
+  const bool stage = ((score_out && !pinned_host(score_out)) || (best_out && !pinned_host(best_out))) &&
+                     !staged_maps_disabled() && nown * 8 <= (size_t(1) << 31);
+  float* st = stage ? static_cast<float*>(ctx->h_maps.ensure(nown * 8)) : nullptr;
+  std::vector<std::array<size_t, 3>> spans;  // (dst offset, planes * plane, event index)
   for (int k = 0; k < K; ++k) {
     const int a = std::max(cut[k], z0), b = std::min(cut[k + 1], z1);
     if (a >= b) continue;
     SX_CUDA(cudaStreamWaitEvent(ps, ctx_event(ctx, 1 + npieces + k), 0));
     const size_t src = (size_t)(a - zc0) * plane, dst = (size_t)(a - z0) * plane;
     const size_t n = (size_t)(b - a) * plane;
+    float* so = stage ? st + dst : score_out + dst;
+    float* bo = stage ? st + nown + dst : best_out + dst;
     if (score_out)
-      SX_CUDA(cudaMemcpyAsync(score_out + dst, run.kp.score + src, n * 4, cudaMemcpyDeviceToHost, ps));
+      SX_CUDA(cudaMemcpyAsync(so, run.kp.score + src, n * 4, cudaMemcpyDeviceToHost, ps));
     if (best_out)
-      SX_CUDA(cudaMemcpyAsync(best_out + dst, run.kp.best + src, n * 4, cudaMemcpyDeviceToHost, ps));
+      SX_CUDA(cudaMemcpyAsync(bo, run.kp.best + src, n * 4, cudaMemcpyDeviceToHost, ps));
+    if (stage) {
+      const size_t ev = 1 + npieces + K + spans.size();
+      SX_CUDA(cudaEventRecord(ctx_event(ctx, ev), ps));
+      spans.push_back({dst, n, ev});
+    }
+    tr.mark(ps, "chunk maps D2H done");
+  }
+  tr.host("D2H enqueued");
+  StagedCopier copier;
+  if (stage) {
+    std::vector<std::pair<cudaEvent_t, std::vector<std::array<void*, 3>>>> jobs;
+    for (const auto& sp : spans) {
+      std::vector<std::array<void*, 3>> parts;
+      if (score_out) parts.push_back({score_out + sp[0], st + sp[0], (void*)(sp[1] * 4)});
+      if (best_out) parts.push_back({best_out + sp[0], st + nown + sp[0], (void*)(sp[1] * 4)});
+      jobs.emplace_back(ctx_event(ctx, sp[2]), std::move(parts));
+    }
+    copier.start(ctx->device, std::move(jobs));
   }
   const long long cnt = exch ? 0 : maxima_and_sort(ctx, run, z0, z1);
+  tr.host("maxima sorted");
+  copier.finish();
+  tr.host("host map copies done");
   SX_CUDA(cudaStreamSynchronize(ps));
+  tr.report();
   if (run_out) *run_out = run;
   remember_run(ctx, run, nx, ny, nz, zs0, zs1, z0, z1, bins, scales, n_scales);
   return cnt;
@@ -2556,7 +2756,7 @@ void fetch_maxima(salvox_ctx* ctx, long long cnt, salvox_maximum* out, int64_t c
   SX_CUDA(cudaStreamSynchronize(ctx->stream));
   ctx->stage_valid = true;
   if (out && cap > 0)
-    std::memcpy(out, stage, (size_t)std::min<long long>(cnt, cap) * sizeof(salvox_maximum));
+    parallel_memcpy(out, stage, (size_t)std::min<long long>(cnt, cap) * sizeof(salvox_maximum));
 }
 
 int exhaustive_host(salvox_ctx* ctx, const float* slab, int32_t nx, int32_t ny, int32_t nz,
@@ -2568,6 +2768,7 @@ int exhaustive_host(salvox_ctx* ctx, const float* slab, int32_t nx, int32_t ny, 
     if (!ctx) fail(SALVOX_EINVAL, "null context");
     std::lock_guard<std::mutex> lk(ctx->mu);
     validate_exhaustive(nx, ny, nz, iw, scales, n_scales, kernel, budget);
+    const bool epa = kernel == SALVOX_KERNEL_EPANECHNIKOV;
     if (!slab) fail(SALVOX_EINVAL, "null volume");
     if (!(0 <= zs0 && zs0 <= z0 && z0 < z1 && z1 <= zs1 && zs1 <= nz))
       fail(SALVOX_EINVAL, "exhaustive slab: need 0 <= zs0 <= z0 < z1 <= zs1 <= nz");
@@ -2580,14 +2781,15 @@ int exhaustive_host(salvox_ctx* ctx, const float* slab, int32_t nx, int32_t ny, 
     long long cnt;
     if (!iw->full_range && !pipeline_disabled()) {
       cnt = run_exhaustive_pipelined(ctx, slab, nx, ny, nz, zs0, zs1, z0, z1, iw->low, iw->high,
-                                     iw->bins, scales, n_scales, score_out, best_scale_out, &run);
+                                     iw->bins, scales, n_scales, score_out, best_scale_out, &run,
+                                     false, epa);
     } else {  // full_range needs the whole slab's min/max before any binning
       float* d_vol = static_cast<float*>(ctx->d_vol.ensure(nslab * 4));
       SX_CUDA(cudaMemcpyAsync(d_vol, slab, nslab * 4, cudaMemcpyHostToDevice, ctx->stream));
       double low = iw->low, high = iw->high;
       if (iw->full_range) device_full_range(ctx, d_vol, nslab, &low, &high);
       cnt = run_exhaustive(ctx, d_vol, nx, ny, nz, zs0, zs1, z0, z1, low, high, iw->bins, scales,
-                           n_scales, &run);
+                           n_scales, &run, false, epa);
       const size_t off = (size_t)nx * ny * (z0 - run.zb0);
       if (score_out)
         SX_CUDA(cudaMemcpyAsync(score_out, ctx->d_score.as<float>() + off, nown * 4,
@@ -2636,6 +2838,7 @@ static int exhaustive_device_impl(salvox_ctx* ctx, const float* d_slab, int32_t 
     if (!ctx) fail(SALVOX_EINVAL, "null context");
     std::lock_guard<std::mutex> lk(ctx->mu);
     validate_exhaustive(nx, ny, nz, iw, scales, n_scales, kernel, budget);
+    const bool epa = kernel == SALVOX_KERNEL_EPANECHNIKOV;
     if (!d_slab) fail(SALVOX_EINVAL, "null volume");
     if (!(0 <= zs0 && zs0 <= z0 && z0 < z1 && z1 <= zs1 && zs1 <= nz))
       fail(SALVOX_EINVAL, "exhaustive slab: need 0 <= zs0 <= z0 < z1 <= zs1 <= nz");
@@ -2646,7 +2849,7 @@ static int exhaustive_device_impl(salvox_ctx* ctx, const float* d_slab, int32_t 
     if (iw->full_range) device_full_range(ctx, d_slab, (size_t)nx * ny * (zs1 - zs0), &low, &high);
     ExhRun run;
     const long long cnt = run_exhaustive(ctx, d_slab, nx, ny, nz, zs0, zs1, z0, z1, low, high,
-                                         iw->bins, scales, n_scales, &run);
+                                         iw->bins, scales, n_scales, &run, false, epa);
     const size_t nown = (size_t)nx * ny * (z1 - z0);
     const size_t off = (size_t)nx * ny * (z0 - run.zb0);
     if (d_score)
@@ -2711,6 +2914,7 @@ extern "C" int salvox_exhaustive_slab_scores(salvox_ctx* ctx, const float* slab,
     if (!ctx) fail(SALVOX_EINVAL, "null context");
     std::lock_guard<std::mutex> lk(ctx->mu);
     validate_exhaustive(nx, ny, nz, iw, scales, n_scales, kernel, budget);
+    const bool epa = kernel == SALVOX_KERNEL_EPANECHNIKOV;
     if (!slab) fail(SALVOX_EINVAL, "null volume");
     if (!(0 <= zs0 && zs0 <= z0 && z0 < z1 && z1 <= zs1 && zs1 <= nz))
       fail(SALVOX_EINVAL, "exhaustive slab: need 0 <= zs0 <= z0 < z1 <= zs1 <= nz");
@@ -2721,10 +2925,10 @@ extern "C" int salvox_exhaustive_slab_scores(salvox_ctx* ctx, const float* slab,
     ExhRun run;
     if (!on_device) {
       run_exhaustive_pipelined(ctx, slab, nx, ny, nz, zs0, zs1, z0, z1, iw->low, iw->high, iw->bins,
-                               scales, n_scales, score_out, best_scale_out, &run, true);
+                               scales, n_scales, score_out, best_scale_out, &run, true, epa);
     } else {
       run_exhaustive(ctx, slab, nx, ny, nz, zs0, zs1, z0, z1, iw->low, iw->high, iw->bins, scales,
-                     n_scales, &run, true);
+                     n_scales, &run, true, epa);
       if (score_out)
         SX_CUDA(cudaMemcpyAsync(score_out, run.kp.score, nown * 4, cudaMemcpyDeviceToDevice,
                                 ctx->stream));

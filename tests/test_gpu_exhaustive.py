@@ -18,11 +18,12 @@ pytestmark = pytest.mark.gpu
 RTOL, ATOL = 1e-5, 1e-6
 
 
-def _check_maps(sx, oracle, vol, low, high, bins, scales, mode="literal", budget=10**12):
+def _check_maps(sx, oracle, vol, low, high, bins, scales, mode="literal", budget=10**12,
+                kernel="identity"):
     score, best, maxima, visits = sx.kadir_brady_exhaustive_records(vol, scales, low, high, bins,
-                                                                    budget=budget)
+                                                                    kernel=kernel, budget=budget)
     rs, rb, rv = oracle.exhaustive(vol, low, high, bins, scales, budget=budget, mode=mode,
-                                   threads=8)
+                                   threads=8, kernel=kernel)
     err = np.abs(score.astype(np.float64) - rs) - (RTOL * np.maximum(np.abs(score), np.abs(rs)) + ATOL)
     assert err.max() <= 0.0, f"score mismatch: worst excess {err.max()}"
     diff = best != rb
@@ -349,3 +350,64 @@ def test_pinned_host_maps_direct_equal_copy_back(sx, oracle, slab):
         assert np.array_equal(got[2], ref[2]) and got[3] == ref[3]
     s, b, m, _ = sx.kadir_brady_exhaustive_records(vol, scales, 0, 64, 64, budget=10**10)
     assert np.array_equal(ref[0], s[z0:z1]) and np.array_equal(ref[1], b[z0:z1])
+
+
+# ---------------------------------------------------------- Epanechnikov kernel
+# kb_kernel<EPA>: per-bin counts beside the |o|^2 sums give the exact integer
+# r^2 C_b - S_b = r^2 h_b (K(d) = 1 - d, kernel.hpp:21; the centre has weight 1);
+# same map tolerance as the identity kernel against the literal oracle (the
+# reference's fp64 loop, pinned to the reference's own sources in test_ref_pin).
+
+
+@pytest.mark.parametrize("bins", [16, 32, 64])
+def test_epanechnikov_3d_maps(sx, oracle, bins):
+    vol, _ = oracle.make_phantom(phantoms.ball_3d(32, (15.0, 16.0, 14.0), 6.0, 11, levels=bins))
+    _check_maps(sx, oracle, vol, 0, bins, bins, [3.0, 4.0, 5.0], kernel="epanechnikov")
+
+
+def test_epanechnikov_2d_and_half_integer_scales(sx, oracle):
+    img, _ = oracle.make_phantom(phantoms.square_2d(64, 31.0, 31.0, 8, 64, 77))
+    _check_maps(sx, oracle, img, 0, 64, 64, [4.0, 6.0, 8.0, 10.0], kernel="epanechnikov")
+    vol, _ = oracle.make_phantom(phantoms.ball_3d(24, (11.0, 12.0, 12.5), 5.0, 3))
+    _check_maps(sx, oracle, vol, 0, 64, 64, [2.5, 3.5, 4.5], kernel="epanechnikov")
+
+
+def test_epanechnikov_matches_the_reference(sx):
+    """Against the reference's own kadir_brady_exhaustive(..., Kernel::Epanechnikov)
+    (oracle/_ref): maps within the tolerance, the same maxima positions."""
+    from oracle import ref as R
+
+    if not R.available():
+        pytest.skip("oracle/_ref/libsalvox_ref.so not built")
+    img = R.make_phantom(phantoms.square_2d(96, 31.0, 60.0, 8, 64, 78))[0]
+    scales = [6.0, 8.0, 10.0]
+    rs, rb, rm, rv = R.exhaustive(img, 0.0, 64.0, 64, scales, kernel="epanechnikov",
+                                  budget=10**9)
+    s, b, m, v = sx.kadir_brady_exhaustive_records(img, scales, 0.0, 64.0, 64,
+                                                   kernel="epanechnikov", budget=10**9)
+    err = np.abs(s.astype(np.float64) - rs) - (RTOL * np.maximum(np.abs(s), np.abs(rs)) + ATOL)
+    assert err.max() <= 0.0
+    assert (b != rb).sum() <= 2 and v == rv
+    assert np.array_equal(m["position"][:, :2], rm[:, :2])
+
+
+def test_epanechnikov_slab_pipeline_equals_whole_volume(sx, oracle):
+    vol, _ = oracle.make_phantom(phantoms.ball_3d(48, (23.0, 25.0, 22.0), 9.0, 4))
+    scales = [3.0, 5.0]
+    full = sx.kadir_brady_exhaustive_records(vol, scales, 0, 64, 64, kernel="epanechnikov",
+                                             budget=10**10)
+    nz = vol.shape[0]
+    s, b, m, _ = sx.kadir_brady_exhaustive_slab(vol[2:40], nz, 2, 9, 33, scales, 0, 64, 64,
+                                                kernel="epanechnikov", budget=10**10)
+    assert np.array_equal(s, full[0][9:33]) and np.array_equal(b, full[1][9:33])
+    ident = sx.kadir_brady_exhaustive_records(vol, scales, 0, 64, 64, budget=10**10)
+    assert not np.array_equal(ident[0], full[0])  # a different weighting, not the identity maps
+
+
+def test_exhaustive_kernel_errors(sx):
+    vol = np.zeros((16, 16, 16), np.float32)
+    with pytest.raises(NotImplementedError, match="Gaussian"):
+        sx.kadir_brady_exhaustive_records(vol, [3.0], 0, 1, 8, kernel="gaussian", budget=10**9)
+    with pytest.raises(NotImplementedError, match="half-integer"):
+        sx.kadir_brady_exhaustive_records(vol, [2.3, 3.3], 0, 1, 8, kernel="epanechnikov",
+                                          budget=10**9)
