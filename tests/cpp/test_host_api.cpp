@@ -175,6 +175,16 @@ void gpu_tests() {
     CHECK(std::abs(res.maxima.front().scale - 8.0) <= 2.0);
     CHECK(counter.count() > 0);
   }
+  {  // the same fixture with the Epanechnikov kernel (exact r^2 C_b - S_b on the device)
+    auto [v, gt] = make_phantom(square_2d(64, 31.0, 31.0, 8, 77));
+    const auto res = kadir_brady_exhaustive(v, IntensityWindow(0, 64, 64), {4.0, 6.0, 8.0, 10.0},
+                                            Kernel::Epanechnikov);
+    CHECK(!res.maxima.empty());
+    CHECK((res.maxima.front().position - Eigen::Vector3d(31, 31, 0)).norm() <= 3.0);
+    CHECK_THROWS_AS(kadir_brady_exhaustive(v, IntensityWindow(0, 64, 64), {4.0, 6.0},
+                                           Kernel::Gaussian),
+                    unsupported_error);
+  }
   {  // test_pipeline.cpp:238-245
     Volume v(48, 48, 1);
     for (float& f : v.data()) f = 2.0f;
