@@ -51,9 +51,9 @@ def test_exhaustive_single_voxel_and_unsupported(sx, oracle):
         sx.kadir_brady_exhaustive(np.ones((8, 8, 8), np.float32), [2.5, 3.0], 0, 8, 8)
     with pytest.raises(NotImplementedError):  # halo > 16 voxels
         sx.kadir_brady_exhaustive(np.ones((8, 8, 8), np.float32), [16.0], 0, 8, 8)
-    with pytest.raises(NotImplementedError):  # exhaustive kernels other than identity
+    with pytest.raises(NotImplementedError):  # Gaussian: no exact integer shell form
         sx.kadir_brady_exhaustive(np.ones((8, 8, 8), np.float32), [3.0], 0, 8, 8,
-                                  kernel="epanechnikov")
+                                  kernel="gaussian")
 
 
 def _seek_equal(gpu, ref, exact=True):
