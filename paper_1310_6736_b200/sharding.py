@@ -19,6 +19,10 @@ trajectory lengths). ONE all-gather of the fixed-size detection records
 restores plan order; the population-quantile thresholds and the dedupe then
 run once on the whole population (pipeline.cpp:383-401), so the selection is
 byte-identical to the 1-GPU detect.
+
+detect_batch_sharded (C5, replicas only) gives rank g a contiguous block of a
+batch of volumes, runs it through one batch seek launch and all-gathers the
+fixed-capacity per-volume selections once.
 """
 from __future__ import annotations
 
@@ -322,3 +326,70 @@ def detect_sharded(volume: np.ndarray, method="shift", seed_spacing=16.0, scales
         def select(d):
             return api.select(d, entropy_quantile, pdf_quantile, k, dedupe_radius, ctx=ctx)
     return select(all_dets), all_dets, visits
+
+
+def batch_bounds(batch: int, world: int, rank: int):
+    """Contiguous block of volumes [b0, b1) of a batch for one rank."""
+    return batch * rank // world, batch * (rank + 1) // world
+
+
+def detect_batch_sharded(volumes, method="shift", seed_spacing=16.0, scales=(8.0,), k=20,
+                         dedupe_radius=5.0, window_low=None, window_high=None, bins=64,
+                         entropy_quantile=0.9, pdf_quantile=0.0, group=None, device=None,
+                         compute=None, ctx=None, **extra):
+    """detect() over a batch of volumes (replicas only): rank r
+    runs the contiguous block batch_bounds(B, world, r) through ONE device call
+    (salvox_detect_batch_device over the block uploaded back to back), then one
+    all-gather of fixed-capacity (k records + count per volume) buffers gives
+    every rank the whole batch's selections in volume order.
+
+    `volumes`: host array (B, nz, ny, nx) or (B, ny, nx). Returns
+    ([selected DET_DTYPE per volume], total visits). `compute(b0, b1) ->
+    ([selected per volume], visits)` may replace the device call (the CPU
+    multi-process tests inject the oracle there).
+    """
+    import torch
+    import torch.distributed as dist
+
+    from . import api
+
+    vols = np.asarray(volumes, np.float32)
+    B = vols.shape[0]
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    b0, b1 = batch_bounds(B, world, rank)
+    kk = max(int(k), 1)
+    if compute is None:
+        def compute(a, b):
+            if b <= a:
+                return [], 0
+            dev = (torch.device(device) if device is not None else
+                   torch.device("cuda", torch.cuda.current_device()))
+            d = torch.from_numpy(np.ascontiguousarray(vols[a:b])).to(dev, non_blocking=True)
+            return api.detect_batch_device(d, b - a, vols.shape[1:], method, seed_spacing, scales,
+                                           kk, dedupe_radius, window_low, window_high, bins,
+                                           entropy_quantile, pdf_quantile, ctx=ctx, **extra)
+    local, visits = compute(b0, b1)
+    if world == 1:
+        return list(local), int(visits)
+    cap = (B + world - 1) // world  # largest block
+    rec = np.zeros((cap, kk), DET_DTYPE)
+    cnt = np.zeros(cap, np.int64)
+    for i, sel in enumerate(local):
+        rec[i, : len(sel)] = sel[:kk]
+        cnt[i] = len(sel)
+    dev = collective_device(group, device)
+    raw = torch.from_numpy(rec.view(np.uint8).reshape(cap, -1).copy()).to(dev)
+    meta = torch.from_numpy(np.concatenate([cnt, [visits]]).astype(np.int64)).to(dev)
+    raws = [torch.zeros_like(raw) for _ in range(world)]
+    metas = [torch.zeros_like(meta) for _ in range(world)]
+    dist.all_gather(raws, raw, group=group)
+    dist.all_gather(metas, meta, group=group)
+    out, total = [], 0
+    for r in range(world):
+        a, b = batch_bounds(B, world, r)
+        rr = np.ascontiguousarray(raws[r].cpu().numpy()).view(DET_DTYPE).reshape(cap, kk)
+        mm = metas[r].cpu().numpy()
+        out += [rr[i, : int(mm[i])].copy() for i in range(b - a)]
+        total += int(mm[cap])
+    return out, total

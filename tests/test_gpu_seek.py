@@ -207,3 +207,21 @@ def test_batch_device_equals_per_volume_detect(sx, oracle, method):
         assert g.tobytes() == ref.tobytes()
         tot += vis
     assert visits == tot
+
+
+def test_detect_batch_sharded_single_rank_device_path(sx, oracle):
+    """sharding.detect_batch_sharded without a process group: the rank's block is
+    the whole batch, uploaded and run through one salvox_detect_batch_device."""
+    from paper_1310_6736_b200 import sharding
+
+    vols = np.stack([oracle.make_phantom(phantoms.ball_3d(20, (9.0, 10.0 + i, 9.0), 4.0,
+                                                          70 + i))[0] for i in range(4)])
+    kw = dict(seed_spacing=6.0, scales=[3.0, 4.0], k=5, dedupe_radius=3.0, window_low=0,
+              window_high=64, bins=64)
+    got, visits = sharding.detect_batch_sharded(vols, method="shift", **kw)
+    tot = 0
+    for v, g in zip(vols, got):
+        ref, _, vis = sx.detect_records(v, "shift", **kw)
+        assert g.tobytes() == ref.tobytes()
+        tot += vis
+    assert visits == tot

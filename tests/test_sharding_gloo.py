@@ -278,3 +278,71 @@ def test_exchange_gloo_matches_single_process(oracle, world):
         assert np.array_equal(merged["score"], sc)
     full = np.concatenate([s for _, s in sorted(planes, key=lambda t: t[0])])
     assert np.array_equal(full, s_ref)
+
+
+BATCH_KW = dict(method="shift", seed_spacing=8.0, scales=[3.0, 5.0], top_k=4, dedupe_radius=4.0)
+
+
+def _batch_volumes(oracle, n=5):
+    return np.stack([oracle.make_phantom(phantoms.ball_3d(
+        20, (8.0 + i, 10.0, 11.0 - i), 4.0, 40 + i))[0] for i in range(n)])
+
+
+def _batch_worker(rank, world, port, vols, out):
+    import torch.distributed as dist
+
+    from oracle import oracle as O
+    from paper_1310_6736_b200 import sharding
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        def compute(a, b):  # the oracle stands in for salvox_detect_batch_device
+            sels, vis = [], 0
+            for v in vols[a:b]:
+                s, _, n = O.detect(v, 0, 64, 64, **BATCH_KW)
+                sels.append(s)
+                vis += n
+            return sels, vis
+
+        sels, visits = sharding.detect_batch_sharded(vols, k=BATCH_KW["top_k"], compute=compute)
+        out[rank] = ([s.tobytes() for s in sels], visits)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_batch_replicas_gloo_match_single_process(oracle, world):
+    """C5 (replicas only): each rank runs a contiguous block of the batch, one
+    all-gather of fixed-capacity per-volume selections; every rank ends with the
+    whole batch in volume order, byte-identical to one process."""
+    vols = _batch_volumes(oracle)
+    ref, ref_vis = [], 0
+    for v in vols:
+        s, _, n = oracle.detect(v, 0, 64, 64, **BATCH_KW)
+        ref.append(s.tobytes())
+        ref_vis += n
+    assert any(len(r) for r in ref)
+    mgr = mp.Manager()
+    out = mgr.dict()
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    procs = [ctx.Process(target=_batch_worker, args=(r, world, port, vols, out))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(180)
+        assert p.exitcode == 0
+    for r in range(world):
+        sels, visits = out[r]
+        assert sels == ref and visits == ref_vis
+
+
+def test_batch_bounds_cover():
+    from paper_1310_6736_b200 import sharding
+
+    for B, world in [(64, 8), (5, 3), (2, 4)]:
+        blocks = [sharding.batch_bounds(B, world, r) for r in range(world)]
+        assert [i for a, b in blocks for i in range(a, b)] == list(range(B))
