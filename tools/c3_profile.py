@@ -36,6 +36,8 @@ order = np.argsort(-it, kind="stable")
 for n in (1, 16, 148, 592):
     m, _, _ = run(order[:n])
     print(f"longest {n:4d} seeds: {m:.2f} ms (iterations >= {it[order[n - 1]]})")
+m, _, _ = run(order[-1:])
+print(f"shortest 1 seed: {m:.2f} ms (upload + binning + launch: the fixed part)")
 m, _, _ = run(order[len(order) // 2:])
 print(f"shortest half: {m:.2f} ms")
 for s in (8.0, 12.0):
