@@ -411,3 +411,24 @@ def test_exhaustive_kernel_errors(sx):
     with pytest.raises(NotImplementedError, match="half-integer"):
         sx.kadir_brady_exhaustive_records(vol, [2.3, 3.3], 0, 1, 8, kernel="epanechnikov",
                                           budget=10**9)
+
+
+@pytest.mark.parametrize("shape", [(130, 40, 37), (137, 24, 64), (64, 33, 20)])
+def test_direct_form_two_chunks_ragged(sx, oracle, shape):
+    """Volumes with >= 16 tile layers take the direct form's two chunks (the
+    second a programmatic dependent of the first) with ragged x/y/z edges; the
+    pinned-map result equals the pageable (staged) one and the oracle's maxima."""
+    import torch
+
+    rng = np.random.default_rng(sum(shape))
+    vol = rng.uniform(-2.0, 34.0, size=shape).astype(np.float32)
+    scales = [3.0, 4.0]
+    nz, ny, nx = shape
+    ref = sx.kadir_brady_exhaustive_slab(vol, nz, 0, 0, nz, scales, 0, 32, 32, budget=10**10)
+    out = tuple(torch.empty(shape, dtype=torch.float32).pin_memory().numpy() for _ in range(2))
+    got = sx.kadir_brady_exhaustive_slab(vol, nz, 0, 0, nz, scales, 0, 32, 32, budget=10**10,
+                                         out=out)
+    assert np.array_equal(got[0], ref[0]) and np.array_equal(got[1], ref[1])
+    assert np.array_equal(got[2], ref[2])
+    lin = oracle.local_maxima(got[0], got[1])[3]
+    assert np.array_equal(got[2]["linear_index"], lin)
