@@ -35,3 +35,20 @@ def t(i, reps=15):
 a, b = t(hi), t(lo)
 print(f"longest seed ({it[hi]} iterations, scale {scl[hi]}): {a:.2f} ms; shortest: {b:.2f} ms; "
       f"trajectory latency {a - b:.2f} ms")
+
+# the whole grid in plan order vs sorted longest-trajectory-first (an oracle ordering:
+# the upper bound of what predicting trajectory lengths could buy)
+order = np.argsort(-it, kind="stable")
+
+
+def grid(idx, reps=7):
+    best = 1e9
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        sx.seek_records(vol, pos[idx], scales=scl[idx], ctx=ctx, **win)
+        best = min(best, time.perf_counter() - t0)
+    return best * 1e3
+
+
+print(f"grid, plan order: {grid(np.arange(len(pos))) - b:.2f} ms; longest-first: "
+      f"{grid(order) - b:.2f} ms (fixed part removed)")
