@@ -40,19 +40,85 @@
 namespace sx {
 
 // ----------------------------------------------------------------------------- K1
+// bin + 1 of one intensity: floor((I - low) / (high - low) * bins) clamped to
+// [0, bins - 1] (volume.hpp:102-105), the reference's IEEE fp64 operations in
+// its order. Fast path: t' = (I - low) * (bins / range) is within a few ulp of
+// the reference's t, so when t' is more than 1e-9 away from an integer (and
+// |t'| < 1e6, where a few ulp are < 1e-9) floor(t') == floor(t) exactly; only
+// values within 1e-9 of a bin edge take the reference's division.
+__device__ __forceinline__ uint8_t bin_of(float I, double low, double range, double m,
+                                          double inv, int M) {
+  const double x = __dsub_rn((double)I, low);
+  const double tq = __dmul_rn(x, inv);
+  const double f = floor(tq);
+  double t = tq;
+  if (!(tq - f > 1e-9 && f + 1.0 - tq > 1e-9 && fabs(tq) < 1e6))
+    t = __dmul_rn(__ddiv_rn(x, range), m);
+  int b = (int)floor(t);
+  b = b < 0 ? 0 : (b > M - 1 ? M - 1 : b);
+  return (uint8_t)(b + 1);
+}
+
+// Rows of nx floats in, rows of `pitch` bytes out; 4 voxels per thread through
+// float4 / uchar4 when the row allows it (HBM-bound: 5 B per voxel).
 __global__ void bin_volume_kernel(const float* __restrict__ vol, uint8_t* __restrict__ bins,
                                   int nx, long long rows, int pitch, double low, double range,
                                   double m, int M) {
+  const double inv = m / range;
+  if (pitch == nx && (reinterpret_cast<uintptr_t>(vol) & 15) == 0) {
+    // rows back to back in both arrays (nx % 16 == 0): one flat grid-stride
+    // pass, U independent 16-byte loads in flight per thread
+    constexpr int U = 4;
+    const long long n4 = rows * (nx >> 2);
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    const float4* v4 = reinterpret_cast<const float4*>(vol);
+    uchar4* b4 = reinterpret_cast<uchar4*>(bins);
+    for (long long i0 = (long long)blockIdx.x * blockDim.x + threadIdx.x; i0 < n4; i0 += stride * U) {
+      float4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (i0 + u * stride < n4) v[u] = __ldg(v4 + i0 + u * stride);
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (i0 + u * stride < n4) {
+          uchar4 o;
+          o.x = bin_of(v[u].x, low, range, m, inv, M);
+          o.y = bin_of(v[u].y, low, range, m, inv, M);
+          o.z = bin_of(v[u].z, low, range, m, inv, M);
+          o.w = bin_of(v[u].w, low, range, m, inv, M);
+          b4[i0 + u * stride] = o;
+        }
+    }
+    return;
+  }
+  if ((nx & 3) == 0 && (reinterpret_cast<uintptr_t>(vol) & 15) == 0) {
+    // U rows per block step: U independent 16-byte loads in flight per thread
+    constexpr int U = 4;
+    const int n4 = nx >> 2;
+    for (long long r0 = (long long)blockIdx.x * U; r0 < rows; r0 += (long long)gridDim.x * U) {
+      for (int x4 = threadIdx.x; x4 < n4; x4 += blockDim.x) {
+        float4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (r0 + u < rows) v[u] = __ldg(reinterpret_cast<const float4*>(vol + (r0 + u) * nx) + x4);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (r0 + u < rows) {
+            uchar4 o;
+            o.x = bin_of(v[u].x, low, range, m, inv, M);
+            o.y = bin_of(v[u].y, low, range, m, inv, M);
+            o.z = bin_of(v[u].z, low, range, m, inv, M);
+            o.w = bin_of(v[u].w, low, range, m, inv, M);
+            reinterpret_cast<uchar4*>(bins + (r0 + u) * pitch)[x4] = o;  // pitch % 16 == 0
+          }
+      }
+    }
+    return;
+  }
   for (long long row = blockIdx.x; row < rows; row += gridDim.x) {
     const float* src = vol + row * nx;
     uint8_t* dst = bins + row * pitch;
-    for (int x = threadIdx.x; x < nx; x += blockDim.x) {
-      // floor((I - low) / (high - low) * bins), IEEE ops in the reference order
-      const double t = __dmul_rn(__ddiv_rn(__dsub_rn((double)src[x], low), range), m);
-      int b = (int)floor(t);
-      b = b < 0 ? 0 : (b > M - 1 ? M - 1 : b);
-      dst[x] = (uint8_t)(b + 1);
-    }
+    for (int x = threadIdx.x; x < nx; x += blockDim.x) dst[x] = bin_of(src[x], low, range, m, inv, M);
   }
 }
 
@@ -60,8 +126,15 @@ void launch_bin_volume(salvox_ctx* ctx, const float* d_vol, uint8_t* d_bins, int
                        int nzs, int pitch, double low, double high, int bins,
                        cudaStream_t stream) {
   const long long rows = (long long)ny * nzs;
-  const int grid = (int)std::min<long long>(rows, (long long)ctx->sm_count * 32);
-  const int block = nx >= 256 ? 256 : ((nx + 31) / 32) * 32;
+  const int lanes = (nx & 3) == 0 ? nx / 4 : nx;  // threads one row needs
+  int block = lanes >= 128 ? 128 : ((lanes + 31) / 32) * 32;
+  const long long steps = (nx & 3) == 0 ? (rows + 3) / 4 : rows;  // block steps of 4 / 1 rows
+  int grid = (int)std::min<long long>(steps, (long long)ctx->sm_count * 16);
+  if (pitch == nx) {  // flat form: 256 threads x U = 4 float4 each per block step
+    block = 256;
+    grid = (int)std::max<long long>(1, std::min<long long>((rows * (nx / 4) + 1023) / 1024,
+                                                           (long long)ctx->sm_count * 8));
+  }
   bin_volume_kernel<<<grid, block, 0, stream ? stream : ctx->stream>>>(d_vol, d_bins, nx, rows, pitch, low,
                                                       high - low, (double)bins, bins);
   SX_LAUNCH_CHECK(ctx);

@@ -432,3 +432,19 @@ def test_direct_form_two_chunks_ragged(sx, oracle, shape):
     assert np.array_equal(got[2], ref[2])
     lin = oracle.local_maxima(got[0], got[1])[3]
     assert np.array_equal(got[2]["linear_index"], lin)
+
+
+@pytest.mark.parametrize("window", [(-3.7, 29.3, 32), (0.0, 1.0, 16), (0.1, 64.3, 64)])
+def test_bin_edges_exact(sx, oracle, window):
+    """K1 bins through t' = (I - low) * (bins / range) and falls back to the
+    reference's (I - low) / range * bins within 1e-9 of a bin edge: intensities
+    on and one float ulp around every edge must bin exactly like the reference
+    (any misbinned voxel changes the exact integer histograms, hence the maps)."""
+    low, high, bins = window
+    edges = low + np.arange(bins + 1) * (high - low) / bins
+    e32 = edges.astype(np.float32)
+    vals = np.concatenate([e32, np.nextafter(e32, np.float32(np.inf)),
+                           np.nextafter(e32, np.float32(-np.inf))])
+    rng = np.random.default_rng(bins)
+    vol = rng.choice(vals, size=(20, 21, 24)).astype(np.float32)
+    _check_maps(sx, oracle, vol, low, high, bins, [2.0, 3.0], mode="exact")
