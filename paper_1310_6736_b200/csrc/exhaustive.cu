@@ -30,6 +30,8 @@
 #include <chrono>
 #include <cstring>
 #include <thread>
+
+#include <sys/mman.h>
 #include <climits>
 #include <cmath>
 #include <map>
@@ -2521,6 +2523,25 @@ void parallel_memcpy(void* dst, const void* src, size_t bytes) {
   for (auto& h : hs) h.join();
 }
 
+// Faults the pages of host range [p, p + n) in (huge pages where THP allows),
+// with up to T threads: a fresh pageable buffer written later by a memcpy
+// would otherwise take its page faults inside that copy.
+void prefault(char* p, size_t n, int T) {
+  if (!p || n == 0) return;
+  const uintptr_t a0 = (reinterpret_cast<uintptr_t>(p) + (2u << 20) - 1) & ~uintptr_t((2u << 20) - 1);
+  const uintptr_t a1 = (reinterpret_cast<uintptr_t>(p) + n) & ~uintptr_t((2u << 20) - 1);
+  if (a1 > a0) madvise(reinterpret_cast<void*>(a0), a1 - a0, MADV_HUGEPAGE);  // errors: harmless
+  const size_t pages = (n + 4095) / 4096;
+  auto touch = [=](int t) {
+    for (size_t pg = pages * t / T; pg < pages * (t + 1) / T; ++pg)
+      reinterpret_cast<volatile char*>(p)[pg * 4096] = 0;
+  };
+  std::vector<std::thread> hs;
+  for (int t = 1; t < T; ++t) hs.emplace_back(touch, t);
+  touch(0);
+  for (auto& h : hs) h.join();
+}
+
 // Host side of the staged copy-back: one thread walks the chunks in order,
 // waits for each chunk's DMA event and copies its (dst, src, bytes) parts into
 // the caller's pageable buffers with up to 8 helper threads (first-touch page
@@ -2537,16 +2558,7 @@ struct StagedCopier {
         std::vector<std::pair<char*, size_t>> ranges;
         for (const auto& j : jobs)
           for (const auto& part : j.second) ranges.emplace_back(static_cast<char*>(part[0]), (size_t)part[2]);
-        std::vector<std::thread> hs;
-        for (int t = 0; t < T; ++t)
-          hs.emplace_back([&ranges, t, T] {
-            for (const auto& r : ranges) {
-              const size_t pages = (r.second + 4095) / 4096;
-              for (size_t pg = pages * t / T; pg < pages * (t + 1) / T; ++pg)
-                reinterpret_cast<volatile char*>(r.first)[pg * 4096] = 0;
-            }
-          });
-        for (auto& h : hs) h.join();
+        for (const auto& r : ranges) prefault(r.first, r.second, T);
       }
       for (const auto& j : jobs) {
         const cudaError_t e = cudaEventSynchronize(j.first);
@@ -2850,6 +2862,17 @@ int exhaustive_host(salvox_ctx* ctx, const float* slab, int32_t nx, int32_t ny, 
     SX_CUDA(cudaSetDevice(ctx->device));
     const size_t nslab = (size_t)nx * ny * (zs1 - zs0);
     const size_t nown = (size_t)nx * ny * (z1 - z0);
+    // a pageable maxima buffer: its pages fault in while the pass computes
+    std::thread mx_fault;
+    if (maxima && cap > 0 && !staged_maps_disabled() && !pinned_host(maxima))
+      mx_fault = std::thread(prefault, reinterpret_cast<char*>(maxima),
+                             (size_t)cap * sizeof(salvox_maximum), 2);
+    struct Joiner {
+      std::thread& t;
+      ~Joiner() {
+        if (t.joinable()) t.join();
+      }
+    } mx_join{mx_fault};
     ExhRun run;
     long long cnt;
     if (!iw->full_range && !pipeline_disabled()) {
@@ -2871,6 +2894,7 @@ int exhaustive_host(salvox_ctx* ctx, const float* slab, int32_t nx, int32_t ny, 
         SX_CUDA(cudaMemcpyAsync(best_scale_out, ctx->d_best.as<float>() + off, nown * 4,
                                 cudaMemcpyDeviceToHost, ctx->stream));
     }
+    if (mx_fault.joinable()) mx_fault.join();
     fetch_maxima(ctx, cnt, maxima, cap);
     if (n_maxima) *n_maxima = cnt;
     if (visits) *visits += closed_form_visits(run.pl, nown);
