@@ -3,6 +3,8 @@
 #include "salvox/pipeline.hpp"
 
 #include <algorithm>
+#include <atomic>
+#include <thread>
 #include <cmath>
 #include <limits>
 
@@ -94,21 +96,54 @@ ExhaustiveResult kadir_brady_exhaustive(const Volume& v, const IntensityWindow& 
                                 " voxel-scale evaluations)");
   ExhaustiveResult res;
   res.map.dims = Eigen::Vector3i(v.nx(), v.ny(), v.nz());
-  res.map.score.resize(v.size());
-  res.map.best_scale.resize(v.size());
   const salvox_window w{iw.low, iw.high, iw.bins, 0};
   int64_t n = 0;
   uint64_t visits = 0;
   salvox_ctx* c = ctx();
+  // The result's std::vectors value-initialise their storage (2 x 4 B per voxel
+  // plus the maxima list: ~160 MB of first-touch page faults at 256^3), so they
+  // are allocated on host threads WHILE the pass runs with its maps left on the
+  // device, then filled by salvox_last_maps / salvox_last_maxima.
+  static std::atomic<int64_t> maxima_hint{0};  // list size of the last call
+  const size_t hint = size_t(maxima_hint.load() * 11 / 10);
+  std::vector<salvox_maximum> mx;
+  std::thread a1([&] { res.map.score.resize(v.size()); });
+  std::thread a2([&] { res.map.best_scale.resize(v.size()); });
+  std::thread a3([&] {
+    mx.resize(hint);
+    res.maxima.resize(hint);
+  });
+  struct Join {
+    std::thread* t[3];
+    ~Join() {
+      for (std::thread* x : t)
+        if (x->joinable()) x->join();
+    }
+  } join{{&a1, &a2, &a3}};
   check_status(salvox_exhaustive(c, v.data().data(), v.nx(), v.ny(), v.nz(), &w, scales.data(),
-                                 int(scales.size()), int(kernel), budget, res.map.score.data(),
-                                 res.map.best_scale.data(), nullptr, 0, &n, &visits));
-  std::vector<salvox_maximum> mx(static_cast<size_t>(n));
+                                 int(scales.size()), int(kernel), budget, nullptr, nullptr,
+                                 nullptr, 0, &n, &visits));
+  a1.join();
+  a2.join();
+  a3.join();
+  maxima_hint.store(n);
+  check_status(salvox_last_maps(c, res.map.score.data(), res.map.best_scale.data()));
+  mx.resize(size_t(n));
+  res.maxima.resize(size_t(n));
   if (n > 0) check_status(salvox_last_maxima(c, mx.data(), n, &n));
-  res.maxima.reserve(size_t(n));
-  for (const salvox_maximum& m : mx)
-    res.maxima.push_back(
-        {Eigen::Vector3d(m.position[0], m.position[1], m.position[2]), m.score, m.scale});
+  // records -> SaliencyMaximum (pipeline.hpp:32-36), a few threads for long lists
+  const size_t nm = size_t(n);
+  const size_t T = nm > 65536 ? 4 : 1;
+  auto conv = [&](size_t t) {
+    for (size_t i = nm * t / T; i < nm * (t + 1) / T; ++i) {
+      const salvox_maximum& m = mx[i];
+      res.maxima[i] = {Eigen::Vector3d(m.position[0], m.position[1], m.position[2]), m.score, m.scale};
+    }
+  };
+  std::vector<std::thread> cv;
+  for (size_t t = 1; t < T; ++t) cv.emplace_back(conv, t);
+  conv(0);
+  for (auto& t : cv) t.join();
   if (counter) counter->add(visits);
   return res;
 }

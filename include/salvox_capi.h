@@ -243,6 +243,14 @@ SALVOX_API int salvox_exhaustive_slab_maxima(salvox_ctx* ctx, const float* d_bel
 
 /* Copies the maxima of the last exhaustive call on ctx. */
 SALVOX_API int salvox_last_maxima(salvox_ctx* ctx, salvox_maximum* out, int64_t cap, int64_t* n_out);
+
+/* The owned-plane score / best-scale maps ((z1-z0)*ny*nx floats each; either
+ * nullable) of the last exhaustive call on ctx, which keeps them on the device.
+ * A caller can run the pass with null maps, allocate its result arrays while
+ * it runs, and fetch them here (the C++ drop-in's kadir_brady_exhaustive does).
+ * Pinned buffers take one DMA; pageable ones go through pinned staging.
+ * SALVOX_EINVAL when ctx has run no exhaustive call. */
+SALVOX_API int salvox_last_maps(salvox_ctx* ctx, float* score_out, float* best_scale_out);
 /* Device form: the last call's maxima into a device buffer (D2D). */
 SALVOX_API int salvox_last_maxima_device(salvox_ctx* ctx, salvox_maximum* d_out, int64_t cap,
                                          int64_t* n_out);

@@ -129,6 +129,7 @@ EXPORTS = [
     "salvox_exhaustive_slab", "salvox_exhaustive_device", "salvox_exhaustive_slab_device",
     "salvox_exhaustive_slab_scores", "salvox_exhaustive_slab_edges",
     "salvox_exhaustive_slab_maxima", "salvox_last_maxima", "salvox_last_maxima_device",
+    "salvox_last_maps",
     "salvox_merge_maxima_device",
     "salvox_exhaustive_debug_hist", "salvox_detect", "salvox_detect_batch_device",
     "salvox_detect_shard", "salvox_seek",
@@ -192,6 +193,7 @@ def _declare(L):
     L.salvox_exhaustive_slab_edges.argtypes = [_vp, _vp, _vp]
     L.salvox_exhaustive_slab_maxima.argtypes = [_vp, _vp, _vp, _vp, _i64, _pi64]
     L.salvox_last_maxima.argtypes = [_vp, _vp, _i64, _pi64]
+    L.salvox_last_maps.argtypes = [_vp, _vp, _vp]
     L.salvox_last_maxima_device.argtypes = [_vp, _vp, _i64, _pi64]
     L.salvox_merge_maxima_device.argtypes = [_vp, _vp, _i64, _vp]
     L.salvox_exhaustive_debug_hist.argtypes = [_vp, _vp, _i32, _vp, _vp, C.POINTER(_i32)]

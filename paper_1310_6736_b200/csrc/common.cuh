@@ -99,6 +99,7 @@ struct HostBuf {
 struct ExhState {
   bool valid = false;
   int nx = 0, ny = 0, nz = 0, zs0 = 0, zs1 = 0, z0 = 0, z1 = 0;
+  int zb0 = 0;  // first plane held in ctx->d_score / d_best (salvox_last_maps)
   int bins = 0;
   std::vector<double> radii;
   std::vector<double> scales;

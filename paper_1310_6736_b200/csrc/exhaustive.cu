@@ -2402,6 +2402,7 @@ void remember_run(salvox_ctx* ctx, const ExhRun& run, int nx, int ny, int nz, in
   ctx->exh.zs1 = zs1;
   ctx->exh.z0 = z0;
   ctx->exh.z1 = z1;
+  ctx->exh.zb0 = run.zb0;
   ctx->exh.bins = bins;
   ctx->exh.radii = run.pl.radii;
   ctx->exh.scales.assign(scales, scales + n_scales);
@@ -3176,6 +3177,47 @@ extern "C" int salvox_merge_maxima_device(salvox_ctx* ctx, const salvox_maximum*
   });
 }
 
+// Device map -> host buffer: pinned takes one DMA; pageable goes through two
+// 16 MB pinned staging slots, the host copy of one chunk overlapping the DMA of
+// the next.
+void maps_to_host(salvox_ctx* ctx, const float* d, float* h, size_t n) {
+  if (!h || n == 0) return;
+  if (pinned_host(h)) {
+    SX_CUDA(cudaMemcpyAsync(h, d, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    SX_CUDA(cudaStreamSynchronize(ctx->stream));
+    return;
+  }
+  const size_t chunk = size_t(4) << 20;  // floats
+  float* st = static_cast<float*>(ctx->h_maps.ensure(2 * chunk * 4));
+  const size_t nch = (n + chunk - 1) / chunk;
+  auto dma = [&](size_t i) {
+    const size_t o = i * chunk, m = std::min(chunk, n - o);
+    SX_CUDA(cudaMemcpyAsync(st + (i & 1) * chunk, d + o, m * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    SX_CUDA(cudaEventRecord(ctx_event(ctx, i & 1), ctx->stream));
+  };
+  dma(0);
+  for (size_t i = 0; i < nch; ++i) {
+    if (i + 1 < nch) dma(i + 1);  // its slot's previous chunk (i - 1) is already copied out
+    SX_CUDA(cudaEventSynchronize(ctx_event(ctx, i & 1)));
+    const size_t o = i * chunk;
+    parallel_memcpy(h + o, st + (i & 1) * chunk, std::min(chunk, n - o) * 4);
+  }
+}
+
+extern "C" int salvox_last_maps(salvox_ctx* ctx, float* score_out, float* best_scale_out) {
+  return guarded([&] {
+    if (!ctx) fail(SALVOX_EINVAL, "null context");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (!ctx->exh.valid) fail(SALVOX_EINVAL, "salvox_last_maps: no exhaustive call on this context");
+    SX_CUDA(cudaSetDevice(ctx->device));
+    const sx::ExhState& e = ctx->exh;
+    const size_t plane = (size_t)e.nx * e.ny;
+    const size_t n = plane * (e.z1 - e.z0), off = plane * (e.z0 - e.zb0);
+    maps_to_host(ctx, ctx->d_score.as<float>() + off, score_out, n);
+    maps_to_host(ctx, ctx->d_best.as<float>() + off, best_scale_out, n);
+  });
+}
+
 extern "C" int salvox_last_maxima(salvox_ctx* ctx, salvox_maximum* out, int64_t cap,
                                   int64_t* n_out) {
   return guarded([&] {
@@ -3185,7 +3227,7 @@ extern "C" int salvox_last_maxima(salvox_ctx* ctx, salvox_maximum* out, int64_t 
     if (out && cap > 0 && n > 0) {
       const size_t bytes = (size_t)std::min(n, cap) * sizeof(salvox_maximum);
       if (ctx->stage_valid) {
-        std::memcpy(out, ctx->h_stage.p, bytes);
+        parallel_memcpy(out, ctx->h_stage.p, bytes);
       } else {  // the device copy of the last call's maxima is still resident
         SX_CUDA(cudaSetDevice(ctx->device));
         SX_CUDA(cudaMemcpyAsync(out, ctx->d_maxima.p, bytes, cudaMemcpyDeviceToHost, ctx->stream));

@@ -448,3 +448,33 @@ def test_bin_edges_exact(sx, oracle, window):
     rng = np.random.default_rng(bins)
     vol = rng.choice(vals, size=(20, 21, 24)).astype(np.float32)
     _check_maps(sx, oracle, vol, low, high, bins, [2.0, 3.0], mode="exact")
+
+
+def test_last_maps_equal_the_call_maps(sx, oracle):
+    """salvox_last_maps: the pass run with null maps keeps them on the device;
+    fetching them afterwards (pageable and pinned buffers) gives the maps the
+    call itself returns; a context with no exhaustive call is an error."""
+    import ctypes as C
+
+    import torch
+
+    from paper_1310_6736_b200 import _lib
+
+    vol, _ = oracle.make_phantom(phantoms.ball_3d(40, (20.0, 18.0, 21.0), 7.0, 9))
+    ctx = sx.Context(0)
+    s, b, m, v = sx.kadir_brady_exhaustive_records(vol, [3.0, 5.0], 0, 64, 64, budget=10**10,
+                                                   ctx=ctx)
+    lib = _lib.load()
+    for pinned in (False, True):
+        if pinned:
+            ls, lb = (torch.empty(vol.shape, dtype=torch.float32).pin_memory().numpy()
+                      for _ in range(2))
+        else:
+            ls, lb = np.empty(vol.shape, np.float32), np.empty(vol.shape, np.float32)
+        _lib.check(lib.salvox_last_maps(ctx.handle, _lib.ptr(ls), _lib.ptr(lb)))
+        assert np.array_equal(ls, s) and np.array_equal(lb, b)
+    fresh = sx.Context(0)
+    with pytest.raises(ValueError, match="no exhaustive call"):
+        _lib.check(lib.salvox_last_maps(fresh.handle, C.c_void_p(0), C.c_void_p(0)))
+    fresh.close()
+    ctx.close()
