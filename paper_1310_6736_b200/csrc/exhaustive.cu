@@ -67,11 +67,15 @@ __global__ void bin_volume_kernel(const float* __restrict__ vol, uint8_t* __rest
                                   int nx, long long rows, int pitch, double low, double range,
                                   double m, int M) {
   const double inv = m / range;
-  if (pitch == nx && (reinterpret_cast<uintptr_t>(vol) & 15) == 0) {
-    // rows back to back in both arrays (nx % 16 == 0): one flat grid-stride
-    // pass, U independent 16-byte loads in flight per thread
+  if (pitch == nx && (reinterpret_cast<uintptr_t>(vol) & 15) == 0 &&
+      (reinterpret_cast<uintptr_t>(bins) & 3) == 0) {
+    // rows back to back in both arrays (the exhaustive layout when nx % 16 == 0,
+    // the seek layout always): one flat grid-stride pass over the whole slab, U
+    // independent 16-byte loads in flight per thread, the last n % 4 voxels scalar
     constexpr int U = 4;
-    const long long n4 = rows * (nx >> 2);
+    const long long n = rows * nx, n4 = n >> 2;
+    if (blockIdx.x == 0 && threadIdx.x < (n & 3))
+      bins[n4 * 4 + threadIdx.x] = bin_of(vol[n4 * 4 + threadIdx.x], low, range, m, inv, M);
     const long long stride = (long long)gridDim.x * blockDim.x;
     const float4* v4 = reinterpret_cast<const float4*>(vol);
     uchar4* b4 = reinterpret_cast<uchar4*>(bins);
@@ -134,7 +138,7 @@ void launch_bin_volume(salvox_ctx* ctx, const float* d_vol, uint8_t* d_bins, int
   int grid = (int)std::min<long long>(steps, (long long)ctx->sm_count * 16);
   if (pitch == nx) {  // flat form: 256 threads x U = 4 float4 each per block step
     block = 256;
-    grid = (int)std::max<long long>(1, std::min<long long>((rows * (nx / 4) + 1023) / 1024,
+    grid = (int)std::max<long long>(1, std::min<long long>((rows * nx / 4 + 1023) / 1024,
                                                            (long long)ctx->sm_count * 8));
   }
   bin_volume_kernel<<<grid, block, 0, stream ? stream : ctx->stream>>>(d_vol, d_bins, nx, rows, pitch, low,
