@@ -1604,7 +1604,10 @@ __global__ void maxima_kernel(const float* __restrict__ score, int nx, int ny, i
 // shared-memory ring while plane z+2 is in flight in registers, so every score
 // is read from L2/HBM ~1.3 times instead of up to 27 times and the load latency
 // overlaps the tests. Out-of-volume neighbours are -inf (they never kill).
-constexpr int kMxTX = 32, kMxTY = 8, kMxZ = 16;
+#ifndef MX_Z  // A/B knob: planes per CTA of the maxima pass
+#define MX_Z 16
+#endif
+constexpr int kMxTX = 32, kMxTY = 8, kMxZ = MX_Z;
 constexpr int kMxPl = (kMxTY + 2) * (kMxTX + 2);  // one plane with its halo
 constexpr int kMxPer = (kMxPl + kMxTX * kMxTY - 1) / (kMxTX * kMxTY);  // elements per thread
 __global__ void __launch_bounds__(kMxTX * kMxTY)
