@@ -26,6 +26,7 @@ is bound by shared-memory atomics, not HBM or tensor cores -- DESIGN.md).
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import subprocess
@@ -385,6 +386,7 @@ def main():
     max_pinned = torch.empty((nx * ny * nz // 24 + 4096) * sx.MAX_DTYPE.itemsize,
                              dtype=torch.uint8).pin_memory().numpy().view(sx.MAX_DTYPE)
     e2e_times, d2h = [], 0
+    gc.collect()  # start the loop with a clean heap (no gen-2 pass inherited from setup)
     for i in range(args.warmup + args.steps):
         torch.cuda.synchronize(dev)
         if world > 1:
@@ -445,7 +447,8 @@ def main():
                        "l2": "flushed between timed steps (256 MiB write)"},
             "e2e": {"value": total_evals / (e2e_ms * 1e-3), "unit": UNIT,
                     "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world,
-                    "ms_per_step": e2e_ms},
+                    "ms_per_step": e2e_ms, "ms_min": float(np.min(e2e_times)),
+                    "ms_max": float(np.max(e2e_times))},
             "roofline": {"bound": "smem", "achieved": achieved, "peak": peak_atoms_only,
                          "unit": "histogram updates/s",
                          "frac": (achieved / peak_atoms_only) if achieved else None,
