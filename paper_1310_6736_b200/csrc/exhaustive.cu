@@ -713,12 +713,15 @@ __device__ __forceinline__ void tm_st32(uint32_t taddr, const uint32_t* r) {
       : "memory");
 }
 
-template <int NB, bool DBG>
-__global__ void __launch_bounds__(1024, 1)
+// NT = 1024 (NB <= 33: a 16x8x8 tile) or 512 (NB = 65: 16x8x4, the default
+// 64-bin window of the reference). Either way each warp's lane group owns a
+// 2 * NS column slice and the NT / 128 slices fill the 512 TMEM columns.
+template <int NB, bool DBG, int NT = 1024>
+__global__ void __launch_bounds__(NT, 1)
     kb_tmem_kernel(const __grid_constant__ CUtensorMap tmap, const KbParams p) {
-  constexpr int TX = 16, TY = 8, TZ = 8, NT = 1024;
+  constexpr int TX = 16, TY = 8, TZ = NT / 128;
   constexpr int NS = NB - 1;  // snapshot bins (1..NB-1); multiple of 8
-  static_assert(NS % 8 == 0 && 2 * NS <= 64, "TMEM slice is 64 columns per thread");
+  static_assert(NS % 8 == 0 && 2 * NS * (NT / 128) <= 512, "TMEM: 2 * NS columns per thread");
   extern __shared__ __align__(1024) uint8_t smem[];
   uint32_t* hist = reinterpret_cast<uint32_t*>(smem);
   uint8_t* tile = smem + NB * NT * 4;
@@ -784,7 +787,7 @@ __global__ void __launch_bounds__(1024, 1)
     }
   }
   __syncthreads();
-  // warp footprint 8 (x) x 4 (y): lane -> (x, y); warps tile 2 (x) x 2 (y) x 8 (z)
+  // warp footprint 8 (x) x 4 (y): lane -> (x, y); warps tile 2 (x) x 2 (y) x TZ (z)
   const int lx = (lane & 7) + 8 * (warp & 1);
   const int ly = (lane >> 3) + 4 * ((warp >> 1) & 1);
   const int lz = warp >> 2;
@@ -796,7 +799,8 @@ __global__ void __launch_bounds__(1024, 1)
   // tcgen05.ld/st stay converged; they just never store a result
   const uint8_t* tb = tile + (lz + p.Rz) * p.SZ + (ly + p.R) * p.SY + (lx + p.R + delta);
   uint32_t* hc = hist + tid;
-  const uint32_t lane_base = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(64 * (warp >> 2));
+  const uint32_t lane_base =
+      tbase + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(2 * NS * (warp >> 2));
   uint32_t slotA = lane_base, slotB = lane_base + NS;  // A: older, B: newer
 
   {  // zero both TMEM slots (snapshots of "radius 0")
@@ -1740,6 +1744,12 @@ struct TileCfg {
 
 TileCfg pick_tile(int bins, bool two_d, bool epa = false) {
   const int nb = bins <= 16 ? 17 : (bins <= 32 ? 33 : 65);
+  static const bool kb65_old = [] {  // A/B knob SALVOX_KB65=kb: the 8x8x4 kb_kernel
+    const char* e = std::getenv("SALVOX_KB65");
+    return e && std::string(e) == "kb";
+  }();
+  if (nb == 65 && !two_d && !epa && !kb65_old)
+    return TileCfg{65, 16, 8, 4, false, true};  // kb_tmem_kernel<65, 512 threads>
   if (epa) {  // the plain kb_kernel tiles (64-bit words: 2x the histogram bytes)
     TileCfg t = nb == 65 ? (two_d ? TileCfg{65, 32, 8, 1, false} : TileCfg{65, 8, 8, 4, false})
                          : (two_d ? TileCfg{nb, 32, 16, 1, false} : TileCfg{nb, 8, 8, 8, false});
@@ -2121,6 +2131,13 @@ void dispatch_kb(salvox_ctx* ctx, const TileCfg& tc, const CUtensorMap& map, con
     } else {
       k<<<grid, 256, smem, ctx->stream>>>(map, kp);
     }
+    SX_LAUNCH_CHECK(ctx);
+    return;
+  }
+  if (tc.tmem && tc.nb == 65) {
+    auto k = kb_tmem_kernel<65, DBG, 512>;
+    SX_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k<<<grid, 512, smem, ctx->stream>>>(map, kp);
     SX_LAUNCH_CHECK(ctx);
     return;
   }
