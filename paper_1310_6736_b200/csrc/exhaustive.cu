@@ -992,15 +992,30 @@ __device__ __forceinline__ uint32_t quad_prmt(uint32_t w0, uint32_t w1, uint32_t
   return r;
 }
 
+// Histogram panel of voxel V in column group G. NB <= 33: 16 panels [V * 4 + G]
+// of 64 columns (8 warps: column = lane + 32 * (warp / 4)). NB = 65 (128
+// threads, 4 warps): 8 panels [(V / 2) * 4 + G], voxels 2k and 2k + 1 in the
+// two 32-column halves -- the PRMT address keeps its 256-byte bin rows and the
+// 65 bins x 512 voxels fit in 133 KB.
+template <int NB>
+struct QuadLayout {
+  static constexpr bool PP = NB > 33;            // paired-voxel panels
+  static constexpr int NT = PP ? 128 : 256;      // threads
+  static constexpr int TZ = PP ? 4 : 8;          // tile planes (16 x 8 x TZ voxels / 4 per thread)
+  static constexpr int SL = NB - 1 < 32 ? 32 : NB - 1;  // TMEM columns per snapshot slot
+  static constexpr int panel(int V, int G) { return PP ? (V >> 1) * 4 + G : V * 4 + G; }
+  static constexpr int coloff(int V) { return PP ? 32 * (V & 1) : 0; }  // words
+};
+
 template <int NB, int G, int V>
 __device__ __forceinline__ void quad_red1(uint32_t a, uint32_t n) {
-  constexpr uint32_t IMM = kDsmemBase + (uint32_t)((V * 4 + G) * NB * 256);
+  constexpr uint32_t IMM = kDsmemBase + (uint32_t)(QuadLayout<NB>::panel(V, G) * NB * 256);
   asm volatile("red.shared.add.u32 [%0+%2], %1;" ::"r"(a), "r"(n), "n"(IMM));
 }
 
 template <int NB, int G, int V>
 __device__ __forceinline__ void quad_red2(uint32_t ap, uint32_t am, uint32_t n) {
-  constexpr uint32_t IMM = kDsmemBase + (uint32_t)((V * 4 + G) * NB * 256);
+  constexpr uint32_t IMM = kDsmemBase + (uint32_t)(QuadLayout<NB>::panel(V, G) * NB * 256);
   asm volatile("red.shared.add.u32 [%0+%2], %1;" ::"r"(ap), "r"(n), "n"(IMM));
   asm volatile("red.shared.add.u32 [%0+%2], %1;" ::"r"(am), "r"(n), "n"(IMM));
 }
@@ -1008,10 +1023,12 @@ __device__ __forceinline__ void quad_red2(uint32_t ap, uint32_t am, uint32_t n) 
 template <int NB, int G, int SP, int SM>
 __device__ __forceinline__ void quad_entry_issue(uint32_t p0, uint32_t p1, uint32_t m0, uint32_t m1,
                                                  uint32_t c, uint32_t n) {
+  // odd voxels of paired panels sit 32 columns (128 bytes) to the right
+  const uint32_t co = QuadLayout<NB>::PP ? c + 128u : c;
   const uint32_t a0 = quad_prmt<0 + SP>(p0, p1, c), b0 = quad_prmt<0 + SM>(m0, m1, c);
-  const uint32_t a1 = quad_prmt<1 + SP>(p0, p1, c), b1 = quad_prmt<1 + SM>(m0, m1, c);
+  const uint32_t a1 = quad_prmt<1 + SP>(p0, p1, co), b1 = quad_prmt<1 + SM>(m0, m1, co);
   const uint32_t a2 = quad_prmt<2 + SP>(p0, p1, c), b2 = quad_prmt<2 + SM>(m0, m1, c);
-  const uint32_t a3 = quad_prmt<3 + SP>(p0, p1, c), b3 = quad_prmt<3 + SM>(m0, m1, c);
+  const uint32_t a3 = quad_prmt<3 + SP>(p0, p1, co), b3 = quad_prmt<3 + SM>(m0, m1, co);
 #ifdef KB_PAIR_ORDER  // A/B knob: +o and -o atomics of a voxel back to back
   quad_red2<NB, G, 0>(a0, b0, n);
   quad_red2<NB, G, 1>(a1, b1, n);
@@ -1150,12 +1167,15 @@ __device__ __noinline__ void quad_walk_dbl(const uint8_t* tb, uint32_t c, int g,
 // VB: voxels per boundary iteration (1: one voxel's math at a time, the state
 // rotating through slot 0; 2: two voxels' bins interleaved for ILP)
 template <int NB, bool DBG, bool DBL, int VB = 1>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(QuadLayout<NB>::NT, 1)
     kb_quad_kernel(const __grid_constant__ CUtensorMap tmap, const KbParams p) {
-  constexpr int TX = 16, TY = 8, TZ = 8, NT = 256, NV = 1024;
+  using QL = QuadLayout<NB>;
+  constexpr int TX = 16, TY = 8, TZ = QL::TZ, NT = QL::NT, NV = 4 * NT;
   constexpr int NS = NB - 1;  // snapshot bins (1..NB-1)
+  constexpr int SL = QL::SL;  // TMEM columns per snapshot slot
   constexpr int PANEL = NB * 256;  // bytes: NB bins x 64 columns
-  static_assert(NS % 8 == 0 && 2 * NS <= 64, "TMEM: 64 columns per voxel");
+  static_assert(NS % 8 == 0 && 8 * SL * (NT / 128) <= 512, "TMEM: 4 voxels x 2 slots x SL columns");
+  static_assert(!QL::PP || VB == 1, "paired panels: one voxel per boundary iteration");
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* hist = smem;  // 16 panels [v * 4 + G][bin][64 columns]
   uint8_t* tile = smem + NB * NV * 4;
@@ -1240,11 +1260,12 @@ __global__ void __launch_bounds__(256, 1)
   const uint32_t hs0 = smem_u32(smem);
   if ((hs0 & 0xffffu) != kDsmemBase) __trap();  // the immediates below assume it
   const uint32_t cb = (hs0 & 0xffff0000u) | (4u * (uint32_t)col);  // bytes 0, 2, 3 of every address
-  const uint32_t lane_base = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(256 * (warp >> 2));
+  const uint32_t lane_base =
+      tbase + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(8 * SL * (warp >> 2));
   {  // zero all snapshot slots ("radius 0")
     uint32_t z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
-    for (int c = 0; c < 256; c += 8) tm_st8(lane_base + c, z);
+    for (int c = 0; c < 8 * SL; c += 8) tm_st8(lane_base + c, z);
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
   }
   uint32_t TA[4] = {0u, 0u, 0u, 0u}, TB[4] = {0u, 0u, 0u, 0u};
@@ -1415,7 +1436,7 @@ __global__ void __launch_bounds__(256, 1)
     } else {
     uint32_t nxt[NS + 1];
     {
-      const uint32_t* hc = reinterpret_cast<const uint32_t*>(hist + G * PANEL) + col;
+      const uint32_t* hc = reinterpret_cast<const uint32_t*>(hist + QL::panel(0, G) * PANEL) + col;
 #pragma unroll
       for (int j = 0; j <= NS; ++j) nxt[j] = hc[j * 64];
     }
@@ -1427,7 +1448,8 @@ __global__ void __launch_bounds__(256, 1)
       for (int j = 0; j < NS; ++j) cur[j] = nxt[1 + j];
       const uint32_t T = bd.W - nxt[0];
       if (v < 3) {
-        const uint32_t* hn = reinterpret_cast<const uint32_t*>(hist + ((v + 1) * 4 + G) * PANEL) + col;
+        const uint32_t* hn = reinterpret_cast<const uint32_t*>(hist + QL::panel(v + 1, G) * PANEL) +
+                             col + QL::coloff(v + 1);
 #pragma unroll
         for (int j = 0; j <= NS; ++j) nxt[j] = hn[j * 64];
       }
@@ -1437,7 +1459,7 @@ __global__ void __launch_bounds__(256, 1)
       float hacc = 0.f;
       uint32_t dom = 0u;
       unsigned long long num = 0ull;
-      const uint32_t slot = lane_base + 64u * v + (uint32_t)(32 * older);
+      const uint32_t slot = lane_base + (uint32_t)(2 * SL * v + SL * older);
       // one tcgen05.ld wait per voxel: the whole older slot and the live column
       // are fetched first; then the bins are reduced with independent partial
       // sums (the boundary was ~30% of the kernel's time with the serial,
@@ -1744,11 +1766,18 @@ struct TileCfg {
 
 TileCfg pick_tile(int bins, bool two_d, bool epa = false) {
   const int nb = bins <= 16 ? 17 : (bins <= 32 ? 33 : 65);
-  static const bool kb65_old = [] {  // A/B knob SALVOX_KB65=kb: the 8x8x4 kb_kernel
+  // 3D, 65 bins (A/B knob SALVOX_KB65): "quad" (default) kb_quad_kernel<65> with
+  // paired-voxel panels, 128 threads; "tmem" kb_tmem_kernel<65, 512 threads>;
+  // "kb" the 8x8x4 kb_kernel
+  static const int kb65 = [] {
     const char* e = std::getenv("SALVOX_KB65");
-    return e && std::string(e) == "kb";
+    if (e && std::string(e) == "kb") return 2;
+    if (e && std::string(e) == "tmem") return 1;
+    return 0;
   }();
-  if (nb == 65 && !two_d && !epa && !kb65_old)
+  if (nb == 65 && !two_d && !epa && kb65 == 0)
+    return TileCfg{65, 16, 8, 4, false, false, true, true, false};
+  if (nb == 65 && !two_d && !epa && kb65 == 1)
     return TileCfg{65, 16, 8, 4, false, true};  // kb_tmem_kernel<65, 512 threads>
   if (epa) {  // the plain kb_kernel tiles (64-bit words: 2x the histogram bytes)
     TileCfg t = nb == 65 ? (two_d ? TileCfg{65, 32, 8, 1, false} : TileCfg{65, 8, 8, 4, false})
@@ -2112,14 +2141,16 @@ void dispatch_kb(salvox_ctx* ctx, const TileCfg& tc, const CUtensorMap& map, con
     return;                                                                                  \
   }
   if (tc.quad) {
-    auto k = tc.dbl ? (tc.nb == 17 ? (tc.vb2 ? kb_quad_kernel<17, DBG, true, 2> : kb_quad_kernel<17, DBG, true, 1>)
+    auto k = tc.nb == 65 ? (tc.dbl ? kb_quad_kernel<65, DBG, true, 1> : kb_quad_kernel<65, DBG, false, 1>)
+           : tc.dbl ? (tc.nb == 17 ? (tc.vb2 ? kb_quad_kernel<17, DBG, true, 2> : kb_quad_kernel<17, DBG, true, 1>)
                                    : (tc.vb2 ? kb_quad_kernel<33, DBG, true, 2> : kb_quad_kernel<33, DBG, true, 1>))
                     : (tc.nb == 17 ? kb_quad_kernel<17, DBG, false> : kb_quad_kernel<33, DBG, false>);
+    const int threads = tc.nb == 65 ? QuadLayout<65>::NT : 256;
     SX_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     if (pdl && !DBG) {
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = grid;
-      cfg.blockDim = dim3(256);
+      cfg.blockDim = dim3(threads);
       cfg.dynamicSmemBytes = smem;
       cfg.stream = ctx->stream;
       cudaLaunchAttribute at[1];
@@ -2129,7 +2160,7 @@ void dispatch_kb(salvox_ctx* ctx, const TileCfg& tc, const CUtensorMap& map, con
       cfg.numAttrs = 1;
       SX_CUDA(cudaLaunchKernelEx(&cfg, k, map, kp));
     } else {
-      k<<<grid, 256, smem, ctx->stream>>>(map, kp);
+      k<<<grid, threads, smem, ctx->stream>>>(map, kp);
     }
     SX_LAUNCH_CHECK(ctx);
     return;
