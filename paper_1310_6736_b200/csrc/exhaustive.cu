@@ -669,7 +669,7 @@ __global__ void __launch_bounds__(4 * TY * TZ, 1)
   }
 }
 
-// K2'' (3D, NB <= 33; SALVOX_KB_VARIANT=2): 1024 threads per CTA (32 warps/SM, twice kb_kernel's
+// K2'' (3D; SALVOX_KB_VARIANT=2 at NB <= 33, SALVOX_KB65=tmem at 65 with 512 threads): 1024 threads per CTA (32 warps/SM, twice kb_kernel's
 // latency hiding) with the two radius snapshots held in TENSOR MEMORY. At 1024
 // threads the register file allows 64 registers per thread, too few for the
 // 2 x 32 snapshot words, so each thread parks them in its TMEM lane: warp w
@@ -924,7 +924,8 @@ __global__ void __launch_bounds__(NT, 1)
   }
 }
 
-// K2-quad (3D, NB <= 33; the default): 256 threads, FOUR x-adjacent
+// K2-quad (3D, the default; NB = 65 runs 128 threads with paired-voxel panels,
+// see QuadLayout): 256 threads, FOUR x-adjacent
 // voxels per thread, built so an update costs ~2.9 instructions and ~1.44
 // shared-pipe wavefronts instead of kb_tmem_kernel's ~4 and 2:
 //  * bins: the tile row pitch and box start are multiples of 16 and each
@@ -1758,7 +1759,7 @@ struct TileCfg {
   int nb, tx, ty, tz;
   bool pair;          // kb_pair_kernel (two voxels per thread, tx = 8)
   bool tmem = false;  // kb_tmem_kernel (1024 threads, snapshots in TMEM)
-  bool quad = false;  // kb_quad_kernel (256 threads x 4 voxels, snapshots in TMEM)
+  bool quad = false;  // kb_quad_kernel (256 threads x 4 voxels -- 128 at 65 bins -- snapshots in TMEM)
   bool dbl = false;  // kb_quad_kernel<DBL>: x-adjacent offset doubles share bin words
   bool vb2 = false;  // kb_quad_kernel<.., VB = 2>: two voxels per boundary iteration
   bool epa = false;  // kb_kernel<.., EPA>: Epanechnikov, 64-bit count|sum words
