@@ -478,3 +478,24 @@ def test_last_maps_equal_the_call_maps(sx, oracle):
         _lib.check(lib.salvox_last_maps(fresh.handle, C.c_void_p(0), C.c_void_p(0)))
     fresh.close()
     ctx.close()
+
+
+def test_default_64_bins_match_the_reference(sx):
+    """The reference's default window has 64 bins (volume.hpp:94): the 65-bin
+    quad kernel (paired-voxel panels) against the reference's own
+    kadir_brady_exhaustive (oracle/_ref) on a 3D phantom: maps within the
+    tolerance, the same maxima positions, the same EvalCounter visits."""
+    from oracle import ref as R
+
+    if not R.available():
+        pytest.skip("oracle/_ref/libsalvox_ref.so not built")
+    vol = R.make_phantom(phantoms.ball_3d(36, (17.0, 18.0, 16.5), 7.0, 64,
+                                         background={"type": "gaussian", "mean": 20.0,
+                                                     "sigma": 6.0}))[0]
+    scales = [3.0, 4.0, 5.0, 6.0]
+    rs, rb, rm, rv = R.exhaustive(vol, 0.0, 64.0, 64, scales, budget=10**9)
+    s, b, m, v = sx.kadir_brady_exhaustive_records(vol, scales, 0.0, 64.0, 64, budget=10**9)
+    err = np.abs(s.astype(np.float64) - rs) - (RTOL * np.maximum(np.abs(s), np.abs(rs)) + ATOL)
+    assert err.max() <= 0.0
+    assert (b != rb).sum() <= max(2, vol.size // 5000) and v == rv
+    assert np.array_equal(m["position"], rm[:, :3])
