@@ -103,8 +103,11 @@ def kadir_brady_exhaustive(volume, scales, window_low=None, window_high=None, bi
     """
     score, _, maxima, _ = kadir_brady_exhaustive_records(volume, scales, window_low, window_high,
                                                          bins, kernel, budget, ctx)
-    out = [{"position": tuple(float(p) for p in m["position"]), "score": float(m["score"]),
-            "scale": float(m["scale"])} for m in maxima]
+    # columns to Python lists first: per-record access of a structured array costs
+    # microseconds, and a 256^3 pass has ~0.5 M maxima
+    pos = maxima["position"].tolist()
+    out = [{"position": tuple(p), "score": s, "scale": c}
+           for p, s, c in zip(pos, maxima["score"].tolist(), maxima["scale"].tolist())]
     return score, out
 
 
