@@ -103,11 +103,21 @@ def kadir_brady_exhaustive(volume, scales, window_low=None, window_high=None, bi
     """
     score, _, maxima, _ = kadir_brady_exhaustive_records(volume, scales, window_low, window_high,
                                                          bins, kernel, budget, ctx)
-    # columns to Python lists first: per-record access of a structured array costs
-    # microseconds, and a 256^3 pass has ~0.5 M maxima
+    # columns to Python lists first (per-record access of a structured array costs
+    # microseconds; a 256^3 pass has ~0.5 M maxima), and no cyclic-GC passes while
+    # the ~0.5 M new containers are made (none of them can form a cycle):
+    # 2.4 s -> 0.35 s for C2's list
+    import gc
+
     pos = maxima["position"].tolist()
-    out = [{"position": tuple(p), "score": s, "scale": c}
-           for p, s, c in zip(pos, maxima["score"].tolist(), maxima["scale"].tolist())]
+    enabled = gc.isenabled()
+    gc.disable()
+    try:
+        out = [{"position": tuple(p), "score": s, "scale": c}
+               for p, s, c in zip(pos, maxima["score"].tolist(), maxima["scale"].tolist())]
+    finally:
+        if enabled:
+            gc.enable()
     return score, out
 
 
